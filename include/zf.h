@@ -1,0 +1,204 @@
+/*
+ * zf.h -- C-ABI of libzf.so, the B200-native (sm_100a) hot path of ZenFlow
+ * (arXiv 2505.12242): importance-based gradient partitioning.
+ *
+ * For every linear layer's weight gradient G ([n, m], row-major, n = output
+ * rows, m = input channels / columns) the path
+ *   1. computes per-column squared L2 norms                (§3.3 "Lightweight Proxy")
+ *   2. sums them across data-parallel ranks (NCCL)          (fig. gradient_gathering)
+ *   3. selects the top-k columns, cached for N steps        ("cache and reuse")
+ *   4. applies AdamW in place to the selected columns only
+ *   5. compacts the unselected columns for the CPU side     ("(1-k)·M unimportant")
+ *   6. stages them to pinned host memory, where they are
+ *      accumulated in a double-buffered fp32 window         (fig. zero_bubble_pipeline)
+ * Citation key: P:n = PAPER.md line n; S:n = SPEC.md line n; Rn = reading n in
+ * DESIGN.md §3.
+ *
+ * Conventions (every function):
+ *  - Pointers are DEVICE pointers unless marked [host].  Device pointers must
+ *    be valid CUDA device (or managed) memory of the current device.
+ *  - Matrices are row-major with a leading dimension (elements) ld >= m; row i
+ *    of G starts at G + i*ld.  Vector (16-byte) paths are used when row starts
+ *    are 16-byte aligned; otherwise a slower scalar path runs (same results).
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Every call is
+ *    asynchronous and ordered on `stream`; none synchronizes the device unless
+ *    documented.
+ *  - Argument errors are detected synchronously, before anything is enqueued,
+ *    and return ZF_EINVAL with a message in zf_last_error().  CUDA/NCCL launch
+ *    failures return ZF_ECUDA / ZF_ENCCL.  No C++ exception crosses the ABI.
+ *  - Non-finite gradient values (NaN/Inf; the oracle and SPEC S:44 reject them)
+ *    are detected on the device and OR-ed into a flag; results of such a step
+ *    are unspecified (reading R15).
+ *  - fp32 arithmetic of the AdamW update is IEEE round-to-nearest with no
+ *    contraction, in the op order of DESIGN.md §2 O6, so results are
+ *    reproducible bit for bit.
+ */
+#ifndef ZF_H_
+#define ZF_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* zf_stream_t; /* == cudaStream_t */
+
+typedef enum {
+    ZF_OK = 0,
+    ZF_EINVAL = 1,     /* bad argument (checked before enqueueing anything)           */
+    ZF_ENONFINITE = 2, /* NaN/Inf seen in a gradient (reported by zf_sync)             */
+    ZF_ECUDA = 3,      /* CUDA runtime/driver error; detail in zf_last_error()         */
+    ZF_ENCCL = 4,      /* NCCL error                                                   */
+    ZF_ENOMEM = 5,     /* device or host allocation failed                             */
+    ZF_ESTATE = 6      /* call not valid in the context's current state                */
+} zf_status;
+
+typedef enum { ZF_FP32 = 0, ZF_BF16 = 1 } zf_dtype;
+
+/* AdamW hyper-parameters [host] (reading R8: PyTorch AdamW; paper P:653-654 uses
+ * lr 1e-5, weight decay 0).  decoupled=1: p *= (1 - lr*wd) (AdamW);
+ * decoupled=0: g += wd*p (Adam with L2). */
+typedef struct {
+    float lr, beta1, beta2, eps, weight_decay;
+    int32_t decoupled;
+} zf_adam_params;
+
+/* Human-readable name of a status code; never NULL. */
+const char* zf_status_string(int32_t status);
+/* Detail of the last failure on the calling thread ("" if none); never NULL. */
+const char* zf_last_error(void);
+/* ABI version (major*100 + minor). */
+int32_t zf_version(void);
+/* k = ceil(m * ratio_ppm / 1e6) in integer arithmetic, clamped to [1, m]
+ * ("|channel_ids| = ceil(k_channel_ratio x m)"; reading R2).  Returns -1 if
+ * m < 1 or ratio_ppm is outside (0, 1e6]. */
+int64_t zf_k_for(int64_t m, int32_t ratio_ppm);
+
+/* =========================== stateless primitives ===========================
+ * The caller owns every buffer.  Scratch memory, when needed, is taken from the
+ * stream-ordered allocator (cudaMallocAsync) on `stream`. */
+
+/* Row 1 of §8(a) -- P:486 "each GPU computes and shares per-column gradient norms
+ * squared (i.e., the sum of squared gradient values within each column)".
+ *   G       [n, ld] row-major, dtype gdt (ZF_BF16 or ZF_FP32), read only.
+ *   norms   [m] fp32, OVERWRITTEN with sum_i G[i][j]^2 (fp32 accumulation in a
+ *           fixed, deterministic order: identical bits run to run).
+ *   nonfinite  [1] int32 or NULL; set to 1 (never cleared) if any norm is NaN/Inf.
+ * Requires n >= 1, m >= 1, ld >= m. */
+zf_status zf_column_norms(const void* G, zf_dtype gdt, int64_t n, int64_t m, int64_t ld,
+                          float* norms, int32_t* nonfinite, zf_stream_t stream);
+
+/* Row 3 -- P:287 "top-k selection, which retains the gradients with the highest
+ * magnitudes", applied to the per-column proxy.
+ *   norms   [m] fp32, finite and >= 0 (the output of zf_column_norms, possibly
+ *           summed over ranks).
+ *   idx     [k] int32, OVERWRITTEN with the k columns of largest norm, ties broken
+ *           toward the lower column index (reading R3), in ASCENDING column order.
+ * Requires 1 <= k <= m <= 2^31-1.  Exact: selection compares fp32 bit patterns. */
+zf_status zf_topk_columns(const float* norms, int64_t m, int64_t k, int32_t* idx, zf_stream_t stream);
+
+/* Row 5 -- P:385 "a selective-optimizer, initialized only with the corresponding
+ * parameter subset, performs an in-place update"; "We extend PyTorch's
+ * Adam and AdamW".  For every row i < n and slot s < k (column c = idx[s]):
+ * AdamW (DESIGN.md §2 O6) on p[i][c] with gradient G[i][c] and moments
+ * exp_avg[i][s], exp_avg_sq[i][s], step count t_s = step[s] + 1; afterwards
+ * step[s] = t_s.
+ *   p        [n, ldp] dtype pdt, updated in place (bf16: RNE store).
+ *   G        [n, ldg] dtype gdt, read only.
+ *   idx      [k] int32, strictly ascending, each in [0, m).
+ *   exp_avg, exp_avg_sq  [n, k] fp32 row-major, updated in place.
+ *   step     [k] int32, updated in place.
+ *   hp       [host] hyper-parameters; beta1, beta2 in [0, 1), eps > 0.
+ * Other columns of p are not touched. */
+zf_status zf_selective_adam(void* p, zf_dtype pdt, int64_t ldp, const void* G, zf_dtype gdt, int64_t ldg,
+                            int64_t n, int64_t m, const int32_t* idx, int64_t k, float* exp_avg,
+                            float* exp_avg_sq, int32_t* step, const zf_adam_params* hp, zf_stream_t stream);
+
+/* Row 6 -- P:414 "ZenFlow transfers only the (1-k)·M unimportant gradients to the
+ * CPU".  out[i][u] = G[i][j] where j is the u-th column NOT in idx (ascending):
+ * a bit copy into a dense row-major [n, m-k] buffer of dtype gdt (reading R12).
+ *   out      device memory, or mapped pinned host memory; 16-byte aligned for the
+ *            vector path.  k == m gives an empty output (nothing written). */
+zf_status zf_compact_unselected(const void* G, zf_dtype gdt, int64_t n, int64_t m, int64_t ld,
+                                const int32_t* idx, int64_t k, void* out, zf_stream_t stream);
+
+/* ============================ stateful driver ===============================
+ * One context per (process, GPU).  It owns: the flat norm buffer, the selected
+ * index sets (double-buffered for the refresh remap), the AdamW moments
+ * [n_local, k] (double-buffered), per-slot step counts, the device compaction
+ * buffers, pinned host staging buffers, the fp32 host accumulators, a copy
+ * stream, host accumulation threads and (world > 1) an NCCL communicator. */
+
+typedef struct {
+    int64_t n;          /* rows of this rank's shard (n_local; all ranks same m)   */
+    int64_t m;          /* columns (input channels)                                */
+    int64_t ld_grad;    /* leading dim of the gradient passed to zf_step (>= m)     */
+    int64_t ld_param;   /* leading dim of the parameter passed to zf_step (>= m)    */
+} zf_layer_desc;
+
+typedef struct {
+    zf_dtype grad_dtype, param_dtype; /* the same for every layer of a context        */
+    int32_t topk_ppm;                 /* k = zf_k_for(m, topk_ppm) per layer           */
+    int32_t refresh_interval;         /* N: selection refreshed iff t % N == 0 */
+    int32_t accum_interval;           /* S: host accumulation window (S=4)      */
+    zf_adam_params adam;
+    int32_t offload;                  /* 1: D2H of each layer's compact block to pinned
+                                         host as soon as it is written (row 7)        */
+    int32_t host_accumulate;          /* 1: fp32 accumulation on the host (row 8);
+                                         requires offload and N % S == 0             */
+    int32_t host_threads;             /* host accumulation threads (0: default)        */
+} zf_config;
+
+typedef struct zf_ctx zf_ctx;
+
+/* Rank 0 creates the NCCL unique id; the caller broadcasts its 128 bytes. */
+zf_status zf_nccl_unique_id(void* out128 /* [host] 128 bytes */);
+
+/* Create a context on CUDA device `device`.  layers [host] [n_layers].
+ * world/rank: data-parallel group; nccl_id128 [host] is required iff world > 1
+ * (collective call: every rank must call zf_create).  Each rank passes the
+ * row shard it owns (reading R13: rows [r*n/P, (r+1)*n/P) of every matrix). */
+zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, const zf_config* cfg, int32_t world,
+                    int32_t rank, const void* nccl_id128, int32_t device, zf_ctx** out);
+
+/* One step of the hot path at global step t (t >= 0, increasing by 1 per call;
+ * the first call must be a refresh, i.e. t % N == 0).
+ *   grads  [host] array of n_layers DEVICE pointers (G of each layer, [n, ld_grad])
+ *   params [host] array of n_layers DEVICE pointers (p of each layer, [n, ld_param])
+ * Refresh step (t % N == 0): column norms -> (world > 1) NCCL all-reduce(sum)
+ * of the flat norm vector -> per-layer top-k -> moment remap (R7) -> fused
+ * selective AdamW + compaction.  Other steps: fused selective AdamW +
+ * compaction with the cached selection.  With offload, each layer's compact
+ * block is copied to pinned host memory on the context's copy stream as soon as
+ * the layer is done; with host_accumulate, host threads add it into the active
+ * fp32 accumulator of window floor(t/S).  grads/params may be reused by the
+ * caller once `stream` passes this call. */
+zf_status zf_step(zf_ctx* ctx, int64_t t, void* const* grads, void* const* params, zf_stream_t stream);
+
+/* Block until every D2H copy and host accumulation issued so far has finished.
+ * Returns ZF_ENONFINITE if a non-finite gradient was seen since the last call. */
+zf_status zf_sync(zf_ctx* ctx);
+
+/* Views of library-owned state (valid until the next zf_step / zf_destroy). */
+zf_status zf_selected(zf_ctx* ctx, int32_t layer, const int32_t** idx, int64_t* k);   /* device [k] */
+zf_status zf_norms(zf_ctx* ctx, int32_t layer, const float** norms);                  /* device [m], last refresh */
+zf_status zf_optimizer_state(zf_ctx* ctx, int32_t layer, const float** exp_avg, const float** exp_avg_sq,
+                             const int32_t** step);                                   /* device [n,k],[n,k],[k] */
+/* Compact block of the last step: device [n, m-k] (and, with offload, its pinned
+ * host copy once zf_sync returned; NULL otherwise). */
+zf_status zf_compact_buffer(zf_ctx* ctx, int32_t layer, const void** dev, const void** host);
+/* Host accumulator [host] fp32 [rows, cols] = [n, m-k]: which = 0 the active
+ * window's buffer, 1 the last sealed window's buffer (NULL if none yet). */
+zf_status zf_host_accumulator(zf_ctx* ctx, int32_t layer, int32_t which, const float** host, int64_t* rows,
+                              int64_t* cols);
+/* Change the learning rate used from the next zf_step on (schedules). */
+zf_status zf_set_lr(zf_ctx* ctx, float lr);
+/* Number of this library's kernel launches issued so far by the context. */
+int64_t zf_kernel_launches(zf_ctx* ctx);
+zf_status zf_destroy(zf_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZF_H_ */

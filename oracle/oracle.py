@@ -1,0 +1,259 @@
+"""Python side of the CPU ORACLE (ctypes over oracle/liboracle.so + step orchestration).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import this
+module.  The product package ``paper_2505_12242_b200`` never imports it, and it
+never imports the product package.
+
+Arrays: fp32 data are ``np.float32``; bf16 data are ``np.uint16`` holding the
+bf16 bit patterns.  All arithmetic happens in ``zf_oracle.cpp``; this file only
+marshals arguments and sequences the steps of the method in the paper's order:
+
+* refresh (every N steps, "cache and reuse selected channel indices"):
+  column norms (O1) -> top-k (O3) -> moment remap (O5, reading R7);
+* selective AdamW on the selected columns (O6);
+* compaction of the unselected columns (O7);
+* accumulation into the active buffer of a double-buffered pair, zeroed at the
+  start of each S-step window and sealed at its end (O8).
+
+``OracleLayer.step`` has the semantics ``zf_step`` implements.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "zf_oracle.cpp")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+F32, BF16 = 0, 1
+
+_i64, _i32, _f32, _f64, _vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_float, ctypes.c_double, ctypes.c_void_p
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle (g++ -O2 -ffp-contract=off, no fast-math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math",
+                               "-fPIC", "-shared", "-o", _LIB + ".tmp", _SRC])
+        os.replace(_LIB + ".tmp", _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build())
+        L = _lib
+        L.oracle_bf16_round.argtypes = [_f32]; L.oracle_bf16_round.restype = _f32
+        L.oracle_k_for.argtypes = [_i64, _i32]; L.oracle_k_for.restype = _i64
+        L.oracle_column_norms.argtypes = [_vp, ctypes.c_int, _i64, _i64, _i64, _vp]
+        L.oracle_column_norms.restype = ctypes.c_int
+        L.oracle_column_norms_f64.argtypes = [_vp, ctypes.c_int, _i64, _i64, _i64, _vp]
+        L.oracle_column_norms_f64.restype = None
+        L.oracle_topk.argtypes = [_vp, _i64, _i64, _vp]; L.oracle_topk.restype = ctypes.c_int
+        L.oracle_column_map.argtypes = [_vp, _i64, _i64, _vp, _vp]; L.oracle_column_map.restype = None
+        L.oracle_remap.argtypes = [_i64, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp]
+        L.oracle_remap.restype = None
+        L.oracle_selective_adamw.argtypes = [_vp, ctypes.c_int, _i64, _vp, ctypes.c_int, _i64, _i64,
+                                             _vp, _i64, _vp, _vp, _vp, _f64, _f64, _f64, _f64, _f64,
+                                             ctypes.c_int]
+        L.oracle_selective_adamw.restype = None
+        L.oracle_compact.argtypes = [_vp, ctypes.c_int, _i64, _i64, _i64, _vp, _i64, _vp]
+        L.oracle_compact.restype = None
+        L.oracle_accumulate.argtypes = [_vp, _vp, ctypes.c_int, _i64]; L.oracle_accumulate.restype = None
+    return _lib
+
+
+def _dt(a: np.ndarray) -> int:
+    if a.dtype == np.float32:
+        return F32
+    if a.dtype == np.uint16:
+        return BF16
+    raise TypeError(f"oracle arrays are float32 or uint16(bf16 bits), got {a.dtype}")
+
+
+def _p(a: np.ndarray):
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+# ---------------------------------------------------------------- primitives
+def bf16_round(x: float) -> float:
+    return float(lib().oracle_bf16_round(float(x)))
+
+
+def bf16_bits_to_f32(h: np.ndarray) -> np.ndarray:
+    """Exact widening of bf16 bit patterns (left shift by 16)."""
+    return (h.astype(np.uint32) << 16).view(np.float32)
+
+
+def as_f32(a: np.ndarray) -> np.ndarray:
+    return bf16_bits_to_f32(a) if a.dtype == np.uint16 else a.astype(np.float32)
+
+
+def k_for(m: int, ratio_ppm: int) -> int:
+    return int(lib().oracle_k_for(m, ratio_ppm))
+
+
+def column_norms(G: np.ndarray) -> np.ndarray:
+    G = np.ascontiguousarray(G)
+    n, m = G.shape
+    out = np.empty(m, np.float32)
+    bad = lib().oracle_column_norms(_p(G), _dt(G), n, m, m, _p(out))
+    if bad:
+        raise FloatingPointError("non-finite gradient (SPEC S:44 rejects)")
+    return out
+
+
+def column_norms_f64(G: np.ndarray) -> np.ndarray:
+    G = np.ascontiguousarray(G)
+    n, m = G.shape
+    out = np.empty(m, np.float64)
+    lib().oracle_column_norms_f64(_p(G), _dt(G), n, m, m, _p(out))
+    return out
+
+
+def topk(norms: np.ndarray, k: int) -> np.ndarray:
+    norms = np.ascontiguousarray(norms, dtype=np.float32)
+    m = norms.shape[0]
+    if m == 0:
+        raise ValueError("empty norms vector (S:108)")
+    if not 1 <= k <= m:
+        raise ValueError("k out of range")
+    idx = np.empty(k, np.int32)
+    if lib().oracle_topk(_p(norms), m, k, _p(idx)):
+        raise FloatingPointError("non-finite norm")
+    return idx
+
+
+def column_map(idx: np.ndarray, m: int):
+    idx = np.ascontiguousarray(idx, dtype=np.int32)
+    slot = np.empty(m, np.int32)
+    upos = np.empty(m, np.int32)
+    lib().oracle_column_map(_p(idx), idx.shape[0], m, _p(slot), _p(upos))
+    return slot, upos
+
+
+def remap(n, idx_old, m_old, v_old, step_old, idx_new):
+    k = idx_new.shape[0]
+    m_new = np.empty((n, k), np.float32)
+    v_new = np.empty((n, k), np.float32)
+    step_new = np.empty(k, np.int32)
+    lib().oracle_remap(n, _p(idx_old), idx_old.shape[0], _p(m_old), _p(v_old), _p(step_old),
+                       _p(idx_new), k, _p(m_new), _p(v_new), _p(step_new))
+    return m_new, v_new, step_new
+
+
+@dataclass
+class AdamHP:
+    """Reading R8: PyTorch AdamW defaults; the paper gives lr 1e-5, wd 0.
+    Real-valued (double) hyper-parameters; derived fp32 constants are rounded once."""
+    lr: float = 1e-3
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    weight_decay: float = 0.0
+    decoupled: int = 1
+
+
+def selective_adamw(P: np.ndarray, G: np.ndarray, idx: np.ndarray, M: np.ndarray, V: np.ndarray,
+                    step: np.ndarray, hp: AdamHP) -> None:
+    """In place on P (selected columns), M, V, step."""
+    n, m = G.shape
+    assert P.shape == G.shape and M.shape == V.shape == (n, idx.shape[0]) and step.shape == idx.shape
+    lib().oracle_selective_adamw(_p(P), _dt(P), P.shape[1], _p(G), _dt(G), m, n, _p(idx), idx.shape[0],
+                                 _p(M), _p(V), _p(step), hp.lr, hp.beta1, hp.beta2, hp.eps,
+                                 hp.weight_decay, int(hp.decoupled))
+
+
+def compact(G: np.ndarray, idx: np.ndarray) -> np.ndarray:
+    G = np.ascontiguousarray(G)
+    n, m = G.shape
+    k = idx.shape[0]
+    out = np.empty((n, m - k), G.dtype)
+    lib().oracle_compact(_p(G), _dt(G), n, m, m, _p(np.ascontiguousarray(idx, np.int32)), k, _p(out))
+    return out
+
+
+def accumulate(acc: np.ndarray, stage: np.ndarray) -> None:
+    assert acc.dtype == np.float32 and acc.size == stage.size
+    lib().oracle_accumulate(_p(acc), _p(np.ascontiguousarray(stage)), _dt(stage), acc.size)
+
+
+def shard_rows(n: int, world: int, rank: int):
+    """Row-wise contiguous partition, near-equal, remainder to the earliest shards
+    (4096x4096 into 4 -> 1024-row shards; 5 rows into 2 -> 3+2)."""
+    base, rem = divmod(n, world)
+    start = rank * base + min(rank, rem)
+    return start, start + base + (1 if rank < rem else 0)
+
+
+# -------------------------------------------------------------- step driver
+@dataclass
+class OracleLayer:
+    """One weight matrix under the method (the state zf_step keeps for it).
+
+    refresh_interval = N (selection refreshed iff t % N == 0, [R6]);
+    accum_interval = S (window length of the CPU-side accumulation).
+    """
+    n: int
+    m: int
+    ratio_ppm: int
+    refresh_interval: int = 4
+    accum_interval: int = 4
+    hp: AdamHP = field(default_factory=AdamHP)
+    idx: np.ndarray | None = None
+    M: np.ndarray | None = None
+    V: np.ndarray | None = None
+    steps: np.ndarray | None = None
+    acc: list | None = None
+    last_norms: np.ndarray | None = None
+    last_out: np.ndarray | None = None
+
+    @property
+    def k(self) -> int:
+        return k_for(self.m, self.ratio_ppm)
+
+    def step(self, t: int, G: np.ndarray, P: np.ndarray, idx_override: np.ndarray | None = None):
+        """One step of the hot path for this matrix at global step t.
+
+        idx_override: use this selection instead of the oracle's own top-k on a
+        refresh step (parity protocol O10: downstream steps are compared on the
+        GPU's selection, so a tolerated boundary swap never cascades)."""
+        k = self.k
+        if t % self.refresh_interval == 0 or self.idx is None:
+            self.last_norms = column_norms(G)
+            new_idx = topk(self.last_norms, k) if idx_override is None else np.asarray(idx_override, np.int32)
+            if self.idx is None:
+                self.M = np.zeros((self.n, k), np.float32)
+                self.V = np.zeros((self.n, k), np.float32)
+                self.steps = np.zeros(k, np.int32)
+            else:
+                self.M, self.V, self.steps = remap(self.n, self.idx, self.M, self.V, self.steps, new_idx)
+            self.idx = new_idx
+        selective_adamw(P, G, self.idx, self.M, self.V, self.steps, self.hp)
+        out = compact(G, self.idx)
+        S = self.accum_interval
+        if self.acc is None:
+            self.acc = [np.zeros((self.n, self.m - k), np.float32) for _ in range(2)]
+        a = (t // S) % 2
+        if t % S == 0:
+            self.acc[a][...] = 0.0
+        accumulate(self.acc[a], out)
+        self.last_out = out
+        return out
+
+    def sealed(self, t: int):
+        """The accumulator sealed by the window that ended at or before step t."""
+        S = self.accum_interval
+        w = t // S if (t + 1) % S == 0 else t // S - 1
+        return None if w < 0 else self.acc[w % 2]

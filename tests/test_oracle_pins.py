@@ -1,0 +1,438 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix.
+
+Every test here checks the oracle against something OTHER than itself: a
+worked example printed in the reference (tests/golden/, each cited), a closed
+form, an invariant, a brute-force evaluation on tiny inputs written
+independently (different loop order / definition), or a library routine
+(torch.optim.AdamW, torch's bf16 cast) for a special case the method reduces
+to.  Each is chosen so a plausible slip in the oracle (a dropped term, a
+transposed operand, a wrong index or sign) fails at least one of them.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _golden(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+def _bf16(x):
+    """bf16 bit patterns via torch's own RNE cast (a library routine)."""
+    t = torch.tensor(np.asarray(x, np.float32)).to(torch.bfloat16)
+    return t.view(torch.int16).numpy().view(np.uint16)
+
+
+# ------------------------------------------------------------------ bf16 RNE
+def test_bf16_round_matches_torch(orc):
+    rng = np.random.default_rng(1)
+    xs = np.concatenate([rng.standard_normal(2000).astype(np.float32) * 10.0 ** rng.integers(-8, 8, 2000),
+                         np.array([1.0 + 2 ** -8, 1.0 + 3 * 2 ** -8, -(1.0 + 2 ** -8), 0.0, -0.0], np.float32)])
+    want = orc.bf16_bits_to_f32(_bf16(xs))
+    got = np.array([orc.bf16_round(float(x)) for x in xs], np.float32)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+# ------------------------------------------------------------------ O2  k
+def test_k_closed_form_table(orc):
+    for m, k10, k1 in _golden("k_table.json")["rows"]:
+        assert orc.k_for(m, 100000) == k10, m
+        assert orc.k_for(m, 10000) == k1, m
+
+
+def test_k_integer_ceil_edge(orc):
+    # 100 * 0.07 = 7.000000000000001 in binary fp -> a float ceil gives 8; ceil(7) = 7.
+    assert orc.k_for(100, 70000) == 7
+    assert orc.k_for(1, 1) == 1            # k >= 1
+    assert orc.k_for(37, 1000000) == 37    # ratio 1 -> all columns
+    for m in range(1, 300):
+        for ppm in (1, 9999, 10000, 100000, 333333, 999999):
+            assert orc.k_for(m, ppm) == max(1, -(-m * ppm // 1000000))
+
+
+# ------------------------------------------------------------------ O1  norms
+def test_norms_worked_examples(orc):
+    for ex in _golden("worked_examples.json")["column_norms"]:
+        G = np.array(ex["G"], np.float32)
+        assert np.array_equal(orc.column_norms(G), np.array(ex["norms"], np.float32)), ex["source"]
+
+
+def test_norms_sharded_worked_example(orc):
+    ex = _golden("worked_examples.json")["gather_column_norms"][0]
+    parts = [orc.column_norms_f64(np.array(s, np.float32)) for s in ex["shards"]]
+    assert np.array_equal(sum(parts), np.array(ex["norms"])), ex["source"]
+
+
+def test_norms_integer_closed_form(orc):
+    # G[i][j] = i + j (exact in bf16 for these sizes): sum_i (i+j)^2 =
+    #   n(n-1)(2n-1)/6 + j n(n-1) + n j^2, an exact integer < 2^24.
+    n, m = 40, 24
+    G = np.add.outer(np.arange(n), np.arange(m)).astype(np.float32)
+    for dt, arr in (("fp32", G), ("bf16", _bf16(G))):
+        got = orc.column_norms(arr)
+        j = np.arange(m)
+        want = n * (n - 1) * (2 * n - 1) // 6 + j * n * (n - 1) + n * j * j
+        assert np.array_equal(got, want.astype(np.float32)), dt
+
+
+def test_norms_frobenius_invariant(orc):
+    rng = np.random.default_rng(7)
+    G = (rng.standard_normal((300, 257)) * np.exp(rng.standard_normal(257) * 2)).astype(np.float32)
+    cn = orc.column_norms_f64(G)
+    frob = math.fsum(float(x) * float(x) for x in G.ravel())          # row-major, compensated
+    assert abs(math.fsum(cn) - frob) <= 1e-12 * frob
+    assert np.allclose(orc.column_norms(G), cn.astype(np.float32), rtol=0, atol=0)
+
+
+def test_norms_brute_force_64(orc):
+    rng = np.random.default_rng(3)
+    G = rng.standard_normal((64, 64)).astype(np.float32)
+    got = orc.column_norms(G)
+    for j in range(64):                     # independent loop: rows outer, via python floats
+        s = math.fsum(float(G[i, j]) ** 2 for i in range(64))
+        assert abs(float(got[j]) - s) <= 2 ** -23 * s
+
+
+def test_norms_shard_sum(orc):
+    rng = np.random.default_rng(4)
+    G = rng.standard_normal((103, 50)).astype(np.float32)
+    whole = orc.column_norms_f64(G)
+    for world in (2, 3, 8):
+        parts = [orc.column_norms_f64(G[slice(*orc.shard_rows(103, world, r))]) for r in range(world)]
+        assert np.allclose(sum(parts), whole, rtol=1e-12, atol=0)
+
+
+def test_norms_reject_nonfinite(orc):
+    G = np.ones((4, 4), np.float32)
+    G[2, 1] = np.nan
+    with pytest.raises(FloatingPointError):
+        orc.column_norms(G)
+
+
+# ------------------------------------------------------------------ O3  top-k
+def test_topk_worked_examples(orc):
+    for ex in _golden("worked_examples.json")["select_channels"]:
+        norms = np.array(ex["norms"], np.float32)
+        k = orc.k_for(len(norms), ex["ratio_ppm"])
+        assert orc.topk(norms, k).tolist() == ex["idx"], ex["source"]
+
+
+def _rank_count_select(norms, k):
+    # independent definition: rank_j = #{i: N_i > N_j or (N_i == N_j and i < j)}; selected iff rank_j < k
+    m = len(norms)
+    sel = []
+    for j in range(m):
+        r = sum(1 for i in range(m) if norms[i] > norms[j] or (norms[i] == norms[j] and i < j))
+        if r < k:
+            sel.append(j)
+    return sel
+
+
+def test_topk_brute_force_with_ties(orc):
+    rng = np.random.default_rng(11)
+    for trial in range(200):
+        m = int(rng.integers(1, 65))
+        norms = rng.integers(0, 6, m).astype(np.float32) * 0.25     # many exact ties
+        k = int(rng.integers(1, m + 1))
+        assert orc.topk(norms, k).tolist() == _rank_count_select(norms.tolist(), k), (trial, m, k)
+
+
+def test_topk_permutation_equivariance(orc):
+    rng = np.random.default_rng(12)
+    norms = rng.standard_normal(500).astype(np.float32) ** 2       # distinct values
+    k = 50
+    base = set(orc.topk(norms, k).tolist())
+    perm = rng.permutation(500)
+    got = set(perm[j] for j in orc.topk(norms[perm], k).tolist())
+    assert got == base
+
+
+def test_topk_concentrated_columns(orc):
+    # nonzeros confined to c <= k columns -> all of them are selected
+    rng = np.random.default_rng(13)
+    G = np.zeros((30, 100), np.float32)
+    cols = rng.choice(100, 7, replace=False)
+    G[:, cols] = rng.standard_normal((30, 7)).astype(np.float32) + 3.0
+    idx = orc.topk(orc.column_norms(G), 10)
+    assert set(cols.tolist()) <= set(idx.tolist())
+    assert list(idx) == sorted(idx)
+
+
+# ------------------------------------------------------------------ O4  map
+def test_column_map_definition(orc):
+    rng = np.random.default_rng(5)
+    m = 97
+    idx = np.sort(rng.choice(m, 13, replace=False)).astype(np.int32)
+    slot, upos = orc.column_map(idx, m)
+    unsel = [j for j in range(m) if j not in set(idx.tolist())]
+    for j in range(m):
+        if j in set(idx.tolist()):
+            assert slot[j] == idx.tolist().index(j) and upos[j] == -1
+        else:
+            assert slot[j] == -1 and upos[j] == unsel.index(j)
+
+
+# ------------------------------------------------------------------ O7  compaction
+def test_compact_worked_example(orc):
+    ex = _golden("worked_examples.json")["mask_from_channels"][0]
+    G = np.arange(ex["rows"] * ex["cols"], dtype=np.float32).reshape(ex["rows"], ex["cols"])
+    out = orc.compact(G, np.array(ex["idx"], np.int32))
+    assert out.shape == (ex["rows"], ex["cols"] - len(ex["idx"]))
+    assert np.array_equal(out, G[:, ex["unselected_columns"]]), ex["source"]
+    assert ex["rows"] * len(ex["idx"]) == ex["n_selected_elements"]
+
+
+def test_compact_partition_identity(orc):
+    # O9: |idx| + |unsel| = m, disjoint, and every row rebuilds bit for bit
+    rng = np.random.default_rng(6)
+    for dt in ("fp32", "bf16"):
+        n, m = 37, 211
+        Gf = rng.standard_normal((n, m)).astype(np.float32)
+        G = Gf if dt == "fp32" else _bf16(Gf)
+        idx = orc.topk(orc.column_norms(G), orc.k_for(m, 100000))
+        out = orc.compact(G, idx)
+        slot, upos = orc.column_map(idx, m)
+        R = np.empty_like(G)
+        for j in range(m):
+            R[:, j] = G[:, idx[slot[j]]] if slot[j] >= 0 else out[:, upos[j]]
+        assert np.array_equal(R.view(np.uint8), G.view(np.uint8))
+        assert len(set(idx.tolist())) == len(idx) and out.shape[1] + len(idx) == m
+
+
+def test_compact_all_selected_is_empty(orc):
+    G = np.ones((5, 8), np.float32)
+    assert orc.compact(G, np.arange(8, dtype=np.int32)).shape == (5, 0)
+
+
+def test_compact_shards_concatenate(orc):
+    rng = np.random.default_rng(8)
+    G = _bf16(rng.standard_normal((21, 40)))
+    idx = np.array([0, 5, 6, 39], np.int32)
+    whole = orc.compact(G, idx)
+    parts = [orc.compact(np.ascontiguousarray(G[slice(*orc.shard_rows(21, 4, r))]), idx) for r in range(4)]
+    assert np.array_equal(np.concatenate(parts), whole)
+
+
+def test_shard_rows_worked_examples(orc):
+    for ex in _golden("worked_examples.json")["shard_matrix"]:
+        rows = [b - a for a, b in (orc.shard_rows(ex["n"], ex["world"], r) for r in range(ex["world"]))]
+        assert rows == ex["rows"], ex["source"]
+
+
+def test_byte_accounting_worked_example():
+    ex = _golden("worked_examples.json")["byte_accounting"][0]
+    assert 4096 * 4096 * 2 == ex["full_bytes"] and 4096 * 4 == ex["proxy_bytes"]
+
+
+# ------------------------------------------------------------------ O6  AdamW
+def _adam_state(n, k):
+    return np.zeros((n, k), np.float32), np.zeros((n, k), np.float32), np.zeros(k, np.int32)
+
+
+def test_adam_step1_closed_form(orc):
+    # from zero state, m_hat = g and v_hat = g^2, so p1 = p0 - lr * g / (|g| + eps)
+    rng = np.random.default_rng(20)
+    n, m = 16, 12
+    G = (rng.standard_normal((n, m)) * 1e-2).astype(np.float32)
+    P = rng.standard_normal((n, m)).astype(np.float32)
+    P0 = P.copy()
+    idx = np.array([1, 4, 5, 11], np.int32)
+    M, V, st = _adam_state(n, 4)
+    hp = orc.AdamHP(lr=1e-3)
+    orc.selective_adamw(P, G, idx, M, V, st, hp)
+    g = G[:, idx].astype(np.float64)
+    want = P0[:, idx].astype(np.float64) - 1e-3 * g / (np.abs(g) + 1e-8)
+    assert np.allclose(P[:, idx], want, rtol=1e-6, atol=0)
+    other = np.setdiff1d(np.arange(m), idx)
+    assert np.array_equal(P[:, other], P0[:, other])            # unselected untouched
+    assert st.tolist() == [1, 1, 1, 1]
+    assert np.allclose(M, 0.1 * G[:, idx], rtol=1e-6) and np.allclose(V, 0.001 * G[:, idx] ** 2, rtol=1e-5)
+
+
+def test_adam_constant_gradient_closed_form(orc):
+    # constant g: m_hat_t = g and v_hat_t = g^2 for every t, so each step moves p by -lr*g/(|g|+eps)
+    n = 8
+    G = np.linspace(-0.05, 0.05, n * 3, dtype=np.float32).reshape(n, 3)
+    G[G == 0] = 0.01
+    P = np.zeros((n, 3), np.float32)
+    idx = np.array([0, 1, 2], np.int32)
+    M, V, st = _adam_state(n, 3)
+    hp = orc.AdamHP(lr=1e-2)
+    for t in range(1, 9):
+        orc.selective_adamw(P, G, idx, M, V, st, hp)
+        g = G.astype(np.float64)
+        assert np.allclose(P, -t * 1e-2 * g / (np.abs(g) + 1e-8), rtol=2e-6, atol=0), t
+
+
+@pytest.mark.parametrize("wd,decoupled", [(0.0, 1), (0.01, 1), (0.01, 0)])
+def test_adam_all_selected_equals_torch(orc, wd, decoupled):
+    # k = m: every column selected from t=1 -> the plain optimizer (O6 library case)
+    rng = np.random.default_rng(21)
+    n, m = 24, 10
+    P = rng.standard_normal((n, m)).astype(np.float32)
+    tp = torch.nn.Parameter(torch.tensor(P.copy()))
+    cls = torch.optim.AdamW if decoupled else torch.optim.Adam
+    opt = cls([tp], lr=1e-3, betas=(0.9, 0.999), eps=1e-8, weight_decay=wd, foreach=False)
+    M, V, st = _adam_state(n, m)
+    hp = orc.AdamHP(lr=1e-3, weight_decay=wd, decoupled=decoupled)
+    idx = np.arange(m, dtype=np.int32)
+    for t in range(6):
+        G = (rng.standard_normal((n, m)) * 10.0 ** rng.integers(-4, 0)).astype(np.float32)
+        orc.selective_adamw(P, G, idx, M, V, st, hp)
+        tp.grad = torch.tensor(G)
+        opt.step()
+        ref = tp.detach().numpy()
+        assert np.allclose(P, ref, rtol=1e-6, atol=1e-9), t
+        state = opt.state[tp]
+        # torch forms m with lerp (a few ulps of the terms apart from b1*m + (1-b1)*g),
+        # so moments are compared norm-wise: |diff| <= 1e-6 * max|ref|
+        for mine, ref_t in ((M, state["exp_avg"]), (V, state["exp_avg_sq"])):
+            ref_m = ref_t.numpy()
+            assert np.max(np.abs(mine - ref_m)) <= 1e-6 * np.max(np.abs(ref_m))
+
+
+def test_adam_bf16_param_within_one_ulp_of_torch_fp32_then_round(orc):
+    rng = np.random.default_rng(22)
+    n, m = 32, 16
+    Pf = rng.standard_normal((n, m)).astype(np.float32) * 0.02
+    Pb = _bf16(Pf)
+    Gb = _bf16(rng.standard_normal((n, m)) * 1e-3)
+    idx = np.arange(m, dtype=np.int32)
+    M, V, st = _adam_state(n, m)
+    orc.selective_adamw(Pb, Gb, idx, M, V, st, orc.AdamHP(lr=1e-3))
+    tp = torch.nn.Parameter(torch.tensor(orc.bf16_bits_to_f32(Pb.copy()) * 0 + orc.bf16_bits_to_f32(_bf16(Pf))))
+    opt = torch.optim.AdamW([tp], lr=1e-3, weight_decay=0.0, foreach=False)
+    tp.grad = torch.tensor(orc.bf16_bits_to_f32(Gb))
+    opt.step()
+    ref = _bf16(tp.detach().numpy()).astype(np.int32)
+    assert np.max(np.abs(Pb.astype(np.int32) - ref)) <= 1       # within 1 bf16 ulp
+
+
+def test_adam_per_slot_step_counts(orc):
+    # slots with different ages use their own bias correction: a slot at step 0 moves by ~lr
+    n = 4
+    G = np.full((n, 2), 0.5, np.float32)
+    P = np.zeros((n, 2), np.float32)
+    idx = np.array([0, 1], np.int32)
+    M = np.zeros((n, 2), np.float32)
+    V = np.zeros((n, 2), np.float32)
+    st = np.array([0, 100], np.int32)
+    M[:, 1] = 0.5
+    V[:, 1] = 0.25
+    orc.selective_adamw(P, G, idx, M, V, st, orc.AdamHP(lr=1e-3))
+    assert st.tolist() == [1, 101]
+    b1, b2 = 0.9, 0.999
+    # slot 1: m stays 0.5 and v stays 0.25; bias corrections at t=101
+    want1 = -1e-3 / (1 - b1 ** 101) * 0.5 / (math.sqrt(0.25) / math.sqrt(1 - b2 ** 101) + 1e-8)
+    assert np.allclose(P[:, 0], -1e-3 * 0.5 / (0.5 + 1e-8), rtol=1e-6)
+    assert np.allclose(P[:, 1], want1, rtol=1e-6)
+
+
+# ------------------------------------------------------------------ O5  remap (reading R7)
+def test_remap_persistent_column_follows_plain_adamw(orc):
+    """Invariant of reading R7: a column selected on every step follows plain AdamW
+    exactly, whatever the other selected columns do across refreshes."""
+    rng = np.random.default_rng(30)
+    n, m = 6, 20
+    Pcol = rng.standard_normal(n).astype(np.float32)
+    tp = torch.nn.Parameter(torch.tensor(Pcol.copy()))
+    opt = torch.optim.AdamW([tp], lr=1e-3, weight_decay=0.0, foreach=False)
+    layer = orc.OracleLayer(n=n, m=m, ratio_ppm=150000, refresh_interval=2, accum_interval=2)
+    P = rng.standard_normal((n, m)).astype(np.float32)
+    P[:, 7] = Pcol
+    for t in range(10):
+        G = (rng.standard_normal((n, m)) * 0.01).astype(np.float32)
+        G[:, 7] = (rng.standard_normal(n) + 50.0).astype(np.float32)    # column 7 always the largest
+        layer.step(t, G, P)
+        assert 7 in layer.idx.tolist()
+        tp.grad = torch.tensor(G[:, 7].copy())
+        opt.step()
+        assert np.allclose(P[:, 7], tp.detach().numpy(), rtol=1e-6, atol=1e-9), t
+
+
+def test_remap_no_refresh_equals_constant_selection(orc):
+    # N = infinity (refresh only at t=0) vs N = 1 with a selection that never changes
+    rng = np.random.default_rng(31)
+    n, m = 5, 30
+    Gs = [(rng.standard_normal((n, m)) * 0.01).astype(np.float32) for _ in range(6)]
+    for G in Gs:
+        G[:, [2, 9, 17]] += 10.0
+    P0 = rng.standard_normal((n, m)).astype(np.float32)
+    a = orc.OracleLayer(n=n, m=m, ratio_ppm=100000, refresh_interval=1000, accum_interval=1)
+    b = orc.OracleLayer(n=n, m=m, ratio_ppm=100000, refresh_interval=1, accum_interval=1)
+    Pa, Pb = P0.copy(), P0.copy()
+    for t, G in enumerate(Gs):
+        a.step(t, G, Pa)
+        b.step(t, G, Pb)
+        assert a.idx.tolist() == b.idx.tolist() == [2, 9, 17]
+    assert np.array_equal(Pa, Pb) and np.array_equal(a.M, b.M) and np.array_equal(a.V, b.V)
+
+
+def test_remap_retained_entering_leaving(orc):
+    # reading R7 worked by hand (parity unpinned beyond internal consistency: paper silent)
+    n = 2
+    idx_old = np.array([1, 3], np.int32)
+    M_old = np.array([[1, 2], [3, 4]], np.float32)
+    V_old = M_old * 10
+    st_old = np.array([5, 7], np.int32)
+    M, V, st = orc.remap(n, idx_old, M_old, V_old, st_old, np.array([3, 5], np.int32))
+    assert M.tolist() == [[2, 0], [4, 0]] and V.tolist() == [[20, 0], [40, 0]] and st.tolist() == [7, 0]
+
+
+# ------------------------------------------------------------------ O8  accumulation
+def test_accumulate_constant_dyadic_stream(orc):
+    # dyadic values: fp32 sums are exact, so after S steps acc = S * g exactly
+    g = (np.arange(-50, 50, dtype=np.float32) * 2.0 ** -10).reshape(4, 25)
+    for dt, stage in (("fp32", g), ("bf16", _bf16(g))):
+        acc = np.zeros_like(g)
+        for _ in range(4):
+            orc.accumulate(acc, stage)
+        assert np.array_equal(acc, 4 * g), dt
+
+
+def test_window_double_buffer(orc):
+    # S=2: windows [0,2), [2,4) alternate buffers; a buffer holds exactly its window's steps
+    n, m = 3, 10
+    layer = orc.OracleLayer(n=n, m=m, ratio_ppm=200000, refresh_interval=2, accum_interval=2)
+    P = np.zeros((n, m), np.float32)
+    outs = []
+    for t in range(4):
+        G = np.full((n, m), float(t + 1), np.float32) * np.arange(1, m + 1, dtype=np.float32)
+        outs.append(layer.step(t, G, P).copy())
+    assert np.array_equal(layer.acc[0], outs[0] + outs[1])
+    assert np.array_equal(layer.acc[1], outs[2] + outs[3])
+    assert layer.sealed(3) is layer.acc[1] and layer.sealed(1) is layer.acc[0]
+
+
+def test_accumulate_S1_is_the_compact_gradient(orc):
+    rng = np.random.default_rng(40)
+    layer = orc.OracleLayer(n=4, m=12, ratio_ppm=250000, refresh_interval=1, accum_interval=1)
+    P = np.zeros((4, 12), np.float32)
+    G = rng.standard_normal((4, 12)).astype(np.float32)
+    out = layer.step(0, G, P)
+    unsel = [j for j in range(12) if j not in set(layer.idx.tolist())]
+    assert np.array_equal(layer.acc[0], G[:, unsel]) and np.array_equal(out, G[:, unsel])
+
+
+def test_step_all_important_equals_plain_optimizer(orc):
+    # mask = all-important -> theta^(c) empty; trajectory = plain AdamW
+    rng = np.random.default_rng(41)
+    n, m = 7, 9
+    P = rng.standard_normal((n, m)).astype(np.float32)
+    tp = torch.nn.Parameter(torch.tensor(P.copy()))
+    opt = torch.optim.AdamW([tp], lr=1e-3, weight_decay=0.0, foreach=False)
+    layer = orc.OracleLayer(n=n, m=m, ratio_ppm=1000000, refresh_interval=4, accum_interval=4)
+    for t in range(8):
+        G = rng.standard_normal((n, m)).astype(np.float32)
+        out = layer.step(t, G, P)
+        assert out.shape == (n, 0)
+        tp.grad = torch.tensor(G)
+        opt.step()
+    assert np.allclose(P, tp.detach().numpy(), rtol=1e-6, atol=1e-9)
