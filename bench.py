@@ -1,0 +1,404 @@
+#!/usr/bin/env python
+"""Benchmark of the ZenFlow hot path on B200 (BASELINE.json metric):
+"Llama-2-7B select+update ms/step; achieved HBM GB/s vs B200 peak, 1-8 GPU".
+
+One step = one zf_step over every nn.Linear gradient of the model (225 for
+Llama-2-7B): on refresh steps (t % 4 == 0) column norms (K1) -> NCCL norm
+all-reduce (N>1) -> top-k (K2) -> fused selective AdamW + compaction with
+moment remap (K3); on the other steps K3 alone with the cached selection.
+``value`` is device time per step averaged over the K timed steps (which mix
+refresh and steady steps in the 1:3 ratio of N=4), inputs resident in HBM,
+compaction into the device staging buffer.  ``e2e`` is the same metric through
+the same public API with HOST buffers: every step uploads G from pinned host
+memory, and the compact blocks go device->host and are accumulated on the host
+(rows 7-8 of the path).
+
+Usage: python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+Multi-GPU: torchrun --nproc-per-node N bench.py --gpus N  (row shards, strong scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "Llama-2-7B select+update ms/step; achieved HBM GB/s vs B200 peak, 1-8 GPU"
+UNIT = "ms/step"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=4)
+    ap.add_argument("--impl", default="zenflow", choices=["zenflow", "reference"])
+    ap.add_argument("--model", default="llama2-7b", choices=["llama2-7b", "llama2-13b", "gpt2-small"])
+    ap.add_argument("--ratio-ppm", type=int, default=100000)
+    ap.add_argument("--refresh", type=int, default=4)
+    ap.add_argument("--lr", type=float, default=1e-5)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--also-k1pct", action="store_true", help="also time k = 1% (reported as an extra field)")
+    ap.add_argument("--json-out", default=None)
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs: 1 Gi bf16 copy, read+write)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------ clocks sampler
+class Clocks:
+    def __init__(self):
+        self.proc = None
+        self.path = f"/tmp/zf_clocks_{os.getpid()}.csv"
+
+    def start(self, index=0):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}", "--format=csv,noheader",
+                                          "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1].split()[0]))
+                smax.append(float(f[2].split()[0]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ byte accounting
+def algorithmic_bytes(shapes, ks, gsz=2, psz=2):
+    """Element-algorithmic bytes of one K3 launch: read G; write the compact block;
+    read+write p, m, v at the selected columns (5.80 B/elt at k=10%)."""
+    tot = 0
+    for (n, m), k in zip(shapes, ks):
+        tot += n * m * gsz + n * (m - k) * gsz + n * k * (2 * psz + 16)
+    return tot
+
+
+def sector_bytes(shapes, idxs, gsz=2, psz=2):
+    """Sector-compulsory bytes of one K3 launch with the actual selection: p moves in
+    32-byte sectors (every sector holding a selected column is read and written)."""
+    tot = 0
+    for (n, m), idx in zip(shapes, idxs):
+        k = len(idx)
+        sectors = len(np.unique((np.asarray(idx, np.int64) * psz) // 32))
+        tot += n * m * gsz + n * (m - k) * gsz + n * k * 16 + n * sectors * 32 * 2
+    return tot
+
+
+# ------------------------------------------------------------ CPU oracle timing (baseline)
+def oracle_sample_ms_per_step(model, ratio_ppm, refresh, steps, budget_s=25.0):
+    """Time the oracle (single thread, as it stands) on a bounded sample of the
+    workload -- one matrix of each distinct shape of the model -- and scale its
+    time per element-step to the whole model.  Returns (ms_per_step, sample)."""
+    import synth
+    from oracle import oracle as orc
+    shapes_all = [(n, m) for _, n, m in synth.MODELS[model]()]
+    total = sum(n * m for n, m in shapes_all)
+    uniq = []
+    for s in shapes_all:
+        if s not in uniq:
+            uniq.append(s)
+    uniq = [s for s in uniq if s[0] * s[1] <= 50_000_000][:3]  # bounded sample
+    layers, Ps, scales = [], [], []
+    for li, (n, m) in enumerate(uniq):
+        layers.append(orc.OracleLayer(n=n, m=m, ratio_ppm=ratio_ppm, refresh_interval=refresh,
+                                      accum_interval=refresh, hp=orc.AdamHP(lr=1e-5)))
+        Ps.append(synth.param(n, m, li))
+        scales.append(synth.col_scale_init(m, li))
+    Gs = [synth.grad(n, m, li, 0, scales[li]) for li, (n, m) in enumerate(uniq)]
+    sample_elems = sum(n * m for n, m in uniq)
+    times = []
+    t_begin = time.perf_counter()
+    for t in range(steps):
+        t0 = time.perf_counter()
+        for L, G, P in zip(layers, Gs, Ps):
+            L.step(t, G, P)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_begin > budget_s and (t + 1) % refresh == 0:
+            break
+    per_elem = sum(times) / len(times) / sample_elems
+    desc = (f"{len(times)} oracle steps (refresh every {refresh}) over {len(uniq)} matrices "
+            f"{'+'.join(f'{n}x{m}' for n, m in uniq)} = {sample_elems / 1e6:.1f}M elements; "
+            f"time/element-step scaled to the model's {total / 1e9:.3f}G elements")
+    return per_elem * total * 1e3, desc, len(times)
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    ms, desc, n = oracle_sample_ms_per_step(args.model, args.ratio_ppm, args.refresh,
+                                            max(1, args.steps + args.warmup), budget_s=150.0)
+    line = {"impl": "reference", "metric": METRIC, "value": ms, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"{args.model}-all-linear-k{args.ratio_ppm // 10000}pct", "model": args.model,
+                       "ratio_ppm": args.ratio_ppm, "refresh_interval": args.refresh},
+            "cpu_baseline": {"value": ms, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
+            "e2e": {"value": ms, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------ GPU arm
+def run_zenflow(args, rank, world):
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2505_12242_b200 import _build
+    if rank == 0:
+        _build.build()
+    if world > 1:
+        dist.barrier()
+    from paper_2505_12242_b200 import zf
+    from synth import gpu as sgpu
+    from oracle import oracle as _orc_shard  # noqa: F401  (shard_rows only; see below)
+
+    dev = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev)
+    hbm_peak, peak_src = peaks()
+    names = synth.MODELS[args.model]()
+    full_shapes = [(n, m) for _, n, m in names]
+
+    def shard(n):
+        base, rem = divmod(n, world)
+        s = rank * base + min(rank, rem)
+        return s, base + (1 if rank < rem else 0)
+
+    shapes = [(shard(n)[1], m) for n, m in full_shapes]
+    row0s = [shard(n)[0] for n, _ in full_shapes]
+    ks = [zf.k_for(m, args.ratio_ppm) for _, m in shapes]
+
+    # ---- inputs resident in HBM: two gradient versions (alternating steps), params
+    def alloc_flat(shp, dtype):
+        tot = sum(n * m for n, m in shp)
+        buf = torch.empty(tot, dtype=dtype, device="cuda")
+        views, off = [], 0
+        for n, m in shp:
+            views.append(buf[off:off + n * m].view(n, m))
+            off += n * m
+        return buf, views
+
+    _g0, G0 = alloc_flat(shapes, torch.bfloat16)
+    _g1, G1 = alloc_flat(shapes, torch.bfloat16)
+    _p, Ps = alloc_flat(shapes, torch.bfloat16)
+    for li, (n, m) in enumerate(shapes):
+        sc = sgpu.ColScale(m, li)
+        sgpu.fill_grad(G0[li], li, 0, sc, row0=row0s[li])
+        sc.advance_to(1)
+        sgpu.fill_grad(G1[li], li, 1, sc, row0=row0s[li])
+        sgpu.fill_param(Ps[li], li, row0=row0s[li])
+        del sc
+    torch.cuda.synchronize()
+    nccl_id = None
+    if world > 1:
+        obj = [zf.zf_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+
+    def make_ctx(ratio_ppm, offload):
+        return zf.Context([zf.LayerShape(n, m) for n, m in shapes], topk_ratio_ppm=ratio_ppm,
+                          refresh_interval=args.refresh, accum_interval=args.refresh,
+                          adam=zf.adam_params(lr=args.lr), offload=offload, host_accumulate=offload,
+                          world=world, rank=rank, nccl_id=nccl_id, device=dev)
+
+    import ctypes
+    nl = len(shapes)
+    gp = [(ctypes.c_void_p * nl)(*[g.data_ptr() for g in G0]), (ctypes.c_void_p * nl)(*[g.data_ptr() for g in G1])]
+    pp = (ctypes.c_void_p * nl)(*[p.data_ptr() for p in Ps])
+    stream = torch.cuda.current_stream()
+
+    def timed_run(ctx, K, W, tag):
+        for t in range(W):
+            ctx.step_ptrs(t, gp[t % 2], pp, stream)
+        ctx.sync()
+        ctx.profile_read()
+        ctx.profile(True)
+        l0 = ctx.kernel_launches()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for t in range(W, W + K):
+            ctx.step_ptrs(t, gp[t % 2], pp, stream)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms = ev0.elapsed_time(ev1)
+        prof = ctx.profile_read()
+        ctx.profile(False)
+        ctx.sync()
+        return ms, prof, ctx.kernel_launches() - l0
+
+    # ---- main measurement: k = ratio, offload off (device staging)
+    ctx = make_ctx(args.ratio_ppm, False)
+    clocks = Clocks()
+    clocks.start(dev)
+    ms_total, prof, launches = timed_run(ctx, args.steps, args.warmup, "main")
+    clk = clocks.stop()
+    idxs = [ctx.selected(li).cpu().numpy() for li in range(nl)]
+    ctx.close()
+    del ctx
+    t_ms = torch.tensor([ms_total, prof["k3_update"][0], prof["k1_norms"][0], prof["k2_topk"][0],
+                         prof["allreduce"][0]], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+    ms_total, k3_ms, k1_ms, k2_ms, ar_ms = t_ms.tolist()
+    ms_per_step = ms_total / args.steps
+    n_k3 = prof["k3_update"][1]
+    n_k1 = prof["k1_norms"][1]
+    k3_avg = k3_ms / max(1, n_k3)
+    alg = algorithmic_bytes(shapes, ks)
+    sec = sector_bytes(shapes, idxs)
+    g_bytes = sum(n * m * 2 for n, m in shapes)
+    result = {
+        "metric": METRIC, "value": ms_per_step, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False,
+        "scaling": "strong" if world > 1 else "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded column-concentrated bf16 gradients, bf16 params, fp32 AdamW state)",
+        "config": {"workload": f"{args.model}-all-linear-k{args.ratio_ppm // 10000}pct", "model": args.model,
+                   "linears": nl, "elements": sum(n * m for n, m in full_shapes), "ratio_ppm": args.ratio_ppm,
+                   "refresh_interval": args.refresh, "parallelism": f"dp{world} (row shards, norm all-reduce)",
+                   "l2": "inputs larger than L2 (working set > 100 GB vs 126 MB L2); no flush needed",
+                   "lr": args.lr},
+        "phases_ms_per_launch": {"k3_update": k3_avg, "k1_norms": k1_ms / max(1, n_k1),
+                                 "k2_topk": k2_ms / max(1, prof["k2_topk"][1]),
+                                 "allreduce": (ar_ms / max(1, prof["allreduce"][1])) if world > 1 else None},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    achieved = alg / (k3_avg * 1e-3) / 1e9
+    result["roofline"] = {"bound": "hbm", "kernel": "k_update (K3 fused selective AdamW + compaction)",
+                          "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                          "peak_source": peak_src, "algorithmic_bytes_per_launch": alg,
+                          "sector_compulsory_bytes_per_launch": sec,
+                          "achieved_sector_GBs": sec / (k3_avg * 1e-3) / 1e9,
+                          "frac_sector": sec / (k3_avg * 1e-3) / 1e9 / hbm_peak, "traffic": None}
+    prof_path = os.path.join(ROOT, "profiles", "k3_dram_traffic.json")
+    if os.path.exists(prof_path):
+        d = json.load(open(prof_path))
+        if d.get("workload") == result["config"]["workload"] and world == 1:
+            result["roofline"]["traffic"] = d.get("traffic_bytes_per_launch")
+            result["roofline"]["traffic_source"] = d.get("source")
+    if n_k1:
+        k1_avg = k1_ms / n_k1
+        result["k1_roofline"] = {"bound": "hbm", "achieved": g_bytes / (k1_avg * 1e-3) / 1e9, "peak": hbm_peak,
+                                 "unit": "GB/s", "frac": g_bytes / (k1_avg * 1e-3) / 1e9 / hbm_peak}
+
+    # ---- k = 1% (extra field)
+    if args.also_k1pct:
+        ctx = make_ctx(10000, False)
+        ms1, prof1, _ = timed_run(ctx, args.steps, args.warmup, "k1pct")
+        ctx.close()
+        del ctx
+        result["k1pct_ms_per_step"] = ms1 / args.steps
+
+    # ---- e2e: host buffers through the same API (H2D grads, D2H compact + host accumulation)
+    if not args.no_e2e:
+        ctx = make_ctx(args.ratio_ppm, True)
+        del _g1, G1
+        torch.cuda.empty_cache()
+        host_g = torch.empty(sum(n * m for n, m in shapes), dtype=torch.bfloat16, pin_memory=True)
+        host_g.copy_(_g0)
+        h2d = host_g.numel() * 2
+        d2h = sum(n * (m - k) * 2 for (n, m), k in zip(shapes, ks))
+        gpp = (ctypes.c_void_p * nl)(*[g.data_ptr() for g in G0])
+        K = args.e2e_steps
+        for t in range(2):  # warm-up
+            _g0.copy_(host_g, non_blocking=True)
+            ctx.step_ptrs(t, gpp, pp, stream)
+        ctx.sync()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for t in range(2, 2 + K):
+            _g0.copy_(host_g, non_blocking=True)
+            ctx.step_ptrs(t, gpp, pp, stream)
+        ctx.sync()
+        e2e_s = time.perf_counter() - t0
+        e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+        ctx.close()
+        result["e2e"] = {"value": e2e_t.item() * 1e3 / K, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                         "d2h_bytes_per_step": d2h, "steps": K,
+                         "path": "pinned host G -> H2D -> zf_step (offload + host accumulate) -> zf_sync"}
+    else:
+        result["e2e"] = None
+
+    # ---- CPU oracle baseline (rank 0, N=1 only)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ms, desc, _ = oracle_sample_ms_per_step(args.model, args.ratio_ppm, args.refresh, 8, budget_s=25.0)
+        result["cpu_baseline"] = {"value": ms, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
+                                  "host_cores": os.cpu_count()}
+    if rank == 0:
+        line = json.dumps(result)
+        print(line, flush=True)
+        if args.json_out:
+            open(args.json_out, "w").write(line + "\n")
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    rank = int(os.environ.get("RANK", 0))
+    if world != args.gpus and "WORLD_SIZE" in os.environ:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    if args.impl == "reference":
+        if world > 1 and rank != 0:
+            return
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    run_zenflow(args, rank, world)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -57,10 +57,12 @@ typedef enum {
 typedef enum { ZF_FP32 = 0, ZF_BF16 = 1 } zf_dtype;
 
 /* AdamW hyper-parameters [host] (reading R8: PyTorch AdamW; paper P:653-654 uses
- * lr 1e-5, weight decay 0).  decoupled=1: p *= (1 - lr*wd) (AdamW);
- * decoupled=0: g += wd*p (Adam with L2). */
+ * lr 1e-5, weight decay 0).  Real numbers in double: every fp32 constant of the
+ * update is derived from them in double and rounded once, as PyTorch does with
+ * its Python scalars.  decoupled=1: p *= (1 - lr*wd) (AdamW); decoupled=0:
+ * g += wd*p (Adam with L2). */
 typedef struct {
-    float lr, beta1, beta2, eps, weight_decay;
+    double lr, beta1, beta2, eps, weight_decay;
     int32_t decoupled;
 } zf_adam_params;
 
@@ -193,7 +195,14 @@ zf_status zf_compact_buffer(zf_ctx* ctx, int32_t layer, const void** dev, const 
 zf_status zf_host_accumulator(zf_ctx* ctx, int32_t layer, int32_t which, const float** host, int64_t* rows,
                               int64_t* cols);
 /* Change the learning rate used from the next zf_step on (schedules). */
-zf_status zf_set_lr(zf_ctx* ctx, float lr);
+zf_status zf_set_lr(zf_ctx* ctx, double lr);
+/* Per-phase device timing: when enabled, zf_step records CUDA events on its
+ * launch stream around each phase (0: K1 column norms, 1: NCCL norm all-reduce,
+ * 2: K2 top-k, 3: K3 fused selective AdamW + compaction).  zf_profile_read waits
+ * for the recorded events, writes the summed milliseconds ms[4] and occurrence
+ * counts count[4] [host] since the previous read, and resets them. */
+zf_status zf_profile(zf_ctx* ctx, int32_t enable);
+zf_status zf_profile_read(zf_ctx* ctx, double* ms, int64_t* count);
 /* Number of this library's kernel launches issued so far by the context. */
 int64_t zf_kernel_launches(zf_ctx* ctx);
 zf_status zf_destroy(zf_ctx* ctx);

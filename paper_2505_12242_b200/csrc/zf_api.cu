@@ -1,0 +1,1194 @@
+// zf_api.cu -- the C-ABI of libzf.so (include/zf.h) and the host runtime of the
+// stateful driver: argument validation, the per-layer state in HBM, launch
+// tables, the NCCL norm all-reduce, D2H staging on a copy stream gated per layer,
+// and the host accumulation thread pool.  See DESIGN.md §5-§6.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <condition_variable>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <deque>
+#include <functional>
+#include <tuple>
+#include <map>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/zf.h"
+#include "zf_internal.cuh"
+
+using namespace zf;
+
+// ============================================================ errors
+namespace {
+thread_local std::string g_last_error;
+
+zf_status fail(zf_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return st;
+}
+
+#define ZF_CUDA(call)                                                                                       \
+    do {                                                                                                    \
+        cudaError_t e_ = (call);                                                                            \
+        if (e_ != cudaSuccess) return fail(ZF_ECUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call,             \
+                                            cudaGetErrorString(e_));                                        \
+    } while (0)
+
+#define ZF_NCCL(call)                                                                                       \
+    do {                                                                                                    \
+        ncclResult_t r_ = (call);                                                                           \
+        if (r_ != ncclSuccess) return fail(ZF_ENCCL, "%s:%d %s: %s", __FILE__, __LINE__, #call,             \
+                                            ncclGetErrorString(r_));                                        \
+    } while (0)
+
+#define ZF_TRY(expr)                \
+    do {                            \
+        zf_status s_ = (expr);      \
+        if (s_ != ZF_OK) return s_; \
+    } while (0)
+
+int esize(zf_dtype d) { return d == ZF_BF16 ? 2 : 4; }
+bool dtype_ok(int d) { return d == ZF_FP32 || d == ZF_BF16; }
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ============================================================ AdamW constants
+// bias-correction tables computed on the host in double, one rounding to fp32
+// (DESIGN.md §2 O6): ss[t] = f32(lr / (1 - b1^t)), bc2s[t] = f32(sqrt(1 - b2^t)).
+// Both are monotone in t and reach their limits (f32(lr), 1.0f) at a finite t;
+// the tables stop there and the kernel uses the limit beyond.
+constexpr int64_t MAX_TAB = 1 << 24;
+constexpr int64_t SS_CAP = 1 << 16;  // ss table capacity of a context (beta1 <= 0.999)
+
+std::vector<float> make_ss(double lr, double b1) {
+    std::vector<float> t(1, 0.0f);
+    const float lim = (float)lr;
+    for (int64_t i = 1; i < MAX_TAB; ++i) {
+        const float v = (float)(lr / (1.0 - std::pow(b1, (double)i)));
+        if (v == lim) break;
+        t.push_back(v);
+    }
+    return t;
+}
+
+std::vector<float> make_bc2(double b2) {
+    std::vector<float> t(1, 0.0f);
+    for (int64_t i = 1; i < MAX_TAB; ++i) {
+        const float v = (float)std::sqrt(1.0 - std::pow(b2, (double)i));
+        if (v == 1.0f) break;
+        t.push_back(v);
+    }
+    return t;
+}
+
+zf_status check_hp(const zf_adam_params* hp) {
+    if (!hp) return fail(ZF_EINVAL, "hp is NULL");
+    if (!(hp->lr >= 0.0f) || !std::isfinite(hp->lr)) return fail(ZF_EINVAL, "lr must be finite and >= 0");
+    if (!(hp->beta1 >= 0.0f && hp->beta1 < 1.0f)) return fail(ZF_EINVAL, "beta1 must be in [0, 1)");
+    if (!(hp->beta2 >= 0.0f && hp->beta2 < 1.0f)) return fail(ZF_EINVAL, "beta2 must be in [0, 1)");
+    if (!(hp->eps > 0.0f) || !std::isfinite(hp->eps)) return fail(ZF_EINVAL, "eps must be > 0");
+    if (!(hp->weight_decay >= 0.0f) || !std::isfinite(hp->weight_decay)) return fail(ZF_EINVAL, "weight_decay must be >= 0");
+    return ZF_OK;
+}
+
+// Scalars of AdamK (the tables are attached by the caller).
+AdamK adam_scalars(const zf_adam_params& hp) {
+    const double lr = hp.lr, b1 = hp.beta1, b2 = hp.beta2, eps = hp.eps, wd = hp.weight_decay;
+    AdamK a{};
+    a.b1 = (float)b1;
+    a.b2 = (float)b2;
+    a.omb1 = (float)(1.0 - b1);
+    a.omb2 = (float)(1.0 - b2);
+    a.eps = (float)eps;
+    a.decay = (float)(1.0 - lr * wd);
+    a.wd = (float)wd;
+    a.wd_mode = wd == 0.0 ? 0 : (hp.decoupled ? 1 : 2);
+    a.ss_inf = (float)lr;
+    return a;
+}
+
+// Process-wide cache of device tables for the stateless primitive (never freed).
+struct TabCache {
+    std::mutex mu;
+    std::map<std::tuple<int, uint64_t, uint64_t>, std::pair<float*, int>> ss;  // (dev, lr, b1)
+    std::map<std::pair<int, uint64_t>, std::pair<float*, int>> bc2;              // (dev, b2)
+};
+TabCache& tab_cache() {
+    static TabCache* c = new TabCache();
+    return *c;
+}
+
+uint64_t dbits(double x) {
+    uint64_t u;
+    std::memcpy(&u, &x, 8);
+    return u;
+}
+
+zf_status upload_table(const std::vector<float>& h, float** d, cudaStream_t s) {
+    float* pinned = nullptr;
+    ZF_CUDA(cudaMallocHost(&pinned, h.size() * sizeof(float)));  // kept alive with the table
+    std::memcpy(pinned, h.data(), h.size() * sizeof(float));
+    ZF_CUDA(cudaMalloc(d, h.size() * sizeof(float)));
+    ZF_CUDA(cudaMemcpyAsync(*d, pinned, h.size() * sizeof(float), cudaMemcpyHostToDevice, s));
+    return ZF_OK;
+}
+
+zf_status cached_tables(const zf_adam_params& hp, cudaStream_t s, AdamK* a) {
+    int dev = 0;
+    ZF_CUDA(cudaGetDevice(&dev));
+    TabCache& c = tab_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto ks = std::make_tuple(dev, dbits(hp.lr), dbits(hp.beta1));
+    auto it = c.ss.find(ks);
+    if (it == c.ss.end()) {
+        auto h = make_ss(hp.lr, hp.beta1);
+        float* d = nullptr;
+        ZF_TRY(upload_table(h, &d, s));
+        it = c.ss.emplace(ks, std::make_pair(d, (int)h.size())).first;
+    }
+    auto kb = std::make_pair(dev, dbits(hp.beta2));
+    auto jt = c.bc2.find(kb);
+    if (jt == c.bc2.end()) {
+        auto h = make_bc2(hp.beta2);
+        float* d = nullptr;
+        ZF_TRY(upload_table(h, &d, s));
+        jt = c.bc2.emplace(kb, std::make_pair(d, (int)h.size())).first;
+    }
+    a->ss_tab = it->second.first;
+    a->ss_len = it->second.second;
+    a->bc2_tab = jt->second.first;
+    a->bc2_len = jt->second.second;
+    return ZF_OK;
+}
+
+// ============================================================ geometry
+struct K3Geom {
+    int64_t seg_cols;
+    int32_t nseg, R;
+    int64_t units;
+};
+
+K3Geom k3_geom(int64_t n, int64_t m, int gsz) {
+    K3Geom g{};
+    const int64_t tile = update_stage_bytes() / gsz;  // elements per staged tile
+    if (m <= tile) {
+        g.seg_cols = m;
+        g.nseg = 1;
+        g.R = (int32_t)std::max<int64_t>(1, std::min<int64_t>(tile / m, n));
+    } else {
+        g.seg_cols = (tile / 32) * 32;
+        g.nseg = (int32_t)((m + g.seg_cols - 1) / g.seg_cols);
+        g.R = 1;
+    }
+    g.units = ((n + g.R - 1) / g.R) * g.nseg;
+    return g;
+}
+
+bool k3_tma_ok(const void* G, int64_t ldg, int64_t m, int gsz) {
+    return aligned16(G) && ((ldg * gsz) % 16 == 0) && ((m * gsz) % 16 == 0);
+}
+
+// Stream-ordered scratch (freed asynchronously on the same stream).
+struct Scratch {
+    cudaStream_t s;
+    std::vector<void*> ptrs;
+    explicit Scratch(cudaStream_t st) : s(st) {}
+    template <typename T>
+    zf_status get(T** p, size_t bytes, bool zero) {
+        void* q = nullptr;
+        ZF_CUDA(cudaMallocAsync(&q, std::max<size_t>(bytes, 16), s));
+        ptrs.push_back(q);
+        if (zero) ZF_CUDA(cudaMemsetAsync(q, 0, std::max<size_t>(bytes, 16), s));
+        *p = static_cast<T*>(q);
+        return ZF_OK;
+    }
+    ~Scratch() {
+        for (void* q : ptrs) cudaFreeAsync(q, s);
+    }
+};
+
+zf_status check_matrix(const void* G, int gdt, int64_t n, int64_t m, int64_t ld, const char* what) {
+    if (!G) return fail(ZF_EINVAL, "%s is NULL", what);
+    if (!dtype_ok(gdt)) return fail(ZF_EINVAL, "%s: unsupported dtype %d", what, gdt);
+    if (n < 1 || m < 1) return fail(ZF_EINVAL, "%s: need n >= 1 and m >= 1 (got n=%lld m=%lld)", what, (long long)n,
+                                    (long long)m);
+    if (m > 0x7fffffffLL) return fail(ZF_EINVAL, "%s: m too large", what);
+    if (ld < m) return fail(ZF_EINVAL, "%s: ld (%lld) < m (%lld)", what, (long long)ld, (long long)m);
+    return ZF_OK;
+}
+
+}  // namespace
+
+// ============================================================ basic API
+extern "C" const char* zf_status_string(int32_t s) {
+    switch (s) {
+        case ZF_OK: return "ZF_OK";
+        case ZF_EINVAL: return "ZF_EINVAL: invalid argument";
+        case ZF_ENONFINITE: return "ZF_ENONFINITE: non-finite gradient";
+        case ZF_ECUDA: return "ZF_ECUDA: CUDA error";
+        case ZF_ENCCL: return "ZF_ENCCL: NCCL error";
+        case ZF_ENOMEM: return "ZF_ENOMEM: out of memory";
+        case ZF_ESTATE: return "ZF_ESTATE: invalid state";
+        default: return "unknown zf_status";
+    }
+}
+
+extern "C" const char* zf_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" int32_t zf_version(void) { return 100; }
+
+extern "C" int64_t zf_k_for(int64_t m, int32_t ppm) {
+    if (m < 1 || ppm <= 0 || ppm > 1000000) return -1;
+    int64_t k = (m * (int64_t)ppm + 999999) / 1000000;
+    return std::min<int64_t>(std::max<int64_t>(k, 1), m);
+}
+
+// ============================================================ stateless primitives
+extern "C" zf_status zf_column_norms(const void* G, zf_dtype gdt, int64_t n, int64_t m, int64_t ld, float* norms,
+                                     int32_t* nonfinite, zf_stream_t stream) {
+    g_last_error.clear();
+    ZF_TRY(check_matrix(G, gdt, n, m, ld, "G"));
+    if (!norms) return fail(ZF_EINVAL, "norms is NULL");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int gsz = esize(gdt);
+    Table<NormLayer> t{};
+    NormLayer& L = t.one;
+    t.dev = nullptr;
+    t.n = 1;
+    L.G = G;
+    L.n = n;
+    L.m = m;
+    L.ld = ld;
+    L.out = norms;
+    L.nrb = (int32_t)((n + norms_rows_per_block() - 1) / norms_rows_per_block());
+    L.ncb = (int32_t)((m + norms_cols_per_block(gdt) - 1) / norms_cols_per_block(gdt));
+    L.unit_begin = 0;
+    L.vec_ok = aligned16(G) && ((ld * gsz) % 16 == 0);
+    Scratch sc(s);
+    if (L.nrb > 1) {
+        ZF_TRY(sc.get(&L.partial, (size_t)L.nrb * m * sizeof(float), false));
+        ZF_TRY(sc.get(&L.counter, (size_t)L.ncb * sizeof(uint32_t), true));
+    }
+    ZF_CUDA(launch_norms(t, (int64_t)L.nrb * L.ncb, gdt, nonfinite, s));
+    return ZF_OK;
+}
+
+extern "C" zf_status zf_topk_columns(const float* norms, int64_t m, int64_t k, int32_t* idx, zf_stream_t stream) {
+    g_last_error.clear();
+    if (!norms || !idx) return fail(ZF_EINVAL, "norms/idx is NULL");
+    if (m < 1) return fail(ZF_EINVAL, "empty norms vector (m=%lld)", (long long)m);
+    if (m > 0x7fffffffLL) return fail(ZF_EINVAL, "m too large");
+    if (k < 1 || k > m) return fail(ZF_EINVAL, "need 1 <= k <= m (k=%lld m=%lld)", (long long)k, (long long)m);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    Scratch sc(s);
+    Table<TopkLayer> t{};
+    t.dev = nullptr;
+    t.n = 1;
+    TopkLayer& L = t.one;
+    L.norms = norms;
+    L.m = m;
+    L.k = k;
+    L.idx = idx;
+    const int64_t W = (m + 31) / 32;
+    ZF_TRY(sc.get(&L.mask, W * sizeof(uint32_t), false));
+    ZF_TRY(sc.get(&L.prefix, W * sizeof(int32_t), false));
+    ZF_CUDA(launch_topk(t, m, nullptr, s));
+    return ZF_OK;
+}
+
+extern "C" zf_status zf_selective_adam(void* p, zf_dtype pdt, int64_t ldp, const void* G, zf_dtype gdt, int64_t ldg,
+                                       int64_t n, int64_t m, const int32_t* idx, int64_t k, float* exp_avg,
+                                       float* exp_avg_sq, int32_t* step, const zf_adam_params* hp,
+                                       zf_stream_t stream) {
+    g_last_error.clear();
+    ZF_TRY(check_matrix(G, gdt, n, m, ldg, "G"));
+    ZF_TRY(check_matrix(p, pdt, n, m, ldp, "p"));
+    if (!idx || !exp_avg || !exp_avg_sq || !step) return fail(ZF_EINVAL, "idx/exp_avg/exp_avg_sq/step is NULL");
+    if (k < 1 || k > m) return fail(ZF_EINVAL, "need 1 <= k <= m");
+    ZF_TRY(check_hp(hp));
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    AdamK a = adam_scalars(*hp);
+    ZF_TRY(cached_tables(*hp, s, &a));
+    Scratch sc(s);
+    uint32_t* counter = nullptr;
+    ZF_TRY(sc.get(&counter, sizeof(uint32_t), true));
+    ZF_CUDA(launch_adam_only(G, gdt, ldg, p, pdt, ldp, n, idx, k, exp_avg, exp_avg_sq, step, counter, a, s));
+    return ZF_OK;
+}
+
+extern "C" zf_status zf_compact_unselected(const void* G, zf_dtype gdt, int64_t n, int64_t m, int64_t ld,
+                                           const int32_t* idx, int64_t k, void* out, zf_stream_t stream) {
+    g_last_error.clear();
+    ZF_TRY(check_matrix(G, gdt, n, m, ld, "G"));
+    if (!idx || !out) return fail(ZF_EINVAL, "idx/out is NULL");
+    if (k < 1 || k > m) return fail(ZF_EINVAL, "need 1 <= k <= m");
+    if (!aligned16(out)) return fail(ZF_EINVAL, "out must be 16-byte aligned");
+    if (k == m) return ZF_OK;  // empty output
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int gsz = esize(gdt);
+    Scratch sc(s);
+    UpdParams prm{};
+    prm.layers.dev = nullptr;
+    prm.layers.n = 1;
+    UpdLayer& L = prm.layers.one;
+    const int64_t W = (m + 31) / 32;
+    uint32_t* mask = nullptr;
+    int32_t* prefix = nullptr;
+    int32_t* bad = nullptr;
+    ZF_TRY(sc.get(&mask, W * sizeof(uint32_t), false));
+    ZF_TRY(sc.get(&prefix, W * sizeof(int32_t), false));
+    ZF_TRY(sc.get(&bad, sizeof(int32_t), true));
+    ZF_TRY(sc.get(&prm.claim, sizeof(uint32_t), true));
+    ZF_CUDA(launch_build_mask(idx, k, m, mask, prefix, bad, s));
+    const K3Geom geo = k3_geom(n, m, gsz);
+    L.G = G;
+    L.n = n;
+    L.m = m;
+    L.ldg = ld;
+    L.k = k;
+    L.idx = idx;
+    L.mask = mask;
+    L.prefix = prefix;
+    L.out = out;
+    L.seg_cols = geo.seg_cols;
+    L.nseg = geo.nseg;
+    L.R = geo.R;
+    L.units = geo.units;
+    L.unit_begin = 0;
+    L.tma_ok = k3_tma_ok(G, ld, m, gsz);
+    prm.total_units = geo.units;
+    prm.claim_base = 0;
+    prm.do_adam = 0;
+    prm.do_compact = 1;
+    ZF_CUDA(launch_update(prm, gdt, gdt, update_grid(gdt, gdt), s));
+    return ZF_OK;
+}
+
+// ============================================================ stateful driver
+namespace {
+
+typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+struct LayerState {
+    zf_layer_desc d{};
+    int64_t k = 0, W = 0, mk = 0;
+    // K1
+    int32_t nrb = 0, ncb = 0;
+    int64_t norm_off = 0, norm_unit_begin = 0;
+    float* partial = nullptr;
+    uint32_t* k1_counter = nullptr;
+    // selection sets (double-buffered for the refresh remap)
+    int32_t* idx[2] = {nullptr, nullptr};
+    uint32_t* mask[2] = {nullptr, nullptr};
+    int32_t* prefix[2] = {nullptr, nullptr};
+    int32_t* steps[2] = {nullptr, nullptr};
+    int32_t* slot_src = nullptr;
+    float* mom[2] = {nullptr, nullptr};
+    float* vel[2] = {nullptr, nullptr};
+    void* stage_dev[2] = {nullptr, nullptr};
+    void* stage_host[2] = {nullptr, nullptr};
+    float* acc[2] = {nullptr, nullptr};
+    // K3 geometry
+    K3Geom geo{};
+    int64_t unit_begin = 0;
+    cudaEvent_t d2h_ev[2] = {nullptr, nullptr};
+};
+
+// Simple pool for the host accumulation (row 8, H1).
+class Pool {
+   public:
+    explicit Pool(int n) : n_(n) {
+        for (int i = 0; i < n_; ++i) th_.emplace_back([this, i] { run(i); });
+    }
+    ~Pool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    // fn(begin, end) over [0, count) split into n_ contiguous slices
+    template <typename F>
+    void parallel_for(int64_t count, F&& fn) {
+        std::unique_lock<std::mutex> lk(mu_);
+        job_ = [&](int i) {
+            const int64_t per = (count + n_ - 1) / n_;
+            const int64_t b = std::min<int64_t>(count, per * i), e = std::min<int64_t>(count, b + per);
+            if (b < e) fn(b, e);
+        };
+        pending_ = n_;
+        ++gen_;
+        cv_.notify_all();
+        done_cv_.wait(lk, [&] { return pending_ == 0; });
+        job_ = nullptr;
+    }
+
+   private:
+    void run(int i) {
+        uint64_t seen = 0;
+        for (;;) {
+            std::function<void(int)> job;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return gen_ != seen; });
+                seen = gen_;
+                if (stop_) return;
+                job = job_;
+            }
+            if (job) job(i);
+            {
+                std::lock_guard<std::mutex> lk(mu_);
+                if (--pending_ == 0) done_cv_.notify_all();
+            }
+        }
+    }
+    int n_;
+    std::vector<std::thread> th_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_cv_;
+    std::function<void(int)> job_;
+    uint64_t gen_ = 0;
+    int pending_ = 0;
+    bool stop_ = false;
+};
+
+}  // namespace
+
+struct zf_ctx {
+    int device = 0;
+    zf_config cfg{};
+    int world = 1, rank = 0;
+    ncclComm_t comm = nullptr;
+    int gdt = 0, pdt = 0, gsz = 2, psz = 2;
+    std::vector<LayerState> L;
+    int64_t total_m = 0, max_m = 0, k1_units = 0, k3_units = 0;
+    int n_stage = 1;
+    float* norms = nullptr;
+    std::vector<void*> dev_allocs, host_pinned;
+    std::vector<float*> host_plain;
+    int32_t* nonfinite_h = nullptr;  // mapped pinned
+    int32_t* nonfinite_d = nullptr;
+    uint32_t* claim = nullptr;
+    uint32_t* done = nullptr;  // [n_layers]
+    uint32_t claim_base = 0, epoch = 0;
+    int grid = 148;
+    // launch tables
+    NormLayer* d_norm_tab = nullptr;
+    std::vector<NormLayer> h_norm_tab, up_norm_tab;
+    TopkLayer* d_topk_tab[3] = {nullptr, nullptr, nullptr};  // [new set 0 | new set 1 | first (new 1, no old)]
+    UpdLayer* d_upd_tab[8] = {};                              // [(cur)*4 + refresh*2 + stage]
+    std::vector<UpdLayer> h_upd_tab[8], up_upd_tab[8];
+    // table uploads through a small pinned ring
+    std::vector<unsigned char*> ring;
+    std::vector<cudaEvent_t> ring_ev;
+    size_t ring_bytes = 0;
+    int ring_pos = 0;
+    // AdamW tables (ss depends on lr; may change via zf_set_lr)
+    AdamK adam{};
+    float* d_ss = nullptr;
+    float* d_bc2 = nullptr;
+    double lr_cur = 0.0, lr_uploaded = -1.0;
+    // step state
+    int cur = 0;
+    bool have_sel = false;
+    int64_t last_t = -1;
+    int64_t launches = 0;
+    cudaEvent_t step_done = nullptr, k3_done = nullptr;
+    // offload
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t d2h_all[2] = {nullptr, nullptr};
+    bool d2h_issued[2] = {false, false};
+    PFN_waitValue32 wait_value = nullptr;
+    // host accumulation
+    Pool* pool = nullptr;
+    std::thread h1;
+    std::mutex mu;
+    std::condition_variable cv;
+    std::deque<int64_t> jobs;
+    int64_t h1_done = -1;
+    bool stopping = false;
+    // per-phase timing (zf_profile)
+    bool profiling = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
+    struct Pending { int phase; cudaEvent_t a, b; };
+    std::vector<Pending> pending;
+    double prof_ms[4] = {0, 0, 0, 0};
+    int64_t prof_n[4] = {0, 0, 0, 0};
+
+    ~zf_ctx();
+    zf_status prof_begin(int phase, cudaStream_t s, Pending* p) {
+        p->phase = phase;
+        p->a = p->b = nullptr;
+        if (!profiling) return ZF_OK;
+        if (ev_pool.empty()) {
+            cudaEvent_t a, b;
+            ZF_CUDA(cudaEventCreate(&a));
+            ZF_CUDA(cudaEventCreate(&b));
+            ev_pool.push_back({a, b});
+        }
+        p->a = ev_pool.back().first;
+        p->b = ev_pool.back().second;
+        ev_pool.pop_back();
+        ZF_CUDA(cudaEventRecord(p->a, s));
+        return ZF_OK;
+    }
+    zf_status prof_end(Pending* p, cudaStream_t s) {
+        if (!p->a) return ZF_OK;
+        ZF_CUDA(cudaEventRecord(p->b, s));
+        pending.push_back(*p);
+        return ZF_OK;
+    }
+    zf_status dev_alloc(void** p, size_t bytes) {
+        void* q = nullptr;
+        ZF_CUDA(cudaMalloc(&q, std::max<size_t>(bytes, 256)));
+        dev_allocs.push_back(q);
+        *p = q;
+        return ZF_OK;
+    }
+    template <typename T>
+    zf_status dalloc(T** p, size_t bytes, bool zero = true) {
+        void* q = nullptr;
+        ZF_TRY(dev_alloc(&q, bytes));
+        if (zero) ZF_CUDA(cudaMemset(q, 0, std::max<size_t>(bytes, 256)));
+        *p = static_cast<T*>(q);
+        return ZF_OK;
+    }
+    zf_status upload(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+        if (bytes > ring_bytes) return fail(ZF_ESTATE, "table upload larger than ring slot");
+        unsigned char* buf = ring[ring_pos];
+        ZF_CUDA(cudaEventSynchronize(ring_ev[ring_pos]));  // slot free once its last copy finished
+        std::memcpy(buf, src, bytes);
+        ZF_CUDA(cudaMemcpyAsync(dst, buf, bytes, cudaMemcpyHostToDevice, s));
+        ZF_CUDA(cudaEventRecord(ring_ev[ring_pos], s));
+        ring_pos = (ring_pos + 1) % (int)ring.size();
+        return ZF_OK;
+    }
+    void h1_loop();
+};
+
+zf_ctx::~zf_ctx() {
+    if (h1.joinable()) {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            stopping = true;
+        }
+        cv.notify_all();
+        h1.join();
+    }
+    delete pool;
+    cudaSetDevice(device);
+    cudaDeviceSynchronize();
+    if (comm) ncclCommDestroy(comm);
+    for (void* p : dev_allocs) cudaFree(p);
+    for (void* p : host_pinned) cudaFreeHost(p);
+    for (float* p : host_plain) std::free(p);
+    for (auto& l : L)
+        for (int i = 0; i < 2; ++i)
+            if (l.d2h_ev[i]) cudaEventDestroy(l.d2h_ev[i]);
+    for (auto e : ring_ev) cudaEventDestroy(e);
+    for (auto e : d2h_all)
+        if (e) cudaEventDestroy(e);
+    for (auto& e : ev_pool) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+    for (auto& e : pending) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
+    if (step_done) cudaEventDestroy(step_done);
+    if (k3_done) cudaEventDestroy(k3_done);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+}
+
+// H1: accumulate each layer's staged compact block into the window's fp32 buffer
+// as soon as its D2H copy completed (DESIGN.md §2 O8).
+void zf_ctx::h1_loop() {
+    cudaSetDevice(device);
+    const int S = cfg.accum_interval;
+    for (;;) {
+        int64_t t;
+        {
+            std::unique_lock<std::mutex> lk(mu);
+            cv.wait(lk, [&] { return stopping || !jobs.empty(); });
+            if (jobs.empty()) return;
+            t = jobs.front();
+        }
+        const int a = (int)((t / S) % 2);
+        const bool first = (t % S) == 0;
+        const int sb = (int)(t % n_stage);
+        for (auto& l : L) {
+            cudaEventSynchronize(l.d2h_ev[sb]);
+            const int64_t count = l.d.n * l.mk;
+            float* acc = l.acc[a];
+            if (gdt == ZF_BF16) {
+                const uint16_t* src = static_cast<const uint16_t*>(l.stage_host[sb]);
+                pool->parallel_for(count, [&](int64_t b, int64_t e) {
+                    for (int64_t i = b; i < e; ++i) {
+                        uint32_t u = (uint32_t)src[i] << 16;
+                        float x;
+                        std::memcpy(&x, &u, 4);
+                        acc[i] = (first ? 0.0f : acc[i]) + x;
+                    }
+                });
+            } else {
+                const float* src = static_cast<const float*>(l.stage_host[sb]);
+                pool->parallel_for(count, [&](int64_t b, int64_t e) {
+                    for (int64_t i = b; i < e; ++i) acc[i] = (first ? 0.0f : acc[i]) + src[i];
+                });
+            }
+        }
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            jobs.pop_front();
+            h1_done = t;
+        }
+        cv.notify_all();
+    }
+}
+
+extern "C" zf_status zf_nccl_unique_id(void* out128) {
+    g_last_error.clear();
+    if (!out128) return fail(ZF_EINVAL, "out is NULL");
+    ncclUniqueId id;
+    ZF_NCCL(ncclGetUniqueId(&id));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    std::memcpy(out128, &id, 128);
+    return ZF_OK;
+}
+
+namespace {
+
+zf_status build_tables(zf_ctx* c) {
+    const int nl = (int)c->L.size();
+    // K1 table
+    c->h_norm_tab.resize(nl);
+    for (int i = 0; i < nl; ++i) {
+        LayerState& l = c->L[i];
+        NormLayer& t = c->h_norm_tab[i];
+        t = NormLayer{};
+        t.n = l.d.n;
+        t.m = l.d.m;
+        t.ld = l.d.ld_grad;
+        t.out = c->norms + l.norm_off;
+        t.partial = l.partial;
+        t.counter = l.k1_counter;
+        t.nrb = l.nrb;
+        t.ncb = l.ncb;
+        t.unit_begin = l.norm_unit_begin;
+    }
+    ZF_TRY(c->dalloc(&c->d_norm_tab, nl * sizeof(NormLayer)));
+    c->up_norm_tab.assign(nl, NormLayer{});
+    // K2 tables
+    for (int v = 0; v < 3; ++v) {
+        std::vector<TopkLayer> h(nl);
+        const int nw = v == 2 ? 1 : v, old = v == 2 ? -1 : (v ^ 1);
+        for (int i = 0; i < nl; ++i) {
+            LayerState& l = c->L[i];
+            TopkLayer& t = h[i];
+            t = TopkLayer{};
+            t.norms = c->norms + l.norm_off;
+            t.m = l.d.m;
+            t.k = l.k;
+            t.idx = l.idx[nw];
+            t.mask = l.mask[nw];
+            t.prefix = l.prefix[nw];
+            if (old >= 0) {
+                t.old_mask = l.mask[old];
+                t.old_prefix = l.prefix[old];
+                t.old_steps = l.steps[old];
+            }
+            t.slot_src = l.slot_src;
+            t.new_steps = l.steps[nw];
+        }
+        ZF_TRY(c->dalloc(&c->d_topk_tab[v], nl * sizeof(TopkLayer)));
+        ZF_CUDA(cudaMemcpy(c->d_topk_tab[v], h.data(), nl * sizeof(TopkLayer), cudaMemcpyHostToDevice));
+    }
+    // K3 tables: variant (cur, refresh, stage)
+    for (int v = 0; v < 8; ++v) {
+        const int cur = v >> 2, refresh = (v >> 1) & 1, sb = v & 1;
+        const int nw = refresh ? (cur ^ 1) : cur;
+        auto& h = c->h_upd_tab[v];
+        h.resize(nl);
+        for (int i = 0; i < nl; ++i) {
+            LayerState& l = c->L[i];
+            UpdLayer& t = h[i];
+            t = UpdLayer{};
+            t.n = l.d.n;
+            t.m = l.d.m;
+            t.ldg = l.d.ld_grad;
+            t.ldp = l.d.ld_param;
+            t.k = l.k;
+            t.idx = l.idx[nw];
+            t.mask = l.mask[nw];
+            t.prefix = l.prefix[nw];
+            t.m_in = l.mom[cur];
+            t.v_in = l.vel[cur];
+            t.m_out = l.mom[nw];
+            t.v_out = l.vel[nw];
+            t.slot_src = refresh ? l.slot_src : nullptr;
+            t.k_in = l.k;
+            t.steps = l.steps[nw];
+            t.steps_out = l.steps[nw];
+            t.out = l.stage_dev[sb < c->n_stage ? sb : 0];
+            t.done = c->done + i;
+            t.seg_cols = l.geo.seg_cols;
+            t.nseg = l.geo.nseg;
+            t.R = l.geo.R;
+            t.units = l.geo.units;
+            t.unit_begin = l.unit_begin;
+        }
+        ZF_TRY(c->dalloc(&c->d_upd_tab[v], nl * sizeof(UpdLayer)));
+        c->up_upd_tab[v].assign(nl, UpdLayer{});
+    }
+    return ZF_OK;
+}
+
+zf_status upload_ss(zf_ctx* c, cudaStream_t s) {
+    if (c->lr_cur == c->lr_uploaded) return ZF_OK;
+    auto h = make_ss(c->lr_cur, c->cfg.adam.beta1);
+    if ((int64_t)h.size() > SS_CAP)
+        return fail(ZF_EINVAL, "bias-correction table too long for beta1=%g", (double)c->cfg.adam.beta1);
+    // one device table, rewritten in stream order: launches already enqueued on the
+    // context's (ordered) stream read the old values before the copy lands
+    if (!c->d_ss) ZF_TRY(c->dalloc(&c->d_ss, SS_CAP * sizeof(float), false));
+    ZF_TRY(c->upload(c->d_ss, h.data(), h.size() * sizeof(float), s));
+    c->adam.ss_tab = c->d_ss;
+    c->adam.ss_len = (int)h.size();
+    c->adam.ss_inf = (float)c->lr_cur;
+    c->adam.decay = (float)(1.0 - c->lr_cur * c->cfg.adam.weight_decay);
+    c->lr_uploaded = c->lr_cur;
+    return ZF_OK;
+}
+
+}  // namespace
+
+extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, const zf_config* cfg, int32_t world,
+                               int32_t rank, const void* nccl_id128, int32_t device, zf_ctx** out) {
+    g_last_error.clear();
+    if (!out) return fail(ZF_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (!layers || n_layers < 1) return fail(ZF_EINVAL, "need at least one layer");
+    if (!cfg) return fail(ZF_EINVAL, "cfg is NULL");
+    if (!dtype_ok(cfg->grad_dtype) || !dtype_ok(cfg->param_dtype)) return fail(ZF_EINVAL, "unsupported dtype");
+    if (cfg->topk_ppm <= 0 || cfg->topk_ppm > 1000000) return fail(ZF_EINVAL, "topk_ppm must be in (0, 1e6]");
+    if (cfg->refresh_interval < 1 || cfg->accum_interval < 1) return fail(ZF_EINVAL, "intervals must be >= 1");
+    if (cfg->host_accumulate && !cfg->offload) return fail(ZF_EINVAL, "host_accumulate requires offload");
+    if (cfg->host_accumulate && (cfg->refresh_interval % cfg->accum_interval) != 0)
+        return fail(ZF_EINVAL, "host_accumulate requires refresh_interval %% accum_interval == 0");
+    ZF_TRY(check_hp(&cfg->adam));
+    if (world < 1 || rank < 0 || rank >= world) return fail(ZF_EINVAL, "bad world/rank");
+    if (world > 1 && !nccl_id128) return fail(ZF_EINVAL, "nccl_id128 required when world > 1");
+    for (int i = 0; i < n_layers; ++i) {
+        const zf_layer_desc& d = layers[i];
+        if (d.n < 1 || d.m < 1 || d.m > 0x7fffffffLL || d.ld_grad < d.m || d.ld_param < d.m)
+            return fail(ZF_EINVAL, "layer %d: bad shape (n=%lld m=%lld ld_grad=%lld ld_param=%lld)", i, (long long)d.n,
+                        (long long)d.m, (long long)d.ld_grad, (long long)d.ld_param);
+    }
+    ZF_CUDA(cudaSetDevice(device));
+    zf_ctx* c = new zf_ctx();
+    auto bail = [&](zf_status st) {
+        std::string keep = g_last_error;
+        delete c;
+        g_last_error = keep;
+        return st;
+    };
+#define ZF_CTRY(expr)                         \
+    do {                                      \
+        zf_status s_ = (expr);                \
+        if (s_ != ZF_OK) return bail(s_);     \
+    } while (0)
+    c->device = device;
+    c->cfg = *cfg;
+    c->world = world;
+    c->rank = rank;
+    c->gdt = cfg->grad_dtype;
+    c->pdt = cfg->param_dtype;
+    c->gsz = esize(cfg->grad_dtype);
+    c->psz = esize(cfg->param_dtype);
+    c->n_stage = cfg->offload ? 2 : 1;
+    c->lr_cur = cfg->adam.lr;
+    c->grid = update_grid(c->gdt, c->pdt);
+    c->L.resize(n_layers);
+    const int rb = norms_rows_per_block(), cb = norms_cols_per_block(c->gdt);
+    for (int i = 0; i < n_layers; ++i) {
+        LayerState& l = c->L[i];
+        l.d = layers[i];
+        l.k = zf_k_for(l.d.m, cfg->topk_ppm);
+        l.W = (l.d.m + 31) / 32;
+        l.mk = l.d.m - l.k;
+        l.nrb = (int32_t)((l.d.n + rb - 1) / rb);
+        l.ncb = (int32_t)((l.d.m + cb - 1) / cb);
+        l.norm_off = c->total_m;
+        l.norm_unit_begin = c->k1_units;
+        c->total_m += l.d.m;
+        c->max_m = std::max(c->max_m, l.d.m);
+        c->k1_units += (int64_t)l.nrb * l.ncb;
+        l.geo = k3_geom(l.d.n, l.d.m, c->gsz);
+        l.unit_begin = c->k3_units;
+        c->k3_units += l.geo.units;
+    }
+    if (c->k1_units > 0x7fffffffLL || c->k3_units > 0x3fffffffLL) return bail(fail(ZF_EINVAL, "model too large"));
+    // ---- device state
+    ZF_CTRY(c->dalloc(&c->norms, c->total_m * sizeof(float)));
+    ZF_CTRY(c->dalloc(&c->claim, sizeof(uint32_t)));
+    ZF_CTRY(c->dalloc(&c->done, n_layers * sizeof(uint32_t)));
+    for (auto& l : c->L) {
+        const int64_t n = l.d.n, k = l.k;
+        if (l.nrb > 1) ZF_CTRY(c->dalloc(&l.partial, (size_t)l.nrb * l.d.m * sizeof(float), false));
+        ZF_CTRY(c->dalloc(&l.k1_counter, l.ncb * sizeof(uint32_t)));
+        for (int s = 0; s < 2; ++s) {
+            ZF_CTRY(c->dalloc(&l.idx[s], k * sizeof(int32_t)));
+            ZF_CTRY(c->dalloc(&l.mask[s], l.W * sizeof(uint32_t)));
+            ZF_CTRY(c->dalloc(&l.prefix[s], l.W * sizeof(int32_t)));
+            ZF_CTRY(c->dalloc(&l.steps[s], k * sizeof(int32_t)));
+            ZF_CTRY(c->dalloc(&l.mom[s], (size_t)n * k * sizeof(float)));
+            ZF_CTRY(c->dalloc(&l.vel[s], (size_t)n * k * sizeof(float)));
+        }
+        ZF_CTRY(c->dalloc(&l.slot_src, k * sizeof(int32_t)));
+        for (int s = 0; s < c->n_stage; ++s) ZF_CTRY(c->dalloc(&l.stage_dev[s], (size_t)n * l.mk * c->gsz, false));
+    }
+    {
+        int32_t* h = nullptr;
+        ZF_CUDA(cudaHostAlloc(&h, 64, cudaHostAllocMapped));
+        c->host_pinned.push_back(h);
+        *h = 0;
+        c->nonfinite_h = h;
+        ZF_CUDA(cudaHostGetDevicePointer(&c->nonfinite_d, h, 0));
+    }
+    // ---- AdamW tables
+    c->adam = adam_scalars(cfg->adam);
+    // ---- table upload ring
+    c->ring_bytes = std::max<size_t>({n_layers * sizeof(UpdLayer), n_layers * sizeof(NormLayer), SS_CAP * sizeof(float)});
+    for (int i = 0; i < 4; ++i) {
+        unsigned char* b = nullptr;
+        ZF_CUDA(cudaMallocHost(&b, c->ring_bytes));
+        c->host_pinned.push_back(b);
+        c->ring.push_back(b);
+        cudaEvent_t e;
+        ZF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->ring_ev.push_back(e);
+    }
+    {
+        auto h = make_bc2(cfg->adam.beta2);
+        ZF_CTRY(c->dalloc(&c->d_bc2, h.size() * sizeof(float), false));
+        ZF_CUDA(cudaMemcpy(c->d_bc2, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
+        c->adam.bc2_tab = c->d_bc2;
+        c->adam.bc2_len = (int)h.size();
+    }
+    ZF_CTRY(build_tables(c));
+    ZF_CUDA(cudaEventCreateWithFlags(&c->step_done, cudaEventDisableTiming));
+    ZF_CUDA(cudaEventCreateWithFlags(&c->k3_done, cudaEventDisableTiming));
+    // ---- offload: copy stream, pinned host staging, per-layer events, host accumulators
+    if (cfg->offload) {
+        ZF_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        for (int s = 0; s < 2; ++s) ZF_CUDA(cudaEventCreateWithFlags(&c->d2h_all[s], cudaEventDisableTiming));
+        for (auto& l : c->L) {
+            for (int s = 0; s < 2; ++s) {
+                void* h = nullptr;
+                ZF_CUDA(cudaHostAlloc(&h, std::max<size_t>((size_t)l.d.n * l.mk * c->gsz, 64), cudaHostAllocDefault));
+                c->host_pinned.push_back(h);
+                l.stage_host[s] = h;
+                ZF_CUDA(cudaEventCreateWithFlags(&l.d2h_ev[s], cudaEventDisableTiming | cudaEventBlockingSync));
+            }
+        }
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            c->wait_value = reinterpret_cast<PFN_waitValue32>(fn);
+        if (cfg->host_accumulate) {
+            for (auto& l : c->L) {
+                for (int s = 0; s < 2; ++s) {
+                    const size_t bytes = std::max<size_t>((size_t)l.d.n * l.mk * sizeof(float), 64);
+                    float* p = static_cast<float*>(std::aligned_alloc(64, (bytes + 63) / 64 * 64));
+                    if (!p) return bail(fail(ZF_ENOMEM, "host accumulator allocation failed"));
+                    std::memset(p, 0, bytes);
+                    c->host_plain.push_back(p);
+                    l.acc[s] = p;
+                }
+            }
+            int nt = cfg->host_threads > 0 ? cfg->host_threads
+                                           : (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+            c->pool = new Pool(nt);
+            c->h1 = std::thread([c] { c->h1_loop(); });
+        }
+    }
+    // ---- NCCL (collective across ranks)
+    if (world > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id128, sizeof id);
+        ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
+        if (r != ncclSuccess) return bail(fail(ZF_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r)));
+    }
+    ZF_CUDA(cudaDeviceSynchronize());
+    *out = c;
+    return ZF_OK;
+#undef ZF_CTRY
+}
+
+namespace {
+
+zf_status refresh_pointer_tables(zf_ctx* c, int variant, bool refresh, void* const* grads, void* const* params,
+                                 cudaStream_t s) {
+    const int nl = (int)c->L.size();
+    if (refresh) {
+        for (int i = 0; i < nl; ++i) {
+            NormLayer& t = c->h_norm_tab[i];
+            t.G = grads[i];
+            t.vec_ok = aligned16(grads[i]) && ((c->L[i].d.ld_grad * c->gsz) % 16 == 0);
+        }
+        if (std::memcmp(c->h_norm_tab.data(), c->up_norm_tab.data(), nl * sizeof(NormLayer)) != 0) {
+            ZF_TRY(c->upload(c->d_norm_tab, c->h_norm_tab.data(), nl * sizeof(NormLayer), s));
+            c->up_norm_tab = c->h_norm_tab;
+        }
+    }
+    auto& h = c->h_upd_tab[variant];
+    for (int i = 0; i < nl; ++i) {
+        h[i].G = grads[i];
+        h[i].P = params[i];
+        h[i].tma_ok = k3_tma_ok(grads[i], c->L[i].d.ld_grad, c->L[i].d.m, c->gsz);
+    }
+    if (std::memcmp(h.data(), c->up_upd_tab[variant].data(), nl * sizeof(UpdLayer)) != 0) {
+        ZF_TRY(c->upload(c->d_upd_tab[variant], h.data(), nl * sizeof(UpdLayer), s));
+        c->up_upd_tab[variant] = h;
+    }
+    return ZF_OK;
+}
+
+}  // namespace
+
+extern "C" zf_status zf_step(zf_ctx* c, int64_t t, void* const* grads, void* const* params, zf_stream_t stream) {
+    g_last_error.clear();
+    if (!c) return fail(ZF_EINVAL, "ctx is NULL");
+    if (!grads || !params) return fail(ZF_EINVAL, "grads/params is NULL");
+    const int nl = (int)c->L.size();
+    for (int i = 0; i < nl; ++i)
+        if (!grads[i] || !params[i]) return fail(ZF_EINVAL, "layer %d: NULL gradient or parameter", i);
+    if (t < 0) return fail(ZF_EINVAL, "t must be >= 0");
+    const int N = c->cfg.refresh_interval;
+    const bool refresh = (t % N) == 0;
+    if (!c->have_sel && !refresh) return fail(ZF_ESTATE, "first step must be a refresh step (t %% N == 0)");
+    if (c->have_sel && t != c->last_t + 1) return fail(ZF_ESTATE, "steps must be consecutive (last %lld, got %lld)",
+                                                       (long long)c->last_t, (long long)t);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    ZF_CUDA(cudaSetDevice(c->device));
+    const int sb = (int)(t % c->n_stage);
+    const int variant = c->cur * 4 + (refresh ? 2 : 0) + (sb & 1);
+    ZF_TRY(upload_ss(c, s));
+    ZF_TRY(refresh_pointer_tables(c, variant, refresh, grads, params, s));
+
+    if (c->cfg.offload) {
+        // the device staging buffer sb is free once the D2H copies issued two steps ago finished
+        if (c->d2h_issued[sb]) ZF_CUDA(cudaStreamWaitEvent(s, c->d2h_all[sb], 0));
+        if (c->cfg.host_accumulate) {
+            // host staging buffer sb is free once H1 consumed step t-2
+            std::unique_lock<std::mutex> lk(c->mu);
+            c->cv.wait(lk, [&] { return c->h1_done >= t - 2 || c->last_t < t - 2; });
+        }
+    }
+    if (refresh) {
+        zf_ctx::Pending pe;
+        Table<NormLayer> tn{};
+        tn.dev = c->d_norm_tab;
+        tn.n = nl;
+        ZF_TRY(c->prof_begin(0, s, &pe));
+        ZF_CUDA(launch_norms(tn, c->k1_units, c->gdt, c->nonfinite_d, s));
+        ZF_TRY(c->prof_end(&pe, s));
+        c->launches++;
+        if (c->world > 1) {
+            ZF_TRY(c->prof_begin(1, s, &pe));
+            ZF_NCCL(ncclAllReduce(c->norms, c->norms, (size_t)c->total_m, ncclFloat32, ncclSum, c->comm, s));
+            ZF_TRY(c->prof_end(&pe, s));
+        }
+        Table<TopkLayer> tk{};
+        tk.dev = c->have_sel ? c->d_topk_tab[c->cur ^ 1] : c->d_topk_tab[2];
+        tk.n = nl;
+        ZF_TRY(c->prof_begin(2, s, &pe));
+        ZF_CUDA(launch_topk(tk, c->max_m, c->nonfinite_d, s));
+        ZF_TRY(c->prof_end(&pe, s));
+        c->launches++;
+    }
+    // first refresh writes set 1 (variant built with cur=0, refresh=1 -> new set 1)
+    UpdParams prm{};
+    prm.layers.dev = c->d_upd_tab[variant];
+    prm.layers.n = nl;
+    prm.total_units = c->k3_units;
+    prm.claim = c->claim;
+    prm.claim_base = c->claim_base;
+    prm.epoch = c->epoch;
+    prm.do_adam = 1;
+    prm.do_compact = 1;
+    prm.nonfinite = c->nonfinite_d;
+    prm.adam = c->adam;
+    const int grid = (int)std::min<int64_t>(c->grid, c->k3_units);
+    zf_ctx::Pending pe3;
+    ZF_TRY(c->prof_begin(3, s, &pe3));
+    ZF_CUDA(launch_update(prm, c->gdt, c->pdt, grid, s));
+    ZF_TRY(c->prof_end(&pe3, s));
+    c->launches++;
+    c->claim_base += (uint32_t)(c->k3_units + grid);
+    c->epoch += 1;
+    if (refresh) {
+        c->cur ^= 1;
+        c->have_sel = true;
+    }
+    c->last_t = t;
+    ZF_CUDA(cudaEventRecord(c->step_done, s));
+
+    if (c->cfg.offload) {
+        // X1: per-layer D2H as soon as the layer's last unit finished (cyclic counter)
+        if (!c->wait_value) ZF_CUDA(cudaStreamWaitEvent(c->copy_stream, c->step_done, 0));
+        for (int i = 0; i < nl; ++i) {
+            LayerState& l = c->L[i];
+            if (c->wait_value) {
+                const uint32_t target = c->epoch * (uint32_t)l.geo.units;
+                CUresult r = c->wait_value(reinterpret_cast<CUstream>(c->copy_stream),
+                                           reinterpret_cast<CUdeviceptr>(c->done + i), target,
+                                           CU_STREAM_WAIT_VALUE_GEQ);
+                if (r != CUDA_SUCCESS) {  // stream memory ops unavailable: gate on the whole step
+                    c->wait_value = nullptr;
+                    ZF_CUDA(cudaStreamWaitEvent(c->copy_stream, c->step_done, 0));
+                }
+            }
+            const size_t bytes = (size_t)l.d.n * l.mk * c->gsz;
+            if (bytes) ZF_CUDA(cudaMemcpyAsync(l.stage_host[sb], l.stage_dev[sb], bytes, cudaMemcpyDeviceToHost,
+                                               c->copy_stream));
+            ZF_CUDA(cudaEventRecord(l.d2h_ev[sb], c->copy_stream));
+        }
+        ZF_CUDA(cudaEventRecord(c->d2h_all[sb], c->copy_stream));
+        c->d2h_issued[sb] = true;
+        if (c->cfg.host_accumulate) {
+            {
+                std::lock_guard<std::mutex> lk(c->mu);
+                c->jobs.push_back(t);
+            }
+            c->cv.notify_all();
+        }
+    }
+    return ZF_OK;
+}
+
+extern "C" zf_status zf_sync(zf_ctx* c) {
+    g_last_error.clear();
+    if (!c) return fail(ZF_EINVAL, "ctx is NULL");
+    ZF_CUDA(cudaSetDevice(c->device));
+    ZF_CUDA(cudaEventSynchronize(c->step_done));
+    if (c->copy_stream) ZF_CUDA(cudaStreamSynchronize(c->copy_stream));
+    if (c->cfg.host_accumulate) {
+        std::unique_lock<std::mutex> lk(c->mu);
+        c->cv.wait(lk, [&] { return c->jobs.empty(); });
+    }
+    volatile int32_t* f = c->nonfinite_h;
+    if (*f) {
+        *f = 0;
+        return fail(ZF_ENONFINITE, "non-finite gradient value seen");
+    }
+    return ZF_OK;
+}
+
+extern "C" zf_status zf_selected(zf_ctx* c, int32_t layer, const int32_t** idx, int64_t* k) {
+    if (!c || layer < 0 || layer >= (int)c->L.size()) return fail(ZF_EINVAL, "bad ctx/layer");
+    if (!c->have_sel) return fail(ZF_ESTATE, "no selection yet");
+    if (idx) *idx = c->L[layer].idx[c->cur];
+    if (k) *k = c->L[layer].k;
+    return ZF_OK;
+}
+
+extern "C" zf_status zf_norms(zf_ctx* c, int32_t layer, const float** norms) {
+    if (!c || layer < 0 || layer >= (int)c->L.size()) return fail(ZF_EINVAL, "bad ctx/layer");
+    if (norms) *norms = c->norms + c->L[layer].norm_off;
+    return ZF_OK;
+}
+
+extern "C" zf_status zf_optimizer_state(zf_ctx* c, int32_t layer, const float** exp_avg, const float** exp_avg_sq,
+                                        const int32_t** step) {
+    if (!c || layer < 0 || layer >= (int)c->L.size()) return fail(ZF_EINVAL, "bad ctx/layer");
+    if (!c->have_sel) return fail(ZF_ESTATE, "no state yet");
+    const LayerState& l = c->L[layer];
+    if (exp_avg) *exp_avg = l.mom[c->cur];
+    if (exp_avg_sq) *exp_avg_sq = l.vel[c->cur];
+    if (step) *step = l.steps[c->cur];
+    return ZF_OK;
+}
+
+extern "C" zf_status zf_compact_buffer(zf_ctx* c, int32_t layer, const void** dev, const void** host) {
+    if (!c || layer < 0 || layer >= (int)c->L.size()) return fail(ZF_EINVAL, "bad ctx/layer");
+    if (c->last_t < 0) return fail(ZF_ESTATE, "no step yet");
+    const int sb = (int)(c->last_t % c->n_stage);
+    if (dev) *dev = c->L[layer].stage_dev[sb];
+    if (host) *host = c->cfg.offload ? c->L[layer].stage_host[sb] : nullptr;
+    return ZF_OK;
+}
+
+extern "C" zf_status zf_host_accumulator(zf_ctx* c, int32_t layer, int32_t which, const float** host, int64_t* rows,
+                                         int64_t* cols) {
+    if (!c || layer < 0 || layer >= (int)c->L.size()) return fail(ZF_EINVAL, "bad ctx/layer");
+    if (!c->cfg.host_accumulate) return fail(ZF_ESTATE, "host accumulation is off");
+    const int S = c->cfg.accum_interval;
+    const LayerState& l = c->L[layer];
+    const float* p = nullptr;
+    if (c->last_t >= 0) {
+        if (which == 0) {
+            p = l.acc[(c->last_t / S) % 2];
+        } else {
+            const int64_t w = (c->last_t + 1) / S - 1;  // last completed window
+            if (w >= 0) p = l.acc[w % 2];
+        }
+    }
+    if (host) *host = p;
+    if (rows) *rows = l.d.n;
+    if (cols) *cols = l.mk;
+    return ZF_OK;
+}
+
+extern "C" zf_status zf_set_lr(zf_ctx* c, double lr) {
+    if (!c) return fail(ZF_EINVAL, "ctx is NULL");
+    if (!(lr >= 0.0f) || !std::isfinite(lr)) return fail(ZF_EINVAL, "lr must be finite and >= 0");
+    c->lr_cur = lr;
+    return ZF_OK;
+}
+
+extern "C" int64_t zf_kernel_launches(zf_ctx* c) { return c ? c->launches : -1; }
+
+extern "C" zf_status zf_profile(zf_ctx* c, int32_t enable) {
+    if (!c) return fail(ZF_EINVAL, "ctx is NULL");
+    c->profiling = enable != 0;
+    return ZF_OK;
+}
+
+extern "C" zf_status zf_profile_read(zf_ctx* c, double* ms, int64_t* count) {
+    if (!c) return fail(ZF_EINVAL, "ctx is NULL");
+    for (auto& p : c->pending) {
+        ZF_CUDA(cudaEventSynchronize(p.b));
+        float e = 0.0f;
+        ZF_CUDA(cudaEventElapsedTime(&e, p.a, p.b));
+        c->prof_ms[p.phase] += e;
+        c->prof_n[p.phase] += 1;
+        c->ev_pool.push_back({p.a, p.b});
+    }
+    c->pending.clear();
+    for (int i = 0; i < 4; ++i) {
+        if (ms) ms[i] = c->prof_ms[i];
+        if (count) count[i] = c->prof_n[i];
+        c->prof_ms[i] = 0;
+        c->prof_n[i] = 0;
+    }
+    return ZF_OK;
+}
+
+extern "C" zf_status zf_destroy(zf_ctx* c) {
+    if (!c) return ZF_OK;
+    delete c;
+    return ZF_OK;
+}

@@ -1,0 +1,277 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle, element by
+element, on the same seeded inputs.  Bars (BASELINE.json north_star): selection
+and compaction bit-exact (boundary swaps allowed only within the norm tolerance,
+reading R3), norms within rel 1e-5, fp32 params/moments within rel 1e-6 and bf16
+params within 1 ulp -- the kernels follow the oracle's op order, so the update
+is also checked bit for bit."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from gpu_util import (assert_bits_equal, assert_close_rel, bf16_ulp_diff, from_np, selection_ok, to_np)
+
+pytestmark = pytest.mark.gpu
+
+TDT = {"bf16": torch.bfloat16, "fp32": torch.float32}
+
+
+@pytest.fixture(scope="module")
+def zf():
+    from paper_2505_12242_b200 import _build
+    _build.build()
+    from paper_2505_12242_b200 import zf as z
+    return z
+
+
+@pytest.fixture(scope="module")
+def orc():
+    from oracle import oracle as o
+    o.lib()
+    return o
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    from synth import gpu as g
+    return g
+
+
+def _grad(gpu, n, m, dt, layer=0, step=0, ld=None, tie=False):
+    ld = ld or m
+    buf = torch.empty(n, ld, dtype=TDT[dt], device="cuda")
+    G = buf[:, :m]
+    if tie:
+        gpu.fill_grad_tie(G, layer, step)
+    else:
+        sc = gpu.ColScale(m, layer)
+        sc.advance_to(step)
+        gpu.fill_grad(G, layer, step, sc)
+    return G
+
+
+# ------------------------------------------------------------------ K1 norms
+NORM_CASES = [(256, 512, "fp32", None), (4096, 4096, "bf16", None), (1000, 1000, "bf16", None),
+              (37, 1001, "bf16", 1003), (130, 257, "fp32", None), (513, 768, "bf16", 776), (1, 9, "bf16", None),
+              (11008, 4096, "bf16", None), (300, 13824, "bf16", None)]
+
+
+@pytest.mark.parametrize("n,m,dt,ld", NORM_CASES)
+def test_column_norms(zf, orc, gpu, n, m, dt, ld):
+    G = _grad(gpu, n, m, dt, layer=n % 7, ld=ld)
+    out = torch.full((m,), -1.0, device="cuda")
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    zf.zf_column_norms(G, out, flag)
+    out2 = torch.empty_like(out)
+    zf.zf_column_norms(G, out2)
+    torch.cuda.synchronize()
+    want = orc.column_norms(np.ascontiguousarray(to_np(G)))
+    got = to_np(out)
+    assert_close_rel(got, want, 1e-5, "norms")
+    assert_bits_equal(to_np(out2), got, "norms determinism")
+    assert int(flag.item()) == 0
+
+
+def test_column_norms_tie_heavy_exact(zf, orc, gpu):
+    # tie-heavy values are multiples of 2^-8 with small sums: every partial sum is exact
+    G = _grad(gpu, 200, 3000, "bf16", tie=True)
+    out = torch.empty(3000, device="cuda")
+    zf.zf_column_norms(G, out)
+    assert_bits_equal(to_np(out), orc.column_norms(to_np(G)), "tie norms")
+
+
+def test_column_norms_nonfinite_flag(zf, gpu):
+    G = _grad(gpu, 300, 512, "bf16")
+    G[123, 77] = float("nan")
+    out = torch.empty(512, device="cuda")
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    zf.zf_column_norms(G, out, flag)
+    assert int(flag.item()) == 1
+
+
+# ------------------------------------------------------------------ K2 top-k
+@pytest.mark.parametrize("m,ppm", [(8, 250000), (100, 100000), (768, 100000), (768, 10000), (4096, 100000),
+                                   (4096, 10000), (11008, 100000), (13824, 10000), (50000, 100000), (5000, 1),
+                                   (333, 1000000)])
+def test_topk_exact(zf, orc, m, ppm):
+    rng = np.random.default_rng(m + ppm)
+    norms = (rng.standard_normal(m) ** 2 * np.exp(rng.standard_normal(m) * 2)).astype(np.float32)
+    norms[rng.choice(m, m // 5, replace=False)] = norms[0]          # many exact ties incl. at the boundary
+    k = orc.k_for(m, ppm)
+    idx = torch.empty(k, dtype=torch.int32, device="cuda")
+    zf.zf_topk_columns(from_np(norms), k, idx)
+    assert to_np(idx).tolist() == orc.topk(norms, k).tolist()
+
+
+def test_topk_integer_ties(zf, orc):
+    rng = np.random.default_rng(5)
+    for m in (1, 2, 31, 32, 33, 1000, 4097):
+        norms = rng.integers(0, 4, m).astype(np.float32)
+        for k in sorted({1, max(1, m // 3), m}):
+            idx = torch.empty(k, dtype=torch.int32, device="cuda")
+            zf.zf_topk_columns(from_np(norms), k, idx)
+            assert to_np(idx).tolist() == orc.topk(norms, k).tolist(), (m, k)
+
+
+# ------------------------------------------------------------------ K3 AdamW (standalone)
+@pytest.mark.parametrize("n,m,gdt,pdt,wd,dec,ldp", [(256, 512, "fp32", "fp32", 0.0, 1, None),
+                                                   (300, 4096, "bf16", "bf16", 0.0, 1, None),
+                                                   (77, 1001, "bf16", "bf16", 0.01, 1, 1009),
+                                                   (64, 640, "bf16", "fp32", 0.01, 0, None),
+                                                   (50, 200, "fp32", "bf16", 0.01, 1, None)])
+def test_selective_adam_bitexact(zf, orc, gpu, n, m, gdt, pdt, wd, dec, ldp):
+    rng = np.random.default_rng(n * m)
+    G = _grad(gpu, n, m, gdt, layer=1)
+    Pbuf = torch.empty(n, ldp or m, dtype=TDT[pdt], device="cuda")
+    P = Pbuf[:, :m]
+    gpu.fill_param(P, 1)
+    k = orc.k_for(m, 100000)
+    idx_np = np.sort(rng.choice(m, k, replace=False)).astype(np.int32)
+    M0 = (rng.standard_normal((n, k)) * 1e-3).astype(np.float32)
+    V0 = (rng.random((n, k)) * 1e-6).astype(np.float32)
+    st0 = rng.integers(0, 20, k).astype(np.int32)
+    hp = orc.AdamHP(lr=1e-3, weight_decay=wd, decoupled=dec)
+    Pn, Gn = np.ascontiguousarray(to_np(P)), np.ascontiguousarray(to_np(G))
+    M1, V1, st1 = M0.copy(), V0.copy(), st0.copy()
+    orc.selective_adamw(Pn, Gn, idx_np, M1, V1, st1, hp)
+    Md, Vd, sd = from_np(M0), from_np(V0), from_np(st0)
+    zf.zf_selective_adam(P, G, from_np(idx_np), Md, Vd, sd, zf.adam_params(lr=1e-3, weight_decay=wd, decoupled=dec))
+    torch.cuda.synchronize()
+    assert_bits_equal(to_np(sd), st1, "steps")
+    assert_bits_equal(to_np(Md), M1, "exp_avg")
+    assert_bits_equal(to_np(Vd), V1, "exp_avg_sq")
+    assert_bits_equal(np.ascontiguousarray(to_np(P)), Pn, "params")
+    if ldp:  # padding columns untouched
+        pad = to_np(Pbuf[:, m:])
+        assert np.array_equal(pad, to_np(Pbuf[:, m:]))
+
+
+# ------------------------------------------------------------------ K3 compaction (standalone)
+@pytest.mark.parametrize("n,m,dt,ld,ppm", [(256, 512, "fp32", None, 100000), (4096, 4096, "bf16", None, 100000),
+                                           (1000, 1000, "bf16", None, 10000), (37, 1001, "bf16", 1003, 100000),
+                                           (5, 20000, "bf16", None, 100000), (3, 40000, "fp32", None, 10000),
+                                           (21, 768, "bf16", 776, 100000), (7, 13, "fp32", None, 500000),
+                                           (9, 64, "bf16", None, 1000000)])
+def test_compact_bitexact(zf, orc, gpu, n, m, dt, ld, ppm):
+    rng = np.random.default_rng(n + m)
+    G = _grad(gpu, n, m, dt, layer=2, ld=ld)
+    k = orc.k_for(m, ppm)
+    idx_np = np.sort(rng.choice(m, k, replace=False)).astype(np.int32)
+    out = torch.full((max(1, n * (m - k)),), 7, dtype=TDT[dt], device="cuda")
+    zf.zf_compact_unselected(G, from_np(idx_np), out)
+    want = orc.compact(np.ascontiguousarray(to_np(G)), idx_np)
+    assert_bits_equal(to_np(out)[: n * (m - k)].reshape(n, m - k), want, "compact")
+
+
+# ------------------------------------------------------------------ zf_step vs oracle, multi-step
+def _run_stateful(zf, orc, gpu, shapes, gdt, pdt, ppm, N, S, steps, offload, lr=1e-3, wd=0.0, check_every=1,
+                  tie=False, ld_pad=0):
+    hp_o = orc.AdamHP(lr=lr, weight_decay=wd)
+    ctx = zf.Context([zf.LayerShape(n, m, m + ld_pad, m + ld_pad) for n, m in shapes], grad_dtype=TDT[gdt],
+                     param_dtype=TDT[pdt], topk_ratio_ppm=ppm, refresh_interval=N, accum_interval=S,
+                     adam=zf.adam_params(lr=lr, weight_decay=wd), offload=offload, host_accumulate=offload)
+    scales = [gpu.ColScale(m, li) for li, (n, m) in enumerate(shapes)]
+    Gs = [torch.empty(n, m + ld_pad, dtype=TDT[gdt], device="cuda")[:, :m] for n, m in shapes]
+    Ps = [torch.empty(n, m + ld_pad, dtype=TDT[pdt], device="cuda")[:, :m] for n, m in shapes]
+    for li, P in enumerate(Ps):
+        gpu.fill_param(P, li)
+    layers = [orc.OracleLayer(n=n, m=m, ratio_ppm=ppm, refresh_interval=N, accum_interval=S, hp=hp_o)
+              for n, m in shapes]
+    Po = [np.ascontiguousarray(to_np(P)) for P in Ps]
+    swaps = 0
+    for t in range(steps):
+        for li, (G, sc) in enumerate(zip(Gs, scales)):
+            if tie:
+                gpu.fill_grad_tie(G, li, t)
+            else:
+                sc.advance_to(t)
+                gpu.fill_grad(G, li, t, sc)
+        Gn = [np.ascontiguousarray(to_np(G)) for G in Gs]
+        ctx.step(t, Gs, Ps)
+        ctx.sync()
+        refresh = t % N == 0
+        for li, (n, m) in enumerate(shapes):
+            L = layers[li]
+            gidx = to_np(ctx.selected(li))
+            if refresh:
+                onorms = orc.column_norms(Gn[li])
+                assert_close_rel(to_np(ctx.norms(li)), onorms, 1e-5, f"norms t={t} l={li}")
+                swaps += selection_ok(gidx, orc.topk(onorms, L.k), onorms)
+            out = L.step(t, Gn[li], Po[li], idx_override=gidx if refresh else None)
+            if t % check_every and t != steps - 1:
+                continue
+            assert_bits_equal(gidx, L.idx, f"idx t={t} l={li}")
+            M, V, st = ctx.optimizer_state(li)
+            assert_bits_equal(to_np(st), L.steps, f"steps t={t} l={li}")
+            assert_bits_equal(to_np(M), L.M, f"exp_avg t={t} l={li}")
+            assert_bits_equal(to_np(V), L.V, f"exp_avg_sq t={t} l={li}")
+            assert_bits_equal(np.ascontiguousarray(to_np(Ps[li])), Po[li], f"params t={t} l={li}")
+            assert_bits_equal(to_np(ctx.compact_buffer(li)), out, f"compact t={t} l={li}")
+            if offload:
+                assert_bits_equal(ctx.compact_host(li).copy(), out, f"compact host t={t} l={li}")
+                assert_bits_equal(ctx.host_accumulator(li, 0).copy(), L.acc[(t // S) % 2], f"acc t={t} l={li}")
+                sealed = ctx.host_accumulator(li, 1)
+                osealed = L.sealed(t)
+                assert (sealed is None) == (osealed is None)
+                if sealed is not None:
+                    assert_bits_equal(sealed.copy(), osealed, f"sealed acc t={t} l={li}")
+    launches = ctx.kernel_launches()
+    ctx.close()
+    return swaps, launches
+
+
+@pytest.mark.parametrize("NS", [1, 2, 4])
+def test_step_config1_fp32(zf, orc, gpu, NS):
+    """BASELINE config 1: one 256x512 fp32 gradient, top-10%, selective AdamW +
+    unselected accumulation; N = S in {1, 2, 4}, 8 steps (two windows at S=4)."""
+    swaps, launches = _run_stateful(zf, orc, gpu, [(256, 512)], "fp32", "fp32", 100000, NS, NS, 8, offload=True)
+    assert launches == 8 + 2 * (8 // NS)
+    assert swaps == 0
+
+
+def test_step_config1_weight_decay(zf, orc, gpu):
+    _run_stateful(zf, orc, gpu, [(256, 512)], "fp32", "fp32", 100000, 4, 4, 6, offload=True, wd=0.01)
+
+
+def test_step_ragged_multilayer_bf16(zf, orc, gpu):
+    shapes = [(37, 1001), (513, 768), (130, 257), (5, 20000), (1, 64), (64, 4096)]
+    _run_stateful(zf, orc, gpu, shapes, "bf16", "bf16", 100000, 2, 2, 5, offload=True, ld_pad=8)
+
+
+def test_step_tie_heavy(zf, orc, gpu):
+    _run_stateful(zf, orc, gpu, [(64, 1000), (16, 333)], "bf16", "bf16", 10000, 2, 2, 4, offload=False, tie=True)
+
+
+def test_step_gpt2_small_bf16(zf, orc, gpu):
+    """BASELINE config 2: GPT-2 small, all 49 linears, bf16, k=10%, N=4 (refresh at 0 and 4)."""
+    shapes = [(n, m) for _, n, m in synth.gpt2_small_linears()]
+    _run_stateful(zf, orc, gpu, shapes, "bf16", "bf16", 100000, 4, 4, 5, offload=False, check_every=4)
+
+
+def test_step_nonfinite_reported(zf, gpu):
+    ctx = zf.Context([zf.LayerShape(64, 512)], topk_ratio_ppm=100000, refresh_interval=2, accum_interval=2)
+    G = _grad(gpu, 64, 512, "bf16")
+    P = torch.zeros(64, 512, dtype=torch.bfloat16, device="cuda")
+    ctx.step(0, [G], [P])
+    ctx.sync()
+    G[3, 5] = float("inf")
+    ctx.step(1, [G], [P])
+    with pytest.raises(zf.ZFError) as e:
+        ctx.sync()
+    assert e.value.status == zf.ZF_ENONFINITE
+    ctx.step(2, [_grad(gpu, 64, 512, "bf16")], [P])
+    ctx.sync()  # flag cleared
+    ctx.close()
+
+
+def test_step_state_errors(zf, gpu):
+    ctx = zf.Context([zf.LayerShape(8, 64)], refresh_interval=4, accum_interval=4)
+    G = _grad(gpu, 8, 64, "bf16")
+    P = torch.zeros(8, 64, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(zf.ZFError) as e:
+        ctx.step(1, [G], [P])            # first step must refresh
+    assert e.value.status == zf.ZF_ESTATE
+    ctx.step(0, [G], [P])
+    with pytest.raises(zf.ZFError):
+        ctx.step(2, [G], [P])            # not consecutive
+    ctx.close()

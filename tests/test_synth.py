@@ -1,0 +1,84 @@
+"""The seeded input generator: deterministic, shard-consistent, shaped like the
+paper's workloads; its GPU twin is bit-identical to the numpy recipe."""
+import numpy as np
+import pytest
+
+import synth
+
+
+def test_deterministic_and_seeded():
+    e = synth.col_scale_init(300, layer=3)
+    a = synth.grad(17, 300, layer=3, step=5, scale_exp=e)
+    b = synth.grad(17, 300, layer=3, step=5, scale_exp=e)
+    c = synth.grad(17, 300, layer=3, step=6, scale_exp=e)
+    assert a.dtype == np.uint16 and np.array_equal(a, b) and not np.array_equal(a, c)
+
+
+def test_row_shards_concatenate():
+    e = synth.col_scale_init(64, layer=1)
+    whole = synth.grad(40, 64, 1, 2, e)
+    parts = [synth.grad(10, 64, 1, 2, e, row0=10 * r) for r in range(4)]
+    assert np.array_equal(np.concatenate(parts), whole)
+    assert np.array_equal(np.concatenate([synth.param(20, 64, 1, row0=0), synth.param(20, 64, 1, row0=20)]),
+                          synth.param(40, 64, 1))
+
+
+def test_values_exact_in_fp32_and_column_structure():
+    e = synth.col_scale_init(512, layer=0)
+    g32 = synth.grad(256, 512, 0, 0, e, dtype="fp32")
+    # an 18-bit integer times a power of two: the fp32 value is exact, |z| <= 2 * 2^(e-10)
+    z = g32 / np.ldexp(1.0, e.astype(np.int32) - 26)[None, :]
+    assert np.array_equal(z, np.round(z)) and np.all(np.abs(z) <= 131070)
+    # column-concentrated energy (P:204 reports the top 1% of gradients carrying ~89% of norm^2)
+    col = (g32.astype(np.float64) ** 2).sum(0)
+    top = np.sort(col)[::-1]
+    assert top[: len(top) // 10].sum() / top.sum() > 0.5
+
+
+def test_scale_redraw_rate_about_one_percent():
+    e0 = synth.col_scale_init(20000, layer=2)
+    e1 = synth.col_scale_advance(e0, 1, layer=2)
+    j = np.arange(20000, dtype=np.uint64)
+    hr = synth._hash(synth.stream_key(synth.SEED, synth.TAG_REDRAW, 2, 1), j)
+    frac = np.mean((hr & np.uint64(0xFFFFFFFF)) < np.uint64(synth.REDRAW_THRESHOLD))
+    assert 0.007 < frac < 0.013
+    assert np.mean(e0 != e1) <= frac
+
+
+def test_tie_mode_has_ties():
+    g = synth.grad_tie(8, 100, 0, 0, dtype="fp32")
+    assert set(np.unique(g * 256).tolist()) <= {-2.0, -1.0, 0.0, 1.0, 2.0}
+
+
+def test_model_shapes():
+    L7 = synth.llama2_7b_linears()
+    assert len(L7) == 225 and sum(n * m for _, n, m in L7) == 6_607_077_376
+    L13 = synth.llama2_13b_linears()
+    assert len(L13) == 281 and sum(n * m for _, n, m in L13) == 12_851_609_600
+    G2 = synth.gpt2_small_linears()
+    assert len(G2) == 49 and sum(n * m for _, n, m in G2) == 123_532_032
+
+
+@pytest.mark.gpu
+def test_gpu_generator_bit_identical():
+    import torch
+    from synth import gpu
+    for dt, tdt in (("bf16", torch.bfloat16), ("fp32", torch.float32)):
+        n, m, layer = 333, 1000, 7
+        sc = gpu.ColScale(m, layer)
+        sc.advance_to(3)
+        out = torch.empty(n, m, dtype=tdt, device="cuda")
+        gpu.fill_grad(out, layer, 3, sc, row0=50)
+        e = synth.col_scale_at(m, 3, layer)
+        assert np.array_equal(sc.e.cpu().numpy(), e)
+        want = synth.grad(n, m, layer, 3, e, dtype=dt, row0=50)
+        got = out.cpu().view(torch.int16).numpy().view(np.uint16) if dt == "bf16" else out.cpu().numpy()
+        assert np.array_equal(got.view(np.uint8), want.view(np.uint8)), dt
+        gpu.fill_param(out, layer, row0=50)
+        want = synth.param(n, m, layer, dtype=dt, row0=50)
+        got = out.cpu().view(torch.int16).numpy().view(np.uint16) if dt == "bf16" else out.cpu().numpy()
+        assert np.array_equal(got.view(np.uint8), want.view(np.uint8)), dt
+        gpu.fill_grad_tie(out, layer, 2)
+        want = synth.grad_tie(n, m, layer, 2, dtype=dt)
+        got = out.cpu().view(torch.int16).numpy().view(np.uint16) if dt == "bf16" else out.cpu().numpy()
+        assert np.array_equal(got.view(np.uint8), want.view(np.uint8)), dt
