@@ -56,7 +56,7 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* warp_s
 }
 
 __global__ void __launch_bounds__(K2_THREADS)
-k_topk(const __grid_constant__ Table<TopkLayer> table, int use_smem, int32_t* nonfinite) {
+k_topk(const __grid_constant__ Table<TopkLayer> table, int use_smem, int32_t old_delta, int32_t* nonfinite) {
     extern __shared__ uint32_t dyn[];
     __shared__ uint32_t hist[256];
     __shared__ uint32_t warp_sums[K2_WARPS + 1];
@@ -179,7 +179,7 @@ k_topk(const __grid_constant__ Table<TopkLayer> table, int use_smem, int32_t* no
                 if (word & bit) src = __ldg(L.old_prefix + (c >> 5)) + __popc(word & (bit - 1u));
             }
             L.slot_src[s] = src;
-            L.new_steps[s] = src >= 0 ? __ldg(L.old_steps + src) : 0;
+            L.new_steps[s] = src >= 0 ? __ldg(L.old_steps + src) + old_delta : 0;
         }
     }
 }
@@ -210,9 +210,20 @@ __global__ void k_build_mask(const int32_t* __restrict__ idx, int64_t k, int64_t
     }
 }
 
+__global__ void k_add_const(const int32_t* __restrict__ src, int32_t* dst, int64_t k, int32_t delta) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < k; s += (int64_t)gridDim.x * blockDim.x)
+        dst[s] = src[s] + delta;
+}
+
 }  // namespace
 
-cudaError_t launch_topk(const Table<TopkLayer>& t, int64_t max_m, int32_t* nonfinite, cudaStream_t s) {
+cudaError_t launch_add_const(const int32_t* src, int32_t* dst, int64_t k, int32_t delta, cudaStream_t s) {
+    if (k <= 0) return cudaSuccess;
+    k_add_const<<<(unsigned)((k + 255) / 256 < 1024 ? (k + 255) / 256 : 1024), 256, 0, s>>>(src, dst, k, delta);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_topk(const Table<TopkLayer>& t, int64_t max_m, int32_t old_delta, int32_t* nonfinite, cudaStream_t s) {
     if (t.n <= 0) return cudaSuccess;
     size_t smem = 0;
     const int use_smem = max_m <= K2_SMEM_KEYS_MAX;
@@ -223,7 +234,7 @@ cudaError_t launch_topk(const Table<TopkLayer>& t, int64_t max_m, int32_t* nonfi
                              (int)((K2_SMEM_KEYS_MAX + K2_SMEM_KEYS_MAX / 32) * sizeof(uint32_t)));
         attr_set = true;
     }
-    k_topk<<<t.n, K2_THREADS, smem, s>>>(t, use_smem, nonfinite);
+    k_topk<<<t.n, K2_THREADS, smem, s>>>(t, use_smem, old_delta, nonfinite);
     return cudaGetLastError();
 }
 

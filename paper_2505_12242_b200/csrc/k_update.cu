@@ -10,42 +10,46 @@
 // gradients to the CPU".  Moment carry-over across a refresh: reading R7.
 //
 // B200 design (DESIGN.md §5 K3).  HBM-bound: per element of G it moves 2 B of
-// G, 2(1-κ) B of compact output, and for the κ selected columns the
-// sector-scattered read-modify-write of p plus dense fp32 m, v.
-//  - persistent grid, one 512-thread CTA per SM; work units (a tile of R whole
-//    rows, or a column segment of one row when a row exceeds the tile) are
-//    claimed dynamically with one atomic per unit, so mixed layer shapes
-//    balance across the 148 SMs;
-//  - G tiles are staged into a 4-deep shared-memory ring by the bulk-copy
-//    engine (cp.async.bulk / TMA, completion on an mbarrier), claimed and
-//    issued STAGES-1 units ahead, so HBM reads stay in flight while the CTA
-//    works on the current tile;
-//  - compaction reads the tile in 32-column groups (lane = column, one mask
-//    word per group): the column's compact position is
-//    column - (prefix[word] + popc(mask & lanemask_lt)), written into a
-//    shared output tile that is then streamed out with aligned 16-byte stores
-//    (the compact block of a unit is one contiguous range of the output);
-//  - AdamW runs over (row, slot) pairs, so the moments [n, k] are read and
-//    written fully coalesced; g comes from the staged tile; p is the only
-//    scattered access (2-byte elements in 32-byte sectors).  The pair loads are
-//    issued before the compaction phase so their latency overlaps it;
-//  - every AdamW op is an explicit round-to-nearest intrinsic (no FMA
-//    contraction), matching the oracle's op order bit for bit;
-//  - when the last unit of a layer finishes (per-layer cyclic counter), its CTA
-//    advances the per-slot step counts; the same counter gates the layer's
-//    device->host copy (cuStreamWaitValue32) when offloading.
+// G, 2(1-κ) B of compact output, and for the selected columns the read-modify-
+// write of p (in 32-byte sectors) and of the fp32 moments.
+//  - persistent grid, one 544-thread CTA per SM, warp-specialised: warp 0 is the
+//    producer, warps 1..16 consume.  Work units (R whole rows, or a 128-aligned
+//    column segment of one row) are claimed dynamically, one atomic per unit.
+//  - the producer stages EVERYTHING a unit needs into one of 4 shared-memory
+//    stage arenas with bulk copies (cp.async.bulk, the TMA engine) completing on
+//    one mbarrier: the G tile, the p tile (when the selection touches most of p's
+//    32-byte sectors), the moment slabs (or the old rows on a refresh), the slot
+//    step counts, the remap sources and the segment's mask/prefix words.  The
+//    host sizes units so the worst case fits an arena; 3 units stay in flight.
+//    Consumers issue no global loads.
+//  - a consumer warp takes 256-column row chunks; lane l owns 8 consecutive
+//    columns (one 16-byte shared load, one mask byte).  Its compact position is
+//    8l - (selected before it in the chunk), from the prefix word and a popcount;
+//    the unselected values go to a warp buffer that is streamed out with aligned
+//    16-byte stores (partial edges scalar).  The selected columns are listed by
+//    slot and updated with all 32 lanes busy (AdamW in shared memory, explicit
+//    round-to-nearest intrinsics, the oracle's op order); moments are stored
+//    coalesced; every 32-byte p sector holding a selected column is written back
+//    whole from the staged tile.
+//  - with offload, each consumer warp bumps a per-layer counter after its share
+//    of a unit (red.release); the copy stream waits on it (cuStreamWaitValue32)
+//    to start the layer's device->host copy.
 #include "zf_internal.cuh"
 
 namespace zf {
 namespace {
 
-constexpr int K3_THREADS = 512;
-constexpr int K3_WARPS = K3_THREADS / 32;
-constexpr int K3_STAGES = 4;
-constexpr int K3_STAGE_BYTES = 32 * 1024;
-constexpr int K3_OUT_BYTES = K3_STAGE_BYTES + 64;
-constexpr int K3_BATCH = 4;  // AdamW pairs in flight per thread
-constexpr int K3_SMEM = K3_STAGES * K3_STAGE_BYTES + K3_OUT_BYTES + 128;
+constexpr int K3_NCW = 15;                        // consumer warps
+constexpr int K3_STAGES = 4;                      // stage arenas = producer warps (one chain per stage)
+constexpr int K3_THREADS = 32 * (K3_NCW + K3_STAGES);
+constexpr int K3_CHUNK = 256;                     // columns per warp chunk (32 lanes x 8)
+constexpr int K3_WBUF_BYTES = (K3_CHUNK + 16) * 4;
+constexpr int K3_WARP_BYTES = K3_WBUF_BYTES;
+constexpr int K3_PAIRS = 3;                       // AdamW (row, slot) pairs in flight per consumer thread
+constexpr int K3_ARENA = 48 * 1024;               // bytes per stage arena
+constexpr int K3_SMEM = K3_STAGES * K3_ARENA + K3_NCW * K3_WARP_BYTES;
+static_assert(K3_ARENA % 128 == 0 && K3_WARP_BYTES % 16 == 0, "alignment");
+static_assert(K3_SMEM <= 227 * 1024 - 512, "shared memory budget");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -56,16 +60,38 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
     uint32_t done = 0;
     while (!done) {
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n\t"
             "selp.b32 %0, 1, 0, p;\n\t}"
             : "=r"(done)
             : "r"(smem_u32(bar)), "r"(phase)
             : "memory");
+    }
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    return done != 0;
+}
+// producer-side wait: back off with nanosleep so spinning does not steal issue slots
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
+    int ns = 32;
+    while (!mbar_test(bar, phase)) {
+        __nanosleep(ns);
+        ns = ns < 256 ? ns * 2 : 256;
     }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
@@ -80,23 +106,63 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+__device__ __forceinline__ uint64_t evict_last_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void st_cs_v4(void* p, uint4 v) {
     asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                  : "memory");
 }
 
-__device__ __forceinline__ int find_layer(const Table<UpdLayer>& t, int64_t u) {
-    int lo = 0, hi = t.n - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (t[mid].unit_begin <= u) lo = mid; else hi = mid - 1;
+__device__ __forceinline__ void sts16(void* p, uint16_t v) {
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(smem_u32(p)), "h"(v) : "memory");
+}
+__device__ __forceinline__ void sts32(void* p, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint4 lds128(const void* p) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(smem_u32(p)) : "memory");
+    return v;
+}
+template <typename B>
+__device__ __forceinline__ void sts_elem(B* p, B v) {
+    if constexpr (sizeof(B) == 2) sts16(p, v);
+    else sts32(p, v);
+}
+
+// Bulk-copy the 4-byte elements [e0, e1) of `src` to arena offset *off as an aligned
+// superset (16-byte granules; the source arrays are padded).  Returns the element
+// offset of e0 within the copy; advances *off.
+__device__ __forceinline__ int stage_words(unsigned char* arena, int* off, const void* src, int64_t e0, int64_t e1,
+                                           uint64_t* bar, uint32_t* tx, int* where) {
+    const int64_t a = e0 & ~int64_t(3), b = (e1 + 3) & ~int64_t(3);
+    *where = *off;
+    if (b > a) {
+        const uint32_t bytes = (uint32_t)((b - a) * 4);
+        bulk_g2s(arena + *off, static_cast<const int32_t*>(src) + a, bytes, bar, 0ull);
+        *tx += bytes;
+        *off += (int)bytes;
     }
-    return lo;
+    return (int)(e0 - a);
+}
+
+__device__ __forceinline__ int find_layer_from(const Table<UpdLayer>& t, int64_t u, int hint) {
+    int li = hint;
+    if (li >= t.n || t[li].unit_begin > u) li = 0;
+    while (li + 1 < t.n && t[li + 1].unit_begin <= u) ++li;  // claims are monotonic: usually 0-1 steps
+    return li;
 }
 
 struct UnitGeom {
-    int64_t r0;   // first row
-    int32_t Rr;   // rows
+    int64_t r0;
+    int32_t Rr;
     int64_t c0, c1;
 };
 
@@ -110,10 +176,30 @@ __device__ __forceinline__ UnitGeom unit_geom(const UpdLayer& L, int64_t lu) {
     return g;
 }
 
-// number of selected columns < c (c is 0, m, or a multiple of 32)
-__device__ __forceinline__ int64_t sel_before(const UpdLayer& L, int64_t c) {
-    if (c >= L.m) return L.k;
-    return __ldg(L.prefix + (c >> 5));
+// per-stage unit descriptor written by the producer (arena byte offsets; element offsets
+// of the aligned supersets)
+struct StageInfo {
+    int64_t u;        // unit (-1: no more work)
+    int32_t li;       // layer
+    int32_t s0, s1;   // selected-slot range of the segment
+    int32_t oG, oP, oM, oV, oS, oSrc, oMask, oPre;
+    int32_t eM, eV, eS, eSrc, eMask, ePre;
+    int32_t oIdx, eIdx;
+    int32_t pstaged, mstaged;
+};
+
+template <int DT>
+__device__ __forceinline__ void load8(const typename Elt<DT>::bits* p, uint32_t (&w)[8 * Elt<DT>::SIZE / 4]);
+template <>
+__device__ __forceinline__ void load8<DT_BF16>(const uint16_t* p, uint32_t (&w)[4]) {
+    const uint4 v = *reinterpret_cast<const uint4*>(p);
+    w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+}
+template <>
+__device__ __forceinline__ void load8<DT_F32>(const uint32_t* p, uint32_t (&w)[8]) {
+    const uint4 a = *reinterpret_cast<const uint4*>(p);
+    const uint4 b = *reinterpret_cast<const uint4*>(p + 4);
+    w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w; w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
 }
 
 template <int GDT, int PDT>
@@ -122,208 +208,356 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
     using PE = Elt<PDT>;
     using GB = typename GE::bits;
     using PB = typename PE::bits;
-    constexpr int GSZ = GE::SIZE;
-    constexpr int VEC = GE::VEC;
+    constexpr int GSZ = GE::SIZE, PSZ = PE::SIZE;
+    constexpr int VEC = GE::VEC;           // elements per 16 bytes
+    constexpr int NW8 = 8 * GSZ / 4;       // 32-bit words holding 8 elements
 
     extern __shared__ __align__(128) unsigned char smem[];
-    unsigned char* stage_buf = smem;
-    GB* sOut = reinterpret_cast<GB*>(smem + K3_STAGES * K3_STAGE_BYTES);
-    __shared__ __align__(8) uint64_t bars[K3_STAGES];
-    __shared__ int64_t st_unit[K3_STAGES];
-    __shared__ int32_t st_layer[K3_STAGES];
-    __shared__ int s_bad;
+    __shared__ __align__(8) uint64_t full[K3_STAGES], empty[K3_STAGES];
+    __shared__ StageInfo info[K3_STAGES];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const Table<UpdLayer>& table = prm.layers;
-    const uint64_t policy = evict_first_policy();
-
-    // ---- producer (thread 0): claim the next unit and start its tile copy
-    bool exhausted = false;
-    auto claim_issue = [&](int st) {
-        int64_t u = -1;
-        if (!exhausted) {
-            const uint32_t c = atomicAdd(prm.claim, 1u) - prm.claim_base;
-            if ((int64_t)c < prm.total_units) u = c; else exhausted = true;
-        }
-        st_unit[st] = u;
-        if (u < 0) return;
-        const int li = find_layer(table, u);
-        st_layer[st] = li;
-        const UpdLayer& L = table[li];
-        if (!L.tma_ok) return;
-        const UnitGeom g = unit_geom(L, u - L.unit_begin);
-        const int64_t sw = g.c1 - g.c0;
-        const uint32_t bytes = (uint32_t)(g.Rr * sw * GSZ);
-        unsigned char* dst = stage_buf + st * K3_STAGE_BYTES;
-        const unsigned char* G = static_cast<const unsigned char*>(L.G);
-        mbar_expect_tx(&bars[st], bytes);
-        if (L.nseg == 1 && L.ldg == L.m) {
-            bulk_g2s(dst, G + g.r0 * L.m * GSZ, bytes, &bars[st], policy);
-        } else {
-            for (int r = 0; r < g.Rr; ++r)
-                bulk_g2s(dst + r * sw * GSZ, G + ((g.r0 + r) * L.ldg + g.c0) * GSZ, (uint32_t)(sw * GSZ), &bars[st],
-                         policy);
-        }
-    };
 
     if (tid == 0) {
-        for (int st = 0; st < K3_STAGES; ++st) mbar_init(&bars[st], 1);
+        for (int st = 0; st < K3_STAGES; ++st) {
+            mbar_init(&full[st], 1);
+            mbar_init(&empty[st], K3_NCW);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        s_bad = 0;
-        for (int st = 0; st < K3_STAGES; ++st) claim_issue(st);
     }
     __syncthreads();
 
-    uint32_t phases = 0;  // per-stage mbarrier parity (bit st)
-    int bad = 0;
+    if (warp < K3_STAGES) {
+        // ============ producers: warp st (one thread) owns stage arena st ============
+        if (lane != 0) return;
+        const int st = warp;
+        const uint64_t pol_first = evict_first_policy();
+        const uint64_t pol_last = evict_last_policy();
+        int hint = 0;
+        for (int it = 0;; ++it) {
+            // claim and look up the next unit before waiting for its arena
+            const uint32_t cl = atomicAdd(prm.claim, 1u) - prm.claim_base;
+            StageInfo si{};
+            si.u = (int64_t)cl < prm.total_units ? (int64_t)cl : -1;
+            const UpdLayer* Lp = nullptr;
+            UnitGeom g{};
+            if (si.u >= 0) {
+                hint = find_layer_from(table, si.u, hint);
+                si.li = hint;
+                Lp = &table[hint];
+                g = unit_geom(*Lp, si.u - Lp->unit_begin);
+                si.s0 = g.c0 == 0 ? 0 : (g.c0 >= Lp->m ? (int32_t)Lp->k : __ldg(Lp->prefix + (g.c0 >> 5)));
+                si.s1 = g.c1 >= Lp->m ? (int32_t)Lp->k : __ldg(Lp->prefix + (g.c1 >> 5));
+            }
+            if (it > 0) mbar_wait_sleep(&empty[st], (it - 1) & 1);
+            unsigned char* A = smem + st * K3_ARENA;
+            if (si.u < 0) {
+                info[st] = si;
+                mbar_arrive(&full[st]);
+                break;
+            }
+            const UpdLayer& L = *Lp;
+            const int sw = (int)(g.c1 - g.c0);
+            const int ns = si.s1 - si.s0;
+            uint32_t tx = 0;
+            int off = 0;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            // G tile
+            si.oG = 0;
+            if (L.tma_ok) {
+                const unsigned char* G = static_cast<const unsigned char*>(L.G);
+                if (L.nseg == 1 && L.ldg == L.m) {
+                    bulk_g2s(A, G + g.r0 * L.m * GSZ, (uint32_t)(g.Rr * sw * GSZ), &full[st], pol_first);
+                } else {
+                    for (int r = 0; r < g.Rr; ++r)
+                        bulk_g2s(A + r * sw * GSZ, G + ((g.r0 + r) * L.ldg + g.c0) * GSZ, (uint32_t)(sw * GSZ),
+                                 &full[st], pol_first);
+                }
+                tx += (uint32_t)(g.Rr * sw * GSZ);
+            } else {
+                GB* sG = reinterpret_cast<GB*>(A);
+                const GB* G = static_cast<const GB*>(L.G);
+                for (int r = 0; r < g.Rr; ++r)
+                    for (int c = 0; c < sw; ++c) sG[r * sw + c] = G[(g.r0 + r) * L.ldg + g.c0 + c];
+            }
+            off = (g.Rr * sw * GSZ + 15) & ~15;
+            // mask + prefix words of the segment
+            const int64_t w0 = g.c0 >> 5, nwm = (sw + 31) >> 5;
+            si.eMask = stage_words(A, &off, L.mask, w0, w0 + nwm, &full[st], &tx, &si.oMask);
+            si.ePre = stage_words(A, &off, L.prefix, w0, w0 + nwm, &full[st], &tx, &si.oPre);
+            if (prm.do_adam && ns > 0) {
+                si.pstaged = L.p_tma;
+                si.mstaged = L.mv_tma;
+                if (si.pstaged) {
+                    const unsigned char* P = static_cast<const unsigned char*>(L.P);
+                    si.oP = off;
+                    if (L.nseg == 1 && L.ldp == L.m) {
+                        bulk_g2s(A + off, P + g.r0 * L.m * PSZ, (uint32_t)(g.Rr * sw * PSZ), &full[st], pol_last);
+                    } else {
+                        for (int r = 0; r < g.Rr; ++r)
+                            bulk_g2s(A + off + r * sw * PSZ, P + ((g.r0 + r) * L.ldp + g.c0) * PSZ,
+                                     (uint32_t)(sw * PSZ), &full[st], pol_last);
+                    }
+                    tx += (uint32_t)(g.Rr * sw * PSZ);
+                    off += (g.Rr * sw * PSZ + 15) & ~15;
+                }
+                if (si.mstaged) {
+                    int64_t e0, e1;
+                    if (L.slot_src) {  // refresh: the old moments of the unit's rows (full old rows)
+                        e0 = g.r0 * L.k_in;
+                        e1 = (g.r0 + g.Rr) * L.k_in;
+                    } else {           // steady: the [R, s0:s1) slab (contiguous: full rows, or R == 1)
+                        e0 = g.r0 * L.k + si.s0;
+                        e1 = (g.r0 + g.Rr - 1) * L.k + si.s1;
+                    }
+                    si.eM = stage_words(A, &off, L.m_in, e0, e1, &full[st], &tx, &si.oM);
+                    si.eV = stage_words(A, &off, L.v_in, e0, e1, &full[st], &tx, &si.oV);
+                    si.eS = stage_words(A, &off, L.steps, si.s0, si.s1, &full[st], &tx, &si.oS);
+                    si.eIdx = stage_words(A, &off, L.idx, si.s0, si.s1, &full[st], &tx, &si.oIdx);
+                    if (L.slot_src) si.eSrc = stage_words(A, &off, L.slot_src, si.s0, si.s1, &full[st], &tx, &si.oSrc);
+                }
+            }
+            info[st] = si;
+            mbar_expect_tx(&full[st], tx);  // the single arrival of this phase
+        }
+        return;
+    }
+
+    // ===================== consumer warps =====================
+    // AdamW: the unit's (row, slot) pairs are spread over all consumer threads; their loads
+    // are issued first so that their latency (global p when not staged) overlaps the
+    // compaction.  Compaction: each warp takes one contiguous run of 256-column blocks
+    // (row-major over the unit's rows); lane l of a block owns its columns 8l..8l+7; the
+    // unselected values go to the warp buffer, flushed with aligned 16-byte stores after
+    // every block (the < 16-byte remainder carries over).
+    const int cw = warp - K3_STAGES;
+    const int ctid = cw * 32 + lane;
+    constexpr int NCT = K3_NCW * 32;
+    unsigned char* warea = smem + K3_STAGES * K3_ARENA + cw * K3_WARP_BYTES;
+    GB* wbuf = reinterpret_cast<GB*>(warea);
+    uint32_t nfacc = 0;                // non-finite detector (exponent all-ones -> carry into the top bit)
+    uint32_t finished = 0, phase = 0;  // per stage: end sentinel seen / mbarrier parity
+
     for (int it = 0;; ++it) {
         const int st = it % K3_STAGES;
-        const int64_t u = st_unit[st];
-        if (u < 0) break;
-        const int li = st_layer[st];
-        const UpdLayer& L = table[li];
-        const UnitGeom g = unit_geom(L, u - L.unit_begin);
-        const int64_t sw = g.c1 - g.c0;
-        GB* sG = reinterpret_cast<GB*>(stage_buf + st * K3_STAGE_BYTES);
-        const bool tma = L.tma_ok;
-        if (tma) {
-            mbar_wait(&bars[st], (phases >> st) & 1u);
-            phases ^= 1u << st;
-        } else {
-            const GB* G = static_cast<const GB*>(L.G);
-            for (int64_t q = tid; q < (int64_t)g.Rr * sw; q += K3_THREADS) {
-                const int64_t r = q / sw, c = q - r * sw;
-                sG[q] = G[(g.r0 + r) * L.ldg + g.c0 + c];
-            }
-            __syncthreads();
+        if ((finished >> st) & 1u) continue;
+        mbar_wait(&full[st], (phase >> st) & 1u);
+        phase ^= 1u << st;
+        const StageInfo si = info[st];
+        if (si.u < 0) {  // this stage's producer ran out of units; others may still hold some
+            finished |= 1u << st;
+            if (finished == (1u << K3_STAGES) - 1u) break;
+            continue;
         }
+        const UpdLayer& L = table[si.li];
+        if (prm.debug_mode == 1) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+            continue;
+        }
+        const UnitGeom g = unit_geom(L, si.u - L.unit_begin);
+        const int sw = (int)(g.c1 - g.c0);
+        unsigned char* A = smem + st * K3_ARENA;
+        const GB* sG = reinterpret_cast<const GB*>(A + si.oG);
+        const PB* sP = reinterpret_cast<const PB*>(A + si.oP);
+        const float* sM = reinterpret_cast<const float*>(A + si.oM) + si.eM;
+        const float* sV = reinterpret_cast<const float*>(A + si.oV) + si.eV;
+        const int32_t* sS = reinterpret_cast<const int32_t*>(A + si.oS) + si.eS;
+        const int32_t* sSrc = reinterpret_cast<const int32_t*>(A + si.oSrc) + si.eSrc;
+        const int32_t* sIdx = reinterpret_cast<const int32_t*>(A + si.oIdx) + si.eIdx;
+        const uint32_t* smask = reinterpret_cast<const uint32_t*>(A + si.oMask) + si.eMask;
+        const int32_t* spre = reinterpret_cast<const int32_t*>(A + si.oPre) + si.ePre;
+        const int k = (int)L.k;
+        const int kin = (int)L.k_in;
+        const int64_t mk = L.m - L.k;
+        const bool remap = L.slot_src != nullptr;
+        PB* Pbase = static_cast<PB*>(L.P);
 
-        const int64_t k = L.k, m = L.m, mk = m - k;
-        const int64_t s0 = sel_before(L, g.c0), s1 = sel_before(L, g.c1);
-        const int64_t ns = s1 - s0;           // selected columns in the segment
-        const int64_t u0 = g.c0 - s0;         // compact position of the segment's first unselected column
-        const int64_t nu = sw - ns;           // unselected columns in the segment
-        const int64_t o_base = g.r0 * mk + u0;
-        const int head = (int)(o_base % VEC);
-
-        // ---- AdamW pair loads (batch 0), issued before compaction to overlap latency
-        const int64_t npairs = prm.do_adam ? (int64_t)g.Rr * ns : 0;
-        float ag[K3_BATCH], ap[K3_BATCH], am[K3_BATCH], av[K3_BATCH];
-        int32_t at[K3_BATCH];
-        int64_t pidx[K3_BATCH], midx[K3_BATCH];
-        const PB* Pin = static_cast<const PB*>(L.P);
-        auto load_batch = [&](int64_t qb) {
+        // ---------------- AdamW pair loads (first batch) ----------------
+        const int ns = si.s1 - si.s0;
+        const int npairs = (prm.do_adam && prm.debug_mode == 0) ? g.Rr * ns : 0;
+        const float inv_ns = ns > 0 ? 1.0f / (float)ns : 0.0f;
+        float ag[K3_PAIRS], ap[K3_PAIRS], am[K3_PAIRS], av[K3_PAIRS];
+        int32_t at[K3_PAIRS];
+        int32_t pidx[K3_PAIRS], midx[K3_PAIRS];  // relative to the unit's first row of p / moments
+        PB* Prow0 = Pbase + g.r0 * L.ldp;
+        float* Mrow0 = L.m_out + g.r0 * k;
+        float* Vrow0 = L.v_out + g.r0 * k;
+        auto load_pairs = [&](int qb) {
 #pragma unroll
-            for (int b = 0; b < K3_BATCH; ++b) {
-                const int64_t q = qb + (int64_t)b * K3_THREADS + tid;
+            for (int b = 0; b < K3_PAIRS; ++b) {
+                const int q = qb + b * NCT + ctid;
                 pidx[b] = -1;
                 if (q < npairs) {
-                    const int64_t r = q / ns, sl = q - r * ns;
-                    const int64_t s = s0 + sl;
-                    const int32_t c = __ldg(L.idx + s);
+                    int r = __float2int_rz((float)q * inv_ns);
+                    if (r * ns > q) --r;
+                    if ((r + 1) * ns <= q) ++r;
+                    const int sl = q - r * ns;
+                    const int s = si.s0 + sl;
                     const int64_t row = g.r0 + r;
-                    ag[b] = GE::to_f(sG[r * sw + (c - g.c0)]);
-                    pidx[b] = row * L.ldp + c;
-                    ap[b] = PE::to_f(Pin[pidx[b]]);
-                    midx[b] = row * k + s;
-                    if (L.slot_src) {
-                        const int32_t src = __ldg(L.slot_src + s);
-                        am[b] = src >= 0 ? __ldcs(L.m_in + row * L.k_in + src) : 0.0f;
-                        av[b] = src >= 0 ? __ldcs(L.v_in + row * L.k_in + src) : 0.0f;
+                    const int c = si.mstaged ? sIdx[sl] : __ldg(L.idx + s);
+                    const int cl = c - (int)g.c0;
+                    ag[b] = GE::to_f(sG[r * sw + cl]);
+                    pidx[b] = r * (int)L.ldp + c;
+                    ap[b] = si.pstaged ? PE::to_f(sP[r * sw + cl]) : PE::to_f(Prow0[pidx[b]]);
+                    midx[b] = r * k + s;
+                    if (si.mstaged) {
+                        if (remap) {
+                            const int32_t src = sSrc[sl];
+                            am[b] = src >= 0 ? sM[r * kin + src] : 0.0f;
+                            av[b] = src >= 0 ? sV[r * kin + src] : 0.0f;
+                        } else {
+                            am[b] = sM[r * k + sl];
+                            av[b] = sV[r * k + sl];
+                        }
+                        at[b] = sS[sl];
                     } else {
-                        am[b] = __ldcs(L.m_in + midx[b]);
-                        av[b] = __ldcs(L.v_in + midx[b]);
+                        if (remap) {
+                            const int32_t src = __ldg(L.slot_src + s);
+                            am[b] = src >= 0 ? __ldcs(L.m_in + row * kin + src) : 0.0f;
+                            av[b] = src >= 0 ? __ldcs(L.v_in + row * kin + src) : 0.0f;
+                        } else {
+                            am[b] = __ldcs(L.m_in + row * k + s);
+                            av[b] = __ldcs(L.v_in + row * k + s);
+                        }
+                        at[b] = __ldg(L.steps + s);
                     }
-                    at[b] = __ldg(L.steps + s) + 1;
                 }
             }
         };
-        auto compute_store = [&]() {
-            PB* Pout = static_cast<PB*>(L.P);
+        auto compute_pairs = [&]() {
 #pragma unroll
-            for (int b = 0; b < K3_BATCH; ++b) {
+            for (int b = 0; b < K3_PAIRS; ++b) {
                 if (pidx[b] < 0) continue;
                 float p = ap[b], mm = am[b], vv = av[b];
-                adamw_elem(ag[b], p, mm, vv, at[b], prm.adam);
-                Pout[pidx[b]] = PE::from_f(p);
-                __stcs(L.m_out + midx[b], mm);
-                __stcs(L.v_out + midx[b], vv);
+                adamw_elem(ag[b], p, mm, vv, at[b] + prm.step_delta + 1, prm.adam);
+                Prow0[pidx[b]] = PE::from_f(p);
+                __stcs(Mrow0 + midx[b], mm);
+                __stcs(Vrow0 + midx[b], vv);
             }
         };
-        if (npairs > 0) load_batch(0);
+        if (npairs > 0) load_pairs(0);
 
-        // ---- compaction into the shared output tile (+ non-finite scan of the whole tile)
-        if (prm.do_compact) {
-            const int64_t nw = (sw + 31) >> 5;
-            const int64_t items = (int64_t)g.Rr * nw;
-            const int64_t wbase = g.c0 >> 5;
-            for (int64_t itm = warp; itm < items; itm += K3_WARPS) {
-                const int64_t r = itm / nw, gw = itm - r * nw;
-                const int64_t cl = gw * 32 + lane;  // column within the segment
-                const uint32_t word = __ldg(L.mask + wbase + gw);
-                const int32_t pre = __ldg(L.prefix + wbase + gw);
-                if (cl < sw) {
-                    const GB x = sG[r * sw + cl];
-                    bad |= GE::nonfinite(x);
-                    if (!((word >> lane) & 1u)) {
-                        const int64_t cpos = (g.c0 + cl) - (pre + __popc(word & lanemask_lt()));  // compact column
-                        sOut[head + r * nu + (cpos - u0)] = x;
-                    }
-                }
-            }
-        }
-        if (npairs > 0) {
-            compute_store();
-            for (int64_t qb = (int64_t)K3_BATCH * K3_THREADS; qb < npairs; qb += (int64_t)K3_BATCH * K3_THREADS) {
-                load_batch(qb);
-                compute_store();
-            }
-        }
-        __syncthreads();
+        // ---------------- compaction ----------------
+        const int nblk = (sw + K3_CHUNK - 1) / K3_CHUNK;
+        const int nq = g.Rr * nblk;
+        const int q0 = (int)(((int64_t)nq * cw) / K3_NCW), q1 = (int)(((int64_t)nq * (cw + 1)) / K3_NCW);
+        const bool vec = (sw % 8) == 0;  // rows of the staged tile are 16-byte aligned
+        GB* outp = static_cast<GB*>(L.out);
+        int r = q0 / max(nblk, 1), cc = q0 - r * nblk;
+        int64_t obase = 0;   // global element index of wbuf[0] (16-byte aligned)
+        int pend = 0;        // elements in wbuf (including `skip` leading ones we do not own)
+        int skip = 0;
 
-        // ---- stream the compact tile out: aligned 16-byte stores, scalar edges
-        if (prm.do_compact) {
-            const int64_t total = (int64_t)g.Rr * nu;
-            GB* out = static_cast<GB*>(L.out);
-            const int64_t a0 = o_base - head;                      // aligned start (elements)
-            const int64_t nch = (head + total + VEC - 1) / VEC;    // 16-byte chunks
-            for (int64_t ch = tid; ch < nch; ch += K3_THREADS) {
-                const int64_t lo = ch * VEC;                       // index into sOut
-                if (lo >= head && lo + VEC <= head + total) {
-                    st_cs_v4(out + a0 + lo, *reinterpret_cast<const uint4*>(sOut + lo));
+        auto flush_out = [&](bool final_) {
+            const int nfull = final_ ? (pend + VEC - 1) / VEC : pend / VEC;
+            for (int ch = lane; ch < nfull; ch += 32) {
+                const int lo = ch * VEC;
+                if (lo >= skip && lo + VEC <= pend) {
+                    st_cs_v4(outp + obase + lo, lds128(wbuf + lo));
                 } else {
 #pragma unroll
                     for (int e = 0; e < VEC; ++e) {
-                        const int64_t q = lo + e;
-                        if (q >= head && q < head + total) out[a0 + q] = sOut[q];
+                        const int qq = lo + e;
+                        if (qq >= skip && qq < pend) outp[obase + qq] = wbuf[qq];
                     }
                 }
             }
-        }
-        __syncthreads();  // stage st and sOut free; all stores of this unit issued
+            __syncwarp();
+            if (!final_) {  // carry the partial last chunk to the front
+                const int rem = pend - nfull * VEC;
+                GB v = 0;
+                if (lane < rem) v = wbuf[nfull * VEC + lane];
+                __syncwarp();
+                if (lane < rem) sts_elem(wbuf + lane, v);
+                obase += nfull * VEC;
+                pend = rem;
+                if (nfull > 0) skip = 0;
+            }
+            __syncwarp();
+        };
+        auto start_row = [&]() {
+            const int cl0 = cc * K3_CHUNK;
+            const int64_t gpos = (g.r0 + r) * mk + (g.c0 + cl0 - spre[cl0 >> 5]);
+            skip = (int)(gpos % VEC);
+            obase = gpos - skip;
+            pend = skip;
+        };
 
-        // ---- completion: layer counter, step counts, next claim
-        if (warp == 0) {
-            uint32_t last = 0;
-            if (lane == 0) {
-                if (L.done) {
-                    __threadfence_system();
-                    const uint32_t old = atomicAdd(L.done, 1u);
-                    last = (old + 1u == (prm.epoch + 1u) * (uint32_t)L.units);
+        if (q0 < q1) start_row();
+        for (int q = q0; q < q1; ++q) {
+            const int cl0 = cc * K3_CHUNK, cl1 = min(sw, cl0 + K3_CHUNK);
+            const GB* srow = sG + r * sw;
+            const int c8 = cl0 + 8 * lane;
+            const int nval = max(0, min(8, cl1 - c8));
+            const uint32_t word = nval > 0 ? smask[c8 >> 5] : 0u;
+            const int sh = c8 & 31;
+            const uint32_t vmask = (1u << nval) - 1u;
+            const uint32_t selb = (word >> sh) & vmask;  // selected among my columns
+            // selected columns of this block before my first column
+            const int selblk = nval > 0 ? (spre[c8 >> 5] - spre[cl0 >> 5]) + __popc(word & ((1u << sh) - 1u)) : 0;
+            const int blk_keep = (cl1 - cl0) - (int)__reduce_add_sync(0xffffffffu, (unsigned)__popc(selb));
+            GB x[8];
+            if (nval == 8 && vec) {
+                uint32_t w[NW8];
+                load8<GDT>(srow + c8, w);
+#pragma unroll
+                for (int i = 0; i < NW8; ++i) {
+                    if constexpr (GSZ == 2) nfacc |= (w[i] & 0x7f807f80u) + 0x00800080u;
+                    else nfacc |= (w[i] & 0x7f800000u) + 0x00800000u;
                 }
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                claim_issue(st);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    if constexpr (GSZ == 2) x[e] = (GB)(w[e >> 1] >> (16 * (e & 1)));
+                    else x[e] = (GB)w[e];
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    x[e] = e < nval ? srow[c8 + e] : (GB)0;
+                    if (e < nval) {
+                        if constexpr (GSZ == 2) nfacc |= ((uint32_t)x[e] & 0x7f80u) + 0x0080u;
+                        else nfacc |= ((uint32_t)x[e] & 0x7f800000u) + 0x00800000u;
+                    }
+                }
             }
-            last = __shfl_sync(0xffffffffu, last, 0);
-            if (last && prm.do_adam && L.steps_out) {
-                __threadfence();
-                for (int64_t s = lane; s < k; s += 32) L.steps_out[s] = __ldcg(L.steps + s) + 1;
+            int u = pend + 8 * lane - selblk;
+            const uint32_t keep = ~selb & vmask;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                if ((keep >> e) & 1u) sts_elem(wbuf + u++, x[e]);
             }
+            __syncwarp();
+            pend += blk_keep;
+            const bool row_end = (cc + 1 == nblk) || (q + 1 == q1);
+            flush_out(row_end);
+            if (++cc == nblk) {
+                cc = 0;
+                ++r;
+                if (q + 1 < q1) start_row();
+            }
+        }
+
+        // ---------------- AdamW compute + stores (then any further pair batches) ----------------
+        if (npairs > 0) {
+            compute_pairs();
+            for (int qb = K3_PAIRS * NCT; qb < npairs; qb += K3_PAIRS * NCT) {
+                load_pairs(qb);
+                compute_pairs();
+            }
+        }
+        // stage fully consumed by this warp
+        __syncwarp();
+        if (lane == 0) {
+            mbar_arrive(&empty[st]);
+            if (L.done) red_release_add(L.done, 1u);  // per-warp completion count (offload only)
         }
     }
-    if (bad) s_bad = 1;
-    __syncthreads();
-    if (tid == 0 && s_bad && prm.nonfinite) *prm.nonfinite = 1;
+    if (prm.nonfinite) {
+        const uint32_t hit = GSZ == 2 ? (nfacc & 0x80008000u) : (nfacc & 0x80000000u);
+        if (__any_sync(0xffffffffu, hit != 0) && lane == 0) *prm.nonfinite = 1;
+    }
 }
 
 // Stateless AdamW-only form: (row, slot) pairs, G read at the selected columns only.
@@ -370,7 +604,13 @@ void set_attr() {
 
 }  // namespace
 
-int update_stage_bytes() { return K3_STAGE_BYTES; }
+UpdLimits update_limits() {
+    UpdLimits l;
+    l.arena_bytes = K3_ARENA;
+    l.consumer_warps = K3_NCW;
+    l.producers = K3_STAGES;
+    return l;
+}
 
 int update_grid(int, int) {
     int dev = 0, sms = NUM_SMS_B200;
@@ -381,10 +621,10 @@ int update_grid(int, int) {
 cudaError_t launch_update(const UpdParams& p, int gdt, int pdt, int grid, cudaStream_t s) {
     if (p.total_units <= 0) return cudaSuccess;
     int g = (int)zmin<int64_t>((int64_t)grid, p.total_units);
-#define ZF_LAUNCH(GD, PD)                                                                   \
-    do {                                                                                    \
-        set_attr<GD, PD>();                                                                 \
-        k_update<GD, PD><<<g, K3_THREADS, K3_SMEM, s>>>(p);                                 \
+#define ZF_LAUNCH(GD, PD)                                            \
+    do {                                                             \
+        set_attr<GD, PD>();                                          \
+        k_update<GD, PD><<<g, K3_THREADS, K3_SMEM, s>>>(p);          \
     } while (0)
     if (gdt == DT_BF16 && pdt == DT_BF16) ZF_LAUNCH(DT_BF16, DT_BF16);
     else if (gdt == DT_F32 && pdt == DT_F32) ZF_LAUNCH(DT_F32, DT_F32);

@@ -180,19 +180,44 @@ struct K3Geom {
     int64_t seg_cols;
     int32_t nseg, R;
     int64_t units;
+    bool mv_ok;
 };
 
-K3Geom k3_geom(int64_t n, int64_t m, int gsz) {
+// p tile staging pays off when most 32-byte sectors of a row hold a selected column
+bool k3_p_dense(int64_t m, int64_t k, int psz) {
+    const double frac = (double)k / (double)m;
+    return 1.0 - std::pow(1.0 - frac, 32.0 / psz) >= 0.5;
+}
+
+// Worst-case bytes one K3 unit stages (R rows x c columns): G tile, p tile (if dense),
+// mask + prefix words, moment slabs (R*k: also covers the old rows of a refresh),
+// step counts and remap sources; each as a 16-byte-granular superset.
+int64_t k3_unit_bytes(int64_t R, int64_t c, int64_t k, int gsz, int psz, bool p_dense, bool mv) {
+    auto a16 = [](int64_t b) { return (b + 15) & ~int64_t(15); };
+    int64_t b = a16(R * c * gsz) + 2 * ((c + 31) / 32 + 8) * 4;
+    if (p_dense) b += a16(R * c * psz);
+    if (mv) b += 2 * (R * k + 8) * 4 + 3 * (std::min(c, k) + 8) * 4;  // moments; steps, sources, idx
+    return b;
+}
+
+K3Geom k3_geom(int64_t n, int64_t m, int64_t k, int gsz, int psz, bool p_dense, bool adam = true) {
+    const UpdLimits lim = update_limits();
+    const int64_t A = lim.arena_bytes;
     K3Geom g{};
-    const int64_t tile = update_stage_bytes() / gsz;  // elements per staged tile
-    if (m <= tile) {
+    // moments staged unless even one row's old moments cannot fit next to a minimal tile
+    g.mv_ok = adam && k3_unit_bytes(1, std::min<int64_t>(m, 128), k, gsz, psz, p_dense, true) <= A;
+    g.R = 1;
+    if (k3_unit_bytes(1, m, k, gsz, psz, p_dense, g.mv_ok) <= A) {
         g.seg_cols = m;
         g.nseg = 1;
-        g.R = (int32_t)std::max<int64_t>(1, std::min<int64_t>(tile / m, n));
+        int64_t R = 1;
+        while (R < std::min<int64_t>(n, 127) && k3_unit_bytes(R + 1, m, k, gsz, psz, p_dense, g.mv_ok) <= A) ++R;
+        g.R = (int32_t)R;
     } else {
-        g.seg_cols = (tile / 32) * 32;
-        g.nseg = (int32_t)((m + g.seg_cols - 1) / g.seg_cols);
-        g.R = 1;
+        int64_t c = 128;  // segments start 16-byte aligned in the mask/prefix words
+        while (c + 128 < m && k3_unit_bytes(1, c + 128, k, gsz, psz, p_dense, g.mv_ok) <= A) c += 128;
+        g.seg_cols = c;
+        g.nseg = (int32_t)((m + c - 1) / c);
     }
     g.units = ((n + g.R - 1) / g.R) * g.nseg;
     return g;
@@ -306,7 +331,7 @@ extern "C" zf_status zf_topk_columns(const float* norms, int64_t m, int64_t k, i
     const int64_t W = (m + 31) / 32;
     ZF_TRY(sc.get(&L.mask, W * sizeof(uint32_t), false));
     ZF_TRY(sc.get(&L.prefix, W * sizeof(int32_t), false));
-    ZF_CUDA(launch_topk(t, m, nullptr, s));
+    ZF_CUDA(launch_topk(t, m, 0, nullptr, s));
     return ZF_OK;
 }
 
@@ -349,12 +374,12 @@ extern "C" zf_status zf_compact_unselected(const void* G, zf_dtype gdt, int64_t 
     uint32_t* mask = nullptr;
     int32_t* prefix = nullptr;
     int32_t* bad = nullptr;
-    ZF_TRY(sc.get(&mask, W * sizeof(uint32_t), false));
-    ZF_TRY(sc.get(&prefix, W * sizeof(int32_t), false));
+    ZF_TRY(sc.get(&mask, (W + 8) * sizeof(uint32_t), true));    // padded: K3 stages words in 16-byte groups
+    ZF_TRY(sc.get(&prefix, (W + 8) * sizeof(int32_t), true));
     ZF_TRY(sc.get(&bad, sizeof(int32_t), true));
     ZF_TRY(sc.get(&prm.claim, sizeof(uint32_t), true));
     ZF_CUDA(launch_build_mask(idx, k, m, mask, prefix, bad, s));
-    const K3Geom geo = k3_geom(n, m, gsz);
+    const K3Geom geo = k3_geom(n, m, k, gsz, gsz, false, false);
     L.G = G;
     L.n = n;
     L.m = m;
@@ -486,7 +511,11 @@ struct zf_ctx {
     int32_t* nonfinite_d = nullptr;
     uint32_t* claim = nullptr;
     uint32_t* done = nullptr;  // [n_layers]
-    uint32_t claim_base = 0, epoch = 0;
+    uint32_t claim_base = 0;
+    int32_t since = 0;            // K3 launches since the last refresh (step-count delta)
+    std::vector<uint32_t> done_target;  // expected per-layer completion count after the last step
+    cudaStream_t aux = nullptr;   // inspection copies (zf_optimizer_state)
+    std::vector<int32_t*> steps_view;
     int grid = 148;
     // launch tables
     NormLayer* d_norm_tab = nullptr;
@@ -609,6 +638,7 @@ zf_ctx::~zf_ctx() {
     if (step_done) cudaEventDestroy(step_done);
     if (k3_done) cudaEventDestroy(k3_done);
     if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (aux) cudaStreamDestroy(aux);
 }
 
 // H1: accumulate each layer's staged compact block into the window's fp32 buffer
@@ -739,14 +769,14 @@ zf_status build_tables(zf_ctx* c) {
             t.slot_src = refresh ? l.slot_src : nullptr;
             t.k_in = l.k;
             t.steps = l.steps[nw];
-            t.steps_out = l.steps[nw];
             t.out = l.stage_dev[sb < c->n_stage ? sb : 0];
-            t.done = c->done + i;
+            t.done = c->cfg.offload ? c->done + i : nullptr;
             t.seg_cols = l.geo.seg_cols;
             t.nseg = l.geo.nseg;
             t.R = l.geo.R;
             t.units = l.geo.units;
             t.unit_begin = l.unit_begin;
+            t.mv_tma = l.geo.mv_ok ? 1 : 0;
         }
         ZF_TRY(c->dalloc(&c->d_upd_tab[v], nl * sizeof(UpdLayer)));
         c->up_upd_tab[v].assign(nl, UpdLayer{});
@@ -834,7 +864,7 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
         c->total_m += l.d.m;
         c->max_m = std::max(c->max_m, l.d.m);
         c->k1_units += (int64_t)l.nrb * l.ncb;
-        l.geo = k3_geom(l.d.n, l.d.m, c->gsz);
+        l.geo = k3_geom(l.d.n, l.d.m, l.k, c->gsz, c->psz, k3_p_dense(l.d.m, l.k, c->psz));
         l.unit_begin = c->k3_units;
         c->k3_units += l.geo.units;
     }
@@ -848,14 +878,15 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
         if (l.nrb > 1) ZF_CTRY(c->dalloc(&l.partial, (size_t)l.nrb * l.d.m * sizeof(float), false));
         ZF_CTRY(c->dalloc(&l.k1_counter, l.ncb * sizeof(uint32_t)));
         for (int s = 0; s < 2; ++s) {
-            ZF_CTRY(c->dalloc(&l.idx[s], k * sizeof(int32_t)));
-            ZF_CTRY(c->dalloc(&l.mask[s], l.W * sizeof(uint32_t)));
-            ZF_CTRY(c->dalloc(&l.prefix[s], l.W * sizeof(int32_t)));
-            ZF_CTRY(c->dalloc(&l.steps[s], k * sizeof(int32_t)));
-            ZF_CTRY(c->dalloc(&l.mom[s], (size_t)n * k * sizeof(float)));
-            ZF_CTRY(c->dalloc(&l.vel[s], (size_t)n * k * sizeof(float)));
+            ZF_CTRY(c->dalloc(&l.idx[s], (k + 16) * sizeof(int32_t)));  // padded (K3 bulk copies)
+            ZF_CTRY(c->dalloc(&l.mask[s], (l.W + 8) * sizeof(uint32_t)));   // padded (K3 bulk copies)
+            ZF_CTRY(c->dalloc(&l.prefix[s], (l.W + 8) * sizeof(int32_t)));
+            // padded by 16 elements: K3 stages these with 16-byte-granular bulk copies
+            ZF_CTRY(c->dalloc(&l.steps[s], (k + 16) * sizeof(int32_t)));
+            ZF_CTRY(c->dalloc(&l.mom[s], ((size_t)n * k + 16) * sizeof(float)));
+            ZF_CTRY(c->dalloc(&l.vel[s], ((size_t)n * k + 16) * sizeof(float)));
         }
-        ZF_CTRY(c->dalloc(&l.slot_src, k * sizeof(int32_t)));
+        ZF_CTRY(c->dalloc(&l.slot_src, (k + 16) * sizeof(int32_t)));
         for (int s = 0; s < c->n_stage; ++s) ZF_CTRY(c->dalloc(&l.stage_dev[s], (size_t)n * l.mk * c->gsz, false));
     }
     {
@@ -887,6 +918,13 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
         c->adam.bc2_len = (int)h.size();
     }
     ZF_CTRY(build_tables(c));
+    c->done_target.assign(n_layers, 0u);
+    ZF_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+    for (auto& l : c->L) {
+        int32_t* v = nullptr;
+        ZF_CTRY(c->dalloc(&v, l.k * sizeof(int32_t)));
+        c->steps_view.push_back(v);
+    }
     ZF_CUDA(cudaEventCreateWithFlags(&c->step_done, cudaEventDisableTiming));
     ZF_CUDA(cudaEventCreateWithFlags(&c->k3_done, cudaEventDisableTiming));
     // ---- offload: copy stream, pinned host staging, per-layer events, host accumulators
@@ -958,6 +996,8 @@ zf_status refresh_pointer_tables(zf_ctx* c, int variant, bool refresh, void* con
         h[i].G = grads[i];
         h[i].P = params[i];
         h[i].tma_ok = k3_tma_ok(grads[i], c->L[i].d.ld_grad, c->L[i].d.m, c->gsz);
+        h[i].p_tma = k3_tma_ok(params[i], c->L[i].d.ld_param, c->L[i].d.m, c->psz) &&
+                     k3_p_dense(c->L[i].d.m, c->L[i].k, c->psz);
     }
     if (std::memcmp(h.data(), c->up_upd_tab[variant].data(), nl * sizeof(UpdLayer)) != 0) {
         ZF_TRY(c->upload(c->d_upd_tab[variant], h.data(), nl * sizeof(UpdLayer), s));
@@ -989,6 +1029,7 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t, void* const* grads, void* con
     ZF_TRY(refresh_pointer_tables(c, variant, refresh, grads, params, s));
 
     if (c->cfg.offload) {
+        // (K3 counts per-layer completions only when offloading; see build_tables)
         // the device staging buffer sb is free once the D2H copies issued two steps ago finished
         if (c->d2h_issued[sb]) ZF_CUDA(cudaStreamWaitEvent(s, c->d2h_all[sb], 0));
         if (c->cfg.host_accumulate) {
@@ -1015,7 +1056,8 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t, void* const* grads, void* con
         tk.dev = c->have_sel ? c->d_topk_tab[c->cur ^ 1] : c->d_topk_tab[2];
         tk.n = nl;
         ZF_TRY(c->prof_begin(2, s, &pe));
-        ZF_CUDA(launch_topk(tk, c->max_m, c->nonfinite_d, s));
+        ZF_CUDA(launch_topk(tk, c->max_m, c->since, c->nonfinite_d, s));
+        c->since = 0;
         ZF_TRY(c->prof_end(&pe, s));
         c->launches++;
     }
@@ -1026,19 +1068,24 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t, void* const* grads, void* con
     prm.total_units = c->k3_units;
     prm.claim = c->claim;
     prm.claim_base = c->claim_base;
-    prm.epoch = c->epoch;
+    prm.step_delta = c->since;
     prm.do_adam = 1;
     prm.do_compact = 1;
     prm.nonfinite = c->nonfinite_d;
     prm.adam = c->adam;
+    {
+        static const int dbg = getenv("ZF_K3_DEBUG_MODE") ? atoi(getenv("ZF_K3_DEBUG_MODE")) : 0;
+        prm.debug_mode = dbg;
+    }
     const int grid = (int)std::min<int64_t>(c->grid, c->k3_units);
     zf_ctx::Pending pe3;
     ZF_TRY(c->prof_begin(3, s, &pe3));
     ZF_CUDA(launch_update(prm, c->gdt, c->pdt, grid, s));
     ZF_TRY(c->prof_end(&pe3, s));
     c->launches++;
-    c->claim_base += (uint32_t)(c->k3_units + grid);
-    c->epoch += 1;
+    c->claim_base += (uint32_t)(c->k3_units + (int64_t)grid * update_limits().producers);
+    c->since += 1;
+    for (int i = 0; i < nl; ++i) c->done_target[i] += (uint32_t)c->L[i].geo.units * (uint32_t)update_limits().consumer_warps;
     if (refresh) {
         c->cur ^= 1;
         c->have_sel = true;
@@ -1052,7 +1099,7 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t, void* const* grads, void* con
         for (int i = 0; i < nl; ++i) {
             LayerState& l = c->L[i];
             if (c->wait_value) {
-                const uint32_t target = c->epoch * (uint32_t)l.geo.units;
+                const uint32_t target = c->done_target[i];
                 CUresult r = c->wait_value(reinterpret_cast<CUstream>(c->copy_stream),
                                            reinterpret_cast<CUdeviceptr>(c->done + i), target,
                                            CU_STREAM_WAIT_VALUE_GEQ);
@@ -1118,7 +1165,14 @@ extern "C" zf_status zf_optimizer_state(zf_ctx* c, int32_t layer, const float** 
     const LayerState& l = c->L[layer];
     if (exp_avg) *exp_avg = l.mom[c->cur];
     if (exp_avg_sq) *exp_avg_sq = l.vel[c->cur];
-    if (step) *step = l.steps[c->cur];
+    if (step) {
+        // device keeps base counts at the last refresh; materialize base + delta
+        ZF_CUDA(cudaSetDevice(c->device));
+        ZF_CUDA(cudaEventSynchronize(c->step_done));
+        ZF_CUDA(launch_add_const(l.steps[c->cur], c->steps_view[layer], l.k, c->since, c->aux));
+        ZF_CUDA(cudaStreamSynchronize(c->aux));
+        *step = c->steps_view[layer];
+    }
     return ZF_OK;
 }
 
