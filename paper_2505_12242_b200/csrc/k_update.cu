@@ -42,7 +42,7 @@ namespace {
 constexpr int K3_NCW = 15;                        // consumer warps
 constexpr int K3_STAGES = 4;                      // stage arenas = producer warps (one chain per stage)
 constexpr int K3_THREADS = 32 * (K3_NCW + K3_STAGES);
-constexpr int K3_CHUNK = 256;                     // columns per warp chunk (32 lanes x 8)
+constexpr int K3_CHUNK = 512;                     // columns per warp block (32 lanes x 16)
 constexpr int K3_WBUF_BYTES = (K3_CHUNK + 16) * 4;
 constexpr int K3_WARP_BYTES = K3_WBUF_BYTES;
 constexpr int K3_PAIRS = 3;                       // AdamW (row, slot) pairs in flight per consumer thread
@@ -182,10 +182,22 @@ struct StageInfo {
     int64_t u;        // unit (-1: no more work)
     int32_t li;       // layer
     int32_t s0, s1;   // selected-slot range of the segment
-    int32_t oG, oP, oM, oV, oS, oSrc, oMask, oPre;
-    int32_t eM, eV, eS, eSrc, eMask, ePre;
-    int32_t oIdx, eIdx;
-    int32_t pstaged, mstaged;
+    int32_t oG, oP, oM, oV, oS, oSrc, oMask, oPre, oIdx;
+    int32_t eM, eV, eS, eSrc, eMask, ePre, eIdx;
+    int32_t pstaged, mstaged, remap;
+    // unit geometry and layer fields, so consumers never touch the global layer table
+    int32_t Rr, sw, k, kin, ldp;
+    int64_t r0, c0, mk;
+    void* P;                    // p + r0*ldp (row 0 of the unit)
+    void* out;                  // compact block of the layer
+    float* m_out;               // + r0*k
+    float* v_out;
+    const float* m_in;          // layer base (non-staged path)
+    const float* v_in;
+    const int32_t* steps;       // layer base (non-staged path)
+    const int32_t* slot_src;
+    const int32_t* idx;
+    uint32_t* done;
 };
 
 template <int DT>
@@ -318,6 +330,25 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
                     if (L.slot_src) si.eSrc = stage_words(A, &off, L.slot_src, si.s0, si.s1, &full[st], &tx, &si.oSrc);
                 }
             }
+            si.Rr = g.Rr;
+            si.sw = sw;
+            si.k = (int32_t)L.k;
+            si.kin = (int32_t)L.k_in;
+            si.ldp = (int32_t)L.ldp;
+            si.r0 = g.r0;
+            si.c0 = g.c0;
+            si.mk = L.m - L.k;
+            si.remap = L.slot_src != nullptr;
+            si.P = static_cast<PB*>(L.P) + g.r0 * L.ldp;
+            si.out = L.out;
+            si.m_out = L.m_out + g.r0 * L.k;
+            si.v_out = L.v_out + g.r0 * L.k;
+            si.m_in = L.m_in;
+            si.v_in = L.v_in;
+            si.steps = L.steps;
+            si.slot_src = L.slot_src;
+            si.idx = L.idx;
+            si.done = L.done;
             info[st] = si;
             mbar_expect_tx(&full[st], tx);  // the single arrival of this phase
         }
@@ -327,8 +358,8 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
     // ===================== consumer warps =====================
     // AdamW: the unit's (row, slot) pairs are spread over all consumer threads; their loads
     // are issued first so that their latency (global p when not staged) overlaps the
-    // compaction.  Compaction: each warp takes one contiguous run of 256-column blocks
-    // (row-major over the unit's rows); lane l of a block owns its columns 8l..8l+7; the
+    // compaction.  Compaction: each warp takes one contiguous run of 512-column blocks
+    // (row-major over the unit's rows); lane l of a block owns its columns 16l..16l+15; the
     // unselected values go to the warp buffer, flushed with aligned 16-byte stores after
     // every block (the < 16-byte remainder carries over).
     const int cw = warp - K3_STAGES;
@@ -344,47 +375,39 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
         if ((finished >> st) & 1u) continue;
         mbar_wait(&full[st], (phase >> st) & 1u);
         phase ^= 1u << st;
-        const StageInfo si = info[st];
+        const StageInfo& si = info[st];
         if (si.u < 0) {  // this stage's producer ran out of units; others may still hold some
             finished |= 1u << st;
             if (finished == (1u << K3_STAGES) - 1u) break;
             continue;
         }
-        const UpdLayer& L = table[si.li];
         if (prm.debug_mode == 1) {
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[st]);
             continue;
         }
-        const UnitGeom g = unit_geom(L, si.u - L.unit_begin);
-        const int sw = (int)(g.c1 - g.c0);
+        const int sw = si.sw, Rr = si.Rr;
         unsigned char* A = smem + st * K3_ARENA;
         const GB* sG = reinterpret_cast<const GB*>(A + si.oG);
-        const PB* sP = reinterpret_cast<const PB*>(A + si.oP);
-        const float* sM = reinterpret_cast<const float*>(A + si.oM) + si.eM;
-        const float* sV = reinterpret_cast<const float*>(A + si.oV) + si.eV;
-        const int32_t* sS = reinterpret_cast<const int32_t*>(A + si.oS) + si.eS;
-        const int32_t* sSrc = reinterpret_cast<const int32_t*>(A + si.oSrc) + si.eSrc;
-        const int32_t* sIdx = reinterpret_cast<const int32_t*>(A + si.oIdx) + si.eIdx;
         const uint32_t* smask = reinterpret_cast<const uint32_t*>(A + si.oMask) + si.eMask;
         const int32_t* spre = reinterpret_cast<const int32_t*>(A + si.oPre) + si.ePre;
-        const int k = (int)L.k;
-        const int kin = (int)L.k_in;
-        const int64_t mk = L.m - L.k;
-        const bool remap = L.slot_src != nullptr;
-        PB* Pbase = static_cast<PB*>(L.P);
 
         // ---------------- AdamW pair loads (first batch) ----------------
         const int ns = si.s1 - si.s0;
-        const int npairs = (prm.do_adam && prm.debug_mode == 0) ? g.Rr * ns : 0;
-        const float inv_ns = ns > 0 ? 1.0f / (float)ns : 0.0f;
+        const int npairs = (prm.do_adam && prm.debug_mode == 0) ? Rr * ns : 0;
         float ag[K3_PAIRS], ap[K3_PAIRS], am[K3_PAIRS], av[K3_PAIRS];
-        int32_t at[K3_PAIRS];
-        int32_t pidx[K3_PAIRS], midx[K3_PAIRS];  // relative to the unit's first row of p / moments
-        PB* Prow0 = Pbase + g.r0 * L.ldp;
-        float* Mrow0 = L.m_out + g.r0 * k;
-        float* Vrow0 = L.v_out + g.r0 * k;
+        int32_t at[K3_PAIRS], pidx[K3_PAIRS], midx[K3_PAIRS];  // p / moment offsets from the unit's row 0
         auto load_pairs = [&](int qb) {
+            const float inv_ns = 1.0f / (float)ns;
+            const int k = si.k, kin = si.kin, s0 = si.s0;
+            const bool pst = si.pstaged, mst = si.mstaged, remap = si.remap;
+            const PB* sP = reinterpret_cast<const PB*>(A + si.oP);
+            const float* sM = reinterpret_cast<const float*>(A + si.oM) + si.eM;
+            const float* sV = reinterpret_cast<const float*>(A + si.oV) + si.eV;
+            const int32_t* sS = reinterpret_cast<const int32_t*>(A + si.oS) + si.eS;
+            const int32_t* sSrc = reinterpret_cast<const int32_t*>(A + si.oSrc) + si.eSrc;
+            const int32_t* sIdx = reinterpret_cast<const int32_t*>(A + si.oIdx) + si.eIdx;
+            const int c0 = (int)si.c0;
 #pragma unroll
             for (int b = 0; b < K3_PAIRS; ++b) {
                 const int q = qb + b * NCT + ctid;
@@ -394,15 +417,14 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
                     if (r * ns > q) --r;
                     if ((r + 1) * ns <= q) ++r;
                     const int sl = q - r * ns;
-                    const int s = si.s0 + sl;
-                    const int64_t row = g.r0 + r;
-                    const int c = si.mstaged ? sIdx[sl] : __ldg(L.idx + s);
-                    const int cl = c - (int)g.c0;
+                    const int s = s0 + sl;
+                    const int c = mst ? sIdx[sl] : __ldg(si.idx + s);
+                    const int cl = c - c0;
                     ag[b] = GE::to_f(sG[r * sw + cl]);
-                    pidx[b] = r * (int)L.ldp + c;
-                    ap[b] = si.pstaged ? PE::to_f(sP[r * sw + cl]) : PE::to_f(Prow0[pidx[b]]);
+                    pidx[b] = r * si.ldp + c;
+                    ap[b] = pst ? PE::to_f(sP[r * sw + cl]) : PE::to_f(static_cast<const PB*>(si.P)[pidx[b]]);
                     midx[b] = r * k + s;
-                    if (si.mstaged) {
+                    if (mst) {
                         if (remap) {
                             const int32_t src = sSrc[sl];
                             am[b] = src >= 0 ? sM[r * kin + src] : 0.0f;
@@ -413,125 +435,119 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
                         }
                         at[b] = sS[sl];
                     } else {
+                        const int64_t row = si.r0 + r;
                         if (remap) {
-                            const int32_t src = __ldg(L.slot_src + s);
-                            am[b] = src >= 0 ? __ldcs(L.m_in + row * kin + src) : 0.0f;
-                            av[b] = src >= 0 ? __ldcs(L.v_in + row * kin + src) : 0.0f;
+                            const int32_t src = __ldg(si.slot_src + s);
+                            am[b] = src >= 0 ? __ldcs(si.m_in + row * kin + src) : 0.0f;
+                            av[b] = src >= 0 ? __ldcs(si.v_in + row * kin + src) : 0.0f;
                         } else {
-                            am[b] = __ldcs(L.m_in + row * k + s);
-                            av[b] = __ldcs(L.v_in + row * k + s);
+                            am[b] = __ldcs(si.m_in + row * k + s);
+                            av[b] = __ldcs(si.v_in + row * k + s);
                         }
-                        at[b] = __ldg(L.steps + s);
+                        at[b] = __ldg(si.steps + s);
                     }
                 }
             }
         };
         auto compute_pairs = [&]() {
+            PB* P = static_cast<PB*>(si.P);
+            float* Mo = si.m_out;
+            float* Vo = si.v_out;
 #pragma unroll
             for (int b = 0; b < K3_PAIRS; ++b) {
                 if (pidx[b] < 0) continue;
                 float p = ap[b], mm = am[b], vv = av[b];
                 adamw_elem(ag[b], p, mm, vv, at[b] + prm.step_delta + 1, prm.adam);
-                Prow0[pidx[b]] = PE::from_f(p);
-                __stcs(Mrow0 + midx[b], mm);
-                __stcs(Vrow0 + midx[b], vv);
+                P[pidx[b]] = PE::from_f(p);
+                __stcs(Mo + midx[b], mm);
+                __stcs(Vo + midx[b], vv);
             }
         };
         if (npairs > 0) load_pairs(0);
 
         // ---------------- compaction ----------------
         const int nblk = (sw + K3_CHUNK - 1) / K3_CHUNK;
-        const int nq = g.Rr * nblk;
-        const int q0 = (int)(((int64_t)nq * cw) / K3_NCW), q1 = (int)(((int64_t)nq * (cw + 1)) / K3_NCW);
+        const int nq = Rr * nblk;
+        const int q0 = (nq * cw) / K3_NCW, q1 = (nq * (cw + 1)) / K3_NCW;
         const bool vec = (sw % 8) == 0;  // rows of the staged tile are 16-byte aligned
-        GB* outp = static_cast<GB*>(L.out);
-        int r = q0 / max(nblk, 1), cc = q0 - r * nblk;
+        GB* outp = static_cast<GB*>(si.out);
+        int r = q0 / nblk, cc = q0 - r * nblk;
         int64_t obase = 0;   // global element index of wbuf[0] (16-byte aligned)
         int pend = 0;        // elements in wbuf (including `skip` leading ones we do not own)
         int skip = 0;
 
-        auto flush_out = [&](bool final_) {
-            const int nfull = final_ ? (pend + VEC - 1) / VEC : pend / VEC;
+        auto start_row = [&]() {
+            const int cl0 = cc * K3_CHUNK;
+            const int64_t gpos = (si.r0 + r) * si.mk + (si.c0 + cl0 - spre[cl0 >> 5]);
+            skip = (int)(gpos % VEC);
+            obase = gpos - skip;
+            pend = skip;
+        };
+        if (q0 < q1) start_row();
+        for (int q = q0; q < q1; ++q) {
+            const int cl0 = cc * K3_CHUNK, cl1 = min(sw, cl0 + K3_CHUNK);
+            const int c16 = cl0 + 16 * lane;
+            const int nval = max(0, min(16, cl1 - c16));
+            const uint32_t word = nval > 0 ? smask[c16 >> 5] : 0u;
+            const int sh = c16 & 31;
+            const uint32_t vmask = (1u << nval) - 1u;
+            const uint32_t selb = (word >> sh) & vmask;  // selected among my columns
+            const int selblk = nval > 0 ? (spre[c16 >> 5] - spre[cl0 >> 5]) + __popc(word & ((1u << sh) - 1u)) : 0;
+            const int blk_keep = (cl1 - cl0) - (int)__reduce_add_sync(0xffffffffu, (unsigned)__popc(selb));
+            const GB* src = sG + r * sw + c16;
+            int u = pend + 16 * lane - selblk;
+            const uint32_t keep = ~selb & vmask;
+            if (nval == 16 && vec) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    uint32_t w[NW8];
+                    load8<GDT>(src + 8 * h, w);
+#pragma unroll
+                    for (int i = 0; i < NW8; ++i) {
+                        if constexpr (GSZ == 2) nfacc |= (w[i] & 0x7f807f80u) + 0x00800080u;
+                        else nfacc |= (w[i] & 0x7f800000u) + 0x00800000u;
+                    }
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        GB x;
+                        if constexpr (GSZ == 2) x = (GB)(w[e >> 1] >> (16 * (e & 1)));
+                        else x = (GB)w[e];
+                        if ((keep >> (8 * h + e)) & 1u) sts_elem(wbuf + u++, x);
+                    }
+                }
+            } else {
+                for (int e = 0; e < nval; ++e) {
+                    const GB x = src[e];
+                    if constexpr (GSZ == 2) nfacc |= ((uint32_t)x & 0x7f80u) + 0x0080u;
+                    else nfacc |= ((uint32_t)x & 0x7f800000u) + 0x00800000u;
+                    if ((keep >> e) & 1u) sts_elem(wbuf + u++, x);
+                }
+            }
+            __syncwarp();
+            pend += blk_keep;
+            // flush: full 16-byte chunks (all at a row/run end), carry the partial remainder
+            const bool fin = (cc + 1 == nblk) || (q + 1 == q1);
+            const int nfull = fin ? (pend + VEC - 1) / VEC : pend / VEC;
             for (int ch = lane; ch < nfull; ch += 32) {
                 const int lo = ch * VEC;
                 if (lo >= skip && lo + VEC <= pend) {
                     st_cs_v4(outp + obase + lo, lds128(wbuf + lo));
                 } else {
-#pragma unroll
-                    for (int e = 0; e < VEC; ++e) {
-                        const int qq = lo + e;
-                        if (qq >= skip && qq < pend) outp[obase + qq] = wbuf[qq];
-                    }
+                    for (int e = max(lo, skip); e < min(lo + VEC, pend); ++e) outp[obase + e] = wbuf[e];
                 }
             }
             __syncwarp();
-            if (!final_) {  // carry the partial last chunk to the front
+            if (!fin) {
                 const int rem = pend - nfull * VEC;
                 GB v = 0;
                 if (lane < rem) v = wbuf[nfull * VEC + lane];
                 __syncwarp();
                 if (lane < rem) sts_elem(wbuf + lane, v);
+                __syncwarp();
                 obase += nfull * VEC;
                 pend = rem;
                 if (nfull > 0) skip = 0;
             }
-            __syncwarp();
-        };
-        auto start_row = [&]() {
-            const int cl0 = cc * K3_CHUNK;
-            const int64_t gpos = (g.r0 + r) * mk + (g.c0 + cl0 - spre[cl0 >> 5]);
-            skip = (int)(gpos % VEC);
-            obase = gpos - skip;
-            pend = skip;
-        };
-
-        if (q0 < q1) start_row();
-        for (int q = q0; q < q1; ++q) {
-            const int cl0 = cc * K3_CHUNK, cl1 = min(sw, cl0 + K3_CHUNK);
-            const GB* srow = sG + r * sw;
-            const int c8 = cl0 + 8 * lane;
-            const int nval = max(0, min(8, cl1 - c8));
-            const uint32_t word = nval > 0 ? smask[c8 >> 5] : 0u;
-            const int sh = c8 & 31;
-            const uint32_t vmask = (1u << nval) - 1u;
-            const uint32_t selb = (word >> sh) & vmask;  // selected among my columns
-            // selected columns of this block before my first column
-            const int selblk = nval > 0 ? (spre[c8 >> 5] - spre[cl0 >> 5]) + __popc(word & ((1u << sh) - 1u)) : 0;
-            const int blk_keep = (cl1 - cl0) - (int)__reduce_add_sync(0xffffffffu, (unsigned)__popc(selb));
-            GB x[8];
-            if (nval == 8 && vec) {
-                uint32_t w[NW8];
-                load8<GDT>(srow + c8, w);
-#pragma unroll
-                for (int i = 0; i < NW8; ++i) {
-                    if constexpr (GSZ == 2) nfacc |= (w[i] & 0x7f807f80u) + 0x00800080u;
-                    else nfacc |= (w[i] & 0x7f800000u) + 0x00800000u;
-                }
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    if constexpr (GSZ == 2) x[e] = (GB)(w[e >> 1] >> (16 * (e & 1)));
-                    else x[e] = (GB)w[e];
-                }
-            } else {
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    x[e] = e < nval ? srow[c8 + e] : (GB)0;
-                    if (e < nval) {
-                        if constexpr (GSZ == 2) nfacc |= ((uint32_t)x[e] & 0x7f80u) + 0x0080u;
-                        else nfacc |= ((uint32_t)x[e] & 0x7f800000u) + 0x00800000u;
-                    }
-                }
-            }
-            int u = pend + 8 * lane - selblk;
-            const uint32_t keep = ~selb & vmask;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                if ((keep >> e) & 1u) sts_elem(wbuf + u++, x[e]);
-            }
-            __syncwarp();
-            pend += blk_keep;
-            const bool row_end = (cc + 1 == nblk) || (q + 1 == q1);
-            flush_out(row_end);
             if (++cc == nblk) {
                 cc = 0;
                 ++r;
@@ -550,8 +566,9 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
         // stage fully consumed by this warp
         __syncwarp();
         if (lane == 0) {
+            uint32_t* done = si.done;
             mbar_arrive(&empty[st]);
-            if (L.done) red_release_add(L.done, 1u);  // per-warp completion count (offload only)
+            if (done) red_release_add(done, 1u);  // per-warp completion count (offload only)
         }
     }
     if (prm.nonfinite) {
