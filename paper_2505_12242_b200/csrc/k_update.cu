@@ -39,7 +39,7 @@
 namespace zf {
 namespace {
 
-constexpr int K3_NCW = 15;                        // consumer warps
+constexpr int K3_NCW = 16;                        // consumer warps
 constexpr int K3_STAGES = 4;                      // stage arenas = producer warps (one chain per stage)
 constexpr int K3_THREADS = 32 * (K3_NCW + K3_STAGES);
 constexpr int K3_CHUNK = 512;                     // columns per warp block (32 lanes x 16)
@@ -395,8 +395,11 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
         // ---------------- AdamW pair loads (first batch) ----------------
         const int ns = si.s1 - si.s0;
         const int npairs = (prm.do_adam && prm.debug_mode == 0) ? Rr * ns : 0;
-        float ag[K3_PAIRS], ap[K3_PAIRS], am[K3_PAIRS], av[K3_PAIRS];
-        int32_t at[K3_PAIRS], pidx[K3_PAIRS], midx[K3_PAIRS];  // p / moment offsets from the unit's row 0
+        float ag[K3_PAIRS], am[K3_PAIRS], av[K3_PAIRS];
+        PB apb[K3_PAIRS];  // raw p bits: converted only in compute_pairs, so a global load's latency
+                           // is not waited for before the compaction
+        float ass[K3_PAIRS], abc[K3_PAIRS];  // bias corrections of each pair's step (table loads issued early)
+        int32_t pidx[K3_PAIRS], midx[K3_PAIRS];  // p / moment offsets from the unit's row 0
         auto load_pairs = [&](int qb) {
             const float inv_ns = 1.0f / (float)ns;
             const int k = si.k, kin = si.kin, s0 = si.s0;
@@ -422,7 +425,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
                     const int cl = c - c0;
                     ag[b] = GE::to_f(sG[r * sw + cl]);
                     pidx[b] = r * si.ldp + c;
-                    ap[b] = pst ? PE::to_f(sP[r * sw + cl]) : PE::to_f(static_cast<const PB*>(si.P)[pidx[b]]);
+                    apb[b] = pst ? sP[r * sw + cl] : static_cast<const PB*>(si.P)[pidx[b]];
                     midx[b] = r * k + s;
                     if (mst) {
                         if (remap) {
@@ -433,7 +436,9 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
                             am[b] = sM[r * k + sl];
                             av[b] = sV[r * k + sl];
                         }
-                        at[b] = sS[sl];
+                        const int32_t t = sS[sl] + prm.step_delta + 1;
+                        ass[b] = adam_ss(t, prm.adam);
+                        abc[b] = adam_bc2s(t, prm.adam);
                     } else {
                         const int64_t row = si.r0 + r;
                         if (remap) {
@@ -444,7 +449,9 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
                             am[b] = __ldcs(si.m_in + row * k + s);
                             av[b] = __ldcs(si.v_in + row * k + s);
                         }
-                        at[b] = __ldg(si.steps + s);
+                        const int32_t t = __ldg(si.steps + s) + prm.step_delta + 1;
+                        ass[b] = adam_ss(t, prm.adam);
+                        abc[b] = adam_bc2s(t, prm.adam);
                     }
                 }
             }
@@ -456,8 +463,8 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
 #pragma unroll
             for (int b = 0; b < K3_PAIRS; ++b) {
                 if (pidx[b] < 0) continue;
-                float p = ap[b], mm = am[b], vv = av[b];
-                adamw_elem(ag[b], p, mm, vv, at[b] + prm.step_delta + 1, prm.adam);
+                float p = PE::to_f(apb[b]), mm = am[b], vv = av[b];
+                adamw_elem_t(ag[b], p, mm, vv, ass[b], abc[b], prm.adam);
                 P[pidx[b]] = PE::from_f(p);
                 __stcs(Mo + midx[b], mm);
                 __stcs(Vo + midx[b], vv);
