@@ -190,7 +190,7 @@ def run_zenflow(args, rank, world):
         dist.barrier()
     from paper_2505_12242_b200 import zf
     from synth import gpu as sgpu
-    from oracle import oracle as _orc_shard  # noqa: F401  (shard_rows only; see below)
+    from paper_2505_12242_b200.dist import shard_rows
 
     dev = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(dev)
@@ -198,13 +198,9 @@ def run_zenflow(args, rank, world):
     names = synth.MODELS[args.model]()
     full_shapes = [(n, m) for _, n, m in names]
 
-    def shard(n):
-        base, rem = divmod(n, world)
-        s = rank * base + min(rank, rem)
-        return s, base + (1 if rank < rem else 0)
-
-    shapes = [(shard(n)[1], m) for n, m in full_shapes]
-    row0s = [shard(n)[0] for n, _ in full_shapes]
+    spans = [shard_rows(n, world, rank) for n, _ in full_shapes]
+    shapes = [(b - a, m) for (a, b), (_, m) in zip(spans, full_shapes)]
+    row0s = [a for a, _ in spans]
     ks = [zf.k_for(m, args.ratio_ppm) for _, m in shapes]
 
     # ---- inputs resident in HBM: two gradient versions (alternating steps), params
@@ -230,9 +226,8 @@ def run_zenflow(args, rank, world):
     torch.cuda.synchronize()
     nccl_id = None
     if world > 1:
-        obj = [zf.zf_nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        from paper_2505_12242_b200.dist import broadcast_nccl_id
+        nccl_id = broadcast_nccl_id()
 
     def make_ctx(ratio_ppm, offload):
         return zf.Context([zf.LayerShape(n, m) for n, m in shapes], topk_ratio_ppm=ratio_ppm,
@@ -294,7 +289,7 @@ def run_zenflow(args, rank, world):
     result = {
         "metric": METRIC, "value": ms_per_step, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False,
-        "scaling": "strong" if world > 1 else "strong", "vs_baseline": None, "dtype": "bf16",
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded column-concentrated bf16 gradients, bf16 params, fp32 AdamW state)",
         "config": {"workload": f"{args.model}-all-linear-k{args.ratio_ppm // 10000}pct", "model": args.model,
                    "linears": nl, "elements": sum(n * m for n, m in full_shapes), "ratio_ppm": args.ratio_ppm,

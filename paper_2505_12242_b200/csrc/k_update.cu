@@ -64,15 +64,21 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    // consumer-side wait: hardware try_wait, then short sleeps so that waiting warps do not
+    // take issue slots from the warps still working on a stage
     uint32_t done = 0;
-    while (!done) {
+    int ns = 16;
+    for (;;) {
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
             "selp.b32 %0, 1, 0, p;\n\t}"
             : "=r"(done)
             : "r"(smem_u32(bar)), "r"(phase)
             : "memory");
+        if (done) return;
+        __nanosleep(ns);
+        ns = ns < 128 ? ns * 2 : 128;
     }
 }
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
@@ -88,10 +94,10 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
 }
 // producer-side wait: back off with nanosleep so spinning does not steal issue slots
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
-    int ns = 32;
+    int ns = 64;
     while (!mbar_test(bar, phase)) {
         __nanosleep(ns);
-        ns = ns < 256 ? ns * 2 : 256;
+        ns = ns < 512 ? ns * 2 : 512;
     }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
