@@ -476,7 +476,9 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
                 __stcs(Vo + midx[b], vv);
             }
         };
-        if (npairs > 0) load_pairs(0);
+        // fast path: everything staged, steady step -> shared-memory operands only
+        const bool fast = si.pstaged && si.mstaged && !si.remap;
+        if (npairs > 0 && !fast) load_pairs(0);
 
         // ---------------- compaction ----------------
         const int nblk = (sw + K3_CHUNK - 1) / K3_CHUNK;
@@ -569,7 +571,35 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
         }
 
         // ---------------- AdamW compute + stores (then any further pair batches) ----------------
-        if (npairs > 0) {
+        if (npairs > 0 && fast) {
+            const int k = si.k, s0 = si.s0, ldp = si.ldp, c0 = (int)si.c0;
+            const PB* sP = reinterpret_cast<const PB*>(A + si.oP);
+            const float* sM = reinterpret_cast<const float*>(A + si.oM) + si.eM;
+            const float* sV = reinterpret_cast<const float*>(A + si.oV) + si.eV;
+            const int32_t* sS = reinterpret_cast<const int32_t*>(A + si.oS) + si.eS;
+            const int32_t* sIdx = reinterpret_cast<const int32_t*>(A + si.oIdx) + si.eIdx;
+            PB* P = static_cast<PB*>(si.P);
+            float* Mo = si.m_out + s0;
+            float* Vo = si.v_out + s0;
+            const int tdelta = prm.step_delta + 1;
+            int r = ctid / ns, sl = ctid - r * ns;                 // one division per unit
+            const int dr = NCT / ns, dsl = NCT - dr * ns;
+            for (int q = ctid; q < npairs; q += NCT) {
+                const int c = sIdx[sl];
+                const int cl = c - c0;
+                const float g = GE::to_f(sG[r * sw + cl]);
+                float p = PE::to_f(sP[r * sw + cl]);
+                float mm = sM[r * k + sl], vv = sV[r * k + sl];
+                const int32_t t = sS[sl] + tdelta;
+                adamw_elem_t(g, p, mm, vv, adam_ss(t, prm.adam), adam_bc2s(t, prm.adam), prm.adam);
+                P[r * ldp + c] = PE::from_f(p);
+                __stcs(Mo + r * k + sl, mm);
+                __stcs(Vo + r * k + sl, vv);
+                r += dr;
+                sl += dsl;
+                if (sl >= ns) { sl -= ns; ++r; }
+            }
+        } else if (npairs > 0) {
             compute_pairs();
             for (int qb = K3_PAIRS * NCT; qb < npairs; qb += K3_PAIRS * NCT) {
                 load_pairs(qb);
