@@ -1,0 +1,32 @@
+"""bench.py on CPU: the reference arm (the oracle on a bounded sample) prints the
+contract's JSON line, and the roofline byte accounting matches SURVEY §8(d)."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def test_reference_arm_json_line():
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--model", "gpt2-small",
+                        "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["unit"] == "ms/step" and line["higher_is_better"] is False
+    assert line["value"] > 0 and line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] == 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+
+
+def test_algorithmic_and_sector_bytes():
+    import bench
+    # 5.80 B/elt algorithmic at k = 10% (4096 columns -> k = 410)
+    b = bench.algorithmic_bytes([(4096, 4096)], [410])
+    assert abs(b / (4096 * 4096) - 5.80) < 0.01
+    b1 = bench.algorithmic_bytes([(4096, 4096)], [41])
+    assert abs(b1 / (4096 * 4096) - 4.18) < 0.01
+    # all columns selected in every 32-byte sector -> p moves fully (2 + 2 B/elt)
+    import numpy as np
+    s = bench.sector_bytes([(8, 64)], [np.arange(0, 64, 16)])   # one column per bf16 sector
+    assert s == 8 * 64 * 2 + 8 * 60 * 2 + 8 * 4 * 16 + 8 * 4 * 32 * 2

@@ -275,3 +275,66 @@ def test_step_state_errors(zf, gpu):
     with pytest.raises(zf.ZFError):
         ctx.step(2, [G], [P])            # not consecutive
     ctx.close()
+
+
+# ------------------------------------------------------------------ full-size configs (sampled)
+def _run_fullsize(zf, orc, gpu, names, ppm, steps, sample, offload, row_div=1, lr=1e-5):
+    """Whole model through zf_step in the bench launch configuration; the sampled
+    layers are checked against the oracle one by one (bf16 G and p, fp32 state)."""
+    shapes = [(n // row_div, m) for _, n, m in names]
+    ctx = zf.Context([zf.LayerShape(n, m) for n, m in shapes], topk_ratio_ppm=ppm, refresh_interval=4,
+                     accum_interval=4, adam=zf.adam_params(lr=lr), offload=offload, host_accumulate=offload)
+    hp_o = orc.AdamHP(lr=lr)
+    tot = sum(n * m for n, m in shapes)
+    gbuf = torch.empty(tot, dtype=torch.bfloat16, device="cuda")
+    pbuf = torch.empty(tot, dtype=torch.bfloat16, device="cuda")
+    Gs, Ps, off = [], [], 0
+    for n, m in shapes:
+        Gs.append(gbuf[off:off + n * m].view(n, m))
+        Ps.append(pbuf[off:off + n * m].view(n, m))
+        off += n * m
+    scales = [gpu.ColScale(m, li) for li, (n, m) in enumerate(shapes)]
+    for li, P in enumerate(Ps):
+        gpu.fill_param(P, li)
+    layers = {li: orc.OracleLayer(n=shapes[li][0], m=shapes[li][1], ratio_ppm=ppm, refresh_interval=4,
+                                  accum_interval=4, hp=hp_o) for li in sample}
+    Po = {li: to_np(Ps[li]) for li in sample}
+    for t in range(steps):
+        for li, (G, sc) in enumerate(zip(Gs, scales)):
+            sc.advance_to(t)
+            gpu.fill_grad(G, li, t, sc)
+        Gn = {li: to_np(Gs[li]) for li in sample}
+        ctx.step(t, Gs, Ps)
+        ctx.sync()
+        for li in sample:
+            L = layers[li]
+            gidx = to_np(ctx.selected(li))
+            if t % 4 == 0:
+                onorms = orc.column_norms(Gn[li])
+                assert_close_rel(to_np(ctx.norms(li)), onorms, 1e-5, f"norms t={t} l={li}")
+                selection_ok(gidx, orc.topk(onorms, L.k), onorms)
+            out = L.step(t, Gn[li], Po[li], idx_override=gidx if t % 4 == 0 else None)
+            M, V, st = ctx.optimizer_state(li)
+            assert_bits_equal(to_np(st), L.steps, f"steps t={t} l={li}")
+            assert_bits_equal(to_np(M), L.M, f"exp_avg t={t} l={li}")
+            assert_bits_equal(to_np(V), L.V, f"exp_avg_sq t={t} l={li}")
+            assert_bits_equal(to_np(Ps[li]), Po[li], f"params t={t} l={li}")
+            assert_bits_equal(to_np(ctx.compact_buffer(li)), out, f"compact t={t} l={li}")
+            if offload:
+                assert_bits_equal(ctx.compact_host(li).copy(), out, f"compact host t={t} l={li}")
+                assert_bits_equal(ctx.host_accumulator(li, 0).copy(), L.acc[(t // 4) % 2], f"acc t={t} l={li}")
+    ctx.close()
+
+
+@pytest.mark.slow
+def test_llama2_7b_fullsize_sampled(zf, orc, gpu):
+    """BASELINE config 3 at full size (225 linears, 6.6 G elements, k=10%), refresh at
+    t=0 then a steady step; q_proj, gate_proj, down_proj of layer 0 and lm_head checked."""
+    _run_fullsize(zf, orc, gpu, synth.llama2_7b_linears(), 100000, 2, [0, 4, 6, 224], offload=False)
+
+
+@pytest.mark.slow
+def test_llama2_13b_rank0_shard_offload_sampled(zf, orc, gpu):
+    """BASELINE config 5 on one GPU: the row shard rank 0 of 8 would own (n/8 rows of all
+    281 linears), k=10%, with D2H offload + host accumulation; sampled layers checked."""
+    _run_fullsize(zf, orc, gpu, synth.llama2_13b_linears(), 100000, 2, [0, 5, 6, 280], offload=True, row_div=8)
