@@ -40,6 +40,8 @@ namespace zf {
 namespace {
 
 constexpr int K3_NCW = 16;                        // consumer warps
+constexpr int K3_GROUPS = 2;                      // independent consumer groups; group g owns stages g, g+2, ...
+constexpr int K3_GW = K3_NCW / K3_GROUPS;         // warps per group
 constexpr int K3_STAGES = 4;                      // stage arenas = producer warps (one chain per stage)
 constexpr int K3_THREADS = 32 * (K3_NCW + K3_STAGES);
 constexpr int K3_CHUNK = 512;                     // columns per warp block (32 lanes x 16)
@@ -240,7 +242,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
     if (tid == 0) {
         for (int st = 0; st < K3_STAGES; ++st) {
             mbar_init(&full[st], 1);
-            mbar_init(&empty[st], K3_NCW);
+            mbar_init(&empty[st], K3_GW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -368,15 +370,23 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
     // (row-major over the unit's rows); lane l of a block owns its columns 16l..16l+15; the
     // unselected values go to the warp buffer, flushed with aligned 16-byte stores after
     // every block (the < 16-byte remainder carries over).
-    const int cw = warp - K3_STAGES;
+    const int cwa = warp - K3_STAGES;          // consumer warp index (warp-area slot)
+    const int grp = cwa / K3_GW;               // consumer group
+    const int cw = cwa - grp * K3_GW;          // warp index within the group
     const int ctid = cw * 32 + lane;
-    constexpr int NCT = K3_NCW * 32;
-    unsigned char* warea = smem + K3_STAGES * K3_ARENA + cw * K3_WARP_BYTES;
+    constexpr int NCT = K3_GW * 32;
+    unsigned char* warea = smem + K3_STAGES * K3_ARENA + cwa * K3_WARP_BYTES;
     GB* wbuf = reinterpret_cast<GB*>(warea);
     uint32_t nfacc = 0;                // non-finite detector (exponent all-ones -> carry into the top bit)
     uint32_t finished = 0, phase = 0;  // per stage: end sentinel seen / mbarrier parity
 
-    for (int it = 0;; ++it) {
+    constexpr uint32_t kMine = [] {
+        uint32_t m = 0;
+        for (int st = 0; st < K3_STAGES; st += K3_GROUPS) m |= 1u << st;
+        return m;
+    }();
+    const uint32_t mine = kMine << grp;  // the stages of my group
+    for (int it = grp;; it += K3_GROUPS) {
         const int st = it % K3_STAGES;
         if ((finished >> st) & 1u) continue;
         mbar_wait(&full[st], (phase >> st) & 1u);
@@ -384,7 +394,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
         const StageInfo& si = info[st];
         if (si.u < 0) {  // this stage's producer ran out of units; others may still hold some
             finished |= 1u << st;
-            if (finished == (1u << K3_STAGES) - 1u) break;
+            if (finished == mine) break;
             continue;
         }
         if (prm.debug_mode == 1) {
@@ -483,7 +493,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
         // ---------------- compaction ----------------
         const int nblk = (sw + K3_CHUNK - 1) / K3_CHUNK;
         const int nq = Rr * nblk;
-        const int q0 = (nq * cw) / K3_NCW, q1 = (nq * (cw + 1)) / K3_NCW;
+        const int q0 = (nq * cw) / K3_GW, q1 = (nq * (cw + 1)) / K3_GW;
         const bool vec = (sw % 8) == 0;  // rows of the staged tile are 16-byte aligned
         GB* outp = static_cast<GB*>(si.out);
         int r = q0 / nblk, cc = q0 - r * nblk;
@@ -667,7 +677,7 @@ void set_attr() {
 UpdLimits update_limits() {
     UpdLimits l;
     l.arena_bytes = K3_ARENA;
-    l.consumer_warps = K3_NCW;
+    l.consumer_warps = K3_GW;  // warps that process (and count) each unit
     l.producers = K3_STAGES;
     return l;
 }
