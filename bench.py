@@ -313,8 +313,12 @@ def run_zenflow(args, rank, world):
     if os.path.exists(prof_path):
         d = json.load(open(prof_path))
         if d.get("workload") == result["config"]["workload"] and world == 1:
-            result["roofline"]["traffic"] = d.get("traffic_bytes_per_launch")
+            tr = d.get("traffic_bytes_per_launch")
+            result["roofline"]["traffic"] = tr
             result["roofline"]["traffic_source"] = d.get("source")
+            # DRAM bytes the kernel actually moves (ncu) over its live average duration
+            result["roofline"]["achieved_dram_GBs"] = tr / (k3_avg * 1e-3) / 1e9
+            result["roofline"]["frac_dram"] = tr / (k3_avg * 1e-3) / 1e9 / hbm_peak
     if n_k1:
         k1_avg = k1_ms / n_k1
         result["k1_roofline"] = {"bound": "hbm", "achieved": g_bytes / (k1_avg * 1e-3) / 1e9, "peak": hbm_peak,

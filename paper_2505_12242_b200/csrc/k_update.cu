@@ -378,6 +378,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
     unsigned char* warea = smem + K3_STAGES * K3_ARENA + cwa * K3_WARP_BYTES;
     GB* wbuf = reinterpret_cast<GB*>(warea);
     uint32_t nfacc = 0;                // non-finite detector (exponent all-ones -> carry into the top bit)
+    __nv_bfloat162 nf2 = __float2bfloat162_rn(0.0f);  // bf16 tiles: NaN-propagating max of |x|
     uint32_t finished = 0, phase = 0;  // per stage: end sentinel seen / mbarrier parity
 
     constexpr uint32_t kMine = [] {
@@ -511,41 +512,57 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
         if (q0 < q1) start_row();
         for (int q = q0; q < q1; ++q) {
             const int cl0 = cc * K3_CHUNK, cl1 = min(sw, cl0 + K3_CHUNK);
-            const int c16 = cl0 + 16 * lane;
-            const int nval = max(0, min(16, cl1 - c16));
-            const uint32_t word = nval > 0 ? smask[c16 >> 5] : 0u;
-            const int sh = c16 & 31;
-            const uint32_t vmask = (1u << nval) - 1u;
-            const uint32_t selb = (word >> sh) & vmask;  // selected among my columns
-            const int selblk = nval > 0 ? (spre[c16 >> 5] - spre[cl0 >> 5]) + __popc(word & ((1u << sh) - 1u)) : 0;
-            const int blk_keep = (cl1 - cl0) - (int)__reduce_add_sync(0xffffffffu, (unsigned)__popc(selb));
-            const GB* src = sG + r * sw + c16;
-            int u = pend + 16 * lane - selblk;
-            const uint32_t keep = ~selb & vmask;
-            if (nval == 16 && vec) {
+            // lane l owns columns cl0 + 256h + 8l .. +7 of the block's two halves h = 0, 1:
+            // 16-byte tile reads of a warp are contiguous (bank-conflict free)
+            const int base0 = spre[cl0 >> 5];
+            int keep_total = 0;
+            int u[2], nv[2];
+            uint32_t sb[2];
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < 2; ++h) {
+                const int c8 = cl0 + 256 * h + 8 * lane;
+                nv[h] = max(0, min(8, cl1 - c8));
+                const uint32_t word = nv[h] > 0 ? smask[c8 >> 5] : 0u;
+                const int sh = c8 & 31;
+                sb[h] = (word >> sh) & ((1u << nv[h]) - 1u);
+                const int selh = nv[h] > 0 ? (spre[c8 >> 5] - base0) + __popc(word & ((1u << sh) - 1u)) : 0;
+                u[h] = pend + (256 * h + 8 * lane) - selh;
+            }
+            keep_total = (cl1 - cl0) - (int)__reduce_add_sync(0xffffffffu, (unsigned)(__popc(sb[0]) + __popc(sb[1])));
+            const int blk_keep = keep_total;
+            const GB* srow = sG + r * sw;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int c8 = cl0 + 256 * h + 8 * lane;
+                const uint32_t selb = sb[h];
+                if (nv[h] == 8 && vec) {
+                    // branch-free scatter: the address steps back over each selected column, so
+                    // every kept element is one predicated store at an immediate offset from `a`
+                    uint32_t a = smem_u32(wbuf + u[h]);
                     uint32_t w[NW8];
-                    load8<GDT>(src + 8 * h, w);
+                    load8<GDT>(srow + c8, w);
 #pragma unroll
                     for (int i = 0; i < NW8; ++i) {
-                        if constexpr (GSZ == 2) nfacc |= (w[i] & 0x7f807f80u) + 0x00800080u;
+                        if constexpr (GSZ == 2) nf2 = __hmax2_nan(nf2, __habs2(*reinterpret_cast<const __nv_bfloat162*>(&w[i])));
                         else nfacc |= (w[i] & 0x7f800000u) + 0x00800000u;
                     }
 #pragma unroll
                     for (int e = 0; e < 8; ++e) {
-                        GB x;
-                        if constexpr (GSZ == 2) x = (GB)(w[e >> 1] >> (16 * (e & 1)));
-                        else x = (GB)w[e];
-                        if ((keep >> (8 * h + e)) & 1u) sts_elem(wbuf + u++, x);
+                        uint32_t x;
+                        if constexpr (GSZ == 2) x = (e & 1) ? (w[e >> 1] >> 16) : w[e >> 1];
+                        else x = w[e];
+                        if ((selb >> e) & 1u) a -= GSZ;
+                        else if constexpr (GSZ == 2) asm volatile("st.shared.u16 [%0], %1;" ::"r"(a + 2 * e), "r"(x) : "memory");
+                        else asm volatile("st.shared.u32 [%0], %1;" ::"r"(a + 4 * e), "r"(x) : "memory");
                     }
-                }
-            } else {
-                for (int e = 0; e < nval; ++e) {
-                    const GB x = src[e];
-                    if constexpr (GSZ == 2) nfacc |= ((uint32_t)x & 0x7f80u) + 0x0080u;
-                    else nfacc |= ((uint32_t)x & 0x7f800000u) + 0x00800000u;
-                    if ((keep >> e) & 1u) sts_elem(wbuf + u++, x);
+                } else {
+                    int uu = u[h];
+                    for (int e = 0; e < nv[h]; ++e) {
+                        const GB x = srow[c8 + e];
+                        if constexpr (GSZ == 2) nfacc |= ((uint32_t)x & 0x7f80u) + 0x0080u;
+                        else nfacc |= ((uint32_t)x & 0x7f800000u) + 0x00800000u;
+                        if (!((selb >> e) & 1u)) sts_elem(wbuf + uu++, x);
+                    }
                 }
             }
             __syncwarp();
@@ -625,7 +642,11 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
         }
     }
     if (prm.nonfinite) {
-        const uint32_t hit = GSZ == 2 ? (nfacc & 0x80008000u) : (nfacc & 0x80000000u);
+        uint32_t hit = GSZ == 2 ? (nfacc & 0x80008000u) : (nfacc & 0x80000000u);
+        if constexpr (GSZ == 2) {
+            const uint32_t b = *reinterpret_cast<const uint32_t*>(&nf2);
+            hit |= ((b & 0xffffu) >= 0x7f80u) | ((b >> 16) >= 0x7f80u);
+        }
         if (__any_sync(0xffffffffu, hit != 0) && lane == 0) *prm.nonfinite = 1;
     }
 }
