@@ -150,6 +150,14 @@ typedef struct {
     int32_t host_accumulate;          /* 1: fp32 accumulation on the host (row 8);
                                          requires offload and N % S == 0             */
     int32_t host_threads;             /* host accumulation threads (0: default)        */
+    int32_t cpu_update;               /* 1: deferred CPU AdamW of the unselected columns
+                                         at every window end (next row f1, P:519-531,
+                                         reading R18); requires host_accumulate. The
+                                         window's average gradient acc/S updates an fp32
+                                         host master with host moments; the result is
+                                         uploaded into the parameters before zf_step
+                                         returns (synchronous: zf_step blocks at window
+                                         ends and refreshes)                          */
 } zf_config;
 
 typedef struct zf_ctx zf_ctx;

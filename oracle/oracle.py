@@ -70,6 +70,7 @@ def lib():
         L.oracle_compact.argtypes = [_vp, ctypes.c_int, _i64, _i64, _i64, _vp, _i64, _vp]
         L.oracle_compact.restype = None
         L.oracle_accumulate.argtypes = [_vp, _vp, ctypes.c_int, _i64]; L.oracle_accumulate.restype = None
+        L.oracle_to_bf16.argtypes = [_vp, _vp, _i64]; L.oracle_to_bf16.restype = None
     return _lib
 
 
@@ -98,6 +99,13 @@ def bf16_bits_to_f32(h: np.ndarray) -> np.ndarray:
 
 def as_f32(a: np.ndarray) -> np.ndarray:
     return bf16_bits_to_f32(a) if a.dtype == np.uint16 else a.astype(np.float32)
+
+
+def to_bf16(x: np.ndarray) -> np.ndarray:
+    x = np.ascontiguousarray(x, np.float32)
+    out = np.empty(x.shape, np.uint16)
+    lib().oracle_to_bf16(_p(x), _p(out), x.size)
+    return out
 
 
 def k_for(m: int, ratio_ppm: int) -> int:
@@ -211,6 +219,7 @@ class OracleLayer:
     refresh_interval: int = 4
     accum_interval: int = 4
     hp: AdamHP = field(default_factory=AdamHP)
+    cpu_update: bool = False   # f1: deferred CPU AdamW on the unselected columns (reading R18)
     idx: np.ndarray | None = None
     M: np.ndarray | None = None
     V: np.ndarray | None = None
@@ -218,6 +227,10 @@ class OracleLayer:
     acc: list | None = None
     last_norms: np.ndarray | None = None
     last_out: np.ndarray | None = None
+    master: np.ndarray | None = None     # f1: fp32 master of theta^(c) [n, m] (valid on unselected columns)
+    Mh: np.ndarray | None = None         # f1: host moments [n, m]
+    Vh: np.ndarray | None = None
+    th: np.ndarray | None = None         # f1: host step count per column [m]
 
     @property
     def k(self) -> int:
@@ -230,9 +243,12 @@ class OracleLayer:
         refresh step (parity protocol O10: downstream steps are compared on the
         GPU's selection, so a tolerated boundary swap never cascades)."""
         k = self.k
+        if self.cpu_update:
+            assert self.refresh_interval % self.accum_interval == 0, "R18: refresh only at window starts"
         if t % self.refresh_interval == 0 or self.idx is None:
             self.last_norms = column_norms(G)
             new_idx = topk(self.last_norms, k) if idx_override is None else np.asarray(idx_override, np.int32)
+            old_idx = self.idx
             if self.idx is None:
                 self.M = np.zeros((self.n, k), np.float32)
                 self.V = np.zeros((self.n, k), np.float32)
@@ -240,6 +256,8 @@ class OracleLayer:
             else:
                 self.M, self.V, self.steps = remap(self.n, self.idx, self.M, self.V, self.steps, new_idx)
             self.idx = new_idx
+            if self.cpu_update:
+                self._migrate(old_idx, new_idx, P)
         selective_adamw(P, G, self.idx, self.M, self.V, self.steps, self.hp)
         out = compact(G, self.idx)
         S = self.accum_interval
@@ -250,7 +268,59 @@ class OracleLayer:
             self.acc[a][...] = 0.0
         accumulate(self.acc[a], out)
         self.last_out = out
+        if self.cpu_update and (t + 1) % S == 0:
+            self._deferred_update(self.acc[a], P)
         return out
+
+    # ---------------------------------------------------------------- f1
+    def _unselected(self):
+        mask = np.ones(self.m, bool)
+        mask[self.idx] = False
+        return np.nonzero(mask)[0].astype(np.int32)
+
+    def _migrate(self, old_idx, new_idx, P):
+        """Reading R18 at a refresh: a column entering the CPU-updated set (unselected now,
+        selected before or first step) takes the current parameter value as its fp32
+        master, with zero host moments and step count (as R7 does on the GPU side);
+        a column leaving it keeps nothing."""
+        if self.master is None:
+            self.master = np.zeros((self.n, self.m), np.float32)
+            self.Mh = np.zeros((self.n, self.m), np.float32)
+            self.Vh = np.zeros((self.n, self.m), np.float32)
+            self.th = np.zeros(self.m, np.int32)
+        was_cpu = np.zeros(self.m, bool)
+        if old_idx is not None:
+            was_cpu[:] = True
+            was_cpu[old_idx] = False
+        now_cpu = np.ones(self.m, bool)
+        now_cpu[new_idx] = False
+        entering = np.nonzero(now_cpu & ~was_cpu)[0]
+        self.master[:, entering] = as_f32(P[:, entering])
+        self.Mh[:, entering] = 0.0
+        self.Vh[:, entering] = 0.0
+        self.th[entering] = 0
+
+    def _deferred_update(self, acc, P):
+        """f1 / reading R18: at the end of an S-step window, theta^(c) (the window's
+        unselected columns) takes one AdamW step (formula O6) with the window's
+        average gradient acc / S (theta^(c) -= alpha * (1/S) * sum of the
+        window's gradients, here through AdamW), on the fp32 master with host
+        moments; the parameter then holds the master rounded to its dtype."""
+        unsel = self._unselected()
+        g_avg = acc / np.float32(self.accum_interval)          # one IEEE fp32 division
+        Gfull = np.zeros((self.n, self.m), np.float32)
+        Gfull[:, unsel] = g_avg
+        Mc = np.ascontiguousarray(self.Mh[:, unsel])
+        Vc = np.ascontiguousarray(self.Vh[:, unsel])
+        tc = np.ascontiguousarray(self.th[unsel])
+        selective_adamw(self.master, Gfull, unsel, Mc, Vc, tc, self.hp)
+        self.Mh[:, unsel] = Mc
+        self.Vh[:, unsel] = Vc
+        self.th[unsel] = tc
+        if P.dtype == np.uint16:
+            P[:, unsel] = to_bf16(self.master[:, unsel])
+        else:
+            P[:, unsel] = self.master[:, unsel]
 
     def sealed(self, t: int):
         """The accumulator sealed by the window that ended at or before step t."""

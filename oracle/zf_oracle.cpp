@@ -90,6 +90,11 @@ extern "C" {
 
 float oracle_bf16_round(float x) { return bf16_to_f32(f32_to_bf16_rne(x)); }
 
+/* fp32 -> bf16 bit patterns, round to nearest even (the bf16 parameter store of O6). */
+void oracle_to_bf16(const float* x, uint16_t* out, int64_t count) {
+    for (int64_t e = 0; e < count; ++e) out[e] = f32_to_bf16_rne(x[e]);
+}
+
 /* O2  k = ceil(ratio * m) with ratio = ppm / 1e6, in integer arithmetic
  * ("|channel_ids| = ceil(k_channel_ratio x m)"; reading R2: k >= 1). */
 int64_t oracle_k_for(int64_t m, int32_t ppm) {

@@ -431,6 +431,17 @@ struct LayerState {
     K3Geom geo{};
     int64_t unit_begin = 0;
     cudaEvent_t d2h_ev[2] = {nullptr, nullptr};
+    // f1: deferred CPU AdamW (reading R18)
+    float* master = nullptr;          // [n, m] fp32 host master (valid on CPU-updated columns)
+    float* mh = nullptr;              // [n, m] host moments
+    float* vh = nullptr;
+    std::vector<int32_t> th;          // [m] host step count per column
+    std::vector<int32_t> idx_host;    // current selection (ascending), host copy
+    std::vector<int32_t> unsel_host;  // its complement (ascending)
+    void* p_mirror = nullptr;         // pinned [n, m] copy of p at a refresh
+    void* p_up = nullptr;             // pinned [n, m-k] updated unselected params
+    void* p_up_dev = nullptr;         // device [n, m-k]
+    int32_t* unsel_dev = nullptr;     // device [m-k]
 };
 
 // Simple pool for the host accumulation (row 8, H1).
@@ -448,9 +459,11 @@ class Pool {
         cv_.notify_all();
         for (auto& t : th_) t.join();
     }
-    // fn(begin, end) over [0, count) split into n_ contiguous slices
+    // fn(begin, end) over [0, count) split into n_ contiguous slices; callers from several
+    // threads (H1 and the f1 host update) are serialised.
     template <typename F>
     void parallel_for(int64_t count, F&& fn) {
+        std::lock_guard<std::mutex> call(call_mu_);
         std::unique_lock<std::mutex> lk(mu_);
         job_ = [&](int i) {
             const int64_t per = (count + n_ - 1) / n_;
@@ -485,7 +498,7 @@ class Pool {
     }
     int n_;
     std::vector<std::thread> th_;
-    std::mutex mu_;
+    std::mutex mu_, call_mu_;
     std::condition_variable cv_, done_cv_;
     std::function<void(int)> job_;
     uint64_t gen_ = 0;
@@ -816,6 +829,9 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
     if (cfg->host_accumulate && !cfg->offload) return fail(ZF_EINVAL, "host_accumulate requires offload");
     if (cfg->host_accumulate && (cfg->refresh_interval % cfg->accum_interval) != 0)
         return fail(ZF_EINVAL, "host_accumulate requires refresh_interval %% accum_interval == 0");
+    if (cfg->cpu_update && !cfg->host_accumulate) return fail(ZF_EINVAL, "cpu_update requires host_accumulate");
+    if (cfg->cpu_update && cfg->refresh_interval % cfg->accum_interval != 0)
+        return fail(ZF_EINVAL, "cpu_update requires refresh_interval to be a multiple of accum_interval");
     ZF_TRY(check_hp(&cfg->adam));
     if (world < 1 || rank < 0 || rank >= world) return fail(ZF_EINVAL, "bad world/rank");
     if (world > 1 && !nccl_id128) return fail(ZF_EINVAL, "nccl_id128 required when world > 1");
@@ -956,6 +972,26 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
                     l.acc[s] = p;
                 }
             }
+            if (cfg->cpu_update) {
+                for (auto& l : c->L) {
+                    const size_t nm = (size_t)l.d.n * l.d.m;
+                    for (float** pp : {&l.master, &l.mh, &l.vh}) {
+                        float* q = static_cast<float*>(std::aligned_alloc(64, (nm * sizeof(float) + 63) / 64 * 64));
+                        if (!q) return bail(fail(ZF_ENOMEM, "host optimizer state allocation failed"));
+                        std::memset(q, 0, nm * sizeof(float));
+                        c->host_plain.push_back(q);
+                        *pp = q;
+                    }
+                    l.th.assign(l.d.m, 0);
+                    ZF_CUDA(cudaHostAlloc(&l.p_mirror, std::max<size_t>(nm * c->psz, 64), cudaHostAllocDefault));
+                    c->host_pinned.push_back(l.p_mirror);
+                    ZF_CUDA(cudaHostAlloc(&l.p_up, std::max<size_t>((size_t)l.d.n * l.mk * c->psz, 64),
+                                          cudaHostAllocDefault));
+                    c->host_pinned.push_back(l.p_up);
+                    ZF_CTRY(c->dalloc(&l.p_up_dev, (size_t)l.d.n * l.mk * c->psz, false));
+                    ZF_CTRY(c->dalloc(&l.unsel_dev, (l.mk + 16) * sizeof(int32_t)));
+                }
+            }
             int nt = cfg->host_threads > 0 ? cfg->host_threads
                                            : (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
             c->pool = new Pool(nt);
@@ -1003,6 +1039,140 @@ zf_status refresh_pointer_tables(zf_ctx* c, int variant, bool refresh, void* con
         ZF_TRY(c->upload(c->d_upd_tab[variant], h.data(), nl * sizeof(UpdLayer), s));
         c->up_upd_tab[variant] = h;
     }
+    return ZF_OK;
+}
+
+}  // namespace
+
+// ============================================================ f1: deferred CPU AdamW (reading R18)
+namespace {
+
+uint16_t host_bf16_rne(float x) {
+    uint32_t u;
+    std::memcpy(&u, &x, 4);
+    if ((u & 0x7fffffffu) > 0x7f800000u) return (uint16_t)((u >> 16) | 0x40u);
+    u += 0x7fffu + ((u >> 16) & 1u);
+    return (uint16_t)(u >> 16);
+}
+
+float host_widen(const void* p, int dt, size_t i) {
+    if (dt == ZF_BF16) {
+        uint32_t u = (uint32_t) static_cast<const uint16_t*>(p)[i] << 16;
+        float f;
+        std::memcpy(&f, &u, 4);
+        return f;
+    }
+    return static_cast<const float*>(p)[i];
+}
+
+// At a refresh: columns entering the CPU-updated set take the parameter's current value as
+// their fp32 master with zero host moments/step count; then the new selection is recorded.
+zf_status f1_refresh(zf_ctx* c, void* const* params, cudaStream_t s) {
+    const int nl = (int)c->L.size();
+    std::vector<std::vector<int32_t>> nidx(nl);
+    for (int i = 0; i < nl; ++i) {
+        LayerState& l = c->L[i];
+        nidx[i].resize(l.k);
+        ZF_CUDA(cudaMemcpyAsync(nidx[i].data(), l.idx[c->cur], l.k * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        ZF_CUDA(cudaMemcpy2DAsync(l.p_mirror, l.d.m * c->psz, params[i], l.d.ld_param * c->psz, l.d.m * c->psz, l.d.n,
+                                  cudaMemcpyDeviceToHost, s));
+    }
+    ZF_CUDA(cudaStreamSynchronize(s));
+    for (int i = 0; i < nl; ++i) {
+        LayerState& l = c->L[i];
+        const int64_t m = l.d.m, n = l.d.n;
+        std::vector<char> was_cpu(m, 0), now_cpu(m, 1);
+        if (!l.idx_host.empty()) {
+            std::fill(was_cpu.begin(), was_cpu.end(), 1);
+            for (int32_t col : l.idx_host) was_cpu[col] = 0;
+        }
+        for (int32_t col : nidx[i]) now_cpu[col] = 0;
+        std::vector<int32_t> entering;
+        for (int64_t col = 0; col < m; ++col)
+            if (now_cpu[col] && !was_cpu[col]) entering.push_back((int32_t)col);
+        const int pdt = c->pdt;
+        c->pool->parallel_for(n, [&](int64_t b, int64_t e) {
+            for (int64_t r = b; r < e; ++r)
+                for (int32_t col : entering) {
+                    l.master[r * m + col] = host_widen(l.p_mirror, pdt, (size_t)(r * m + col));
+                    l.mh[r * m + col] = 0.0f;
+                    l.vh[r * m + col] = 0.0f;
+                }
+        });
+        for (int32_t col : entering) l.th[col] = 0;
+        l.idx_host = nidx[i];
+        l.unsel_host.clear();
+        for (int64_t col = 0; col < m; ++col)
+            if (now_cpu[col]) l.unsel_host.push_back((int32_t)col);
+        if (!l.unsel_host.empty())
+            ZF_CUDA(cudaMemcpy(l.unsel_dev, l.unsel_host.data(), l.unsel_host.size() * sizeof(int32_t),
+                               cudaMemcpyHostToDevice));
+    }
+    return ZF_OK;
+}
+
+// At a window end: one AdamW step (O6 op order, double-derived constants rounded once) with
+// the window's average gradient acc/S on the fp32 master of the unselected columns; the
+// rounded results are uploaded and scattered into the parameters.
+zf_status f1_window_end(zf_ctx* c, int64_t t, void* const* params, cudaStream_t s) {
+    const int S = c->cfg.accum_interval;
+    {
+        std::unique_lock<std::mutex> lk(c->mu);
+        c->cv.wait(lk, [&] { return c->h1_done >= t; });
+    }
+    const zf_adam_params& hp = c->cfg.adam;
+    const double lr = c->lr_cur, b1d = hp.beta1, b2d = hp.beta2;
+    const float b1 = (float)b1d, b2 = (float)b2d, omb1 = (float)(1.0 - b1d), omb2 = (float)(1.0 - b2d);
+    const float eps = (float)hp.eps, wd_f = (float)hp.weight_decay, decay = (float)(1.0 - lr * hp.weight_decay);
+    const int wd_mode = hp.weight_decay == 0.0 ? 0 : (hp.decoupled ? 1 : 2);
+    const float Sf = (float)S;
+    const int nl = (int)c->L.size();
+    for (int i = 0; i < nl; ++i) {
+        LayerState& l = c->L[i];
+        const int64_t m = l.d.m, n = l.d.n, mk = l.mk;
+        if (mk == 0) continue;
+        const float* acc = l.acc[(t / S) % 2];
+        std::vector<float> ss(mk), bc2s(mk);
+        for (int64_t u = 0; u < mk; ++u) {
+            const double tt = (double)(l.th[l.unsel_host[u]] + 1);
+            ss[u] = (float)(lr / (1.0 - std::pow(b1d, tt)));
+            bc2s[u] = (float)std::sqrt(1.0 - std::pow(b2d, tt));
+        }
+        const int pdt = c->pdt;
+        c->pool->parallel_for(n, [&](int64_t b, int64_t e) {
+            for (int64_t r = b; r < e; ++r) {
+                for (int64_t u = 0; u < mk; ++u) {
+                    const int64_t col = l.unsel_host[u];
+                    float g = acc[r * mk + u] / Sf;
+                    float p = l.master[r * m + col];
+                    float mm = l.mh[r * m + col], vv = l.vh[r * m + col];
+                    if (wd_mode == 1) p = p * decay;
+                    else if (wd_mode == 2) {
+                        const float wp = wd_f * p;
+                        g = g + wp;
+                    }
+                    const float a1 = b1 * mm, a2 = omb1 * g;
+                    mm = a1 + a2;
+                    const float c1 = b2 * vv, c2 = omb2 * g, c3 = c2 * g;
+                    vv = c1 + c3;
+                    const float den = std::sqrt(vv) / bc2s[u] + eps;
+                    const float upd = mm / den;
+                    const float delta = ss[u] * upd;
+                    p = p - delta;
+                    l.master[r * m + col] = p;
+                    l.mh[r * m + col] = mm;
+                    l.vh[r * m + col] = vv;
+                    if (pdt == ZF_BF16) static_cast<uint16_t*>(l.p_up)[r * mk + u] = host_bf16_rne(p);
+                    else static_cast<float*>(l.p_up)[r * mk + u] = p;
+                }
+            }
+        });
+        for (int64_t u = 0; u < mk; ++u) l.th[l.unsel_host[u]] += 1;
+        ZF_CUDA(cudaMemcpyAsync(l.p_up_dev, l.p_up, (size_t)n * mk * c->psz, cudaMemcpyHostToDevice, s));
+        ZF_CUDA(launch_scatter_unselected(params[i], pdt, l.d.ld_param, n, mk, l.unsel_dev, l.p_up_dev, s));
+        c->launches++;
+    }
+    ZF_CUDA(cudaStreamSynchronize(s));  // pinned upload buffers are reused next window
     return ZF_OK;
 }
 
@@ -1122,6 +1292,10 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t, void* const* grads, void* con
             }
             c->cv.notify_all();
         }
+    }
+    if (c->cfg.cpu_update) {
+        if (refresh) ZF_TRY(f1_refresh(c, params, s));
+        if ((t + 1) % c->cfg.accum_interval == 0) ZF_TRY(f1_window_end(c, t, params, s));
     }
     return ZF_OK;
 }

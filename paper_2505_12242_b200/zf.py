@@ -43,7 +43,8 @@ class LayerDesc(ctypes.Structure):
 class Config(ctypes.Structure):
     _fields_ = [("grad_dtype", ctypes.c_int32), ("param_dtype", ctypes.c_int32), ("topk_ppm", ctypes.c_int32),
                 ("refresh_interval", ctypes.c_int32), ("accum_interval", ctypes.c_int32), ("adam", AdamParams),
-                ("offload", ctypes.c_int32), ("host_accumulate", ctypes.c_int32), ("host_threads", ctypes.c_int32)]
+                ("offload", ctypes.c_int32), ("host_accumulate", ctypes.c_int32), ("host_threads", ctypes.c_int32),
+                ("cpu_update", ctypes.c_int32)]
 
 
 if not os.path.exists(_LIB_PATH):
@@ -195,7 +196,7 @@ class Context:
     def __init__(self, layers, grad_dtype=torch.bfloat16, param_dtype=torch.bfloat16, topk_ratio_ppm=100000,
                  refresh_interval=4, accum_interval=4, adam: AdamParams | None = None, offload=False,
                  host_accumulate=False, host_threads=0, world=1, rank=0, nccl_id: bytes | None = None,
-                 device: int | None = None):
+                 device: int | None = None, cpu_update=False):
         self.layers = [l if isinstance(l, LayerShape) else LayerShape(*l) for l in layers]
         descs = (LayerDesc * len(self.layers))()
         for d, l in zip(descs, self.layers):
@@ -213,6 +214,7 @@ class Context:
         cfg.offload = int(offload)
         cfg.host_accumulate = int(host_accumulate)
         cfg.host_threads = host_threads
+        cfg.cpu_update = int(cpu_update)
         self.cfg = cfg
         self.device = torch.cuda.current_device() if device is None else device
         h = ctypes.c_void_p()

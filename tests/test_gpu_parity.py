@@ -165,18 +165,18 @@ def test_compact_bitexact(zf, orc, gpu, n, m, dt, ld, ppm):
 
 # ------------------------------------------------------------------ zf_step vs oracle, multi-step
 def _run_stateful(zf, orc, gpu, shapes, gdt, pdt, ppm, N, S, steps, offload, lr=1e-3, wd=0.0, check_every=1,
-                  tie=False, ld_pad=0):
+                  tie=False, ld_pad=0, cpu_update=False):
     hp_o = orc.AdamHP(lr=lr, weight_decay=wd)
     ctx = zf.Context([zf.LayerShape(n, m, m + ld_pad, m + ld_pad) for n, m in shapes], grad_dtype=TDT[gdt],
                      param_dtype=TDT[pdt], topk_ratio_ppm=ppm, refresh_interval=N, accum_interval=S,
-                     adam=zf.adam_params(lr=lr, weight_decay=wd), offload=offload, host_accumulate=offload)
+                     adam=zf.adam_params(lr=lr, weight_decay=wd), offload=offload, host_accumulate=offload, cpu_update=cpu_update)
     scales = [gpu.ColScale(m, li) for li, (n, m) in enumerate(shapes)]
     Gs = [torch.empty(n, m + ld_pad, dtype=TDT[gdt], device="cuda")[:, :m] for n, m in shapes]
     Ps = [torch.empty(n, m + ld_pad, dtype=TDT[pdt], device="cuda")[:, :m] for n, m in shapes]
     for li, P in enumerate(Ps):
         gpu.fill_param(P, li)
-    layers = [orc.OracleLayer(n=n, m=m, ratio_ppm=ppm, refresh_interval=N, accum_interval=S, hp=hp_o)
-              for n, m in shapes]
+    layers = [orc.OracleLayer(n=n, m=m, ratio_ppm=ppm, refresh_interval=N, accum_interval=S, hp=hp_o,
+                              cpu_update=cpu_update) for n, m in shapes]
     Po = [np.ascontiguousarray(to_np(P)) for P in Ps]
     swaps = 0
     for t in range(steps):
@@ -227,6 +227,24 @@ def test_step_config1_fp32(zf, orc, gpu, NS):
     swaps, launches = _run_stateful(zf, orc, gpu, [(256, 512)], "fp32", "fp32", 100000, NS, NS, 8, offload=True)
     assert launches == 8 + 2 * (8 // NS)
     assert swaps == 0
+
+
+@pytest.mark.parametrize("NS,pdt,wd", [(1, "fp32", 0.0), (2, "fp32", 0.01), (4, "fp32", 0.0), (4, "bf16", 0.0),
+                                      (2, "bf16", 0.01)])
+def test_step_cpu_update(zf, orc, gpu, NS, pdt, wd):
+    """f1 (reading R18): the unselected columns take one AdamW step per window on the host
+    fp32 master with the window's average gradient; parameters bit-exact against the
+    oracle's deferred update, including migration at refreshes."""
+    swaps, launches = _run_stateful(zf, orc, gpu, [(256, 512), (37, 1001)], "bf16" if pdt == "bf16" else "fp32",
+                                    pdt, 100000, NS, NS, 9, offload=True, wd=wd, cpu_update=True)
+    assert launches == 9 + 2 * len(range(0, 9, NS)) + 2 * (9 // NS)
+    assert swaps == 0
+
+
+def test_cpu_update_needs_aligned_windows(zf):
+    with pytest.raises(zf.ZFError):
+        zf.Context([zf.LayerShape(8, 64)], refresh_interval=2, accum_interval=4, offload=True, host_accumulate=True,
+                   cpu_update=True)
 
 
 def test_step_config1_weight_decay(zf, orc, gpu):

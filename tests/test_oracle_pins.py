@@ -436,3 +436,63 @@ def test_step_all_important_equals_plain_optimizer(orc):
         tp.grad = torch.tensor(G)
         opt.step()
     assert np.allclose(P, tp.detach().numpy(), rtol=1e-6, atol=1e-9)
+
+
+# ------------------------------------------------------------------ f1: deferred CPU AdamW (reading R18)
+def test_f1_S1_constant_selection_is_plain_adamw(orc):
+    """S = N = 1 with a selection that never changes: the GPU side (selected columns) and the
+    deferred CPU side (the rest, flushed every step with the 1-step average) together are
+    plain AdamW on the whole matrix (SPEC S:268 degenerate interval; P:519-531 with S=1)."""
+    rng = np.random.default_rng(50)
+    n, m = 6, 20
+    P = (rng.standard_normal((n, m)) * 0.1).astype(np.float32)
+    tp = torch.nn.Parameter(torch.tensor(P.copy()))
+    opt = torch.optim.AdamW([tp], lr=1e-3, weight_decay=0.0, foreach=False)
+    L = orc.OracleLayer(n=n, m=m, ratio_ppm=150000, refresh_interval=1, accum_interval=1, cpu_update=True)
+    for t in range(8):
+        G = (rng.standard_normal((n, m)) * 0.01).astype(np.float32)
+        G[:, [3, 11, 17]] += 5.0                       # these three columns always selected
+        L.step(t, G, P)
+        assert L.idx.tolist() == [3, 11, 17]
+        tp.grad = torch.tensor(G)
+        opt.step()
+        assert np.allclose(P, tp.detach().numpy(), rtol=1e-6, atol=1e-9), t
+
+
+def test_f1_window_average_closed_form(orc):
+    """S = 2, constant gradient: an unselected column moves only at window ends, each time by
+    one bias-corrected AdamW step with the window average (= g): -lr*g/(|g|+eps) at its
+    first flush (theta^(c) -= alpha * (1/S) * sum over the window)."""
+    n, m = 4, 10
+    G = np.full((n, m), 0.25, np.float32)
+    G[:, 0] = 9.0                                      # column 0 selected (k = 1)
+    P = np.zeros((n, m), np.float32)
+    L = orc.OracleLayer(n=n, m=m, ratio_ppm=100000, refresh_interval=2, accum_interval=2, cpu_update=True)
+    L.step(0, G, P)
+    assert np.all(P[:, 1:] == 0.0)                     # mid-window: CPU columns unchanged
+    L.step(1, G, P)
+    want = -1e-3 * 0.25 / (0.25 + 1e-8)
+    assert np.allclose(P[:, 1:], want, rtol=1e-6)
+    assert L.th[1:].tolist() == [1] * (m - 1) and L.th[0] == 0
+    L.step(2, G, P)
+    assert np.allclose(P[:, 1:], want, rtol=1e-6)      # unchanged until the window ends
+    L.step(3, G, P)
+    assert np.allclose(P[:, 1:], 2 * want, rtol=1e-5)  # constant g: m_hat = g, v_hat = g^2 again
+
+
+def test_f1_migration_takes_current_value(orc):
+    """A column leaving the GPU-updated set takes the parameter's current value as its
+    fp32 master, with zero host moments and step count (reading R18)."""
+    n, m = 3, 8
+    P = np.zeros((n, m), np.float32)
+    L = orc.OracleLayer(n=n, m=m, ratio_ppm=125000, refresh_interval=2, accum_interval=2, cpu_update=True)
+    G = np.full((n, m), 0.5, np.float32)
+    G[:, 2] = 7.0                                      # window 0: column 2 on the GPU
+    L.step(0, G, P)
+    L.step(1, G, P)
+    p2 = P[:, 2].copy()
+    assert np.all(p2 != 0.0) and L.th[2] == 0
+    G2 = np.full((n, m), 0.5, np.float32)
+    G2[:, 5] = 7.0                                     # window 1: column 5 on the GPU, 2 back on the CPU
+    L.step(2, G2, P)
+    assert np.array_equal(L.master[:, 2], p2) and L.th[2] == 0 and np.all(L.Mh[:, 2] == 0)
