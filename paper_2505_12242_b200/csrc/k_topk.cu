@@ -26,6 +26,22 @@ constexpr int K2_THREADS = 1024;
 constexpr int K2_WARPS = K2_THREADS / 32;
 constexpr int64_t K2_SMEM_KEYS_MAX = 48 * 1024;  // keys held in shared memory up to this m
 
+// Unselected columns of one mask word, in order: ucol[j] = byte offset of the column in
+// its K3 segment's tile row.  j0 = index of the word's first unselected column.
+__device__ __forceinline__ void emit_ucol(uint16_t* ucol, uint32_t word, int64_t w, int64_t m, int64_t j0,
+                                          int64_t seg_cols, int gsz) {
+    uint32_t keep = ~word;
+    const int64_t cbase = w * 32;
+    if (cbase + 32 > m) keep &= (1u << (m - cbase)) - 1u;
+    const int64_t segoff = cbase % seg_cols;  // seg_cols is m or a multiple of 32
+    int64_t j = j0;
+    while (keep) {
+        const int b = __ffs(keep) - 1;
+        keep &= keep - 1u;
+        ucol[j++] = (uint16_t)((segoff + b) * gsz);
+    }
+}
+
 // Exclusive block-wide scan of one uint32 per thread; returns the prefix, total in *total.
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* warp_sums, uint32_t* total) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -165,6 +181,7 @@ k_topk(const __grid_constant__ Table<TopkLayer> table, int use_smem, int32_t old
         const uint32_t word = smask ? smask[w] : __ldcg(L.mask + w);
         if (smask) L.mask[w] = word;
         L.prefix[w] = (int32_t)pbase;
+        if (L.ucol) emit_ucol(L.ucol, word, w, m, w * 32 - pbase, L.seg_cols, L.gsz);
         pbase += __popc(word);
     }
     // ---- refresh remap: old slot of each new slot's column (reading R7)
@@ -186,7 +203,7 @@ k_topk(const __grid_constant__ Table<TopkLayer> table, int use_smem, int32_t old
 
 // Stateless helper: mask + prefix from a caller-provided ascending idx.
 __global__ void k_build_mask(const int32_t* __restrict__ idx, int64_t k, int64_t m, uint32_t* mask, int32_t* prefix,
-                             int32_t* bad) {
+                             uint16_t* ucol, int64_t seg_cols, int gsz, int32_t* bad) {
     __shared__ uint32_t warp_sums[K2_WARPS + 1];
     const int tid = threadIdx.x;
     const int64_t W = (m + 31) >> 5;
@@ -205,8 +222,10 @@ __global__ void k_build_mask(const int32_t* __restrict__ idx, int64_t k, int64_t
     uint32_t tot;
     uint32_t pbase = block_excl_scan(pc, warp_sums, &tot);
     for (int64_t w = w0; w < w1; ++w) {
+        const uint32_t word = __ldcg(mask + w);
         prefix[w] = (int32_t)pbase;
-        pbase += __popc(__ldcg(mask + w));
+        if (ucol) emit_ucol(ucol, word, w, m, w * 32 - pbase, seg_cols, gsz);
+        pbase += __popc(word);
     }
 }
 
@@ -238,9 +257,9 @@ cudaError_t launch_topk(const Table<TopkLayer>& t, int64_t max_m, int32_t old_de
     return cudaGetLastError();
 }
 
-cudaError_t launch_build_mask(const int32_t* idx, int64_t k, int64_t m, uint32_t* mask, int32_t* prefix, int32_t* bad,
-                              cudaStream_t s) {
-    k_build_mask<<<1, K2_THREADS, 0, s>>>(idx, k, m, mask, prefix, bad);
+cudaError_t launch_build_mask(const int32_t* idx, int64_t k, int64_t m, uint32_t* mask, int32_t* prefix,
+                              uint16_t* ucol, int64_t seg_cols, int gsz, int32_t* bad, cudaStream_t s) {
+    k_build_mask<<<1, K2_THREADS, 0, s>>>(idx, k, m, mask, prefix, ucol, seg_cols, gsz, bad);
     return cudaGetLastError();
 }
 

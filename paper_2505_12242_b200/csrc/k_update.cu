@@ -12,28 +12,25 @@
 // B200 design (DESIGN.md §5 K3).  HBM-bound: per element of G it moves 2 B of
 // G, 2(1-κ) B of compact output, and for the selected columns the read-modify-
 // write of p (in 32-byte sectors) and of the fp32 moments.
-//  - persistent grid, one 544-thread CTA per SM, warp-specialised: warp 0 is the
-//    producer, warps 1..16 consume.  Work units (R whole rows, or a 128-aligned
-//    column segment of one row) are claimed dynamically, one atomic per unit.
-//  - the producer stages EVERYTHING a unit needs into one of 4 shared-memory
-//    stage arenas with bulk copies (cp.async.bulk, the TMA engine) completing on
-//    one mbarrier: the G tile, the p tile (when the selection touches most of p's
-//    32-byte sectors), the moment slabs (or the old rows on a refresh), the slot
-//    step counts, the remap sources and the segment's mask/prefix words.  The
-//    host sizes units so the worst case fits an arena; 3 units stay in flight.
-//    Consumers issue no global loads.
-//  - a consumer warp takes 256-column row chunks; lane l owns 8 consecutive
-//    columns (one 16-byte shared load, one mask byte).  Its compact position is
-//    8l - (selected before it in the chunk), from the prefix word and a popcount;
-//    the unselected values go to a warp buffer that is streamed out with aligned
-//    16-byte stores (partial edges scalar).  The selected columns are listed by
-//    slot and updated with all 32 lanes busy (AdamW in shared memory, explicit
-//    round-to-nearest intrinsics, the oracle's op order); moments are stored
-//    coalesced; every 32-byte p sector holding a selected column is written back
-//    whole from the staged tile.
-//  - with offload, each consumer warp bumps a per-layer counter after its share
-//    of a unit (red.release); the copy stream waits on it (cuStreamWaitValue32)
-//    to start the layer's device->host copy.
+//  - persistent grid, one CTA per SM, warp-specialised: 4 producer warps (one
+//    thread each, one stage arena each) and 16 consumer warps in two groups of 8.
+//    Work units (R whole rows, or a 128-aligned column segment of one row) are
+//    claimed dynamically, one atomic per unit.
+//  - a producer stages EVERYTHING a unit needs into its 56 KB arena with bulk copies
+//    (cp.async.bulk, the TMA engine) completing on one mbarrier: the G tile, the p
+//    tile (when the selection touches most of p's 32-byte sectors), the moment slabs
+//    (or the old rows on a refresh), the slot step counts, column indices and remap
+//    sources, the mask words and the segment's list of unselected-column byte
+//    offsets (written by K2).  Consumers issue no global loads; waits are
+//    hardware-suspended (mbarrier.try_wait).
+//  - consumers: slot-major AdamW in shared memory (a slot's column, step count and
+//    bias corrections read once for all its rows; explicit round-to-nearest
+//    intrinsics in the oracle's op order), compaction by gather (4 outputs per
+//    thread per vector store, coalesced across the warp), then every 16-byte chunk
+//    of the p tile holding a selected column is written back with one vector store.
+//  - with offload, each consumer warp bumps a per-layer counter after its share of
+//    a unit (red.release); the copy stream waits on it (cuStreamWaitValue32) to
+//    start the layer's device->host copy.
 #include "zf_internal.cuh"
 
 namespace zf {
@@ -44,13 +41,9 @@ constexpr int K3_GROUPS = 2;                      // independent consumer groups
 constexpr int K3_GW = K3_NCW / K3_GROUPS;         // warps per group
 constexpr int K3_STAGES = 4;                      // stage arenas = producer warps (one chain per stage)
 constexpr int K3_THREADS = 32 * (K3_NCW + K3_STAGES);
-constexpr int K3_CHUNK = 512;                     // columns per warp block (32 lanes x 16)
-constexpr int K3_WBUF_BYTES = (K3_CHUNK + 16) * 4;
-constexpr int K3_WARP_BYTES = K3_WBUF_BYTES;
-constexpr int K3_PAIRS = 3;                       // AdamW (row, slot) pairs in flight per consumer thread
-constexpr int K3_ARENA = 48 * 1024;               // bytes per stage arena
-constexpr int K3_SMEM = K3_STAGES * K3_ARENA + K3_NCW * K3_WARP_BYTES;
-static_assert(K3_ARENA % 128 == 0 && K3_WARP_BYTES % 16 == 0, "alignment");
+constexpr int K3_ARENA = 56 * 1024;               // bytes per stage arena
+constexpr int K3_SMEM = K3_STAGES * K3_ARENA;
+static_assert(K3_ARENA % 128 == 0, "alignment");
 static_assert(K3_SMEM <= 227 * 1024 - 512, "shared memory budget");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -65,42 +58,16 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Hardware-suspended wait: try_wait parks the warp until the phase completes (or the
+// suspend-time hint elapses), so waiting warps take no issue slots from working ones.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-    // consumer-side wait: hardware try_wait, then short sleeps so that waiting warps do not
-    // take issue slots from the warps still working on a stage
-    uint32_t done = 0;
-    int ns = 16;
-    for (;;) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.b32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(phase)
-            : "memory");
-        if (done) return;
-        __nanosleep(ns);
-        ns = ns < 128 ? ns * 2 : 128;
-    }
-}
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
-    uint32_t done;
     asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.b32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(phase)
+        "{\n\t.reg .pred p;\n"
+        "ZF_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra ZF_WAIT;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(phase), "r"(0x989680u)
         : "memory");
-    return done != 0;
-}
-// producer-side wait: back off with nanosleep so spinning does not steal issue slots
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
-    int ns = 64;
-    while (!mbar_test(bar, phase)) {
-        __nanosleep(ns);
-        ns = ns < 512 ? ns * 2 : 512;
-    }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
     asm volatile(
@@ -127,38 +94,43 @@ __device__ __forceinline__ void st_cs_v4(void* p, uint4 v) {
                  : "memory");
 }
 
-__device__ __forceinline__ void sts16(void* p, uint16_t v) {
-    asm volatile("st.shared.u16 [%0], %1;" ::"r"(smem_u32(p)), "h"(v) : "memory");
-}
-__device__ __forceinline__ void sts32(void* p, uint32_t v) {
-    asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
-}
 __device__ __forceinline__ uint4 lds128(const void* p) {
     uint4 v;
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                  : "r"(smem_u32(p)) : "memory");
     return v;
 }
-template <typename B>
-__device__ __forceinline__ void sts_elem(B* p, B v) {
-    if constexpr (sizeof(B) == 2) sts16(p, v);
-    else sts32(p, v);
-}
-
-// Bulk-copy the 4-byte elements [e0, e1) of `src` to arena offset *off as an aligned
+// Bulk-copy the ESZ-byte elements [e0, e1) of `src` to arena offset *off as an aligned
 // superset (16-byte granules; the source arrays are padded).  Returns the element
 // offset of e0 within the copy; advances *off.
-__device__ __forceinline__ int stage_words(unsigned char* arena, int* off, const void* src, int64_t e0, int64_t e1,
+template <int ESZ>
+__device__ __forceinline__ int stage_elems(unsigned char* arena, int* off, const void* src, int64_t e0, int64_t e1,
                                            uint64_t* bar, uint32_t* tx, int* where) {
-    const int64_t a = e0 & ~int64_t(3), b = (e1 + 3) & ~int64_t(3);
+    constexpr int64_t G = 16 / ESZ;
+    const int64_t a = e0 & ~(G - 1), b = (e1 + G - 1) & ~(G - 1);
     *where = *off;
     if (b > a) {
-        const uint32_t bytes = (uint32_t)((b - a) * 4);
-        bulk_g2s(arena + *off, static_cast<const int32_t*>(src) + a, bytes, bar, 0ull);
+        const uint32_t bytes = (uint32_t)((b - a) * ESZ);
+        bulk_g2s(arena + *off, static_cast<const unsigned char*>(src) + a * ESZ, bytes, bar, 0ull);
         *tx += bytes;
         *off += (int)bytes;
     }
     return (int)(e0 - a);
+}
+
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+    uint16_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_v4(void* p, uint4 v) {
+    asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
 }
 
 __device__ __forceinline__ int find_layer_from(const Table<UpdLayer>& t, int64_t u, int hint) {
@@ -190,12 +162,15 @@ struct StageInfo {
     int64_t u;        // unit (-1: no more work)
     int32_t li;       // layer
     int32_t s0, s1;   // selected-slot range of the segment
-    int32_t oG, oP, oM, oV, oS, oSrc, oMask, oPre, oIdx;
-    int32_t eM, eV, eS, eSrc, eMask, ePre, eIdx;
+    int32_t oG, oP, oM, oV, oS, oSrc, oMask, oIdx, oU;
+    int32_t eM, eV, eS, eSrc, eMask, eIdx, eU;
     int32_t pstaged, mstaged, remap;
+    int32_t j0, nkeep;          // segment's first output index within a row / outputs per row
+    uint32_t mg_ns;             // ceil(2^24 / ns): x / ns == (x * mg_ns) >> 24 for x <= 256
     // unit geometry and layer fields, so consumers never touch the global layer table
-    int32_t Rr, sw, k, kin, ldp;
-    int64_t r0, c0, mk;
+    int32_t Rr, sw, k, kin;
+    int64_t ldp, out_ld;
+    int64_t r0, c0;
     void* P;                    // p + r0*ldp (row 0 of the unit)
     void* out;                  // compact block of the layer
     float* m_out;               // + r0*k
@@ -208,18 +183,92 @@ struct StageInfo {
     uint32_t* done;
 };
 
-template <int DT>
-__device__ __forceinline__ void load8(const typename Elt<DT>::bits* p, uint32_t (&w)[8 * Elt<DT>::SIZE / 4]);
-template <>
-__device__ __forceinline__ void load8<DT_BF16>(const uint16_t* p, uint32_t (&w)[4]) {
-    const uint4 v = *reinterpret_cast<const uint4*>(p);
-    w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
-}
-template <>
-__device__ __forceinline__ void load8<DT_F32>(const uint32_t* p, uint32_t (&w)[8]) {
-    const uint4 a = *reinterpret_cast<const uint4*>(p);
-    const uint4 b = *reinterpret_cast<const uint4*>(p + 4);
-    w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w; w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+// AdamW over one unit's (row, slot) pairs by the K3_GW*32 threads of a consumer group,
+// slot-major: a slot's column, step count and bias corrections are read once for all of
+// its rows.  PST: p tile staged (updated there, written back later); MST: moments, step
+// counts, column indices (and remap sources) staged; REMAP: refresh step (moments come from
+// the old slots).  Without MST the remap flag is read at run time (global-load path).
+template <int GDT, int PDT, bool PST, bool MST, bool REMAP>
+__device__ __forceinline__ void adam_unit(const StageInfo& si, unsigned char* A, const UpdParams& prm, int ctid,
+                                          uint32_t& nfacc) {
+    using GE = Elt<GDT>;
+    using PE = Elt<PDT>;
+    using GB = typename GE::bits;
+    using PB = typename PE::bits;
+    constexpr int NCT = K3_GW * 32;
+    const int sw = si.sw, Rr = si.Rr, ns = si.s1 - si.s0;
+    const int k = si.k, kin = si.kin, s0 = si.s0, c0 = (int)si.c0;
+    const bool remap = MST ? REMAP : (si.remap != 0);
+    const GB* sG = reinterpret_cast<const GB*>(A + si.oG);
+    PB* sP = reinterpret_cast<PB*>(A + si.oP);
+    const float* sM = reinterpret_cast<const float*>(A + si.oM) + si.eM;
+    const float* sV = reinterpret_cast<const float*>(A + si.oV) + si.eV;
+    const int32_t* sS = reinterpret_cast<const int32_t*>(A + si.oS) + si.eS;
+    const int32_t* sSrc = reinterpret_cast<const int32_t*>(A + si.oSrc) + si.eSrc;
+    const int32_t* sIdx = reinterpret_cast<const int32_t*>(A + si.oIdx) + si.eIdx;
+    PB* gP = static_cast<PB*>(si.P);
+    const int64_t ldp = si.ldp;
+    const int tdelta = prm.step_delta + 1;
+    int sl, rg, nrg;
+    if (ns >= NCT) {
+        sl = ctid; rg = 0; nrg = 1;
+    } else {  // fewer slots than threads: teams of ns threads split the rows
+        rg = (int)(((uint32_t)ctid * si.mg_ns) >> 24);  // ctid / ns (exact for ctid < 256)
+        nrg = (int)(((uint64_t)NCT * si.mg_ns) >> 24);   // NCT / ns
+        sl = ctid - rg * ns;
+        if (rg >= nrg) return;
+    }
+    for (; sl < ns; sl += NCT) {
+        const int s = s0 + sl;
+        int c, stp, src = 0;
+        if constexpr (MST) {
+            c = sIdx[sl];
+            stp = sS[sl];
+            if constexpr (REMAP) src = sSrc[sl];
+        } else {
+            c = __ldg(si.idx + s);
+            stp = __ldg(si.steps + s);
+            if (remap) src = __ldg(si.slot_src + s);
+        }
+        const float2 sb = adam_sb(stp + tdelta, prm.adam);
+        const int cl = c - c0;
+        const GB* g_ = sG + cl;
+        PB* p_ = PST ? sP + cl : gP + c;
+        const int pstride = PST ? sw : (int)0;
+        float* mo = si.m_out + s;
+        float* vo = si.v_out + s;
+#pragma unroll 2
+        for (int r = rg; r < Rr; r += nrg) {
+            const GB gb = g_[r * sw];
+            if constexpr (GE::SIZE == 2) nfacc |= ((uint32_t)gb & 0x7f80u) + 0x0080u;
+            else nfacc |= ((uint32_t)gb & 0x7f800000u) + 0x00800000u;
+            PB* pp = PST ? p_ + r * pstride : p_ + r * ldp;
+            float p = PE::to_f(*pp);
+            float mm, vv;
+            if constexpr (MST) {
+                if constexpr (REMAP) {
+                    mm = src >= 0 ? sM[r * kin + src] : 0.0f;
+                    vv = src >= 0 ? sV[r * kin + src] : 0.0f;
+                } else {
+                    mm = sM[r * k + sl];
+                    vv = sV[r * k + sl];
+                }
+            } else {
+                const int64_t row = si.r0 + r;
+                if (remap) {
+                    mm = src >= 0 ? __ldcs(si.m_in + row * kin + src) : 0.0f;
+                    vv = src >= 0 ? __ldcs(si.v_in + row * kin + src) : 0.0f;
+                } else {
+                    mm = __ldcs(si.m_in + row * k + s);
+                    vv = __ldcs(si.v_in + row * k + s);
+                }
+            }
+            adamw_elem_t(GE::to_f(gb), p, mm, vv, sb.x, sb.y, prm.adam);
+            *pp = PE::from_f(p);
+            __stcs(mo + r * k, mm);
+            __stcs(vo + r * k, vv);
+        }
+    }
 }
 
 template <int GDT, int PDT>
@@ -229,11 +278,9 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
     using GB = typename GE::bits;
     using PB = typename PE::bits;
     constexpr int GSZ = GE::SIZE, PSZ = PE::SIZE;
-    constexpr int VEC = GE::VEC;           // elements per 16 bytes
-    constexpr int NW8 = 8 * GSZ / 4;       // 32-bit words holding 8 elements
 
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t full[K3_STAGES], empty[K3_STAGES];
+    __shared__ __align__(8) uint64_t full[K3_STAGES], empty[K3_STAGES], gbar[K3_GROUPS];
     __shared__ StageInfo info[K3_STAGES];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -244,6 +291,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
             mbar_init(&full[st], 1);
             mbar_init(&empty[st], K3_GW);
         }
+        for (int g = 0; g < K3_GROUPS; ++g) mbar_init(&gbar[g], K3_GW);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -270,7 +318,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
                 si.s0 = g.c0 == 0 ? 0 : (g.c0 >= Lp->m ? (int32_t)Lp->k : __ldg(Lp->prefix + (g.c0 >> 5)));
                 si.s1 = g.c1 >= Lp->m ? (int32_t)Lp->k : __ldg(Lp->prefix + (g.c1 >> 5));
             }
-            if (it > 0) mbar_wait_sleep(&empty[st], (it - 1) & 1);
+            if (it > 0) mbar_wait(&empty[st], (it - 1) & 1);
             unsigned char* A = smem + st * K3_ARENA;
             if (si.u < 0) {
                 info[st] = si;
@@ -302,11 +350,15 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
                     for (int c = 0; c < sw; ++c) sG[r * sw + c] = G[(g.r0 + r) * L.ldg + g.c0 + c];
             }
             off = (g.Rr * sw * GSZ + 15) & ~15;
-            // mask + prefix words of the segment
+            // mask words of the segment (p write-back) and the segment's unselected-column list
             const int64_t w0 = g.c0 >> 5, nwm = (sw + 31) >> 5;
-            si.eMask = stage_words(A, &off, L.mask, w0, w0 + nwm, &full[st], &tx, &si.oMask);
-            si.ePre = stage_words(A, &off, L.prefix, w0, w0 + nwm, &full[st], &tx, &si.oPre);
+            si.eMask = stage_elems<4>(A, &off, L.mask, w0, w0 + nwm, &full[st], &tx, &si.oMask);
+            si.j0 = (int32_t)(g.c0 - si.s0);
+            si.nkeep = sw - ns;
+            if (prm.do_compact && si.nkeep > 0)
+                si.eU = stage_elems<2>(A, &off, L.ucol, si.j0, si.j0 + si.nkeep, &full[st], &tx, &si.oU);
             if (prm.do_adam && ns > 0) {
+                si.mg_ns = (uint32_t)(((1u << 24) + (uint32_t)ns - 1u) / (uint32_t)ns);
                 si.pstaged = L.p_tma;
                 si.mstaged = L.mv_tma;
                 if (si.pstaged) {
@@ -331,21 +383,22 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
                         e0 = g.r0 * L.k + si.s0;
                         e1 = (g.r0 + g.Rr - 1) * L.k + si.s1;
                     }
-                    si.eM = stage_words(A, &off, L.m_in, e0, e1, &full[st], &tx, &si.oM);
-                    si.eV = stage_words(A, &off, L.v_in, e0, e1, &full[st], &tx, &si.oV);
-                    si.eS = stage_words(A, &off, L.steps, si.s0, si.s1, &full[st], &tx, &si.oS);
-                    si.eIdx = stage_words(A, &off, L.idx, si.s0, si.s1, &full[st], &tx, &si.oIdx);
-                    if (L.slot_src) si.eSrc = stage_words(A, &off, L.slot_src, si.s0, si.s1, &full[st], &tx, &si.oSrc);
+                    si.eM = stage_elems<4>(A, &off, L.m_in, e0, e1, &full[st], &tx, &si.oM);
+                    si.eV = stage_elems<4>(A, &off, L.v_in, e0, e1, &full[st], &tx, &si.oV);
+                    si.eS = stage_elems<4>(A, &off, L.steps, si.s0, si.s1, &full[st], &tx, &si.oS);
+                    si.eIdx = stage_elems<4>(A, &off, L.idx, si.s0, si.s1, &full[st], &tx, &si.oIdx);
+                    if (L.slot_src)
+                        si.eSrc = stage_elems<4>(A, &off, L.slot_src, si.s0, si.s1, &full[st], &tx, &si.oSrc);
                 }
             }
             si.Rr = g.Rr;
             si.sw = sw;
             si.k = (int32_t)L.k;
             si.kin = (int32_t)L.k_in;
-            si.ldp = (int32_t)L.ldp;
+            si.ldp = L.ldp;
+            si.out_ld = L.out_ld;
             si.r0 = g.r0;
             si.c0 = g.c0;
-            si.mk = L.m - L.k;
             si.remap = L.slot_src != nullptr;
             si.P = static_cast<PB*>(L.P) + g.r0 * L.ldp;
             si.out = L.out;
@@ -364,22 +417,24 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
     }
 
     // ===================== consumer warps =====================
-    // AdamW: the unit's (row, slot) pairs are spread over all consumer threads; their loads
-    // are issued first so that their latency (global p when not staged) overlaps the
-    // compaction.  Compaction: each warp takes one contiguous run of 512-column blocks
-    // (row-major over the unit's rows); lane l of a block owns its columns 16l..16l+15; the
-    // unselected values go to the warp buffer, flushed with aligned 16-byte stores after
-    // every block (the < 16-byte remainder carries over).
-    const int cwa = warp - K3_STAGES;          // consumer warp index (warp-area slot)
+    // Two groups of K3_GW warps; group g consumes stages g, g+2, ...  Per unit:
+    //  (1) AdamW on the unit's (row, slot) pairs by all threads of the group, slot-major
+    //      (a slot's column, step count and bias corrections read once for all its rows);
+    //      p is updated in the staged tile (or in place in HBM when it was not staged);
+    //      each warp then arrives on the group's mbarrier (split phase: no waiting yet);
+    //  (2) compaction by gather, warp-wide windows of one row: lane l writes outputs
+    //      8l..8l+7 (bf16; 4 for fp32) of the window with one 16-byte store, reading the
+    //      staged tile at the listed unselected-column offsets;
+    //  (3) wait for the group's AdamW, then write back every 16-byte chunk of the p tile
+    //      holding a selected column (warp-wide windows, one chunk per lane).
+    const int cwa = warp - K3_STAGES;          // consumer warp index
     const int grp = cwa / K3_GW;               // consumer group
     const int cw = cwa - grp * K3_GW;          // warp index within the group
     const int ctid = cw * 32 + lane;
-    constexpr int NCT = K3_GW * 32;
-    unsigned char* warea = smem + K3_STAGES * K3_ARENA + cwa * K3_WARP_BYTES;
-    GB* wbuf = reinterpret_cast<GB*>(warea);
     uint32_t nfacc = 0;                // non-finite detector (exponent all-ones -> carry into the top bit)
-    __nv_bfloat162 nf2 = __float2bfloat162_rn(0.0f);  // bf16 tiles: NaN-propagating max of |x|
+    __nv_bfloat162 nf2 = __float2bfloat162_rn(0.0f);  // bf16: NaN-propagating max of |x|
     uint32_t finished = 0, phase = 0;  // per stage: end sentinel seen / mbarrier parity
+    uint32_t gphase = 0;               // parity of this group's AdamW-done barrier
 
     constexpr uint32_t kMine = [] {
         uint32_t m = 0;
@@ -406,231 +461,127 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
         const int sw = si.sw, Rr = si.Rr;
         unsigned char* A = smem + st * K3_ARENA;
         const GB* sG = reinterpret_cast<const GB*>(A + si.oG);
-        const uint32_t* smask = reinterpret_cast<const uint32_t*>(A + si.oMask) + si.eMask;
-        const int32_t* spre = reinterpret_cast<const int32_t*>(A + si.oPre) + si.ePre;
-
-        // ---------------- AdamW pair loads (first batch) ----------------
         const int ns = si.s1 - si.s0;
-        const int npairs = (prm.do_adam && prm.debug_mode == 0) ? Rr * ns : 0;
-        float ag[K3_PAIRS], am[K3_PAIRS], av[K3_PAIRS];
-        PB apb[K3_PAIRS];  // raw p bits: converted only in compute_pairs, so a global load's latency
-                           // is not waited for before the compaction
-        float ass[K3_PAIRS], abc[K3_PAIRS];  // bias corrections of each pair's step (table loads issued early)
-        int32_t pidx[K3_PAIRS], midx[K3_PAIRS];  // p / moment offsets from the unit's row 0
-        auto load_pairs = [&](int qb) {
-            const float inv_ns = 1.0f / (float)ns;
-            const int k = si.k, kin = si.kin, s0 = si.s0;
-            const bool pst = si.pstaged, mst = si.mstaged, remap = si.remap;
-            const PB* sP = reinterpret_cast<const PB*>(A + si.oP);
-            const float* sM = reinterpret_cast<const float*>(A + si.oM) + si.eM;
-            const float* sV = reinterpret_cast<const float*>(A + si.oV) + si.eV;
-            const int32_t* sS = reinterpret_cast<const int32_t*>(A + si.oS) + si.eS;
-            const int32_t* sSrc = reinterpret_cast<const int32_t*>(A + si.oSrc) + si.eSrc;
-            const int32_t* sIdx = reinterpret_cast<const int32_t*>(A + si.oIdx) + si.eIdx;
-            const int c0 = (int)si.c0;
-#pragma unroll
-            for (int b = 0; b < K3_PAIRS; ++b) {
-                const int q = qb + b * NCT + ctid;
-                pidx[b] = -1;
-                if (q < npairs) {
-                    int r = __float2int_rz((float)q * inv_ns);
-                    if (r * ns > q) --r;
-                    if ((r + 1) * ns <= q) ++r;
-                    const int sl = q - r * ns;
-                    const int s = s0 + sl;
-                    const int c = mst ? sIdx[sl] : __ldg(si.idx + s);
-                    const int cl = c - c0;
-                    ag[b] = GE::to_f(sG[r * sw + cl]);
-                    pidx[b] = r * si.ldp + c;
-                    apb[b] = pst ? sP[r * sw + cl] : static_cast<const PB*>(si.P)[pidx[b]];
-                    midx[b] = r * k + s;
-                    if (mst) {
-                        if (remap) {
-                            const int32_t src = sSrc[sl];
-                            am[b] = src >= 0 ? sM[r * kin + src] : 0.0f;
-                            av[b] = src >= 0 ? sV[r * kin + src] : 0.0f;
-                        } else {
-                            am[b] = sM[r * k + sl];
-                            av[b] = sV[r * k + sl];
+        const bool adam = prm.do_adam && (prm.debug_mode == 0 || prm.debug_mode == 3) && ns > 0;
+        const bool pwb = adam && si.pstaged;
+
+        // ---------------- (1) AdamW ----------------
+        if (adam) {
+            if (si.pstaged && si.mstaged) {
+                if (si.remap) adam_unit<GDT, PDT, true, true, true>(si, A, prm, ctid, nfacc);
+                else adam_unit<GDT, PDT, true, true, false>(si, A, prm, ctid, nfacc);
+            } else if (si.pstaged) {
+                adam_unit<GDT, PDT, true, false, false>(si, A, prm, ctid, nfacc);
+            } else if (si.mstaged) {
+                if (si.remap) adam_unit<GDT, PDT, false, true, true>(si, A, prm, ctid, nfacc);
+                else adam_unit<GDT, PDT, false, true, false>(si, A, prm, ctid, nfacc);
+            } else {
+                adam_unit<GDT, PDT, false, false, false>(si, A, prm, ctid, nfacc);
+            }
+        }
+        if (pwb) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&gbar[grp]);  // release: this warp's tile updates
+        }
+
+        // ---------------- (2) compaction by gather ----------------
+        const int nk = si.nkeep;
+        if (prm.do_compact && nk > 0 && prm.debug_mode != 3) {
+            constexpr int OPL = 16 / GSZ;              // outputs per lane (one 16-byte store)
+            const int j0 = si.j0;
+            const int old = (int)si.out_ld;
+            const uint16_t* sU = reinterpret_cast<const uint16_t*>(A + si.oU) + si.eU;
+            const uint32_t sGa = smem_u32(sG);
+            GB* out = static_cast<GB*>(si.out) + si.r0 * si.out_ld + j0;   // row 0, output 0 of the unit
+            if (old % OPL == 0) {
+                // q = qa + OPL*g has (j0 + q) % OPL == 0: aligned offset loads and stores
+                const int qa = min(nk, (OPL - (j0 & (OPL - 1))) & (OPL - 1));
+                const int ng = (nk - qa) / OPL;        // full groups per row
+                const int tail = nk - qa - OPL * ng;
+                const int nwin = (ng + 31) >> 5;       // 32-group windows per row
+                if (nwin > 0) {
+                    int r = 0, w = cw;
+                    while (w >= nwin) { w -= nwin; ++r; }
+                    for (; r < Rr;) {
+                        const int g = (w << 5) + lane;
+                        if (g < ng) {
+                            const int q = qa + OPL * g;
+                            const uint32_t rowa = sGa + (uint32_t)(r * sw * GSZ);
+                            uint4 o;
+                            if constexpr (GSZ == 2) {
+                                const uint4 u = lds128(sU + q);
+                                o.x = lds_u16(rowa + (u.x & 0xffffu)) | (lds_u16(rowa + (u.x >> 16)) << 16);
+                                o.y = lds_u16(rowa + (u.y & 0xffffu)) | (lds_u16(rowa + (u.y >> 16)) << 16);
+                                o.z = lds_u16(rowa + (u.z & 0xffffu)) | (lds_u16(rowa + (u.z >> 16)) << 16);
+                                o.w = lds_u16(rowa + (u.w & 0xffffu)) | (lds_u16(rowa + (u.w >> 16)) << 16);
+                                nf2 = __hmax2_nan(nf2, __hmax2_nan(__habs2(*reinterpret_cast<const __nv_bfloat162*>(&o.x)),
+                                                                   __habs2(*reinterpret_cast<const __nv_bfloat162*>(&o.y))));
+                                nf2 = __hmax2_nan(nf2, __hmax2_nan(__habs2(*reinterpret_cast<const __nv_bfloat162*>(&o.z)),
+                                                                   __habs2(*reinterpret_cast<const __nv_bfloat162*>(&o.w))));
+                            } else {
+                                // fp32: 4 offsets per lane (the first 8 bytes of u)
+                                const uint2 u2 = *reinterpret_cast<const uint2*>(sU + q);
+                                o.x = lds_u32(rowa + (u2.x & 0xffffu));
+                                o.y = lds_u32(rowa + (u2.x >> 16));
+                                o.z = lds_u32(rowa + (u2.y & 0xffffu));
+                                o.w = lds_u32(rowa + (u2.y >> 16));
+                                nfacc |= ((o.x & 0x7f800000u) + 0x00800000u) | ((o.y & 0x7f800000u) + 0x00800000u) |
+                                         ((o.z & 0x7f800000u) + 0x00800000u) | ((o.w & 0x7f800000u) + 0x00800000u);
+                            }
+                            st_cs_v4(out + r * old + q, o);
                         }
-                        const int32_t t = sS[sl] + prm.step_delta + 1;
-                        ass[b] = adam_ss(t, prm.adam);
-                        abc[b] = adam_bc2s(t, prm.adam);
+                        w += K3_GW;
+                        while (w >= nwin) { w -= nwin; ++r; }
+                    }
+                }
+                // per row: the qa head and the tail outputs
+                for (int i = ctid; i < Rr * 2 * OPL; i += K3_GW * 32) {
+                    const int r = i / (2 * OPL), e = i - r * (2 * OPL);
+                    int q;
+                    if (e < OPL) {
+                        if (e >= qa) continue;
+                        q = e;
                     } else {
-                        const int64_t row = si.r0 + r;
-                        if (remap) {
-                            const int32_t src = __ldg(si.slot_src + s);
-                            am[b] = src >= 0 ? __ldcs(si.m_in + row * kin + src) : 0.0f;
-                            av[b] = src >= 0 ? __ldcs(si.v_in + row * kin + src) : 0.0f;
-                        } else {
-                            am[b] = __ldcs(si.m_in + row * k + s);
-                            av[b] = __ldcs(si.v_in + row * k + s);
-                        }
-                        const int32_t t = __ldg(si.steps + s) + prm.step_delta + 1;
-                        ass[b] = adam_ss(t, prm.adam);
-                        abc[b] = adam_bc2s(t, prm.adam);
+                        if (e - OPL >= tail) continue;
+                        q = qa + OPL * ng + (e - OPL);
                     }
+                    const GB x = sG[r * sw + sU[q] / GSZ];
+                    if constexpr (GSZ == 2) nfacc |= ((uint32_t)x & 0x7f80u) + 0x0080u;
+                    else nfacc |= ((uint32_t)x & 0x7f800000u) + 0x00800000u;
+                    out[r * old + q] = x;
                 }
-            }
-        };
-        auto compute_pairs = [&]() {
-            PB* P = static_cast<PB*>(si.P);
-            float* Mo = si.m_out;
-            float* Vo = si.v_out;
-#pragma unroll
-            for (int b = 0; b < K3_PAIRS; ++b) {
-                if (pidx[b] < 0) continue;
-                float p = PE::to_f(apb[b]), mm = am[b], vv = av[b];
-                adamw_elem_t(ag[b], p, mm, vv, ass[b], abc[b], prm.adam);
-                P[pidx[b]] = PE::from_f(p);
-                __stcs(Mo + midx[b], mm);
-                __stcs(Vo + midx[b], vv);
-            }
-        };
-        // fast path: everything staged, steady step -> shared-memory operands only
-        const bool fast = si.pstaged && si.mstaged && !si.remap;
-        if (npairs > 0 && !fast) load_pairs(0);
-
-        // ---------------- compaction ----------------
-        const int nblk = (sw + K3_CHUNK - 1) / K3_CHUNK;
-        const int nq = Rr * nblk;
-        const int q0 = (nq * cw) / K3_GW, q1 = (nq * (cw + 1)) / K3_GW;
-        const bool vec = (sw % 8) == 0;  // rows of the staged tile are 16-byte aligned
-        GB* outp = static_cast<GB*>(si.out);
-        int r = q0 / nblk, cc = q0 - r * nblk;
-        int64_t obase = 0;   // global element index of wbuf[0] (16-byte aligned)
-        int pend = 0;        // elements in wbuf (including `skip` leading ones we do not own)
-        int skip = 0;
-
-        auto start_row = [&]() {
-            const int cl0 = cc * K3_CHUNK;
-            const int64_t gpos = (si.r0 + r) * si.mk + (si.c0 + cl0 - spre[cl0 >> 5]);
-            skip = (int)(gpos % VEC);
-            obase = gpos - skip;
-            pend = skip;
-        };
-        if (q0 < q1) start_row();
-        for (int q = q0; q < q1; ++q) {
-            const int cl0 = cc * K3_CHUNK, cl1 = min(sw, cl0 + K3_CHUNK);
-            // lane l owns columns cl0 + 256h + 8l .. +7 of the block's two halves h = 0, 1:
-            // 16-byte tile reads of a warp are contiguous (bank-conflict free)
-            const int base0 = spre[cl0 >> 5];
-            int keep_total = 0;
-            int u[2], nv[2];
-            uint32_t sb[2];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int c8 = cl0 + 256 * h + 8 * lane;
-                nv[h] = max(0, min(8, cl1 - c8));
-                const uint32_t word = nv[h] > 0 ? smask[c8 >> 5] : 0u;
-                const int sh = c8 & 31;
-                sb[h] = (word >> sh) & ((1u << nv[h]) - 1u);
-                const int selh = nv[h] > 0 ? (spre[c8 >> 5] - base0) + __popc(word & ((1u << sh) - 1u)) : 0;
-                u[h] = pend + (256 * h + 8 * lane) - selh;
-            }
-            keep_total = (cl1 - cl0) - (int)__reduce_add_sync(0xffffffffu, (unsigned)(__popc(sb[0]) + __popc(sb[1])));
-            const int blk_keep = keep_total;
-            const GB* srow = sG + r * sw;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int c8 = cl0 + 256 * h + 8 * lane;
-                const uint32_t selb = sb[h];
-                if (nv[h] == 8 && vec) {
-                    // branch-free scatter: the address steps back over each selected column, so
-                    // every kept element is one predicated store at an immediate offset from `a`
-                    uint32_t a = smem_u32(wbuf + u[h]);
-                    uint32_t w[NW8];
-                    load8<GDT>(srow + c8, w);
-#pragma unroll
-                    for (int i = 0; i < NW8; ++i) {
-                        if constexpr (GSZ == 2) nf2 = __hmax2_nan(nf2, __habs2(*reinterpret_cast<const __nv_bfloat162*>(&w[i])));
-                        else nfacc |= (w[i] & 0x7f800000u) + 0x00800000u;
-                    }
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        uint32_t x;
-                        if constexpr (GSZ == 2) x = (e & 1) ? (w[e >> 1] >> 16) : w[e >> 1];
-                        else x = w[e];
-                        if ((selb >> e) & 1u) a -= GSZ;
-                        else if constexpr (GSZ == 2) asm volatile("st.shared.u16 [%0], %1;" ::"r"(a + 2 * e), "r"(x) : "memory");
-                        else asm volatile("st.shared.u32 [%0], %1;" ::"r"(a + 4 * e), "r"(x) : "memory");
-                    }
-                } else {
-                    int uu = u[h];
-                    for (int e = 0; e < nv[h]; ++e) {
-                        const GB x = srow[c8 + e];
-                        if constexpr (GSZ == 2) nfacc |= ((uint32_t)x & 0x7f80u) + 0x0080u;
-                        else nfacc |= ((uint32_t)x & 0x7f800000u) + 0x00800000u;
-                        if (!((selb >> e) & 1u)) sts_elem(wbuf + uu++, x);
-                    }
+            } else {
+                // unaligned output rows (stateless primitive with a dense [n, m-k] block)
+                for (int i = ctid; i < Rr * nk; i += K3_GW * 32) {
+                    const int r = i / nk, q = i - r * nk;
+                    const GB x = sG[r * sw + sU[q] / GSZ];
+                    if constexpr (GSZ == 2) nfacc |= ((uint32_t)x & 0x7f80u) + 0x0080u;
+                    else nfacc |= ((uint32_t)x & 0x7f800000u) + 0x00800000u;
+                    out[r * old + q] = x;
                 }
-            }
-            __syncwarp();
-            pend += blk_keep;
-            // flush: full 16-byte chunks (all at a row/run end), carry the partial remainder
-            const bool fin = (cc + 1 == nblk) || (q + 1 == q1);
-            const int nfull = fin ? (pend + VEC - 1) / VEC : pend / VEC;
-            for (int ch = lane; ch < nfull; ch += 32) {
-                const int lo = ch * VEC;
-                if (lo >= skip && lo + VEC <= pend) {
-                    st_cs_v4(outp + obase + lo, lds128(wbuf + lo));
-                } else {
-                    for (int e = max(lo, skip); e < min(lo + VEC, pend); ++e) outp[obase + e] = wbuf[e];
-                }
-            }
-            __syncwarp();
-            if (!fin) {
-                const int rem = pend - nfull * VEC;
-                GB v = 0;
-                if (lane < rem) v = wbuf[nfull * VEC + lane];
-                __syncwarp();
-                if (lane < rem) sts_elem(wbuf + lane, v);
-                __syncwarp();
-                obase += nfull * VEC;
-                pend = rem;
-                if (nfull > 0) skip = 0;
-            }
-            if (++cc == nblk) {
-                cc = 0;
-                ++r;
-                if (q + 1 < q1) start_row();
             }
         }
 
-        // ---------------- AdamW compute + stores (then any further pair batches) ----------------
-        if (npairs > 0 && fast) {
-            const int k = si.k, s0 = si.s0, ldp = si.ldp, c0 = (int)si.c0;
+        // ---------------- (3) p write-back of the touched 16-byte chunks ----------------
+        if (pwb) {
+            mbar_wait(&gbar[grp], gphase);  // acquire: every warp of the group finished its AdamW
+            gphase ^= 1u;
+            constexpr int VP = 16 / PSZ;    // p columns per chunk
+            const uint32_t* smask = reinterpret_cast<const uint32_t*>(A + si.oMask) + si.eMask;
             const PB* sP = reinterpret_cast<const PB*>(A + si.oP);
-            const float* sM = reinterpret_cast<const float*>(A + si.oM) + si.eM;
-            const float* sV = reinterpret_cast<const float*>(A + si.oV) + si.eV;
-            const int32_t* sS = reinterpret_cast<const int32_t*>(A + si.oS) + si.eS;
-            const int32_t* sIdx = reinterpret_cast<const int32_t*>(A + si.oIdx) + si.eIdx;
-            PB* P = static_cast<PB*>(si.P);
-            float* Mo = si.m_out + s0;
-            float* Vo = si.v_out + s0;
-            const int tdelta = prm.step_delta + 1;
-            int r = ctid / ns, sl = ctid - r * ns;                 // one division per unit
-            const int dr = NCT / ns, dsl = NCT - dr * ns;
-            for (int q = ctid; q < npairs; q += NCT) {
-                const int c = sIdx[sl];
-                const int cl = c - c0;
-                const float g = GE::to_f(sG[r * sw + cl]);
-                float p = PE::to_f(sP[r * sw + cl]);
-                float mm = sM[r * k + sl], vv = sV[r * k + sl];
-                const int32_t t = sS[sl] + tdelta;
-                adamw_elem_t(g, p, mm, vv, adam_ss(t, prm.adam), adam_bc2s(t, prm.adam), prm.adam);
-                P[r * ldp + c] = PE::from_f(p);
-                __stcs(Mo + r * k + sl, mm);
-                __stcs(Vo + r * k + sl, vv);
-                r += dr;
-                sl += dsl;
-                if (sl >= ns) { sl -= ns; ++r; }
-            }
-        } else if (npairs > 0) {
-            compute_pairs();
-            for (int qb = K3_PAIRS * NCT; qb < npairs; qb += K3_PAIRS * NCT) {
-                load_pairs(qb);
-                compute_pairs();
+            PB* gP = static_cast<PB*>(si.P) + si.c0;
+            const int ldp = (int)si.ldp;
+            const int nwin = (sw + 32 * VP - 1) / (32 * VP);
+            int r = 0, w = cw;
+            while (w >= nwin) { w -= nwin; ++r; }
+            for (; r < Rr;) {
+                const int cl = (w * 32 + lane) * VP;
+                if (cl < sw) {
+                    const uint32_t bits = (smask[cl >> 5] >> (cl & 31)) & ((1u << VP) - 1u);
+                    if (bits) st_v4(gP + r * ldp + cl, lds128(sP + r * sw + cl));
+                }
+                w += K3_GW;
+                while (w >= nwin) { w -= nwin; ++r; }
             }
         }
         // stage fully consumed by this warp

@@ -95,6 +95,18 @@ std::vector<float> make_bc2(double b2) {
     return t;
 }
 
+// {ss[t], bc2s[t]} interleaved over the longer of the two tables, the shorter one's limit
+// filled in beyond its end (one 8-byte load per slot in K3).
+std::vector<float> make_sb(const std::vector<float>& ss, const std::vector<float>& bc2, double lr) {
+    const size_t n = std::max(ss.size(), bc2.size());
+    std::vector<float> t(2 * n);
+    for (size_t i = 0; i < n; ++i) {
+        t[2 * i] = i < ss.size() ? ss[i] : (float)lr;
+        t[2 * i + 1] = i < bc2.size() ? bc2[i] : 1.0f;
+    }
+    return t;
+}
+
 zf_status check_hp(const zf_adam_params* hp) {
     if (!hp) return fail(ZF_EINVAL, "hp is NULL");
     if (!(hp->lr >= 0.0f) || !std::isfinite(hp->lr)) return fail(ZF_EINVAL, "lr must be finite and >= 0");
@@ -126,6 +138,7 @@ struct TabCache {
     std::mutex mu;
     std::map<std::tuple<int, uint64_t, uint64_t>, std::pair<float*, int>> ss;  // (dev, lr, b1)
     std::map<std::pair<int, uint64_t>, std::pair<float*, int>> bc2;              // (dev, b2)
+    std::map<std::tuple<int, uint64_t, uint64_t, uint64_t>, std::pair<float*, int>> sb;  // (dev, lr, b1, b2)
 };
 TabCache& tab_cache() {
     static TabCache* c = new TabCache();
@@ -168,10 +181,20 @@ zf_status cached_tables(const zf_adam_params& hp, cudaStream_t s, AdamK* a) {
         ZF_TRY(upload_table(h, &d, s));
         jt = c.bc2.emplace(kb, std::make_pair(d, (int)h.size())).first;
     }
+    auto kq = std::make_tuple(dev, dbits(hp.lr), dbits(hp.beta1), dbits(hp.beta2));
+    auto qt = c.sb.find(kq);
+    if (qt == c.sb.end()) {
+        auto h = make_sb(make_ss(hp.lr, hp.beta1), make_bc2(hp.beta2), hp.lr);
+        float* d = nullptr;
+        ZF_TRY(upload_table(h, &d, s));
+        qt = c.sb.emplace(kq, std::make_pair(d, (int)(h.size() / 2))).first;
+    }
     a->ss_tab = it->second.first;
     a->ss_len = it->second.second;
     a->bc2_tab = jt->second.first;
     a->bc2_len = jt->second.second;
+    a->sb_tab = reinterpret_cast<const float2*>(qt->second.first);
+    a->sb_len = qt->second.second;
     return ZF_OK;
 }
 
@@ -190,13 +213,14 @@ bool k3_p_dense(int64_t m, int64_t k, int psz) {
 }
 
 // Worst-case bytes one K3 unit stages (R rows x c columns): G tile, p tile (if dense),
-// mask + prefix words, moment slabs (R*k: also covers the old rows of a refresh),
+// mask words, the unselected-column list, moment slabs (R*k: also covers the old rows of a refresh),
 // step counts and remap sources; each as a 16-byte-granular superset.
 int64_t k3_unit_bytes(int64_t R, int64_t c, int64_t k, int gsz, int psz, bool p_dense, bool mv) {
     auto a16 = [](int64_t b) { return (b + 15) & ~int64_t(15); };
     int64_t b = a16(R * c * gsz) + 2 * ((c + 31) / 32 + 8) * 4;
     if (p_dense) b += a16(R * c * psz);
     if (mv) b += 2 * (R * k + 8) * 4 + 3 * (std::min(c, k) + 8) * 4;  // moments; steps, sources, idx
+    b += a16((c + 8) * 2);                                              // unselected-column offsets
     return b;
 }
 
@@ -374,12 +398,14 @@ extern "C" zf_status zf_compact_unselected(const void* G, zf_dtype gdt, int64_t 
     uint32_t* mask = nullptr;
     int32_t* prefix = nullptr;
     int32_t* bad = nullptr;
+    uint16_t* ucol = nullptr;
     ZF_TRY(sc.get(&mask, (W + 8) * sizeof(uint32_t), true));    // padded: K3 stages words in 16-byte groups
     ZF_TRY(sc.get(&prefix, (W + 8) * sizeof(int32_t), true));
+    ZF_TRY(sc.get(&ucol, (m - k + 16) * sizeof(uint16_t), true));
     ZF_TRY(sc.get(&bad, sizeof(int32_t), true));
     ZF_TRY(sc.get(&prm.claim, sizeof(uint32_t), true));
-    ZF_CUDA(launch_build_mask(idx, k, m, mask, prefix, bad, s));
     const K3Geom geo = k3_geom(n, m, k, gsz, gsz, false, false);
+    ZF_CUDA(launch_build_mask(idx, k, m, mask, prefix, ucol, geo.seg_cols, gsz, bad, s));
     L.G = G;
     L.n = n;
     L.m = m;
@@ -388,7 +414,9 @@ extern "C" zf_status zf_compact_unselected(const void* G, zf_dtype gdt, int64_t 
     L.idx = idx;
     L.mask = mask;
     L.prefix = prefix;
+    L.ucol = ucol;
     L.out = out;
+    L.out_ld = m - k;
     L.seg_cols = geo.seg_cols;
     L.nseg = geo.nseg;
     L.R = geo.R;
@@ -411,6 +439,7 @@ typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned 
 struct LayerState {
     zf_layer_desc d{};
     int64_t k = 0, W = 0, mk = 0;
+    int64_t mk_pad = 0;               // device compact block row pitch (16-byte rows)
     // K1
     int32_t nrb = 0, ncb = 0;
     int64_t norm_off = 0, norm_unit_begin = 0;
@@ -420,6 +449,7 @@ struct LayerState {
     int32_t* idx[2] = {nullptr, nullptr};
     uint32_t* mask[2] = {nullptr, nullptr};
     int32_t* prefix[2] = {nullptr, nullptr};
+    uint16_t* ucol[2] = {nullptr, nullptr};
     int32_t* steps[2] = {nullptr, nullptr};
     int32_t* slot_src = nullptr;
     float* mom[2] = {nullptr, nullptr};
@@ -545,6 +575,8 @@ struct zf_ctx {
     AdamK adam{};
     float* d_ss = nullptr;
     float* d_bc2 = nullptr;
+    float* d_sb = nullptr;
+    std::vector<float> bc2_host;
     double lr_cur = 0.0, lr_uploaded = -1.0;
     // step state
     int cur = 0;
@@ -753,6 +785,9 @@ zf_status build_tables(zf_ctx* c) {
             }
             t.slot_src = l.slot_src;
             t.new_steps = l.steps[nw];
+            t.ucol = l.ucol[nw];
+            t.seg_cols = l.geo.seg_cols;
+            t.gsz = c->gsz;
         }
         ZF_TRY(c->dalloc(&c->d_topk_tab[v], nl * sizeof(TopkLayer)));
         ZF_CUDA(cudaMemcpy(c->d_topk_tab[v], h.data(), nl * sizeof(TopkLayer), cudaMemcpyHostToDevice));
@@ -783,6 +818,8 @@ zf_status build_tables(zf_ctx* c) {
             t.k_in = l.k;
             t.steps = l.steps[nw];
             t.out = l.stage_dev[sb < c->n_stage ? sb : 0];
+            t.out_ld = l.mk_pad;
+            t.ucol = l.ucol[nw];
             t.done = c->cfg.offload ? c->done + i : nullptr;
             t.seg_cols = l.geo.seg_cols;
             t.nseg = l.geo.nseg;
@@ -808,6 +845,11 @@ zf_status upload_ss(zf_ctx* c, cudaStream_t s) {
     ZF_TRY(c->upload(c->d_ss, h.data(), h.size() * sizeof(float), s));
     c->adam.ss_tab = c->d_ss;
     c->adam.ss_len = (int)h.size();
+    auto sb = make_sb(h, c->bc2_host, c->lr_cur);
+    if (!c->d_sb) ZF_TRY(c->dalloc(&c->d_sb, (std::max<int64_t>(SS_CAP, (int64_t)c->bc2_host.size())) * 2 * sizeof(float), false));
+    ZF_TRY(c->upload(c->d_sb, sb.data(), sb.size() * sizeof(float), s));
+    c->adam.sb_tab = reinterpret_cast<const float2*>(c->d_sb);
+    c->adam.sb_len = (int)(sb.size() / 2);
     c->adam.ss_inf = (float)c->lr_cur;
     c->adam.decay = (float)(1.0 - c->lr_cur * c->cfg.adam.weight_decay);
     c->lr_uploaded = c->lr_cur;
@@ -873,6 +915,7 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
         l.k = zf_k_for(l.d.m, cfg->topk_ppm);
         l.W = (l.d.m + 31) / 32;
         l.mk = l.d.m - l.k;
+        l.mk_pad = (l.mk + 7) & ~int64_t(7);
         l.nrb = (int32_t)((l.d.n + rb - 1) / rb);
         l.ncb = (int32_t)((l.d.m + cb - 1) / cb);
         l.norm_off = c->total_m;
@@ -897,13 +940,14 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
             ZF_CTRY(c->dalloc(&l.idx[s], (k + 16) * sizeof(int32_t)));  // padded (K3 bulk copies)
             ZF_CTRY(c->dalloc(&l.mask[s], (l.W + 8) * sizeof(uint32_t)));   // padded (K3 bulk copies)
             ZF_CTRY(c->dalloc(&l.prefix[s], (l.W + 8) * sizeof(int32_t)));
+            ZF_CTRY(c->dalloc(&l.ucol[s], (l.mk + 16) * sizeof(uint16_t)));  // padded (K3 bulk copies)
             // padded by 16 elements: K3 stages these with 16-byte-granular bulk copies
             ZF_CTRY(c->dalloc(&l.steps[s], (k + 16) * sizeof(int32_t)));
             ZF_CTRY(c->dalloc(&l.mom[s], ((size_t)n * k + 16) * sizeof(float)));
             ZF_CTRY(c->dalloc(&l.vel[s], ((size_t)n * k + 16) * sizeof(float)));
         }
         ZF_CTRY(c->dalloc(&l.slot_src, (k + 16) * sizeof(int32_t)));
-        for (int s = 0; s < c->n_stage; ++s) ZF_CTRY(c->dalloc(&l.stage_dev[s], (size_t)n * l.mk * c->gsz, false));
+        for (int s = 0; s < c->n_stage; ++s) ZF_CTRY(c->dalloc(&l.stage_dev[s], (size_t)n * l.mk_pad * c->gsz, false));
     }
     {
         int32_t* h = nullptr;
@@ -916,7 +960,9 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
     // ---- AdamW tables
     c->adam = adam_scalars(cfg->adam);
     // ---- table upload ring
-    c->ring_bytes = std::max<size_t>({n_layers * sizeof(UpdLayer), n_layers * sizeof(NormLayer), SS_CAP * sizeof(float)});
+    c->bc2_host = make_bc2(cfg->adam.beta2);
+    c->ring_bytes = std::max<size_t>({n_layers * sizeof(UpdLayer), n_layers * sizeof(NormLayer), SS_CAP * sizeof(float),
+                                      std::max<size_t>(SS_CAP, c->bc2_host.size()) * 2 * sizeof(float)});
     for (int i = 0; i < 4; ++i) {
         unsigned char* b = nullptr;
         ZF_CUDA(cudaMallocHost(&b, c->ring_bytes));
@@ -927,7 +973,7 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
         c->ring_ev.push_back(e);
     }
     {
-        auto h = make_bc2(cfg->adam.beta2);
+        const auto& h = c->bc2_host;
         ZF_CTRY(c->dalloc(&c->d_bc2, h.size() * sizeof(float), false));
         ZF_CUDA(cudaMemcpy(c->d_bc2, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
         c->adam.bc2_tab = c->d_bc2;
@@ -1278,9 +1324,9 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t, void* const* grads, void* con
                     ZF_CUDA(cudaStreamWaitEvent(c->copy_stream, c->step_done, 0));
                 }
             }
-            const size_t bytes = (size_t)l.d.n * l.mk * c->gsz;
-            if (bytes) ZF_CUDA(cudaMemcpyAsync(l.stage_host[sb], l.stage_dev[sb], bytes, cudaMemcpyDeviceToHost,
-                                               c->copy_stream));
+            // pitched device block -> dense host block [n, m-k]
+            if (l.mk) ZF_CUDA(cudaMemcpy2DAsync(l.stage_host[sb], l.mk * c->gsz, l.stage_dev[sb], l.mk_pad * c->gsz,
+                                                l.mk * c->gsz, l.d.n, cudaMemcpyDeviceToHost, c->copy_stream));
             ZF_CUDA(cudaEventRecord(l.d2h_ev[sb], c->copy_stream));
         }
         ZF_CUDA(cudaEventRecord(c->d2h_all[sb], c->copy_stream));
@@ -1350,11 +1396,13 @@ extern "C" zf_status zf_optimizer_state(zf_ctx* c, int32_t layer, const float** 
     return ZF_OK;
 }
 
-extern "C" zf_status zf_compact_buffer(zf_ctx* c, int32_t layer, const void** dev, const void** host) {
+extern "C" zf_status zf_compact_buffer(zf_ctx* c, int32_t layer, const void** dev, int64_t* dev_ld,
+                                       const void** host) {
     if (!c || layer < 0 || layer >= (int)c->L.size()) return fail(ZF_EINVAL, "bad ctx/layer");
     if (c->last_t < 0) return fail(ZF_ESTATE, "no step yet");
     const int sb = (int)(c->last_t % c->n_stage);
     if (dev) *dev = c->L[layer].stage_dev[sb];
+    if (dev_ld) *dev_ld = c->L[layer].mk_pad;
     if (host) *host = c->cfg.offload ? c->L[layer].stage_host[sb] : nullptr;
     return ZF_OK;
 }

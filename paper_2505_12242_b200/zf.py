@@ -75,7 +75,7 @@ lib.zf_selected.argtypes = [_vp, _i32, ctypes.POINTER(_vp), ctypes.POINTER(_i64)
 lib.zf_norms.argtypes = [_vp, _i32, ctypes.POINTER(_vp)]; lib.zf_norms.restype = _st
 lib.zf_optimizer_state.argtypes = [_vp, _i32, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp)]
 lib.zf_optimizer_state.restype = _st
-lib.zf_compact_buffer.argtypes = [_vp, _i32, ctypes.POINTER(_vp), ctypes.POINTER(_vp)]
+lib.zf_compact_buffer.argtypes = [_vp, _i32, ctypes.POINTER(_vp), ctypes.POINTER(_i64), ctypes.POINTER(_vp)]
 lib.zf_compact_buffer.restype = _st
 lib.zf_host_accumulator.argtypes = [_vp, _i32, _i32, ctypes.POINTER(_vp), ctypes.POINTER(_i64),
                                     ctypes.POINTER(_i64)]
@@ -278,16 +278,18 @@ class Context:
                 _view(s.value, (k,), torch.int32))
 
     def compact_buffer(self, layer: int) -> torch.Tensor:
-        d, h = ctypes.c_void_p(), ctypes.c_void_p()
-        _check(lib.zf_compact_buffer(self._h, layer, ctypes.byref(d), ctypes.byref(h)), "zf_compact_buffer")
+        """Device compact block [n, m-k] (a strided view: rows are padded to 16 bytes)."""
+        d, ld, h = ctypes.c_void_p(), ctypes.c_int64(), ctypes.c_void_p()
+        _check(lib.zf_compact_buffer(self._h, layer, ctypes.byref(d), ctypes.byref(ld), ctypes.byref(h)),
+               "zf_compact_buffer")
         n, mk = self.layers[layer].n, self.layers[layer].m - self.k[layer]
-        return _view(d.value, (n, mk), self.grad_dtype)
+        return _view(d.value, (n, ld.value), self.grad_dtype)[:, :mk]
 
     def compact_host(self, layer: int):
         """numpy view of the pinned host copy (valid after sync()); bf16 as uint16 bits."""
         import numpy as np
         d, h = ctypes.c_void_p(), ctypes.c_void_p()
-        _check(lib.zf_compact_buffer(self._h, layer, ctypes.byref(d), ctypes.byref(h)), "zf_compact_buffer")
+        _check(lib.zf_compact_buffer(self._h, layer, ctypes.byref(d), None, ctypes.byref(h)), "zf_compact_buffer")
         if not h.value:
             return None
         n, mk = self.layers[layer].n, self.layers[layer].m - self.k[layer]
