@@ -195,11 +195,12 @@ zf_status zf_selected(zf_ctx* ctx, int32_t layer, const int32_t** idx, int64_t* 
 zf_status zf_norms(zf_ctx* ctx, int32_t layer, const float** norms);                  /* device [m], last refresh */
 zf_status zf_optimizer_state(zf_ctx* ctx, int32_t layer, const float** exp_avg, const float** exp_avg_sq,
                              const int32_t** step);                                   /* device [n,k],[n,k],[k] */
-/* Compact block of the last step: device [n, m-k] with row pitch *dev_ld elements
+/* Compact block of the last step: device [n, m-k] with row pitch *ld elements
  * (m-k rounded up to a multiple of 8, so every row starts 16-byte aligned), and,
- * with offload, its dense pinned host copy [n, m-k] once zf_sync returned (NULL
- * otherwise).  Any out pointer may be NULL. */
-zf_status zf_compact_buffer(zf_ctx* ctx, int32_t layer, const void** dev, int64_t* dev_ld, const void** host);
+ * with offload, its pinned host copy (same layout and pitch) once zf_sync returned
+ * (NULL otherwise).  The host accumulators are dense [n, m-k].  Any out pointer may
+ * be NULL. */
+zf_status zf_compact_buffer(zf_ctx* ctx, int32_t layer, const void** dev, int64_t* ld, const void** host);
 /* Host accumulator [host] fp32 [rows, cols] = [n, m-k]: which = 0 the active
  * window's buffer, 1 the last sealed window's buffer (NULL if none yet). */
 zf_status zf_host_accumulator(zf_ctx* ctx, int32_t layer, int32_t which, const float** host, int64_t* rows,

@@ -40,8 +40,14 @@ def _stale(target: str, sources: list[str]) -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     nccl = _nccl_dir()
-    common = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-ffp-contract=off", "-Xptxas", "-v" if verbose else "-O3",
+    extra = os.environ.get("ZF_NVCC_EXTRA", "").split()
+    common = ARCH + extra + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-ffp-contract=off", "-Xptxas", "-v" if verbose else "-O3",
                      "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nccl, "include")]
+    # a change of compile flags (e.g. ZF_NVCC_EXTRA experiments) forces a rebuild
+    stamp = os.path.join(BUILD, "flags.txt")
+    flags = " ".join(common)
+    if not os.path.exists(stamp) or open(stamp).read() != flags:
+        force = True
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     hdrs = sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(ROOT, "include", "zf.h")]
     objs = []
@@ -67,6 +73,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             ["-L", os.path.join(nccl, "lib"), "-l:libnccl.so.2", "-Xlinker", f"-rpath,{os.path.join(nccl, 'lib')}",
              "-lpthread"])
         os.replace(LIBZF + ".tmp", LIBZF)
+    with open(stamp, "w") as f:
+        f.write(flags)
     synth_src = os.path.join(ROOT, "synth", "synth.cu")
     if force or _stale(LIBSYNTH, [synth_src]):
         run([NVCC] + ARCH + ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", synth_src, "-o", LIBSYNTH + ".tmp"])

@@ -36,12 +36,24 @@
 namespace zf {
 namespace {
 
-constexpr int K3_NCW = 16;                        // consumer warps
-constexpr int K3_GROUPS = 2;                      // independent consumer groups; group g owns stages g, g+2, ...
+#ifndef ZF_K3_NCW
+#define ZF_K3_NCW 16
+#endif
+constexpr int K3_NCW = ZF_K3_NCW;                 // consumer warps
+#ifndef ZF_K3_GROUPS
+#define ZF_K3_GROUPS 2
+#endif
+constexpr int K3_GROUPS = ZF_K3_GROUPS;           // independent consumer groups; group g owns stages g, g+G, ...
 constexpr int K3_GW = K3_NCW / K3_GROUPS;         // warps per group
-constexpr int K3_STAGES = 4;                      // stage arenas = producer warps (one chain per stage)
+#ifndef ZF_K3_STAGES
+#define ZF_K3_STAGES 4
+#endif
+#ifndef ZF_K3_ARENA_KB
+#define ZF_K3_ARENA_KB 56
+#endif
+constexpr int K3_STAGES = ZF_K3_STAGES;           // stage arenas = producer warps (one chain per stage)
 constexpr int K3_THREADS = 32 * (K3_NCW + K3_STAGES);
-constexpr int K3_ARENA = 56 * 1024;               // bytes per stage arena
+constexpr int K3_ARENA = ZF_K3_ARENA_KB * 1024;   // bytes per stage arena
 constexpr int K3_SMEM = K3_STAGES * K3_ARENA;
 static_assert(K3_ARENA % 128 == 0, "alignment");
 static_assert(K3_SMEM <= 227 * 1024 - 512, "shared memory budget");
@@ -58,16 +70,26 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-// Hardware-suspended wait: try_wait parks the warp until the phase completes (or the
-// suspend-time hint elapses), so waiting warps take no issue slots from working ones.
+// Hardware-suspended wait: try_wait parks the warp until the phase completes or a
+// hardware time window elapses, so waiting warps take few issue slots from working ones.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+#ifdef ZF_MBAR_HINT
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "ZF_WAIT:\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra ZF_WAIT;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(phase), "r"(0x989680u)
+        "r"(phase), "r"(ZF_MBAR_HINT)
         : "memory");
+#else
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "ZF_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra ZF_WAIT;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+#endif
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
     asm volatile(
@@ -166,7 +188,7 @@ struct StageInfo {
     int32_t eM, eV, eS, eSrc, eMask, eIdx, eU;
     int32_t pstaged, mstaged, remap;
     int32_t j0, nkeep;          // segment's first output index within a row / outputs per row
-    uint32_t mg_ns;             // ceil(2^24 / ns): x / ns == (x * mg_ns) >> 24 for x <= 256
+    uint32_t mg_ns;             // ceil(2^24 / ns): x / ns == (x * mg_ns) >> 24 for x <= 512
     // unit geometry and layer fields, so consumers never touch the global layer table
     int32_t Rr, sw, k, kin;
     int64_t ldp, out_ld;
@@ -213,7 +235,7 @@ __device__ __forceinline__ void adam_unit(const StageInfo& si, unsigned char* A,
     if (ns >= NCT) {
         sl = ctid; rg = 0; nrg = 1;
     } else {  // fewer slots than threads: teams of ns threads split the rows
-        rg = (int)(((uint32_t)ctid * si.mg_ns) >> 24);  // ctid / ns (exact for ctid < 256)
+        rg = (int)(((uint64_t)ctid * si.mg_ns) >> 24);  // ctid / ns (exact for ctid <= 512)
         nrg = (int)(((uint64_t)NCT * si.mg_ns) >> 24);   // NCT / ns
         sl = ctid - rg * ns;
         if (rg >= nrg) return;

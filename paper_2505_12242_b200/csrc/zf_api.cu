@@ -686,6 +686,35 @@ zf_ctx::~zf_ctx() {
     if (aux) cudaStreamDestroy(aux);
 }
 
+// One row of H1 (fp32 adds in step order; a window's first step writes 0 + x).  Cloned for
+// the host's vector ISA; -ffp-contract=off keeps every add a single IEEE operation.
+__attribute__((target_clones("avx512f", "avx2", "default")))
+void acc_row_bf16(float* __restrict__ acc, const uint16_t* __restrict__ src, int64_t n, bool first) {
+    if (first) {
+        for (int64_t i = 0; i < n; ++i) {
+            uint32_t u = (uint32_t)src[i] << 16;
+            float x;
+            std::memcpy(&x, &u, 4);
+            acc[i] = 0.0f + x;
+        }
+    } else {
+        for (int64_t i = 0; i < n; ++i) {
+            uint32_t u = (uint32_t)src[i] << 16;
+            float x;
+            std::memcpy(&x, &u, 4);
+            acc[i] = acc[i] + x;
+        }
+    }
+}
+__attribute__((target_clones("avx512f", "avx2", "default")))
+void acc_row_f32(float* __restrict__ acc, const float* __restrict__ src, int64_t n, bool first) {
+    if (first) {
+        for (int64_t i = 0; i < n; ++i) acc[i] = 0.0f + src[i];
+    } else {
+        for (int64_t i = 0; i < n; ++i) acc[i] = acc[i] + src[i];
+    }
+}
+
 // H1: accumulate each layer's staged compact block into the window's fp32 buffer
 // as soon as its D2H copy completed (DESIGN.md §2 O8).
 void zf_ctx::h1_loop() {
@@ -704,24 +733,16 @@ void zf_ctx::h1_loop() {
         const int sb = (int)(t % n_stage);
         for (auto& l : L) {
             cudaEventSynchronize(l.d2h_ev[sb]);
-            const int64_t count = l.d.n * l.mk;
+            const int64_t mk = l.mk, ld = l.mk_pad;
             float* acc = l.acc[a];
-            if (gdt == ZF_BF16) {
-                const uint16_t* src = static_cast<const uint16_t*>(l.stage_host[sb]);
-                pool->parallel_for(count, [&](int64_t b, int64_t e) {
-                    for (int64_t i = b; i < e; ++i) {
-                        uint32_t u = (uint32_t)src[i] << 16;
-                        float x;
-                        std::memcpy(&x, &u, 4);
-                        acc[i] = (first ? 0.0f : acc[i]) + x;
-                    }
-                });
-            } else {
-                const float* src = static_cast<const float*>(l.stage_host[sb]);
-                pool->parallel_for(count, [&](int64_t b, int64_t e) {
-                    for (int64_t i = b; i < e; ++i) acc[i] = (first ? 0.0f : acc[i]) + src[i];
-                });
-            }
+            const void* stage = l.stage_host[sb];
+            const bool bf = gdt == ZF_BF16;
+            pool->parallel_for(l.d.n, [&](int64_t b, int64_t e) {
+                for (int64_t r = b; r < e; ++r) {
+                    if (bf) acc_row_bf16(acc + r * mk, static_cast<const uint16_t*>(stage) + r * ld, mk, first);
+                    else acc_row_f32(acc + r * mk, static_cast<const float*>(stage) + r * ld, mk, first);
+                }
+            });
         }
         {
             std::lock_guard<std::mutex> lk(mu);
@@ -996,7 +1017,7 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
         for (auto& l : c->L) {
             for (int s = 0; s < 2; ++s) {
                 void* h = nullptr;
-                ZF_CUDA(cudaHostAlloc(&h, std::max<size_t>((size_t)l.d.n * l.mk * c->gsz, 64), cudaHostAllocDefault));
+                ZF_CUDA(cudaHostAlloc(&h, std::max<size_t>((size_t)l.d.n * l.mk_pad * c->gsz, 64), cudaHostAllocDefault));
                 c->host_pinned.push_back(h);
                 l.stage_host[s] = h;
                 ZF_CUDA(cudaEventCreateWithFlags(&l.d2h_ev[s], cudaEventDisableTiming | cudaEventBlockingSync));
@@ -1324,9 +1345,9 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t, void* const* grads, void* con
                     ZF_CUDA(cudaStreamWaitEvent(c->copy_stream, c->step_done, 0));
                 }
             }
-            // pitched device block -> dense host block [n, m-k]
-            if (l.mk) ZF_CUDA(cudaMemcpy2DAsync(l.stage_host[sb], l.mk * c->gsz, l.stage_dev[sb], l.mk_pad * c->gsz,
-                                                l.mk * c->gsz, l.d.n, cudaMemcpyDeviceToHost, c->copy_stream));
+            // one flat copy of the pitched block (H1 reads the rows at the same pitch)
+            if (l.mk) ZF_CUDA(cudaMemcpyAsync(l.stage_host[sb], l.stage_dev[sb], (size_t)l.d.n * l.mk_pad * c->gsz,
+                                              cudaMemcpyDeviceToHost, c->copy_stream));
             ZF_CUDA(cudaEventRecord(l.d2h_ev[sb], c->copy_stream));
         }
         ZF_CUDA(cudaEventRecord(c->d2h_all[sb], c->copy_stream));

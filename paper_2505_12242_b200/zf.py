@@ -288,14 +288,15 @@ class Context:
     def compact_host(self, layer: int):
         """numpy view of the pinned host copy (valid after sync()); bf16 as uint16 bits."""
         import numpy as np
-        d, h = ctypes.c_void_p(), ctypes.c_void_p()
-        _check(lib.zf_compact_buffer(self._h, layer, ctypes.byref(d), None, ctypes.byref(h)), "zf_compact_buffer")
+        d, ld, h = ctypes.c_void_p(), ctypes.c_int64(), ctypes.c_void_p()
+        _check(lib.zf_compact_buffer(self._h, layer, ctypes.byref(d), ctypes.byref(ld), ctypes.byref(h)),
+               "zf_compact_buffer")
         if not h.value:
             return None
         n, mk = self.layers[layer].n, self.layers[layer].m - self.k[layer]
         ct = ctypes.c_uint16 if self.grad_dtype == torch.bfloat16 else ctypes.c_float
-        arr = (ct * (n * mk)).from_address(h.value)
-        return np.ctypeslib.as_array(arr).reshape(n, mk)
+        arr = (ct * (n * ld.value)).from_address(h.value)
+        return np.ctypeslib.as_array(arr).reshape(n, ld.value)[:, :mk]
 
     def host_accumulator(self, layer: int, which: int = 0):
         import numpy as np
