@@ -220,6 +220,7 @@ class OracleLayer:
     accum_interval: int = 4
     hp: AdamHP = field(default_factory=AdamHP)
     cpu_update: bool = False   # f1: deferred CPU AdamW on the unselected columns (reading R18)
+    warmup: int = 0            # f2: tau synchronous warm-up steps with k = m (reading R20)
     idx: np.ndarray | None = None
     M: np.ndarray | None = None
     V: np.ndarray | None = None
@@ -242,6 +243,9 @@ class OracleLayer:
         idx_override: use this selection instead of the oracle's own top-k on a
         refresh step (parity protocol O10: downstream steps are compared on the
         GPU's selection, so a tolerated boundary swap never cascades)."""
+        if t < self.warmup:
+            return self._warmup_step(G, P)
+        t -= self.warmup                    # R20: the regular schedule starts at step tau
         k = self.k
         if self.cpu_update:
             assert self.refresh_interval % self.accum_interval == 0, "R18: refresh only at window starts"
@@ -270,6 +274,24 @@ class OracleLayer:
         self.last_out = out
         if self.cpu_update and (t + 1) % S == 0:
             self._deferred_update(self.acc[a], P)
+        return out
+
+    # ---------------------------------------------------------------- f2 warm-up
+    def _warmup_step(self, G, P):
+        """f2 / reading R20 ("synchronous updates (i.e., no staleness) during the
+        initial tau warm-up steps"): every column is important (k = m): the step is plain
+        AdamW (O6) on the whole matrix, nothing is offloaded.  The state is kept as a
+        selection of all m columns, so the first regular refresh (step tau) remaps it by R7:
+        columns selected at tau keep their moments and step counts."""
+        n, m = self.n, self.m
+        if self.idx is None:
+            self.idx = np.arange(m, dtype=np.int32)
+            self.M = np.zeros((n, m), np.float32)
+            self.V = np.zeros((n, m), np.float32)
+            self.steps = np.zeros(m, np.int32)
+        selective_adamw(P, G, self.idx, self.M, self.V, self.steps, self.hp)
+        out = np.empty((n, 0), G.dtype)
+        self.last_out = out
         return out
 
     # ---------------------------------------------------------------- f1
@@ -324,6 +346,7 @@ class OracleLayer:
 
     def sealed(self, t: int):
         """The accumulator sealed by the window that ended at or before step t."""
+        t -= self.warmup
         S = self.accum_interval
         w = t // S if (t + 1) % S == 0 else t // S - 1
         return None if w < 0 else self.acc[w % 2]

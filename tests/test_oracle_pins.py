@@ -496,3 +496,57 @@ def test_f1_migration_takes_current_value(orc):
     G2[:, 5] = 7.0                                     # window 1: column 5 on the GPU, 2 back on the CPU
     L.step(2, G2, P)
     assert np.array_equal(L.master[:, 2], p2) and L.th[2] == 0 and np.all(L.Mh[:, 2] == 0)
+
+
+# ------------------------------------------------------------------ f2: warm-up (reading R20)
+def test_f2_warmup_is_plain_adamw_on_the_whole_matrix(orc):
+    """t < tau: synchronous AdamW on every column = torch.optim.AdamW on the
+    full matrix; nothing is offloaded."""
+    rng = np.random.default_rng(60)
+    n, m = 5, 12
+    P = (rng.standard_normal((n, m)) * 0.1).astype(np.float32)
+    tp = torch.nn.Parameter(torch.tensor(P.copy()))
+    opt = torch.optim.AdamW([tp], lr=1e-3, weight_decay=0.0, foreach=False)
+    L = orc.OracleLayer(n=n, m=m, ratio_ppm=250000, refresh_interval=2, accum_interval=2, warmup=5)
+    for t in range(5):
+        G = rng.standard_normal((n, m)).astype(np.float32)
+        out = L.step(t, G, P)
+        assert out.shape == (n, 0) and L.acc is None
+        tp.grad = torch.tensor(G)
+        opt.step()
+        assert np.allclose(P, tp.detach().numpy(), rtol=1e-6, atol=1e-9), t
+
+
+def test_f2_warmup_zero_is_the_plain_schedule(orc):
+    rng = np.random.default_rng(61)
+    n, m = 4, 16
+    P0 = rng.standard_normal((n, m)).astype(np.float32)
+    A = orc.OracleLayer(n=n, m=m, ratio_ppm=200000, refresh_interval=2, accum_interval=2, warmup=0)
+    B = orc.OracleLayer(n=n, m=m, ratio_ppm=200000, refresh_interval=2, accum_interval=2)
+    PA, PB = P0.copy(), P0.copy()
+    for t in range(5):
+        G = rng.standard_normal((n, m)).astype(np.float32)
+        assert np.array_equal(A.step(t, G, PA), B.step(t, G, PB))
+    assert np.array_equal(PA, PB) and np.array_equal(A.M, B.M)
+
+
+def test_f2_column_selected_at_tau_continues_its_adamw_sequence(orc):
+    """R20 with R7: a column that is selected at the first regular refresh (step tau) keeps
+    the moments and step count it built during warm-up, so a column selected from step tau
+    on follows uninterrupted AdamW from step 0 (compare with torch on that column)."""
+    rng = np.random.default_rng(62)
+    n, m, tau = 3, 10, 3
+    P = (rng.standard_normal((n, m)) * 0.1).astype(np.float32)
+    tp = torch.nn.Parameter(torch.tensor(P[:, [4]].copy()))
+    opt = torch.optim.AdamW([tp], lr=1e-3, weight_decay=0.0, foreach=False)
+    L = orc.OracleLayer(n=n, m=m, ratio_ppm=100000, refresh_interval=2, accum_interval=2, warmup=tau)
+    for t in range(tau + 4):
+        G = (rng.standard_normal((n, m)) * 0.01).astype(np.float32)
+        G[:, 4] += 3.0                                   # column 4 is the top column after warm-up
+        L.step(t, G, P)
+        if t >= tau:
+            assert L.idx.tolist() == [4]
+        tp.grad = torch.tensor(G[:, [4]])
+        opt.step()
+        assert np.allclose(P[:, [4]], tp.detach().numpy(), rtol=1e-6, atol=1e-9), t
+    assert L.steps.tolist() == [tau + 4]               # one uninterrupted step count
