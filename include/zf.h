@@ -158,6 +158,15 @@ typedef struct {
                                          uploaded into the parameters before zf_step
                                          returns (synchronous: zf_step blocks at window
                                          ends and refreshes)                          */
+    int32_t warmup_steps;             /* tau >= 0: steps 0..tau-1 are synchronous warm-up
+                                         steps with every column selected (k = m: full
+                                         AdamW on the GPU, moments [n, m], nothing
+                                         offloaded; next row f2, reading R20).
+                                         The regular schedule (refresh iff (t-tau) % N
+                                         == 0, windows of S steps) starts at step tau,
+                                         whose refresh keeps the moments of the columns
+                                         it selects (R7).  With tau > 0 the first step
+                                         must be t = 0.                              */
 } zf_config;
 
 typedef struct zf_ctx zf_ctx;
@@ -173,7 +182,7 @@ zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, const zf_conf
                     int32_t rank, const void* nccl_id128, int32_t device, zf_ctx** out);
 
 /* One step of the hot path at global step t (t >= 0, increasing by 1 per call;
- * the first call must be a refresh, i.e. t % N == 0).
+ * the first call must be a refresh, i.e. t % N == 0, or t = 0 with warm-up).
  *   grads  [host] array of n_layers DEVICE pointers (G of each layer, [n, ld_grad])
  *   params [host] array of n_layers DEVICE pointers (p of each layer, [n, ld_param])
  * Refresh step (t % N == 0): column norms -> (world > 1) NCCL all-reduce(sum)

@@ -472,6 +472,15 @@ struct LayerState {
     void* p_up = nullptr;             // pinned [n, m-k] updated unselected params
     void* p_up_dev = nullptr;         // device [n, m-k]
     int32_t* unsel_dev = nullptr;     // device [m-k]
+    // f2: warm-up selection set (all m columns; reading R20)
+    int32_t* idx_w = nullptr;
+    uint32_t* mask_w = nullptr;
+    int32_t* prefix_w = nullptr;
+    int32_t* steps_w = nullptr;
+    float* mom_w = nullptr;           // [n, m]
+    float* vel_w = nullptr;
+    K3Geom geo_w{};
+    int64_t unit_begin_w = 0;
 };
 
 // Simple pool for the host accumulation (row 8, H1).
@@ -566,6 +575,15 @@ struct zf_ctx {
     TopkLayer* d_topk_tab[3] = {nullptr, nullptr, nullptr};  // [new set 0 | new set 1 | first (new 1, no old)]
     UpdLayer* d_upd_tab[8] = {};                              // [(cur)*4 + refresh*2 + stage]
     std::vector<UpdLayer> h_upd_tab[8], up_upd_tab[8];
+    // f2 warm-up (reading R20): K3 table of the all-columns set, K2 table of the first
+    // regular refresh (old = warm-up set) and K3 tables of that step (remap from [n, m])
+    int64_t tau = 0, k3_units_w = 0;
+    UpdLayer* d_upd_w = nullptr;
+    std::vector<UpdLayer> h_upd_w, up_upd_w;
+    TopkLayer* d_topk_w = nullptr;
+    UpdLayer* d_upd_x[2] = {};
+    std::vector<UpdLayer> h_upd_x[2], up_upd_x[2];
+    int64_t last_step = -1;       // t of the last zf_step call (warm-up included)
     // table uploads through a small pinned ring
     std::vector<unsigned char*> ring;
     std::vector<cudaEvent_t> ring_ev;
@@ -581,7 +599,7 @@ struct zf_ctx {
     // step state
     int cur = 0;
     bool have_sel = false;
-    int64_t last_t = -1;
+    int64_t last_t = -1;          // regular-schedule index (t - tau) of the last regular step
     int64_t launches = 0;
     cudaEvent_t step_done = nullptr, k3_done = nullptr;
     // offload
@@ -852,6 +870,72 @@ zf_status build_tables(zf_ctx* c) {
         ZF_TRY(c->dalloc(&c->d_upd_tab[v], nl * sizeof(UpdLayer)));
         c->up_upd_tab[v].assign(nl, UpdLayer{});
     }
+    if (c->tau > 0) {
+        // warm-up steps: every column selected, moments [n, m] updated in place, no compaction
+        c->h_upd_w.resize(nl);
+        for (int i = 0; i < nl; ++i) {
+            LayerState& l = c->L[i];
+            UpdLayer& t = c->h_upd_w[i];
+            t = UpdLayer{};
+            t.n = l.d.n;
+            t.m = l.d.m;
+            t.ldg = l.d.ld_grad;
+            t.ldp = l.d.ld_param;
+            t.k = l.d.m;
+            t.idx = l.idx_w;
+            t.mask = l.mask_w;
+            t.prefix = l.prefix_w;
+            t.m_in = t.m_out = l.mom_w;
+            t.v_in = t.v_out = l.vel_w;
+            t.k_in = l.d.m;
+            t.steps = l.steps_w;
+            t.seg_cols = l.geo_w.seg_cols;
+            t.nseg = l.geo_w.nseg;
+            t.R = l.geo_w.R;
+            t.units = l.geo_w.units;
+            t.unit_begin = l.unit_begin_w;
+            t.mv_tma = l.geo_w.mv_ok ? 1 : 0;
+        }
+        ZF_TRY(c->dalloc(&c->d_upd_w, nl * sizeof(UpdLayer)));
+        c->up_upd_w.assign(nl, UpdLayer{});
+        // first regular refresh: new set 1, old = the warm-up set
+        std::vector<TopkLayer> h(nl);
+        for (int i = 0; i < nl; ++i) {
+            LayerState& l = c->L[i];
+            TopkLayer& t = h[i];
+            t = TopkLayer{};
+            t.norms = c->norms + l.norm_off;
+            t.m = l.d.m;
+            t.k = l.k;
+            t.idx = l.idx[1];
+            t.mask = l.mask[1];
+            t.prefix = l.prefix[1];
+            t.old_mask = l.mask_w;
+            t.old_prefix = l.prefix_w;
+            t.old_steps = l.steps_w;
+            t.slot_src = l.slot_src;
+            t.new_steps = l.steps[1];
+            t.ucol = l.ucol[1];
+            t.seg_cols = l.geo.seg_cols;
+            t.gsz = c->gsz;
+        }
+        ZF_TRY(c->dalloc(&c->d_topk_w, nl * sizeof(TopkLayer)));
+        ZF_CUDA(cudaMemcpy(c->d_topk_w, h.data(), nl * sizeof(TopkLayer), cudaMemcpyHostToDevice));
+        // its K3: the regular refresh variant with the old moments read from the [n, m] set
+        // (not staged: one old row is m wide)
+        for (int sb = 0; sb < 2; ++sb) {
+            c->h_upd_x[sb] = c->h_upd_tab[0 * 4 + 2 + sb];
+            for (int i = 0; i < nl; ++i) {
+                UpdLayer& t = c->h_upd_x[sb][i];
+                t.m_in = c->L[i].mom_w;
+                t.v_in = c->L[i].vel_w;
+                t.k_in = c->L[i].d.m;
+                t.mv_tma = 0;
+            }
+            ZF_TRY(c->dalloc(&c->d_upd_x[sb], nl * sizeof(UpdLayer)));
+            c->up_upd_x[sb].assign(nl, UpdLayer{});
+        }
+    }
     return ZF_OK;
 }
 
@@ -895,6 +979,7 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
     if (cfg->cpu_update && !cfg->host_accumulate) return fail(ZF_EINVAL, "cpu_update requires host_accumulate");
     if (cfg->cpu_update && cfg->refresh_interval % cfg->accum_interval != 0)
         return fail(ZF_EINVAL, "cpu_update requires refresh_interval to be a multiple of accum_interval");
+    if (cfg->warmup_steps < 0) return fail(ZF_EINVAL, "warmup_steps must be >= 0");
     ZF_TRY(check_hp(&cfg->adam));
     if (world < 1 || rank < 0 || rank >= world) return fail(ZF_EINVAL, "bad world/rank");
     if (world > 1 && !nccl_id128) return fail(ZF_EINVAL, "nccl_id128 required when world > 1");
@@ -927,6 +1012,7 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
     c->psz = esize(cfg->param_dtype);
     c->n_stage = cfg->offload ? 2 : 1;
     c->lr_cur = cfg->adam.lr;
+    c->tau = cfg->warmup_steps;
     c->grid = update_grid(c->gdt, c->pdt);
     c->L.resize(n_layers);
     const int rb = norms_rows_per_block(), cb = norms_cols_per_block(c->gdt);
@@ -947,7 +1033,13 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
         l.geo = k3_geom(l.d.n, l.d.m, l.k, c->gsz, c->psz, k3_p_dense(l.d.m, l.k, c->psz));
         l.unit_begin = c->k3_units;
         c->k3_units += l.geo.units;
+        if (c->tau > 0) {  // warm-up geometry: k = m
+            l.geo_w = k3_geom(l.d.n, l.d.m, l.d.m, c->gsz, c->psz, true);
+            l.unit_begin_w = c->k3_units_w;
+            c->k3_units_w += l.geo_w.units;
+        }
     }
+    if (c->k3_units_w > 0x3fffffffLL) return bail(fail(ZF_EINVAL, "model too large"));
     if (c->k1_units > 0x7fffffffLL || c->k3_units > 0x3fffffffLL) return bail(fail(ZF_EINVAL, "model too large"));
     // ---- device state
     ZF_CTRY(c->dalloc(&c->norms, c->total_m * sizeof(float)));
@@ -968,6 +1060,24 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
             ZF_CTRY(c->dalloc(&l.vel[s], ((size_t)n * k + 16) * sizeof(float)));
         }
         ZF_CTRY(c->dalloc(&l.slot_src, (k + 16) * sizeof(int32_t)));
+        if (c->tau > 0) {
+            // the warm-up set: all m columns selected (slot = column), zero moments and counts
+            const int64_t m = l.d.m;
+            ZF_CTRY(c->dalloc(&l.idx_w, (m + 16) * sizeof(int32_t)));
+            ZF_CTRY(c->dalloc(&l.mask_w, (l.W + 8) * sizeof(uint32_t)));
+            ZF_CTRY(c->dalloc(&l.prefix_w, (l.W + 8) * sizeof(int32_t)));
+            ZF_CTRY(c->dalloc(&l.steps_w, (m + 16) * sizeof(int32_t)));
+            ZF_CTRY(c->dalloc(&l.mom_w, ((size_t)n * m + 16) * sizeof(float)));
+            ZF_CTRY(c->dalloc(&l.vel_w, ((size_t)n * m + 16) * sizeof(float)));
+            std::vector<int32_t> iw(m), pw(l.W);
+            std::vector<uint32_t> mw(l.W, 0xffffffffu);
+            for (int64_t j = 0; j < m; ++j) iw[j] = (int32_t)j;
+            for (int64_t w = 0; w < l.W; ++w) pw[w] = (int32_t)(32 * w);
+            if (m % 32) mw[l.W - 1] = (1u << (m % 32)) - 1u;
+            ZF_CUDA(cudaMemcpy(l.idx_w, iw.data(), m * sizeof(int32_t), cudaMemcpyHostToDevice));
+            ZF_CUDA(cudaMemcpy(l.mask_w, mw.data(), l.W * sizeof(uint32_t), cudaMemcpyHostToDevice));
+            ZF_CUDA(cudaMemcpy(l.prefix_w, pw.data(), l.W * sizeof(int32_t), cudaMemcpyHostToDevice));
+        }
         for (int s = 0; s < c->n_stage; ++s) ZF_CTRY(c->dalloc(&l.stage_dev[s], (size_t)n * l.mk_pad * c->gsz, false));
     }
     {
@@ -1005,7 +1115,7 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
     ZF_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
     for (auto& l : c->L) {
         int32_t* v = nullptr;
-        ZF_CTRY(c->dalloc(&v, l.k * sizeof(int32_t)));
+        ZF_CTRY(c->dalloc(&v, (c->tau > 0 ? l.d.m : l.k) * sizeof(int32_t)));
         c->steps_view.push_back(v);
     }
     ZF_CUDA(cudaEventCreateWithFlags(&c->step_done, cudaEventDisableTiming));
@@ -1094,17 +1204,21 @@ zf_status refresh_pointer_tables(zf_ctx* c, int variant, bool refresh, void* con
             c->up_norm_tab = c->h_norm_tab;
         }
     }
-    auto& h = c->h_upd_tab[variant];
+    // variant >= 0: regular table; -1: warm-up table; -2 - sb: first refresh after warm-up
+    std::vector<UpdLayer>& h = variant >= 0 ? c->h_upd_tab[variant] : variant == -1 ? c->h_upd_w : c->h_upd_x[-2 - variant];
+    std::vector<UpdLayer>& up =
+        variant >= 0 ? c->up_upd_tab[variant] : variant == -1 ? c->up_upd_w : c->up_upd_x[-2 - variant];
+    UpdLayer* d = variant >= 0 ? c->d_upd_tab[variant] : variant == -1 ? c->d_upd_w : c->d_upd_x[-2 - variant];
     for (int i = 0; i < nl; ++i) {
         h[i].G = grads[i];
         h[i].P = params[i];
         h[i].tma_ok = k3_tma_ok(grads[i], c->L[i].d.ld_grad, c->L[i].d.m, c->gsz);
         h[i].p_tma = k3_tma_ok(params[i], c->L[i].d.ld_param, c->L[i].d.m, c->psz) &&
-                     k3_p_dense(c->L[i].d.m, c->L[i].k, c->psz);
+                     k3_p_dense(c->L[i].d.m, h[i].k, c->psz);
     }
-    if (std::memcmp(h.data(), c->up_upd_tab[variant].data(), nl * sizeof(UpdLayer)) != 0) {
-        ZF_TRY(c->upload(c->d_upd_tab[variant], h.data(), nl * sizeof(UpdLayer), s));
-        c->up_upd_tab[variant] = h;
+    if (std::memcmp(h.data(), up.data(), nl * sizeof(UpdLayer)) != 0) {
+        ZF_TRY(c->upload(d, h.data(), nl * sizeof(UpdLayer), s));
+        up = h;
     }
     return ZF_OK;
 }
@@ -1243,25 +1357,67 @@ zf_status f1_window_end(zf_ctx* c, int64_t t, void* const* params, cudaStream_t 
     return ZF_OK;
 }
 
+// f2 warm-up step (reading R20): every column selected, moments [n, m] updated in place by
+// K3 (no compaction, nothing offloaded).  K3 launches since the set was made = t.
+zf_status warmup_step(zf_ctx* c, int64_t t, void* const* grads, void* const* params, cudaStream_t s) {
+    const int nl = (int)c->L.size();
+    ZF_TRY(upload_ss(c, s));
+    ZF_TRY(refresh_pointer_tables(c, -1, false, grads, params, s));
+    UpdParams prm{};
+    prm.layers.dev = c->d_upd_w;
+    prm.layers.n = nl;
+    prm.total_units = c->k3_units_w;
+    prm.claim = c->claim;
+    prm.claim_base = c->claim_base;
+    prm.step_delta = c->since;
+    prm.do_adam = 1;
+    prm.do_compact = 0;
+    prm.nonfinite = c->nonfinite_d;
+    prm.adam = c->adam;
+    const int grid = (int)std::min<int64_t>(c->grid, c->k3_units_w);
+    zf_ctx::Pending pe3;
+    ZF_TRY(c->prof_begin(3, s, &pe3));
+    ZF_CUDA(launch_update(prm, c->gdt, c->pdt, grid, s));
+    ZF_TRY(c->prof_end(&pe3, s));
+    c->launches++;
+    c->claim_base += (uint32_t)(c->k3_units_w + (int64_t)grid * update_limits().producers);
+    c->since += 1;
+    c->last_step = t;
+    ZF_CUDA(cudaEventRecord(c->step_done, s));
+    return ZF_OK;
+}
+
 }  // namespace
 
-extern "C" zf_status zf_step(zf_ctx* c, int64_t t, void* const* grads, void* const* params, zf_stream_t stream) {
+extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* const* params, zf_stream_t stream) {
     g_last_error.clear();
     if (!c) return fail(ZF_EINVAL, "ctx is NULL");
     if (!grads || !params) return fail(ZF_EINVAL, "grads/params is NULL");
     const int nl = (int)c->L.size();
     for (int i = 0; i < nl; ++i)
         if (!grads[i] || !params[i]) return fail(ZF_EINVAL, "layer %d: NULL gradient or parameter", i);
-    if (t < 0) return fail(ZF_EINVAL, "t must be >= 0");
+    if (t0 < 0) return fail(ZF_EINVAL, "t must be >= 0");
     const int N = c->cfg.refresh_interval;
-    const bool refresh = (t % N) == 0;
-    if (!c->have_sel && !refresh) return fail(ZF_ESTATE, "first step must be a refresh step (t %% N == 0)");
-    if (c->have_sel && t != c->last_t + 1) return fail(ZF_ESTATE, "steps must be consecutive (last %lld, got %lld)",
-                                                       (long long)c->last_t, (long long)t);
+    const int64_t tau = c->tau;
+    if (c->last_step >= 0) {
+        if (t0 != c->last_step + 1)
+            return fail(ZF_ESTATE, "steps must be consecutive (last %lld, got %lld)", (long long)c->last_step,
+                        (long long)t0);
+    } else if (tau > 0) {
+        if (t0 != 0) return fail(ZF_ESTATE, "with warm-up steps the first step must be t = 0");
+    } else if (t0 % N != 0) {
+        return fail(ZF_ESTATE, "first step must be a refresh step (t %% N == 0)");
+    }
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     ZF_CUDA(cudaSetDevice(c->device));
+    if (t0 < tau) return warmup_step(c, t0, grads, params, s);
+    // the regular schedule (refreshes, windows, offload stages) counts from step tau (R20)
+    const int64_t t = t0 - tau;
+    const bool refresh = (t % N) == 0;
     const int sb = (int)(t % c->n_stage);
-    const int variant = c->cur * 4 + (refresh ? 2 : 0) + (sb & 1);
+    // the first refresh after a warm-up remaps from the [n, m] warm-up set (tables -2 - sb)
+    const bool from_warmup = !c->have_sel && tau > 0;
+    const int variant = from_warmup ? -2 - (sb & 1) : c->cur * 4 + (refresh ? 2 : 0) + (sb & 1);
     ZF_TRY(upload_ss(c, s));
     ZF_TRY(refresh_pointer_tables(c, variant, refresh, grads, params, s));
 
@@ -1290,7 +1446,7 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t, void* const* grads, void* con
             ZF_TRY(c->prof_end(&pe, s));
         }
         Table<TopkLayer> tk{};
-        tk.dev = c->have_sel ? c->d_topk_tab[c->cur ^ 1] : c->d_topk_tab[2];
+        tk.dev = c->have_sel ? c->d_topk_tab[c->cur ^ 1] : (from_warmup ? c->d_topk_w : c->d_topk_tab[2]);
         tk.n = nl;
         ZF_TRY(c->prof_begin(2, s, &pe));
         ZF_CUDA(launch_topk(tk, c->max_m, c->since, c->nonfinite_d, s));
@@ -1300,7 +1456,7 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t, void* const* grads, void* con
     }
     // first refresh writes set 1 (variant built with cur=0, refresh=1 -> new set 1)
     UpdParams prm{};
-    prm.layers.dev = c->d_upd_tab[variant];
+    prm.layers.dev = from_warmup ? c->d_upd_x[sb & 1] : c->d_upd_tab[variant];
     prm.layers.n = nl;
     prm.total_units = c->k3_units;
     prm.claim = c->claim;
@@ -1328,6 +1484,7 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t, void* const* grads, void* con
         c->have_sel = true;
     }
     c->last_t = t;
+    c->last_step = t0;
     ZF_CUDA(cudaEventRecord(c->step_done, s));
 
     if (c->cfg.offload) {
@@ -1387,6 +1544,11 @@ extern "C" zf_status zf_sync(zf_ctx* c) {
 
 extern "C" zf_status zf_selected(zf_ctx* c, int32_t layer, const int32_t** idx, int64_t* k) {
     if (!c || layer < 0 || layer >= (int)c->L.size()) return fail(ZF_EINVAL, "bad ctx/layer");
+    if (!c->have_sel && c->tau > 0 && c->last_step >= 0) {  // warm-up: all columns
+        if (idx) *idx = c->L[layer].idx_w;
+        if (k) *k = c->L[layer].d.m;
+        return ZF_OK;
+    }
     if (!c->have_sel) return fail(ZF_ESTATE, "no selection yet");
     if (idx) *idx = c->L[layer].idx[c->cur];
     if (k) *k = c->L[layer].k;
@@ -1402,15 +1564,17 @@ extern "C" zf_status zf_norms(zf_ctx* c, int32_t layer, const float** norms) {
 extern "C" zf_status zf_optimizer_state(zf_ctx* c, int32_t layer, const float** exp_avg, const float** exp_avg_sq,
                                         const int32_t** step) {
     if (!c || layer < 0 || layer >= (int)c->L.size()) return fail(ZF_EINVAL, "bad ctx/layer");
-    if (!c->have_sel) return fail(ZF_ESTATE, "no state yet");
+    const bool warm = !c->have_sel && c->tau > 0 && c->last_step >= 0;
+    if (!c->have_sel && !warm) return fail(ZF_ESTATE, "no state yet");
     const LayerState& l = c->L[layer];
-    if (exp_avg) *exp_avg = l.mom[c->cur];
-    if (exp_avg_sq) *exp_avg_sq = l.vel[c->cur];
+    if (exp_avg) *exp_avg = warm ? l.mom_w : l.mom[c->cur];
+    if (exp_avg_sq) *exp_avg_sq = warm ? l.vel_w : l.vel[c->cur];
     if (step) {
         // device keeps base counts at the last refresh; materialize base + delta
         ZF_CUDA(cudaSetDevice(c->device));
         ZF_CUDA(cudaEventSynchronize(c->step_done));
-        ZF_CUDA(launch_add_const(l.steps[c->cur], c->steps_view[layer], l.k, c->since, c->aux));
+        ZF_CUDA(launch_add_const(warm ? l.steps_w : l.steps[c->cur], c->steps_view[layer], warm ? l.d.m : l.k,
+                                 c->since, c->aux));
         ZF_CUDA(cudaStreamSynchronize(c->aux));
         *step = c->steps_view[layer];
     }

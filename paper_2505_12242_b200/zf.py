@@ -44,7 +44,7 @@ class Config(ctypes.Structure):
     _fields_ = [("grad_dtype", ctypes.c_int32), ("param_dtype", ctypes.c_int32), ("topk_ppm", ctypes.c_int32),
                 ("refresh_interval", ctypes.c_int32), ("accum_interval", ctypes.c_int32), ("adam", AdamParams),
                 ("offload", ctypes.c_int32), ("host_accumulate", ctypes.c_int32), ("host_threads", ctypes.c_int32),
-                ("cpu_update", ctypes.c_int32)]
+                ("cpu_update", ctypes.c_int32), ("warmup_steps", ctypes.c_int32)]
 
 
 if not os.path.exists(_LIB_PATH):
@@ -196,7 +196,7 @@ class Context:
     def __init__(self, layers, grad_dtype=torch.bfloat16, param_dtype=torch.bfloat16, topk_ratio_ppm=100000,
                  refresh_interval=4, accum_interval=4, adam: AdamParams | None = None, offload=False,
                  host_accumulate=False, host_threads=0, world=1, rank=0, nccl_id: bytes | None = None,
-                 device: int | None = None, cpu_update=False):
+                 device: int | None = None, cpu_update=False, warmup_steps=0):
         self.layers = [l if isinstance(l, LayerShape) else LayerShape(*l) for l in layers]
         descs = (LayerDesc * len(self.layers))()
         for d, l in zip(descs, self.layers):
@@ -215,6 +215,7 @@ class Context:
         cfg.host_accumulate = int(host_accumulate)
         cfg.host_threads = host_threads
         cfg.cpu_update = int(cpu_update)
+        cfg.warmup_steps = int(warmup_steps)
         self.cfg = cfg
         self.device = torch.cuda.current_device() if device is None else device
         h = ctypes.c_void_p()
@@ -273,7 +274,7 @@ class Context:
         a, b, s = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
         _check(lib.zf_optimizer_state(self._h, layer, ctypes.byref(a), ctypes.byref(b), ctypes.byref(s)),
                "zf_optimizer_state")
-        n, k = self.layers[layer].n, self.k[layer]
+        n, k = self.layers[layer].n, self.selected(layer).numel()   # k = m during warm-up
         return (_view(a.value, (n, k), torch.float32), _view(b.value, (n, k), torch.float32),
                 _view(s.value, (k,), torch.int32))
 

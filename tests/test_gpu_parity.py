@@ -165,18 +165,19 @@ def test_compact_bitexact(zf, orc, gpu, n, m, dt, ld, ppm):
 
 # ------------------------------------------------------------------ zf_step vs oracle, multi-step
 def _run_stateful(zf, orc, gpu, shapes, gdt, pdt, ppm, N, S, steps, offload, lr=1e-3, wd=0.0, check_every=1,
-                  tie=False, ld_pad=0, cpu_update=False):
+                  tie=False, ld_pad=0, cpu_update=False, warmup=0):
     hp_o = orc.AdamHP(lr=lr, weight_decay=wd)
     ctx = zf.Context([zf.LayerShape(n, m, m + ld_pad, m + ld_pad) for n, m in shapes], grad_dtype=TDT[gdt],
                      param_dtype=TDT[pdt], topk_ratio_ppm=ppm, refresh_interval=N, accum_interval=S,
-                     adam=zf.adam_params(lr=lr, weight_decay=wd), offload=offload, host_accumulate=offload, cpu_update=cpu_update)
+                     adam=zf.adam_params(lr=lr, weight_decay=wd), offload=offload, host_accumulate=offload, cpu_update=cpu_update,
+                     warmup_steps=warmup)
     scales = [gpu.ColScale(m, li) for li, (n, m) in enumerate(shapes)]
     Gs = [torch.empty(n, m + ld_pad, dtype=TDT[gdt], device="cuda")[:, :m] for n, m in shapes]
     Ps = [torch.empty(n, m + ld_pad, dtype=TDT[pdt], device="cuda")[:, :m] for n, m in shapes]
     for li, P in enumerate(Ps):
         gpu.fill_param(P, li)
     layers = [orc.OracleLayer(n=n, m=m, ratio_ppm=ppm, refresh_interval=N, accum_interval=S, hp=hp_o,
-                              cpu_update=cpu_update) for n, m in shapes]
+                              cpu_update=cpu_update, warmup=warmup) for n, m in shapes]
     Po = [np.ascontiguousarray(to_np(P)) for P in Ps]
     swaps = 0
     for t in range(steps):
@@ -189,7 +190,8 @@ def _run_stateful(zf, orc, gpu, shapes, gdt, pdt, ppm, N, S, steps, offload, lr=
         Gn = [np.ascontiguousarray(to_np(G)) for G in Gs]
         ctx.step(t, Gs, Ps)
         ctx.sync()
-        refresh = t % N == 0
+        warm = t < warmup
+        refresh = not warm and (t - warmup) % N == 0
         for li, (n, m) in enumerate(shapes):
             L = layers[li]
             gidx = to_np(ctx.selected(li))
@@ -206,10 +208,13 @@ def _run_stateful(zf, orc, gpu, shapes, gdt, pdt, ppm, N, S, steps, offload, lr=
             assert_bits_equal(to_np(M), L.M, f"exp_avg t={t} l={li}")
             assert_bits_equal(to_np(V), L.V, f"exp_avg_sq t={t} l={li}")
             assert_bits_equal(np.ascontiguousarray(to_np(Ps[li])), Po[li], f"params t={t} l={li}")
+            if warm:
+                assert out.shape == (n, 0)
+                continue
             assert_bits_equal(to_np(ctx.compact_buffer(li)), out, f"compact t={t} l={li}")
             if offload:
                 assert_bits_equal(ctx.compact_host(li).copy(), out, f"compact host t={t} l={li}")
-                assert_bits_equal(ctx.host_accumulator(li, 0).copy(), L.acc[(t // S) % 2], f"acc t={t} l={li}")
+                assert_bits_equal(ctx.host_accumulator(li, 0).copy(), L.acc[((t - warmup) // S) % 2], f"acc t={t} l={li}")
                 sealed = ctx.host_accumulator(li, 1)
                 osealed = L.sealed(t)
                 assert (sealed is None) == (osealed is None)
@@ -239,6 +244,18 @@ def test_step_cpu_update(zf, orc, gpu, NS, pdt, wd):
                                     pdt, 100000, NS, NS, 9, offload=True, wd=wd, cpu_update=True)
     assert launches == 9 + 2 * len(range(0, 9, NS)) + 2 * (9 // NS)
     assert swaps == 0
+
+
+@pytest.mark.parametrize("tau,NS,pdt,cpu", [(1, 2, "bf16", False), (3, 2, "fp32", False), (2, 4, "bf16", True),
+                                           (5, 1, "fp32", True)])
+def test_step_warmup(zf, orc, gpu, tau, NS, pdt, cpu):
+    """f2 warm-up (reading R20): tau synchronous steps with k = m (moments [n, m]), then the
+    regular schedule from step tau with the R7 remap out of the all-columns set; selection,
+    moments, step counts, params, compact blocks and accumulators bit-exact vs the oracle."""
+    shapes = [(64, 512), (37, 1001), (16, 4096)]
+    gdt = "bf16" if pdt == "bf16" else "fp32"
+    _run_stateful(zf, orc, gpu, shapes, gdt, pdt, 100000, NS, NS, tau + 6, offload=True, cpu_update=cpu,
+                  warmup=tau)
 
 
 def test_cpu_update_needs_aligned_windows(zf):
