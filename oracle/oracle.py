@@ -71,6 +71,11 @@ def lib():
         L.oracle_compact.restype = None
         L.oracle_accumulate.argtypes = [_vp, _vp, ctypes.c_int, _i64]; L.oracle_accumulate.restype = None
         L.oracle_to_bf16.argtypes = [_vp, _vp, _i64]; L.oracle_to_bf16.restype = None
+        L.oracle_channel_norm_sums.argtypes = [_vp, _i64, _vp, _i64, _vp]
+        L.oracle_channel_norm_sums.restype = None
+        L.oracle_zen_auto_decide.argtypes = [ctypes.POINTER(_f64), ctypes.POINTER(_i64), ctypes.c_int, _f64, _i64,
+                                             _f64, _i64, _f64, _i64, ctypes.c_int]
+        L.oracle_zen_auto_decide.restype = ctypes.c_int
     return _lib
 
 
@@ -237,12 +242,18 @@ class OracleLayer:
     def k(self) -> int:
         return k_for(self.m, self.ratio_ppm)
 
-    def step(self, t: int, G: np.ndarray, P: np.ndarray, idx_override: np.ndarray | None = None):
+    def step(self, t: int, G: np.ndarray, P: np.ndarray, idx_override: np.ndarray | None = None,
+             window: tuple | None = None):
         """One step of the hot path for this matrix at global step t.
 
         idx_override: use this selection instead of the oracle's own top-k on a
         refresh step (parity protocol O10: downstream steps are compared on the
-        GPU's selection, so a tolerated boundary swap never cascades)."""
+        GPU's selection, so a tolerated boundary swap never cascades).
+
+        window: None for the fixed schedule (windows [wS, (w+1)S) of the regular
+        step index, O8); or (w, first) from ``OracleModel`` under Zen-auto (reading
+        R21): accumulate into buffer w % 2, zeroing it first if ``first``; the window's
+        end (and the f1 update) is then decided by the caller (``end_window``)."""
         if t < self.warmup:
             return self._warmup_step(G, P)
         t -= self.warmup                    # R20: the regular schedule starts at step tau
@@ -267,14 +278,21 @@ class OracleLayer:
         S = self.accum_interval
         if self.acc is None:
             self.acc = [np.zeros((self.n, self.m - k), np.float32) for _ in range(2)]
-        a = (t // S) % 2
-        if t % S == 0:
+        w, first = (t // S, t % S == 0) if window is None else window
+        a = w % 2
+        if first:
             self.acc[a][...] = 0.0
         accumulate(self.acc[a], out)
         self.last_out = out
-        if self.cpu_update and (t + 1) % S == 0:
-            self._deferred_update(self.acc[a], P)
+        if window is None and (t + 1) % S == 0:
+            self.end_window(w, S, P)
         return out
+
+    def end_window(self, w: int, length: int, P: np.ndarray):
+        """Seal window w (buffer w % 2) after `length` steps; with f1 its average gradient
+        updates theta^(c) (reading R18; 1/S of P:527 with S = the window's length)."""
+        if self.cpu_update:
+            self._deferred_update(self.acc[w % 2], P, length)
 
     # ---------------------------------------------------------------- f2 warm-up
     def _warmup_step(self, G, P):
@@ -322,14 +340,15 @@ class OracleLayer:
         self.Vh[:, entering] = 0.0
         self.th[entering] = 0
 
-    def _deferred_update(self, acc, P):
+    def _deferred_update(self, acc, P, length=None):
         """f1 / reading R18: at the end of an S-step window, theta^(c) (the window's
         unselected columns) takes one AdamW step (formula O6) with the window's
         average gradient acc / S (theta^(c) -= alpha * (1/S) * sum of the
         window's gradients, here through AdamW), on the fp32 master with host
         moments; the parameter then holds the master rounded to its dtype."""
         unsel = self._unselected()
-        g_avg = acc / np.float32(self.accum_interval)          # one IEEE fp32 division
+        S = self.accum_interval if length is None else length
+        g_avg = acc / np.float32(S)                            # one IEEE fp32 division
         Gfull = np.zeros((self.n, self.m), np.float32)
         Gfull[:, unsel] = g_avg
         Mc = np.ascontiguousarray(self.Mh[:, unsel])
@@ -350,3 +369,94 @@ class OracleLayer:
         S = self.accum_interval
         w = t // S if (t + 1) % S == 0 else t // S - 1
         return None if w < 0 else self.acc[w % 2]
+
+
+# ------------------------------------------------------------ f2: Zen-auto (R21)
+def channel_norm_sums(norms: np.ndarray, idx: np.ndarray):
+    """O11: (sum of sqrt(norm) over the selected columns, over the unselected columns)."""
+    norms = np.ascontiguousarray(norms, np.float32)
+    idx = np.ascontiguousarray(idx, np.int32)
+    out = np.zeros(2, np.float64)
+    lib().oracle_channel_norm_sums(_p(norms), norms.shape[0], _p(idx), idx.shape[0], _p(out))
+    return float(out[0]), float(out[1])
+
+
+class ZenAuto:
+    """O12 state: Zen-auto's adaptive update interval (reading R21)."""
+
+    def __init__(self, gamma: float, smax: int):
+        assert gamma > 0 and smax >= 1
+        self.gamma, self.smax = float(gamma), int(smax)
+        self.A = ctypes.c_double(0.0)
+        self.len = ctypes.c_int64(0)
+        self.first = True
+
+    def decide(self, sel_sum, sel_cnt, unsel_sum, unsel_cnt, force_end: bool) -> bool:
+        end = bool(lib().oracle_zen_auto_decide(ctypes.byref(self.A), ctypes.byref(self.len), int(self.first),
+                                                sel_sum, sel_cnt, unsel_sum, unsel_cnt, self.gamma, self.smax,
+                                                int(force_end)))
+        self.first = end
+        return end
+
+
+class OracleModel:
+    """All weight matrices of a model under the method, stepped together (``zf_step``
+    over a context's layers).  Without ``auto_gamma`` each layer follows its own fixed
+    S-step windows (identical to stepping the ``OracleLayer`` objects one by one).
+    With ``auto_gamma`` > 0 (Zen-auto, f2, reading R21) the accumulation windows of
+    every layer end together, when the model-wide Zen-auto decision (O11/O12, on every
+    step's column norms) says so, after accum_interval (= S_max) steps, or before a
+    refresh; with f1 each window's CPU update uses its own length as S."""
+
+    def __init__(self, layers: list, auto_gamma: float = 0.0):
+        self.layers = layers
+        l0 = layers[0]
+        for l in layers:
+            assert (l.refresh_interval, l.accum_interval, l.warmup) == \
+                (l0.refresh_interval, l0.accum_interval, l0.warmup)
+        self.N, self.S, self.tau = l0.refresh_interval, l0.accum_interval, l0.warmup
+        self.auto = ZenAuto(auto_gamma, self.S) if auto_gamma > 0 else None
+        self.w = 0                 # index of the current window
+        self.w_len = 0
+        self.ends: list = []       # global step t of every window end (Zen-auto: the interval history)
+        self.stats: list = []      # per regular step: (A, i, u) of the decision
+
+    def step(self, t: int, Gs: list, Ps: list, idx_overrides: list | None = None):
+        outs = []
+        if t < self.tau or self.auto is None:
+            for li, l in enumerate(self.layers):
+                outs.append(l.step(t, Gs[li], Ps[li], None if idx_overrides is None else idx_overrides[li]))
+            if t >= self.tau and (t - self.tau + 1) % self.S == 0:
+                self.ends.append(t)
+            return outs
+        tr = t - self.tau
+        first = self.auto.first
+        sel = [0.0, 0, 0.0, 0]
+        for li, l in enumerate(self.layers):
+            outs.append(l.step(t, Gs[li], Ps[li], None if idx_overrides is None else idx_overrides[li],
+                               window=(self.w, first)))
+            a, b = channel_norm_sums(column_norms(Gs[li]), l.idx)
+            sel[0] += a
+            sel[1] += l.k
+            sel[2] += b
+            sel[3] += l.m - l.k
+        force = (tr + 1) % self.N == 0
+        end = self.auto.decide(sel[0], sel[1], sel[2], sel[3], force)
+        u = sel[2] / sel[3] if sel[3] else 0.0
+        i = sel[0] / sel[1] if sel[1] else 0.0
+        self.stats.append((self.auto.A.value, i, u))
+        if end:
+            length = int(self.auto.len.value)
+            for li, l in enumerate(self.layers):
+                l.end_window(self.w, length, Ps[li])
+            self.ends.append(t)
+            self.w += 1
+        return outs
+
+    def intervals(self):
+        """Window lengths so far (the Zen-auto interval history)."""
+        out, prev = [], self.tau - 1
+        for e in self.ends:
+            out.append(e - prev)
+            prev = e
+        return out

@@ -35,6 +35,8 @@
  *                                and AdamW", "AdamW ... weight decay 0.00"
  *   O7 oracle_compact           P:414 "transfers only the (1-k)·M unimportant
  *                                gradients to the CPU" [R12 layout]
+ *   O11 oracle_channel_norm_sums / O12 oracle_zen_auto_decide
+ *                                Zen-auto (next row f2) [R21]
  *   O8 oracle_accumulate        P:388 "offloaded to the CPU and gradually
  *                                accumulated over several iterations"
  *                                double buffering
@@ -271,6 +273,49 @@ void oracle_accumulate(float* acc, const void* stage, int dt, int64_t count) {
         float x = load(stage, dt, e);
         acc[e] = acc[e] + x;
     }
+}
+
+/* O11  Zen-auto statistic of one matrix (f2, reading R21): from the
+ * per-column squared norms of the current gradient (the O1 proxy -- P:447
+ * "monitors gradient changes across GPUs using a lightweight coordination
+ * proxy"), the sums of the per-channel L2 norms over the selected (sums[0]) and
+ * the unselected (sums[1]) columns; sqrt and sums in double, column order. */
+void oracle_channel_norm_sums(const float* norms, int64_t m, const int32_t* idx, int64_t k, double* sums) {
+    std::vector<char> selected(static_cast<size_t>(m), 0);
+    for (int64_t s = 0; s < k; ++s) selected[static_cast<size_t>(idx[s])] = 1;
+    double sel = 0.0, unsel = 0.0;
+    for (int64_t j = 0; j < m; ++j) {
+        const double x = std::sqrt(static_cast<double>(norms[j]));
+        if (selected[static_cast<size_t>(j)]) sel += x;
+        else unsel += x;
+    }
+    sums[0] = sel;
+    sums[1] = unsel;
+}
+
+/* O12  One Zen-auto decision at the end of a step ("tracks the average
+ * accumulated channel gradient norm and compares it to the average one of the
+ * important part.  Once the unimportant gradient part becomes comparable to
+ * important ones, Zen-auto immediately triggers its CPU-side update"; reading R21):
+ *   u = mean per-channel norm of the unselected columns this step (all matrices),
+ *   i = mean per-channel norm of the selected columns this step,
+ *   A = sum of u over the window's steps so far (the window's accumulated
+ *       unimportant channel norm, averaged over channels),
+ *   the window ends iff force_end (the next step refreshes the selection), or it
+ *   has lasted smax steps (bounded staleness), or A > 0 and A >= gamma*i.
+ * state[0] = A, *len = steps in the window; `first` starts a new window. */
+int oracle_zen_auto_decide(double* A, int64_t* len, int first, double sel_sum, int64_t sel_cnt, double unsel_sum,
+                           int64_t unsel_cnt, double gamma, int64_t smax, int force_end) {
+    const double u = unsel_cnt > 0 ? unsel_sum / static_cast<double>(unsel_cnt) : 0.0;
+    const double i = sel_cnt > 0 ? sel_sum / static_cast<double>(sel_cnt) : 0.0;
+    if (first) {
+        *A = 0.0;
+        *len = 0;
+    }
+    *A = *A + u;
+    *len = *len + 1;
+    if (force_end || *len >= smax) return 1;
+    return (*A > 0.0 && *A >= gamma * i) ? 1 : 0;
 }
 
 }  // extern "C"

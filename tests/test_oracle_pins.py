@@ -550,3 +550,145 @@ def test_f2_column_selected_at_tau_continues_its_adamw_sequence(orc):
         opt.step()
         assert np.allclose(P[:, [4]], tp.detach().numpy(), rtol=1e-6, atol=1e-9), t
     assert L.steps.tolist() == [tau + 4]               # one uninterrupted step count
+
+
+# ------------------------------------------------------------------ f2: Zen-auto (reading R21)
+def _auto_model(orc, n, m, ppm, N, smax, gamma, cpu_update=False, layers=1, warmup=0):
+    Ls = [orc.OracleLayer(n=n, m=m, ratio_ppm=ppm, refresh_interval=N, accum_interval=smax,
+                          cpu_update=cpu_update, warmup=warmup) for _ in range(layers)]
+    return orc.OracleModel(Ls, auto_gamma=gamma)
+
+
+def _two_level(n, m, k, hi, lo):
+    """Constant stream: k important columns of value hi, the rest lo (per-channel L2 norm
+    ratio lo/hi exactly, every step)."""
+    G = np.full((n, m), lo, np.float32)
+    G[:, :k] = hi
+    return G
+
+
+def test_zen_auto_spec_worked_example(orc):
+    """per-channel norm of the unimportant part = 0.25 x the important part,
+    constant stream, gamma = 1 -> the CPU-side update triggers at the 4th step of every
+    window (the accumulated unimportant norm reaches 4 x 0.25 = 1 x important)."""
+    ex = _golden("worked_examples.json")["zen_auto"][0]
+    n, m = 16, 64
+    M = _auto_model(orc, n, m, 100000, N=16, smax=16, gamma=ex["gamma"])
+    k = M.layers[0].k
+    G = _two_level(n, m, k, 1.0, ex["ratio"])
+    P = np.zeros((n, m), np.float32)
+    for t in range(16):
+        M.step(t, [G], [P])
+    assert M.intervals() == [ex["trigger_step"]] * 4
+    assert M.ends == [3, 7, 11, 15]
+
+
+def test_zen_auto_threshold_worked_example(orc):
+    """gamma = 1, accumulated 0.5 vs important 0.6 -> no flush; the comparison
+    is >= (0.6 accumulated flushes)."""
+    ex = _golden("worked_examples.json")["zen_auto"][1]
+    z = orc.ZenAuto(ex["gamma"], 100)
+    assert z.decide(0.6, 1, ex["accumulated"], 1, False) is ex["flush"]
+    z = orc.ZenAuto(ex["gamma"], 100)
+    assert z.decide(0.6, 1, 0.6, 1, False) is True
+
+
+@pytest.mark.parametrize("lo,gamma,want", [(0.25, 1.0, 4), (0.5, 1.0, 2), (0.3, 1.0, 4), (0.25, 0.5, 2),
+                                           (1.0, 1.0, 1), (0.2, 1.0, 5), (0.125, 2.0, 8)])
+def test_zen_auto_steady_interval_closed_form(orc, lo, gamma, want):
+    """Stationary magnitudes: the interval is ceil(gamma * important / unimportant)
+    (SPEC S:449), capped by S_max (here 8 = N, so (0.125, 2) -> 16 is cut to 8)."""
+    n, m = 16, 50
+    M = _auto_model(orc, n, m, 100000, N=8, smax=8, gamma=gamma)
+    G = _two_level(n, m, M.layers[0].k, 1.0, lo)
+    P = np.zeros((n, m), np.float32)
+    for t in range(24):
+        M.step(t, [G], [P])
+    iv = M.intervals()
+    assert want == min(8, math.ceil(gamma / lo - 1e-9))
+    # windows never cross a refresh (every 8 steps)
+    full = [want] * (8 // want) + ([8 % want] if 8 % want else [])
+    assert iv == full * 3, iv
+
+
+def test_zen_auto_zero_stream_never_triggers(orc):
+    """a zero gradient stream never triggers; windows end only at the cap and
+    before refreshes."""
+    n, m = 8, 40
+    M = _auto_model(orc, n, m, 100000, N=6, smax=4, gamma=1.0)
+    P = np.zeros((n, m), np.float32)
+    G = np.zeros((n, m), np.float32)
+    for t in range(12):
+        M.step(t, [G], [P])
+    assert M.intervals() == [4, 2, 4, 2]
+
+
+def test_zen_auto_unimportant_zero_never_triggers(orc):
+    """unimportant columns zero, important nonzero -> no trigger regardless of
+    steps (only the refresh boundary ends the window)."""
+    n, m = 8, 40
+    M = _auto_model(orc, n, m, 100000, N=10, smax=10, gamma=1e-6)
+    G = _two_level(n, m, M.layers[0].k, 3.0, 0.0)
+    P = np.zeros((n, m), np.float32)
+    for t in range(20):
+        M.step(t, [G], [P])
+    assert M.intervals() == [10, 10]
+
+
+def test_zen_auto_monotone_in_unimportant_magnitude(orc):
+    """with a fixed important part, larger unimportant norms never delay the
+    trigger (random stream, important columns kept on top)."""
+    rng = np.random.default_rng(70)
+    n, m = 12, 60
+    base = [rng.standard_normal((n, m)).astype(np.float32) for _ in range(16)]
+    firsts = []
+    for scale in (0.5, 1.0, 2.0, 4.0, 8.0):
+        M = _auto_model(orc, n, m, 100000, N=16, smax=16, gamma=1.0)
+        k = M.layers[0].k
+        P = np.zeros((n, m), np.float32)
+        for t in range(16):
+            G = base[t] * np.float32(scale)
+            G[:, :k] = base[t][:, :k] + np.float32(8.0)
+            M.step(t, [G], [P])
+        firsts.append(M.ends[0])
+    assert firsts == sorted(firsts, reverse=True) and firsts[0] > firsts[-1], firsts
+
+
+def test_zen_auto_huge_gamma_is_the_fixed_schedule(orc):
+    """gamma -> infinity: windows end only at S_max (= S), so Zen-auto reduces to the fixed
+    S-step schedule -- selection, moments, parameters (with f1), compact blocks and both
+    accumulators bit-identical to stepping OracleLayer with fixed windows."""
+    import synth
+    n, m, N, S = 24, 96, 4, 2
+    Ms = _auto_model(orc, n, m, 100000, N=N, smax=S, gamma=1e300, cpu_update=True, layers=2)
+    Fs = [orc.OracleLayer(n=n, m=m, ratio_ppm=100000, refresh_interval=N, accum_interval=S, cpu_update=True)
+          for _ in range(2)]
+    PA = [synth.param(n, m, layer=i, dtype="fp32") for i in range(2)]
+    PB = [p.copy() for p in PA]
+    for t in range(9):
+        Gs = [synth.grad(n, m, i, t, synth.col_scale_at(m, t, i), dtype="fp32") for i in range(2)]
+        outs = Ms.step(t, Gs, PA)
+        for i in range(2):
+            assert np.array_equal(outs[i], Fs[i].step(t, Gs[i], PB[i]))
+            assert np.array_equal(PA[i], PB[i]) and np.array_equal(Ms.layers[i].acc[0], Fs[i].acc[0])
+            assert np.array_equal(Ms.layers[i].acc[1], Fs[i].acc[1])
+    assert Ms.intervals() == [2, 2, 2, 2]
+
+
+def test_zen_auto_cpu_update_uses_the_window_length(orc):
+    """f1 under Zen-auto: a window of L steps updates theta^(c) once with acc / L (P:527 with
+    S = L).  Constant dyadic stream, ratio 0.25, gamma = 1 -> L = 4; at the first flush
+    every unimportant column moves by -lr*g/(|g|+eps) (bias-corrected step 1 with the
+    exact window average g)."""
+    n, m = 16, 64
+    M = _auto_model(orc, n, m, 100000, N=8, smax=8, gamma=1.0, cpu_update=True)
+    k = M.layers[0].k
+    G = _two_level(n, m, k, 1.0, 0.25)
+    P = np.zeros((n, m), np.float32)
+    for t in range(3):
+        M.step(t, [G], [P])
+        assert np.all(P[:, k:] == 0.0)
+    M.step(3, [G], [P])
+    assert M.ends == [3]
+    assert np.allclose(P[:, k:], -1e-3 * 0.25 / (0.25 + 1e-8), rtol=1e-6)
+    assert M.layers[0].th[k:].tolist() == [1] * (m - k)
