@@ -167,6 +167,17 @@ typedef struct {
                                          whose refresh keeps the moments of the columns
                                          it selects (R7).  With tau > 0 the first step
                                          must be t = 0.                              */
+    float auto_gamma;                 /* > 0: Zen-auto (next row f2, reading
+                                         R21): the accumulation windows end adaptively,
+                                         for the whole model at once, when the window's
+                                         accumulated mean unimportant channel norm A
+                                         reaches auto_gamma x the step's mean important
+                                         channel norm (norms from K1, which then runs on
+                                         every step, all-reduced when world > 1), after
+                                         accum_interval (= S_max) steps, or before a
+                                         refresh.  With cpu_update a window of L steps
+                                         applies acc / L.  Requires host_accumulate.
+                                         0: fixed S-step windows.                     */
 } zf_config;
 
 typedef struct zf_ctx zf_ctx;
@@ -214,6 +225,14 @@ zf_status zf_compact_buffer(zf_ctx* ctx, int32_t layer, const void** dev, int64_
  * window's buffer, 1 the last sealed window's buffer (NULL if none yet). */
 zf_status zf_host_accumulator(zf_ctx* ctx, int32_t layer, int32_t which, const float** host, int64_t* rows,
                               int64_t* cols);
+/* Accumulation-window log, one entry per regular step the host accumulation has
+ * processed (call after zf_sync): global step t, whether a window ended there, and
+ * (Zen-auto only, else NaN) the decision's inputs: A = the window's accumulated mean
+ * unimportant channel norm, imp / unimp = the step's mean important / unimportant
+ * channel norm (reading R21).  Entries [0, min(cap, count)) are written to the
+ * [host] arrays that are not NULL; *count = the number of entries so far. */
+zf_status zf_window_log(zf_ctx* ctx, int64_t cap, int64_t* t, int32_t* end, double* A, double* imp, double* unimp,
+                        int64_t* count);
 /* Change the learning rate used from the next zf_step on (schedules). */
 zf_status zf_set_lr(zf_ctx* ctx, double lr);
 /* Per-phase device timing: when enabled, zf_step records CUDA events on its

@@ -615,6 +615,26 @@ struct zf_ctx {
     std::deque<int64_t> jobs;
     int64_t h1_done = -1;
     bool stopping = false;
+    // accumulation windows as H1 sees them (fixed S, or Zen-auto decisions), and the log
+    int64_t h1_win = 0;           // index of the window the next processed step belongs to
+    bool h1_first = true;         // the next processed step starts a window
+    int h1_last_buf = -1;         // buffer the last processed step accumulated into
+    int h1_sealed_buf = -1;       // buffer of the last ended window
+    std::vector<int64_t> log_t;
+    std::vector<int32_t> log_end;
+    std::vector<double> log_A, log_i, log_u;
+    // the same windows as zf_step sees them (f1 updates at window ends)
+    int64_t mw = 0, mw_len = 0;
+    // f2 Zen-auto (reading R21): K6 tables per current set, device state, decision records
+    bool autoz = false;
+    AutoLayer* d_auto_tab[2] = {nullptr, nullptr};
+    double* auto_sums = nullptr;
+    uint32_t* auto_counter = nullptr;
+    AutoState* auto_state = nullptr;
+    AutoRecord* auto_rec_h = nullptr;   // mapped pinned ring [AUTO_RING]
+    AutoRecord* auto_rec_d = nullptr;
+    cudaEvent_t auto_ev[8] = {};
+    static constexpr int AUTO_RING = 8;
     // per-phase timing (zf_profile)
     bool profiling = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
@@ -696,6 +716,8 @@ zf_ctx::~zf_ctx() {
     for (auto e : ring_ev) cudaEventDestroy(e);
     for (auto e : d2h_all)
         if (e) cudaEventDestroy(e);
+    for (auto e : auto_ev)
+        if (e) cudaEventDestroy(e);
     for (auto& e : ev_pool) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
     for (auto& e : pending) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     if (step_done) cudaEventDestroy(step_done);
@@ -746,8 +768,8 @@ void zf_ctx::h1_loop() {
             if (jobs.empty()) return;
             t = jobs.front();
         }
-        const int a = (int)((t / S) % 2);
-        const bool first = (t % S) == 0;
+        const int a = (int)(h1_win % 2);
+        const bool first = h1_first;
         const int sb = (int)(t % n_stage);
         for (auto& l : L) {
             cudaEventSynchronize(l.d2h_ev[sb]);
@@ -762,8 +784,31 @@ void zf_ctx::h1_loop() {
                 }
             });
         }
+        // the window decision of step t: fixed S, or K6's record (Zen-auto, reading R21)
+        bool end = (t + 1) % S == 0;
+        double rA = NAN, ri = NAN, ru = NAN;
+        if (autoz) {
+            const int slot = (int)(t % AUTO_RING);
+            cudaEventSynchronize(auto_ev[slot]);
+            const volatile AutoRecord* r = auto_rec_h + slot;
+            end = r->end != 0;
+            rA = r->A;
+            ri = r->imp;
+            ru = r->unimp;
+        }
         {
             std::lock_guard<std::mutex> lk(mu);
+            h1_last_buf = a;
+            if (end) {
+                h1_sealed_buf = a;
+                ++h1_win;
+            }
+            h1_first = end;
+            log_t.push_back(t + tau);
+            log_end.push_back(end ? 1 : 0);
+            log_A.push_back(rA);
+            log_i.push_back(ri);
+            log_u.push_back(ru);
             jobs.pop_front();
             h1_done = t;
         }
@@ -980,6 +1025,9 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
     if (cfg->cpu_update && cfg->refresh_interval % cfg->accum_interval != 0)
         return fail(ZF_EINVAL, "cpu_update requires refresh_interval to be a multiple of accum_interval");
     if (cfg->warmup_steps < 0) return fail(ZF_EINVAL, "warmup_steps must be >= 0");
+    if (!(cfg->auto_gamma >= 0.0f) || !std::isfinite(cfg->auto_gamma))
+        return fail(ZF_EINVAL, "auto_gamma must be finite and >= 0");
+    if (cfg->auto_gamma > 0.0f && !cfg->host_accumulate) return fail(ZF_EINVAL, "auto_gamma requires host_accumulate");
     ZF_TRY(check_hp(&cfg->adam));
     if (world < 1 || rank < 0 || rank >= world) return fail(ZF_EINVAL, "bad world/rank");
     if (world > 1 && !nccl_id128) return fail(ZF_EINVAL, "nccl_id128 required when world > 1");
@@ -1111,6 +1159,30 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
         c->adam.bc2_len = (int)h.size();
     }
     ZF_CTRY(build_tables(c));
+    // ---- f2 Zen-auto (reading R21): K6 tables over the two selection sets, window state
+    c->autoz = cfg->auto_gamma > 0.0f;
+    if (c->autoz) {
+        for (int v = 0; v < 2; ++v) {
+            std::vector<AutoLayer> h(n_layers);
+            for (int i = 0; i < n_layers; ++i) {
+                const LayerState& l = c->L[i];
+                h[i].norms = c->norms + l.norm_off;
+                h[i].mask = l.mask[v];
+                h[i].m = l.d.m;
+                h[i].k = l.k;
+            }
+            ZF_CTRY(c->dalloc(&c->d_auto_tab[v], n_layers * sizeof(AutoLayer)));
+            ZF_CUDA(cudaMemcpy(c->d_auto_tab[v], h.data(), n_layers * sizeof(AutoLayer), cudaMemcpyHostToDevice));
+        }
+        ZF_CTRY(c->dalloc(&c->auto_sums, 2 * n_layers * sizeof(double)));
+        ZF_CTRY(c->dalloc(&c->auto_counter, sizeof(uint32_t)));
+        ZF_CTRY(c->dalloc(&c->auto_state, sizeof(AutoState)));  // zero: no open window
+        ZF_CUDA(cudaHostAlloc(&c->auto_rec_h, zf_ctx::AUTO_RING * sizeof(AutoRecord), cudaHostAllocMapped));
+        c->host_pinned.push_back(c->auto_rec_h);
+        std::memset(c->auto_rec_h, 0, zf_ctx::AUTO_RING * sizeof(AutoRecord));
+        ZF_CUDA(cudaHostGetDevicePointer(&c->auto_rec_d, c->auto_rec_h, 0));
+        for (auto& e : c->auto_ev) ZF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventBlockingSync));
+    }
     c->done_target.assign(n_layers, 0u);
     ZF_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
     for (auto& l : c->L) {
@@ -1295,8 +1367,7 @@ zf_status f1_refresh(zf_ctx* c, void* const* params, cudaStream_t s) {
 // At a window end: one AdamW step (O6 op order, double-derived constants rounded once) with
 // the window's average gradient acc/S on the fp32 master of the unselected columns; the
 // rounded results are uploaded and scattered into the parameters.
-zf_status f1_window_end(zf_ctx* c, int64_t t, void* const* params, cudaStream_t s) {
-    const int S = c->cfg.accum_interval;
+zf_status f1_window_end(zf_ctx* c, int64_t t, int buf, int64_t len, void* const* params, cudaStream_t s) {
     {
         std::unique_lock<std::mutex> lk(c->mu);
         c->cv.wait(lk, [&] { return c->h1_done >= t; });
@@ -1306,13 +1377,13 @@ zf_status f1_window_end(zf_ctx* c, int64_t t, void* const* params, cudaStream_t 
     const float b1 = (float)b1d, b2 = (float)b2d, omb1 = (float)(1.0 - b1d), omb2 = (float)(1.0 - b2d);
     const float eps = (float)hp.eps, wd_f = (float)hp.weight_decay, decay = (float)(1.0 - lr * hp.weight_decay);
     const int wd_mode = hp.weight_decay == 0.0 ? 0 : (hp.decoupled ? 1 : 2);
-    const float Sf = (float)S;
+    const float Sf = (float)len;  // the window's length: S, or Zen-auto's interval (R21)
     const int nl = (int)c->L.size();
     for (int i = 0; i < nl; ++i) {
         LayerState& l = c->L[i];
         const int64_t m = l.d.m, n = l.d.n, mk = l.mk;
         if (mk == 0) continue;
-        const float* acc = l.acc[(t / S) % 2];
+        const float* acc = l.acc[buf];
         std::vector<float> ss(mk), bc2s(mk);
         for (int64_t u = 0; u < mk; ++u) {
             const double tt = (double)(l.th[l.unsel_host[u]] + 1);
@@ -1419,7 +1490,8 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
     const bool from_warmup = !c->have_sel && tau > 0;
     const int variant = from_warmup ? -2 - (sb & 1) : c->cur * 4 + (refresh ? 2 : 0) + (sb & 1);
     ZF_TRY(upload_ss(c, s));
-    ZF_TRY(refresh_pointer_tables(c, variant, refresh, grads, params, s));
+    const bool norms_now = refresh || c->autoz;  // Zen-auto reads every step's norms (R21)
+    ZF_TRY(refresh_pointer_tables(c, variant, norms_now, grads, params, s));
 
     if (c->cfg.offload) {
         // (K3 counts per-layer completions only when offloading; see build_tables)
@@ -1431,7 +1503,7 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
             c->cv.wait(lk, [&] { return c->h1_done >= t - 2 || c->last_t < t - 2; });
         }
     }
-    if (refresh) {
+    if (norms_now) {
         zf_ctx::Pending pe;
         Table<NormLayer> tn{};
         tn.dev = c->d_norm_tab;
@@ -1445,6 +1517,9 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
             ZF_NCCL(ncclAllReduce(c->norms, c->norms, (size_t)c->total_m, ncclFloat32, ncclSum, c->comm, s));
             ZF_TRY(c->prof_end(&pe, s));
         }
+    }
+    if (refresh) {
+        zf_ctx::Pending pe;
         Table<TopkLayer> tk{};
         tk.dev = c->have_sel ? c->d_topk_tab[c->cur ^ 1] : (from_warmup ? c->d_topk_w : c->d_topk_tab[2]);
         tk.n = nl;
@@ -1483,6 +1558,15 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
         c->cur ^= 1;
         c->have_sel = true;
     }
+    if (c->autoz) {
+        // K6: the step's Zen-auto decision from its norms and the (new) current selection
+        const int slot = (int)(t % zf_ctx::AUTO_RING);
+        ZF_CUDA(launch_zen_auto(c->d_auto_tab[c->cur], nl, c->auto_sums, c->auto_counter, c->auto_state,
+                                c->auto_rec_d + slot, t0, (double)c->cfg.auto_gamma, c->cfg.accum_interval,
+                                (t + 1) % N == 0 ? 1 : 0, s));
+        c->launches++;
+        ZF_CUDA(cudaEventRecord(c->auto_ev[slot], s));
+    }
     c->last_t = t;
     c->last_step = t0;
     ZF_CUDA(cudaEventRecord(c->step_done, s));
@@ -1517,9 +1601,24 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
             c->cv.notify_all();
         }
     }
-    if (c->cfg.cpu_update) {
-        if (refresh) ZF_TRY(f1_refresh(c, params, s));
-        if ((t + 1) % c->cfg.accum_interval == 0) ZF_TRY(f1_window_end(c, t, params, s));
+    if (c->cfg.cpu_update && refresh) ZF_TRY(f1_refresh(c, params, s));
+    if (c->cfg.host_accumulate) {
+        // the window decision of step t (fixed S, or Zen-auto's record) and, with f1, the
+        // CPU update of an ended window (synchronous, reading R18)
+        c->mw_len += 1;
+        bool end = (t + 1) % c->cfg.accum_interval == 0;
+        if (c->autoz && c->cfg.cpu_update) {
+            const int slot = (int)(t % zf_ctx::AUTO_RING);
+            ZF_CUDA(cudaEventSynchronize(c->auto_ev[slot]));
+            end = static_cast<const volatile AutoRecord*>(c->auto_rec_h + slot)->end != 0;
+        } else if (c->autoz) {
+            end = false;  // not needed on this thread without f1 (H1 tracks the windows)
+        }
+        if (c->cfg.cpu_update && end) ZF_TRY(f1_window_end(c, t, (int)(c->mw % 2), c->mw_len, params, s));
+        if (end) {
+            c->mw += 1;
+            c->mw_len = 0;
+        }
     }
     return ZF_OK;
 }
@@ -1596,20 +1695,34 @@ extern "C" zf_status zf_host_accumulator(zf_ctx* c, int32_t layer, int32_t which
                                          int64_t* cols) {
     if (!c || layer < 0 || layer >= (int)c->L.size()) return fail(ZF_EINVAL, "bad ctx/layer");
     if (!c->cfg.host_accumulate) return fail(ZF_ESTATE, "host accumulation is off");
-    const int S = c->cfg.accum_interval;
     const LayerState& l = c->L[layer];
     const float* p = nullptr;
-    if (c->last_t >= 0) {
-        if (which == 0) {
-            p = l.acc[(c->last_t / S) % 2];
-        } else {
-            const int64_t w = (c->last_t + 1) / S - 1;  // last completed window
-            if (w >= 0) p = l.acc[w % 2];
-        }
+    {
+        // windows as the host accumulation processed them (fixed S or Zen-auto)
+        std::lock_guard<std::mutex> lk(c->mu);
+        const int b = which == 0 ? c->h1_last_buf : c->h1_sealed_buf;
+        if (b >= 0) p = l.acc[b];
     }
     if (host) *host = p;
     if (rows) *rows = l.d.n;
     if (cols) *cols = l.mk;
+    return ZF_OK;
+}
+
+extern "C" zf_status zf_window_log(zf_ctx* c, int64_t cap, int64_t* t, int32_t* end, double* A, double* imp,
+                                   double* unimp, int64_t* count) {
+    if (!c) return fail(ZF_EINVAL, "ctx is NULL");
+    if (!c->cfg.host_accumulate) return fail(ZF_ESTATE, "host accumulation is off");
+    std::lock_guard<std::mutex> lk(c->mu);
+    const int64_t n = (int64_t)c->log_t.size();
+    for (int64_t i = 0; i < std::min(cap, n); ++i) {
+        if (t) t[i] = c->log_t[i];
+        if (end) end[i] = c->log_end[i];
+        if (A) A[i] = c->log_A[i];
+        if (imp) imp[i] = c->log_i[i];
+        if (unimp) unimp[i] = c->log_u[i];
+    }
+    if (count) *count = n;
     return ZF_OK;
 }
 

@@ -20,7 +20,7 @@ ZF_FP32, ZF_BF16 = 0, 1
 
 SYMBOLS = ["zf_status_string", "zf_last_error", "zf_version", "zf_k_for", "zf_column_norms", "zf_topk_columns",
            "zf_selective_adam", "zf_compact_unselected", "zf_nccl_unique_id", "zf_create", "zf_step", "zf_sync",
-           "zf_selected", "zf_norms", "zf_optimizer_state", "zf_compact_buffer", "zf_host_accumulator", "zf_set_lr",
+           "zf_selected", "zf_norms", "zf_optimizer_state", "zf_compact_buffer", "zf_host_accumulator", "zf_window_log", "zf_set_lr",
            "zf_kernel_launches", "zf_profile", "zf_profile_read", "zf_destroy"]
 
 
@@ -44,7 +44,8 @@ class Config(ctypes.Structure):
     _fields_ = [("grad_dtype", ctypes.c_int32), ("param_dtype", ctypes.c_int32), ("topk_ppm", ctypes.c_int32),
                 ("refresh_interval", ctypes.c_int32), ("accum_interval", ctypes.c_int32), ("adam", AdamParams),
                 ("offload", ctypes.c_int32), ("host_accumulate", ctypes.c_int32), ("host_threads", ctypes.c_int32),
-                ("cpu_update", ctypes.c_int32), ("warmup_steps", ctypes.c_int32)]
+                ("cpu_update", ctypes.c_int32), ("warmup_steps", ctypes.c_int32),
+                ("auto_gamma", ctypes.c_float)]
 
 
 if not os.path.exists(_LIB_PATH):
@@ -80,6 +81,10 @@ lib.zf_compact_buffer.restype = _st
 lib.zf_host_accumulator.argtypes = [_vp, _i32, _i32, ctypes.POINTER(_vp), ctypes.POINTER(_i64),
                                     ctypes.POINTER(_i64)]
 lib.zf_host_accumulator.restype = _st
+_pd = ctypes.POINTER(ctypes.c_double)
+lib.zf_window_log.argtypes = [_vp, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_i32), _pd, _pd, _pd,
+                              ctypes.POINTER(_i64)]
+lib.zf_window_log.restype = _st
 lib.zf_set_lr.argtypes = [_vp, ctypes.c_double]; lib.zf_set_lr.restype = _st
 lib.zf_kernel_launches.argtypes = [_vp]; lib.zf_kernel_launches.restype = _i64
 lib.zf_destroy.argtypes = [_vp]; lib.zf_destroy.restype = _st
@@ -196,7 +201,7 @@ class Context:
     def __init__(self, layers, grad_dtype=torch.bfloat16, param_dtype=torch.bfloat16, topk_ratio_ppm=100000,
                  refresh_interval=4, accum_interval=4, adam: AdamParams | None = None, offload=False,
                  host_accumulate=False, host_threads=0, world=1, rank=0, nccl_id: bytes | None = None,
-                 device: int | None = None, cpu_update=False, warmup_steps=0):
+                 device: int | None = None, cpu_update=False, warmup_steps=0, auto_gamma=0.0):
         self.layers = [l if isinstance(l, LayerShape) else LayerShape(*l) for l in layers]
         descs = (LayerDesc * len(self.layers))()
         for d, l in zip(descs, self.layers):
@@ -216,6 +221,7 @@ class Context:
         cfg.host_threads = host_threads
         cfg.cpu_update = int(cpu_update)
         cfg.warmup_steps = int(warmup_steps)
+        cfg.auto_gamma = float(auto_gamma)
         self.cfg = cfg
         self.device = torch.cuda.current_device() if device is None else device
         h = ctypes.c_void_p()
@@ -308,6 +314,18 @@ class Context:
             return None
         arr = (ctypes.c_float * (r.value * c.value)).from_address(p.value)
         return np.ctypeslib.as_array(arr).reshape(r.value, c.value)
+
+    def window_log(self):
+        """Accumulation-window log after sync(): list of (t, ended, A, imp, unimp) per regular
+        step (Zen-auto decision inputs; NaN with fixed windows)."""
+        n = ctypes.c_int64()
+        _check(lib.zf_window_log(self._h, 0, None, None, None, None, None, ctypes.byref(n)), "zf_window_log")
+        cnt = n.value
+        t = (ctypes.c_int64 * max(cnt, 1))()
+        e = (ctypes.c_int32 * max(cnt, 1))()
+        A, i, u = ((ctypes.c_double * max(cnt, 1))() for _ in range(3))
+        _check(lib.zf_window_log(self._h, cnt, t, e, A, i, u, ctypes.byref(n)), "zf_window_log")
+        return [(t[q], bool(e[q]), A[q], i[q], u[q]) for q in range(cnt)]
 
     def close(self):
         if getattr(self, "_h", None):

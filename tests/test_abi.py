@@ -95,6 +95,12 @@ def test_create_validation(zf):
     assert L.zf_create(descs, 1, ctypes.byref(cfg), 1, 0, None, 0, ctypes.byref(h)) == zf.ZF_EINVAL
     cfg.refresh_interval = 4
     assert L.zf_create(descs, 1, ctypes.byref(cfg), 2, 0, None, 0, ctypes.byref(h)) == zf.ZF_EINVAL  # no nccl id
+    cfg.auto_gamma = -1.0                                                              # Zen-auto gamma < 0
+    assert L.zf_create(descs, 1, ctypes.byref(cfg), 1, 0, None, 0, ctypes.byref(h)) == zf.ZF_EINVAL
+    cfg.auto_gamma, cfg.host_accumulate = 1.0, 0                                       # Zen-auto needs H1
+    assert L.zf_create(descs, 1, ctypes.byref(cfg), 1, 0, None, 0, ctypes.byref(h)) == zf.ZF_EINVAL
+    assert b"auto_gamma" in L.zf_last_error()
+    cfg.auto_gamma = 0.0
     descs[0].ld_grad = 7
     assert L.zf_create(descs, 1, ctypes.byref(cfg), 1, 0, None, 0, ctypes.byref(h)) == zf.ZF_EINVAL
     assert not h.value

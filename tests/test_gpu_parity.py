@@ -373,3 +373,93 @@ def test_llama2_13b_rank0_shard_offload_sampled(zf, orc, gpu):
     """BASELINE config 5 on one GPU: the row shard rank 0 of 8 would own (n/8 rows of all
     281 linears), k=10%, with D2H offload + host accumulation; sampled layers checked."""
     _run_fullsize(zf, orc, gpu, synth.llama2_13b_linears(), 100000, 2, [0, 5, 6, 280], offload=True, row_div=8)
+
+
+# ------------------------------------------------------------------ f2: Zen-auto (reading R21)
+def _run_auto(zf, orc, gpu, shapes, gdt, pdt, ppm, N, smax, gamma, steps, cpu_update=False, warmup=0, lr=1e-3):
+    """zf_step with auto_gamma against OracleModel: per step the window decision and its
+    inputs (A, mean important / unimportant channel norm), and bit for bit the selection,
+    moments, parameters (incl. f1 updates with the window's length), compact blocks and
+    both host accumulators."""
+    hp_o = orc.AdamHP(lr=lr)
+    ctx = zf.Context([zf.LayerShape(n, m) for n, m in shapes], grad_dtype=TDT[gdt], param_dtype=TDT[pdt],
+                     topk_ratio_ppm=ppm, refresh_interval=N, accum_interval=smax, adam=zf.adam_params(lr=lr),
+                     offload=True, host_accumulate=True, cpu_update=cpu_update, warmup_steps=warmup,
+                     auto_gamma=gamma)
+    scales = [gpu.ColScale(m, li) for li, (n, m) in enumerate(shapes)]
+    Gs = [torch.empty(n, m, dtype=TDT[gdt], device="cuda") for n, m in shapes]
+    Ps = [torch.empty(n, m, dtype=TDT[pdt], device="cuda") for n, m in shapes]
+    for li, P in enumerate(Ps):
+        gpu.fill_param(P, li)
+    model = orc.OracleModel([orc.OracleLayer(n=n, m=m, ratio_ppm=ppm, refresh_interval=N, accum_interval=smax,
+                                             hp=hp_o, cpu_update=cpu_update, warmup=warmup) for n, m in shapes],
+                            auto_gamma=gamma)
+    Po = [np.ascontiguousarray(to_np(P)) for P in Ps]
+    sealed_buf = None
+    for t in range(steps):
+        for li, (G, sc) in enumerate(zip(Gs, scales)):
+            sc.advance_to(t)
+            gpu.fill_grad(G, li, t, sc)
+        Gn = [np.ascontiguousarray(to_np(G)) for G in Gs]
+        ctx.step(t, Gs, Ps)
+        ctx.sync()
+        refresh = t >= warmup and (t - warmup) % N == 0
+        ov = None
+        if refresh:
+            ov = []
+            for li, L in enumerate(model.layers):
+                gidx = to_np(ctx.selected(li))
+                onorms = orc.column_norms(Gn[li])
+                assert selection_ok(gidx, orc.topk(onorms, L.k), onorms) == 0
+                ov.append(gidx)
+        w_before = model.w
+        model.step(t, Gn, Po, idx_overrides=ov)
+        for li, L in enumerate(model.layers):
+            assert_bits_equal(to_np(ctx.selected(li)), L.idx, f"idx t={t} l={li}")
+            M, V, st = ctx.optimizer_state(li)
+            assert_bits_equal(to_np(M), L.M, f"exp_avg t={t} l={li}")
+            assert_bits_equal(to_np(V), L.V, f"exp_avg_sq t={t} l={li}")
+            assert_bits_equal(np.ascontiguousarray(to_np(Ps[li])), Po[li], f"params t={t} l={li}")
+        if t < warmup:
+            continue
+        log = ctx.window_log()
+        lt, lend, lA, li_, lu = log[-1]
+        oA, oi, ou = model.stats[-1]
+        assert lt == t and len(log) == t - warmup + 1
+        assert abs(oA - gamma * oi) > 1e-4 * gamma * oi, "decision too close to call (pick another gamma)"
+        assert lend == (model.ends[-1:] == [t]), f"window decision t={t}"
+        for got, want, what in ((lA, oA, "A"), (li_, oi, "imp"), (lu, ou, "unimp")):
+            assert abs(got - want) <= 1e-5 * abs(want), (t, what, got, want)
+        for li, L in enumerate(model.layers):
+            assert_bits_equal(ctx.host_accumulator(li, 0).copy(), L.acc[w_before % 2], f"acc t={t} l={li}")
+        if lend:
+            sealed_buf = w_before % 2
+        for li, L in enumerate(model.layers):
+            s = ctx.host_accumulator(li, 1)
+            assert (s is None) == (sealed_buf is None)
+            if s is not None:
+                assert_bits_equal(s.copy(), L.acc[sealed_buf], f"sealed acc t={t} l={li}")
+    ends = [e for (e, end, *_r) in ctx.window_log() if end]
+    ctx.close()
+    assert ends == model.ends
+    return model.intervals()
+
+
+AUTO_SHAPES = [(64, 256), (96, 200), (128, 320)]
+
+
+@pytest.mark.parametrize("gamma,cpu,pdt", [(0.15, False, "bf16"), (0.15, True, "bf16"), (0.25, True, "fp32"),
+                                           (0.1, False, "fp32")])
+def test_step_zen_auto(zf, orc, gpu, gamma, cpu, pdt):
+    """Zen-auto (f2, reading R21) on column-concentrated synthetic gradients: intervals vary
+    (not all equal to S_max), windows cut at the refresh every 8 steps."""
+    gdt = "bf16" if pdt == "bf16" else "fp32"
+    iv = _run_auto(zf, orc, gpu, AUTO_SHAPES, gdt, pdt, 100000, 8, 8, gamma, 16, cpu_update=cpu)
+    assert sum(iv) == 16 and min(iv) < 8, iv
+
+
+def test_step_zen_auto_cap_refresh_and_warmup(zf, orc, gpu):
+    """S_max (= accum_interval) and the refresh boundary cut windows; the schedule starts after
+    tau warm-up steps."""
+    iv = _run_auto(zf, orc, gpu, AUTO_SHAPES, "bf16", "bf16", 100000, 6, 3, 0.5, 14, cpu_update=True, warmup=2)
+    assert max(iv) <= 3 and sum(iv) == 12, iv
