@@ -386,14 +386,16 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
                 if (si.pstaged) {
                     const unsigned char* P = static_cast<const unsigned char*>(L.P);
                     si.oP = off;
-                    if (L.nseg == 1 && L.ldp == L.m) {
+                    if (prm.debug_mode == 4) {
+                        // traffic experiment: write back touched p chunks without reading p
+                    } else if (L.nseg == 1 && L.ldp == L.m) {
                         bulk_g2s(A + off, P + g.r0 * L.m * PSZ, (uint32_t)(g.Rr * sw * PSZ), &full[st], pol_last);
                     } else {
                         for (int r = 0; r < g.Rr; ++r)
                             bulk_g2s(A + off + r * sw * PSZ, P + ((g.r0 + r) * L.ldp + g.c0) * PSZ,
                                      (uint32_t)(sw * PSZ), &full[st], pol_last);
                     }
-                    tx += (uint32_t)(g.Rr * sw * PSZ);
+                    if (prm.debug_mode != 4) tx += (uint32_t)(g.Rr * sw * PSZ);
                     off += (g.Rr * sw * PSZ + 15) & ~15;
                 }
                 if (si.mstaged) {
@@ -484,7 +486,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
         unsigned char* A = smem + st * K3_ARENA;
         const GB* sG = reinterpret_cast<const GB*>(A + si.oG);
         const int ns = si.s1 - si.s0;
-        const bool adam = prm.do_adam && (prm.debug_mode == 0 || prm.debug_mode == 3) && ns > 0;
+        const bool adam = prm.do_adam && (prm.debug_mode == 0 || prm.debug_mode >= 3) && ns > 0;
         const bool pwb = adam && si.pstaged;
 
         // ---------------- (1) AdamW ----------------
