@@ -49,6 +49,10 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--also-k1pct", action="store_true", help="also time k = 1% (reported as an extra field)")
+    ap.add_argument("--also-state-offload", action="store_true",
+                    help="also time the f3 state swap-out mode (moments in mapped pinned host memory)")
+    ap.add_argument("--also-auto", type=float, default=0.0, metavar="GAMMA",
+                    help="also time Zen-auto (f2) with this gamma (K1 every step + K6 decision; offload + H1)")
     ap.add_argument("--json-out", default=None)
     return ap.parse_args()
 
@@ -229,11 +233,11 @@ def run_zenflow(args, rank, world):
         from paper_2505_12242_b200.dist import broadcast_nccl_id
         nccl_id = broadcast_nccl_id()
 
-    def make_ctx(ratio_ppm, offload):
+    def make_ctx(ratio_ppm, offload, **kw):
         return zf.Context([zf.LayerShape(n, m) for n, m in shapes], topk_ratio_ppm=ratio_ppm,
                           refresh_interval=args.refresh, accum_interval=args.refresh,
                           adam=zf.adam_params(lr=args.lr), offload=offload, host_accumulate=offload,
-                          world=world, rank=rank, nccl_id=nccl_id, device=dev)
+                          world=world, rank=rank, nccl_id=nccl_id, device=dev, **kw)
 
     import ctypes
     nl = len(shapes)
@@ -331,6 +335,34 @@ def run_zenflow(args, rank, world):
         ctx.close()
         del ctx
         result["k1pct_ms_per_step"] = ms1 / args.steps
+
+    # ---- f3 state swap-out: moments in mapped pinned host memory (extra field)
+    if args.also_state_offload:
+        ctx = make_ctx(args.ratio_ppm, False, state_offload=True)
+        mss, profs, _ = timed_run(ctx, args.steps, args.warmup, "state_offload")
+        ctx.close()
+        del ctx
+        mv = sum(n * k * 16 for (n, _m), k in zip(shapes, ks))  # m, v read + written per step
+        k3s = profs["k3_update"][0] / max(1, profs["k3_update"][1])
+        result["state_offload"] = {"ms_per_step": mss / args.steps, "k3_ms": k3s,
+                                   "host_link_moment_bytes_per_step": mv,
+                                   "host_link_GBs": mv / (k3s * 1e-3) / 1e9}
+
+    # ---- f2 Zen-auto: K1 every step + K6, with offload and host accumulation (extra field)
+    if args.also_auto > 0:
+        ctx = make_ctx(args.ratio_ppm, True, auto_gamma=args.also_auto)
+        msa, profa, la = timed_run(ctx, args.steps, args.warmup, "auto")
+        log = ctx.window_log()
+        ctx.close()
+        del ctx
+        ends = [t for (t, e, *_r) in log if e]
+        dev_ms = sum(v[0] for v in profa.values()) / args.steps
+        result["zen_auto"] = {"gamma": args.also_auto, "kernel_ms_per_step": dev_ms,
+                              "wall_ms_per_step": msa / args.steps,
+                              "k1_launches": profa["k1_norms"][1], "gpu_launches": la,
+                              "window_ends": ends[-12:],
+                              "note": "kernel_ms = K1+K2+K3 event time per step (K6 not profiled, ~us); "
+                                      "wall includes waiting on the host accumulation (offload + H1)"}
 
     # ---- e2e: host buffers through the same API (H2D grads, D2H compact + host accumulation)
     if not args.no_e2e:

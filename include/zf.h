@@ -178,6 +178,16 @@ typedef struct {
                                          refresh.  With cpu_update a window of L steps
                                          applies acc / L.  Requires host_accumulate.
                                          0: fixed S-step windows.                     */
+    int32_t state_offload;            /* 1: swap the selective optimizer's state out of
+                                         HBM (next row f3, "swap out its
+                                         optimizer states to CPU and swap back in before
+                                         next update on GPU"): the moments live in
+                                         mapped pinned host memory and K3 streams each
+                                         unit's slab in over the host link with the same
+                                         bulk copies and writes it back with streaming
+                                         stores -- no moment bytes resident in HBM, at
+                                         the cost of 16 B per selected element per step on
+                                         the host link.  Results are bit-identical.     */
 } zf_config;
 
 typedef struct zf_ctx zf_ctx;

@@ -691,6 +691,18 @@ struct zf_ctx {
         ring_pos = (ring_pos + 1) % (int)ring.size();
         return ZF_OK;
     }
+    // optimizer-state storage: HBM, or mapped pinned host memory (state_offload, row f3)
+    zf_status state_alloc(float** p, size_t elems) {
+        if (!cfg.state_offload) return dalloc(p, elems * sizeof(float));
+        void* h = nullptr;
+        ZF_CUDA(cudaHostAlloc(&h, std::max<size_t>(elems * sizeof(float), 256), cudaHostAllocMapped));
+        host_pinned.push_back(h);
+        std::memset(h, 0, std::max<size_t>(elems * sizeof(float), 256));
+        void* d = nullptr;
+        ZF_CUDA(cudaHostGetDevicePointer(&d, h, 0));
+        *p = static_cast<float*>(d);
+        return ZF_OK;
+    }
     void h1_loop();
 };
 
@@ -1104,8 +1116,8 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
             ZF_CTRY(c->dalloc(&l.ucol[s], (l.mk + 16) * sizeof(uint16_t)));  // padded (K3 bulk copies)
             // padded by 16 elements: K3 stages these with 16-byte-granular bulk copies
             ZF_CTRY(c->dalloc(&l.steps[s], (k + 16) * sizeof(int32_t)));
-            ZF_CTRY(c->dalloc(&l.mom[s], ((size_t)n * k + 16) * sizeof(float)));
-            ZF_CTRY(c->dalloc(&l.vel[s], ((size_t)n * k + 16) * sizeof(float)));
+            ZF_CTRY(c->state_alloc(&l.mom[s], (size_t)n * k + 16));
+            ZF_CTRY(c->state_alloc(&l.vel[s], (size_t)n * k + 16));
         }
         ZF_CTRY(c->dalloc(&l.slot_src, (k + 16) * sizeof(int32_t)));
         if (c->tau > 0) {
@@ -1115,8 +1127,8 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
             ZF_CTRY(c->dalloc(&l.mask_w, (l.W + 8) * sizeof(uint32_t)));
             ZF_CTRY(c->dalloc(&l.prefix_w, (l.W + 8) * sizeof(int32_t)));
             ZF_CTRY(c->dalloc(&l.steps_w, (m + 16) * sizeof(int32_t)));
-            ZF_CTRY(c->dalloc(&l.mom_w, ((size_t)n * m + 16) * sizeof(float)));
-            ZF_CTRY(c->dalloc(&l.vel_w, ((size_t)n * m + 16) * sizeof(float)));
+            ZF_CTRY(c->state_alloc(&l.mom_w, (size_t)n * m + 16));
+            ZF_CTRY(c->state_alloc(&l.vel_w, (size_t)n * m + 16));
             std::vector<int32_t> iw(m), pw(l.W);
             std::vector<uint32_t> mw(l.W, 0xffffffffu);
             for (int64_t j = 0; j < m; ++j) iw[j] = (int32_t)j;

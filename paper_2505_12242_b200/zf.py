@@ -45,7 +45,7 @@ class Config(ctypes.Structure):
                 ("refresh_interval", ctypes.c_int32), ("accum_interval", ctypes.c_int32), ("adam", AdamParams),
                 ("offload", ctypes.c_int32), ("host_accumulate", ctypes.c_int32), ("host_threads", ctypes.c_int32),
                 ("cpu_update", ctypes.c_int32), ("warmup_steps", ctypes.c_int32),
-                ("auto_gamma", ctypes.c_float)]
+                ("auto_gamma", ctypes.c_float), ("state_offload", ctypes.c_int32)]
 
 
 if not os.path.exists(_LIB_PATH):
@@ -201,7 +201,8 @@ class Context:
     def __init__(self, layers, grad_dtype=torch.bfloat16, param_dtype=torch.bfloat16, topk_ratio_ppm=100000,
                  refresh_interval=4, accum_interval=4, adam: AdamParams | None = None, offload=False,
                  host_accumulate=False, host_threads=0, world=1, rank=0, nccl_id: bytes | None = None,
-                 device: int | None = None, cpu_update=False, warmup_steps=0, auto_gamma=0.0):
+                 device: int | None = None, cpu_update=False, warmup_steps=0, auto_gamma=0.0,
+                 state_offload=False):
         self.layers = [l if isinstance(l, LayerShape) else LayerShape(*l) for l in layers]
         descs = (LayerDesc * len(self.layers))()
         for d, l in zip(descs, self.layers):
@@ -222,6 +223,7 @@ class Context:
         cfg.cpu_update = int(cpu_update)
         cfg.warmup_steps = int(warmup_steps)
         cfg.auto_gamma = float(auto_gamma)
+        cfg.state_offload = int(state_offload)
         self.cfg = cfg
         self.device = torch.cuda.current_device() if device is None else device
         h = ctypes.c_void_p()

@@ -165,12 +165,12 @@ def test_compact_bitexact(zf, orc, gpu, n, m, dt, ld, ppm):
 
 # ------------------------------------------------------------------ zf_step vs oracle, multi-step
 def _run_stateful(zf, orc, gpu, shapes, gdt, pdt, ppm, N, S, steps, offload, lr=1e-3, wd=0.0, check_every=1,
-                  tie=False, ld_pad=0, cpu_update=False, warmup=0):
+                  tie=False, ld_pad=0, cpu_update=False, warmup=0, state_offload=False):
     hp_o = orc.AdamHP(lr=lr, weight_decay=wd)
     ctx = zf.Context([zf.LayerShape(n, m, m + ld_pad, m + ld_pad) for n, m in shapes], grad_dtype=TDT[gdt],
                      param_dtype=TDT[pdt], topk_ratio_ppm=ppm, refresh_interval=N, accum_interval=S,
                      adam=zf.adam_params(lr=lr, weight_decay=wd), offload=offload, host_accumulate=offload, cpu_update=cpu_update,
-                     warmup_steps=warmup)
+                     warmup_steps=warmup, state_offload=state_offload)
     scales = [gpu.ColScale(m, li) for li, (n, m) in enumerate(shapes)]
     Gs = [torch.empty(n, m + ld_pad, dtype=TDT[gdt], device="cuda")[:, :m] for n, m in shapes]
     Ps = [torch.empty(n, m + ld_pad, dtype=TDT[pdt], device="cuda")[:, :m] for n, m in shapes]
@@ -256,6 +256,16 @@ def test_step_warmup(zf, orc, gpu, tau, NS, pdt, cpu):
     gdt = "bf16" if pdt == "bf16" else "fp32"
     _run_stateful(zf, orc, gpu, shapes, gdt, pdt, 100000, NS, NS, tau + 6, offload=True, cpu_update=cpu,
                   warmup=tau)
+
+
+@pytest.mark.parametrize("shapes,gdt,NS,tau,cpu", [([(256, 512)], "fp32", 2, 0, False),
+                                                  ([(64, 512), (37, 1001), (16, 4096)], "bf16", 2, 2, True),
+                                                  ([(513, 768), (64, 4096)], "bf16", 4, 0, False)])
+def test_step_state_offload(zf, orc, gpu, shapes, gdt, NS, tau, cpu):
+    """f3 state swap-out: moments in mapped pinned host memory, streamed by K3 over
+    the host link; every result bit-identical to the oracle (and so to the HBM-resident path)."""
+    _run_stateful(zf, orc, gpu, shapes, gdt, gdt, 100000, NS, NS, tau + 5, offload=True, cpu_update=cpu,
+                  warmup=tau, state_offload=True)
 
 
 def test_cpu_update_needs_aligned_windows(zf):
