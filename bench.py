@@ -53,6 +53,8 @@ def parse():
                     help="also time the f3 state swap-out mode (moments in mapped pinned host memory)")
     ap.add_argument("--also-auto", type=float, default=0.0, metavar="GAMMA",
                     help="also time Zen-auto (f2) with this gamma (K1 every step + K6 decision; offload + H1)")
+    ap.add_argument("--partition", default="rows", choices=["rows", "flat"],
+                    help="N>1 data layout: every matrix split by rows (R13), or a row-snapped flat ZeRO partition (f3)")
     ap.add_argument("--json-out", default=None)
     return ap.parse_args()
 
@@ -194,7 +196,7 @@ def run_zenflow(args, rank, world):
         dist.barrier()
     from paper_2505_12242_b200 import zf
     from synth import gpu as sgpu
-    from paper_2505_12242_b200.dist import shard_rows
+    from paper_2505_12242_b200.dist import flat_partition, shard_rows
 
     dev = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(dev)
@@ -202,7 +204,10 @@ def run_zenflow(args, rank, world):
     names = synth.MODELS[args.model]()
     full_shapes = [(n, m) for _, n, m in names]
 
-    spans = [shard_rows(n, world, rank) for n, _ in full_shapes]
+    if args.partition == "flat":
+        spans = flat_partition(full_shapes, world, rank)
+    else:
+        spans = [shard_rows(n, world, rank) for n, _ in full_shapes]
     shapes = [(b - a, m) for (a, b), (_, m) in zip(spans, full_shapes)]
     row0s = [a for a, _ in spans]
     ks = [zf.k_for(m, args.ratio_ppm) for _, m in shapes]
@@ -297,7 +302,7 @@ def run_zenflow(args, rank, world):
         "data": "synthetic (seeded column-concentrated bf16 gradients, bf16 params, fp32 AdamW state)",
         "config": {"workload": f"{args.model}-all-linear-k{args.ratio_ppm // 10000}pct", "model": args.model,
                    "linears": nl, "elements": sum(n * m for n, m in full_shapes), "ratio_ppm": args.ratio_ppm,
-                   "refresh_interval": args.refresh, "parallelism": f"dp{world} (row shards, norm all-reduce)",
+                   "refresh_interval": args.refresh, "parallelism": f"dp{world} ({'flat ZeRO partition' if args.partition == 'flat' else 'row shards'}, norm all-reduce)",
                    "l2": "inputs larger than L2 (working set > 100 GB vs 126 MB L2); no flush needed",
                    "lr": args.lr},
         "phases_ms_per_launch": {"k3_update": k3_avg, "k1_norms": k1_ms / max(1, n_k1),

@@ -133,7 +133,9 @@ zf_status zf_compact_unselected(const void* G, zf_dtype gdt, int64_t n, int64_t 
  * stream, host accumulation threads and (world > 1) an NCCL communicator. */
 
 typedef struct {
-    int64_t n;          /* rows of this rank's shard (n_local; all ranks same m)   */
+    int64_t n;          /* rows of this rank's shard (n_local >= 0; all ranks same m;
+                           0: the matrix has no rows on this rank -- flat partitions,
+                           row f3 -- its pointers may be NULL, it contributes zero norms) */
     int64_t m;          /* columns (input channels)                                */
     int64_t ld_grad;    /* leading dim of the gradient passed to zf_step (>= m)     */
     int64_t ld_param;   /* leading dim of the parameter passed to zf_step (>= m)    */

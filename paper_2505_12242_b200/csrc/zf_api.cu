@@ -555,6 +555,7 @@ struct zf_ctx {
     int gdt = 0, pdt = 0, gsz = 2, psz = 2;
     std::vector<LayerState> L;
     int64_t total_m = 0, max_m = 0, k1_units = 0, k3_units = 0;
+    bool has_empty = false;       // some layer has n = 0 rows on this rank
     int n_stage = 1;
     float* norms = nullptr;
     std::vector<void*> dev_allocs, host_pinned;
@@ -1045,7 +1046,7 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
     if (world > 1 && !nccl_id128) return fail(ZF_EINVAL, "nccl_id128 required when world > 1");
     for (int i = 0; i < n_layers; ++i) {
         const zf_layer_desc& d = layers[i];
-        if (d.n < 1 || d.m < 1 || d.m > 0x7fffffffLL || d.ld_grad < d.m || d.ld_param < d.m)
+        if (d.n < 0 || d.m < 1 || d.m > 0x7fffffffLL || d.ld_grad < d.m || d.ld_param < d.m)
             return fail(ZF_EINVAL, "layer %d: bad shape (n=%lld m=%lld ld_grad=%lld ld_param=%lld)", i, (long long)d.n,
                         (long long)d.m, (long long)d.ld_grad, (long long)d.ld_param);
     }
@@ -1086,6 +1087,7 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
         l.nrb = (int32_t)((l.d.n + rb - 1) / rb);
         l.ncb = (int32_t)((l.d.m + cb - 1) / cb);
         l.norm_off = c->total_m;
+        if (l.d.n == 0) c->has_empty = true;
         l.norm_unit_begin = c->k1_units;
         c->total_m += l.d.m;
         c->max_m = std::max(c->max_m, l.d.m);
@@ -1339,6 +1341,7 @@ zf_status f1_refresh(zf_ctx* c, void* const* params, cudaStream_t s) {
         LayerState& l = c->L[i];
         nidx[i].resize(l.k);
         ZF_CUDA(cudaMemcpyAsync(nidx[i].data(), l.idx[c->cur], l.k * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        if (l.d.n > 0)
         ZF_CUDA(cudaMemcpy2DAsync(l.p_mirror, l.d.m * c->psz, params[i], l.d.ld_param * c->psz, l.d.m * c->psz, l.d.n,
                                   cudaMemcpyDeviceToHost, s));
     }
@@ -1478,7 +1481,8 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
     if (!grads || !params) return fail(ZF_EINVAL, "grads/params is NULL");
     const int nl = (int)c->L.size();
     for (int i = 0; i < nl; ++i)
-        if (!grads[i] || !params[i]) return fail(ZF_EINVAL, "layer %d: NULL gradient or parameter", i);
+        if ((!grads[i] || !params[i]) && c->L[i].d.n > 0)
+            return fail(ZF_EINVAL, "layer %d: NULL gradient or parameter", i);
     if (t0 < 0) return fail(ZF_EINVAL, "t must be >= 0");
     const int N = c->cfg.refresh_interval;
     const int64_t tau = c->tau;
@@ -1517,6 +1521,8 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
     }
     if (norms_now) {
         zf_ctx::Pending pe;
+        // layers with no rows on this rank (flat partitions, row f3) contribute zero norms
+        if (c->has_empty) ZF_CUDA(cudaMemsetAsync(c->norms, 0, c->total_m * sizeof(float), s));
         Table<NormLayer> tn{};
         tn.dev = c->d_norm_tab;
         tn.n = nl;
@@ -1599,7 +1605,7 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
                 }
             }
             // one flat copy of the pitched block (H1 reads the rows at the same pitch)
-            if (l.mk) ZF_CUDA(cudaMemcpyAsync(l.stage_host[sb], l.stage_dev[sb], (size_t)l.d.n * l.mk_pad * c->gsz,
+            if (l.mk && l.d.n) ZF_CUDA(cudaMemcpyAsync(l.stage_host[sb], l.stage_dev[sb], (size_t)l.d.n * l.mk_pad * c->gsz,
                                               cudaMemcpyDeviceToHost, c->copy_stream));
             ZF_CUDA(cudaEventRecord(l.d2h_ev[sb], c->copy_stream));
         }

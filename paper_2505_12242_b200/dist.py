@@ -2,6 +2,17 @@
 
 * ``shard_rows`` -- the row shard a rank owns (reading R13: ZeRO-2 averaged-gradient
   shards; contiguous, near-equal, remainder to the first ranks).
+* ``flat_partition`` -- the row ranges a rank owns under a ZeRO-style flat partition
+  (row f3): the model's gradients concatenated row-major and cut into
+  ``world`` near-equal contiguous ranges, each boundary snapped to the nearest row start
+  so that no row (and so no input channel's slice of a row) is split between ranks.
+  Most matrices then live on one rank (n_local = 0 elsewhere, which ``zf_create``
+  accepts); the ones straddling a boundary are split by rows.  The norm all-reduce sums
+  the ranks' partial norms of every matrix as before.
+* ``segment_map`` -- the (segment_id, offset) table of P:583 for such a partition: for
+  each selected channel (segment_id = its slot) of each matrix this rank holds rows of,
+  the offset of the channel's first element in the rank's flattened storage (stride m,
+  n_local elements).
 * ``broadcast_nccl_id`` -- rank 0 creates the 128-byte NCCL unique id through the
   C-ABI (``zf_nccl_unique_id``) and ``torch.distributed`` broadcasts it; every rank
   then passes it to ``zf_create`` (the norm all-reduce runs inside ``zf_step``).
@@ -24,3 +35,54 @@ def broadcast_nccl_id(group=None) -> bytes:
     obj = [zf.zf_nccl_unique_id() if dist.get_rank(group) == 0 else None]
     dist.broadcast_object_list(obj, src=0, group=group)
     return obj[0]
+
+
+def flat_partition(shapes, world: int, rank: int) -> list[tuple[int, int]]:
+    """[start, stop) rows of every (n, m) matrix owned by `rank` under the row-snapped flat
+    partition (see module doc).  Every row of every matrix belongs to exactly one rank."""
+    if not (world >= 1 and 0 <= rank < world):
+        raise ValueError("bad world/rank")
+    offs = [0]
+    for n, m in shapes:
+        offs.append(offs[-1] + n * m)
+    total = offs[-1]
+
+    def snap(b: int) -> int:
+        # element offset b -> the nearest row start (global flat offset)
+        if b <= 0:
+            return 0
+        if b >= total:
+            return total
+        lo, hi = 0, len(shapes) - 1
+        while lo < hi:                     # matrix holding element b
+            mid = (lo + hi + 1) // 2
+            if offs[mid] <= b:
+                lo = mid
+            else:
+                hi = mid - 1
+        n, m = shapes[lo]
+        i, o = divmod(b - offs[lo], m)
+        return offs[lo] + (i + (1 if 2 * o >= m else 0)) * m
+
+    a = snap(rank * total // world)
+    b = snap((rank + 1) * total // world)
+    out = []
+    for (n, m), o in zip(shapes, offs):
+        r0 = min(n, max(0, -(-(a - o) // m)))
+        r1 = min(n, max(0, -(-(b - o) // m)))
+        out.append((r0, r1))
+    return out
+
+
+def segment_map(shapes, spans, idx_per_matrix):
+    """P:583 segment mapping table for one rank: list of (matrix, segment_id, offset, stride,
+    count) -- the selected channel idx[segment_id] of `matrix` occupies `count` elements at
+    `offset`, `offset + stride`, ... of the rank's flattened (row-major) storage."""
+    out, base = [], 0
+    for li, ((n, m), (r0, r1), idx) in enumerate(zip(shapes, spans, idx_per_matrix)):
+        rows = r1 - r0
+        if rows > 0:
+            for sid, c in enumerate(idx):
+                out.append((li, sid, base + int(c), m, rows))
+        base += rows * m
+    return out

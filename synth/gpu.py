@@ -53,16 +53,22 @@ class ColScale:
 
 def fill_grad(out: torch.Tensor, layer: int, step: int, scale: ColScale, row0: int = 0, seed: int = SEED):
     n, m = out.shape
+    if n == 0:
+        return
     _ok(lib.synth_grad(out.data_ptr(), _dt(out), n, m, out.stride(0), row0, layer, step, scale.e.data_ptr(), seed,
                        _s()), "synth_grad")
 
 
 def fill_grad_tie(out: torch.Tensor, layer: int, step: int, row0: int = 0, seed: int = SEED):
     n, m = out.shape
+    if n == 0:
+        return
     _ok(lib.synth_grad_tie(out.data_ptr(), _dt(out), n, m, out.stride(0), row0, layer, step, seed, _s()),
         "synth_grad_tie")
 
 
 def fill_param(out: torch.Tensor, layer: int, row0: int = 0, seed: int = SEED):
     n, m = out.shape
+    if n == 0:
+        return
     _ok(lib.synth_param(out.data_ptr(), _dt(out), n, m, out.stride(0), row0, layer, seed, _s()), "synth_param")

@@ -268,6 +268,14 @@ def test_step_state_offload(zf, orc, gpu, shapes, gdt, NS, tau, cpu):
                   warmup=tau, state_offload=True)
 
 
+@pytest.mark.parametrize("cpu", [False, True])
+def test_step_layers_without_rows(zf, orc, gpu, cpu):
+    """Flat partitions (row f3): matrices with no rows on this rank (n = 0) ride along --
+    zero norms, the same selection rule, nothing else -- while the others stay bit-exact."""
+    shapes = [(0, 512), (37, 1001), (0, 4096), (64, 512), (0, 77)]
+    _run_stateful(zf, orc, gpu, shapes, "bf16", "bf16", 100000, 2, 2, 5, offload=True, cpu_update=cpu)
+
+
 def test_cpu_update_needs_aligned_windows(zf):
     with pytest.raises(zf.ZFError):
         zf.Context([zf.LayerShape(8, 64)], refresh_interval=2, accum_interval=4, offload=True, host_accumulate=True,
