@@ -190,6 +190,16 @@ typedef struct {
                                          stores -- no moment bytes resident in HBM, at
                                          the cost of 16 B per selected element per step on
                                          the host link.  Results are bit-identical.     */
+    int32_t device_accumulate;        /* 1: the window accumulation (row 8) runs on the GPU
+                                         (K7): both fp32 window accumulators [n, m-k] live
+                                         in HBM, each step's compact block is added in
+                                         place, and only the sealed window is copied to
+                                         pinned host memory, once per window (4 B x (m-k)
+                                         x n per S steps on the host link instead of 2 B x
+                                         (m-k) x n per step; no host accumulation
+                                         traffic).  Requires host_accumulate; with offload
+                                         the per-step compact D2H is replaced by the
+                                         per-window one.  Bit-identical sums.           */
 } zf_config;
 
 typedef struct zf_ctx zf_ctx;
@@ -237,6 +247,12 @@ zf_status zf_compact_buffer(zf_ctx* ctx, int32_t layer, const void** dev, int64_
  * window's buffer, 1 the last sealed window's buffer (NULL if none yet). */
 zf_status zf_host_accumulator(zf_ctx* ctx, int32_t layer, int32_t which, const float** host, int64_t* rows,
                               int64_t* cols);
+/* device_accumulate: the device accumulator [n, m-k] fp32 with row pitch *ld elements
+ * of the active window (which = 0: the buffer the last step added into) or of the
+ * last sealed window (which = 1); NULL before any.  With device_accumulate,
+ * zf_host_accumulator(which = 1) is the pinned host copy of the sealed window (valid
+ * after zf_sync, until the next window seals) and which = 0 gives NULL. */
+zf_status zf_device_accumulator(zf_ctx* ctx, int32_t layer, int32_t which, const float** dev, int64_t* ld);
 /* Accumulation-window log, one entry per regular step the host accumulation has
  * processed (call after zf_sync): global step t, whether a window ended there, and
  * (Zen-auto only, else NaN) the decision's inputs: A = the window's accumulated mean

@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(K6_THREADS) k_zen_auto(const AutoLayer* __rest
     r.len = st.len;
     r.end = end;
     st.open = end ? 0 : 1;
+    if (end) st.win += 1;
     *state = st;
     volatile AutoRecord* vr = rec;
     vr->t = r.t;

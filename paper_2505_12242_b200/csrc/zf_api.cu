@@ -457,6 +457,8 @@ struct LayerState {
     void* stage_dev[2] = {nullptr, nullptr};
     void* stage_host[2] = {nullptr, nullptr};
     float* acc[2] = {nullptr, nullptr};
+    float* dacc[2] = {nullptr, nullptr};  // device_accumulate: [n, mk_pad] fp32 window accumulators
+    float* acc_sealed_h = nullptr;        // device_accumulate: pinned dense [n, mk] copy of the sealed window
     // K3 geometry
     K3Geom geo{};
     int64_t unit_begin = 0;
@@ -636,6 +638,12 @@ struct zf_ctx {
     AutoRecord* auto_rec_d = nullptr;
     cudaEvent_t auto_ev[8] = {};
     static constexpr int AUTO_RING = 8;
+    // device-side window accumulation (K7; device_accumulate)
+    bool devacc = false;
+    AccLayer* d_acc_tab = nullptr;
+    int64_t acc_vecs = 0;
+    cudaEvent_t acc_d2h_ev[2] = {nullptr, nullptr};
+    cudaEvent_t k7_done = nullptr;
     // per-phase timing (zf_profile)
     bool profiling = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
@@ -731,6 +739,9 @@ zf_ctx::~zf_ctx() {
         if (e) cudaEventDestroy(e);
     for (auto e : auto_ev)
         if (e) cudaEventDestroy(e);
+    for (auto e : acc_d2h_ev)
+        if (e) cudaEventDestroy(e);
+    if (k7_done) cudaEventDestroy(k7_done);
     for (auto& e : ev_pool) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
     for (auto& e : pending) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     if (step_done) cudaEventDestroy(step_done);
@@ -1041,6 +1052,8 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
     if (!(cfg->auto_gamma >= 0.0f) || !std::isfinite(cfg->auto_gamma))
         return fail(ZF_EINVAL, "auto_gamma must be finite and >= 0");
     if (cfg->auto_gamma > 0.0f && !cfg->host_accumulate) return fail(ZF_EINVAL, "auto_gamma requires host_accumulate");
+    if (cfg->device_accumulate && !cfg->host_accumulate)
+        return fail(ZF_EINVAL, "device_accumulate requires host_accumulate (it moves that accumulation onto the GPU)");
     ZF_TRY(check_hp(&cfg->adam));
     if (world < 1 || rank < 0 || rank >= world) return fail(ZF_EINVAL, "bad world/rank");
     if (world > 1 && !nccl_id128) return fail(ZF_EINVAL, "nccl_id128 required when world > 1");
@@ -1071,7 +1084,8 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
     c->pdt = cfg->param_dtype;
     c->gsz = esize(cfg->grad_dtype);
     c->psz = esize(cfg->param_dtype);
-    c->n_stage = cfg->offload ? 2 : 1;
+    c->devacc = cfg->device_accumulate != 0;
+    c->n_stage = cfg->offload && !c->devacc ? 2 : 1;
     c->lr_cur = cfg->adam.lr;
     c->tau = cfg->warmup_steps;
     c->grid = update_grid(c->gdt, c->pdt);
@@ -1211,7 +1225,7 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
         ZF_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
         for (int s = 0; s < 2; ++s) ZF_CUDA(cudaEventCreateWithFlags(&c->d2h_all[s], cudaEventDisableTiming));
         for (auto& l : c->L) {
-            for (int s = 0; s < 2; ++s) {
+            for (int s = 0; s < (c->devacc ? 0 : 2); ++s) {  // per-step compact D2H (not with K7)
                 void* h = nullptr;
                 ZF_CUDA(cudaHostAlloc(&h, std::max<size_t>((size_t)l.d.n * l.mk_pad * c->gsz, 64), cudaHostAllocDefault));
                 c->host_pinned.push_back(h);
@@ -1224,7 +1238,28 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
         if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
             c->wait_value = reinterpret_cast<PFN_waitValue32>(fn);
-        if (cfg->host_accumulate) {
+        if (cfg->host_accumulate && c->devacc) {
+            // K7 accumulates on the device; one pinned dense copy of the sealed window per layer
+            std::vector<AccLayer> h(c->L.size());
+            for (size_t i = 0; i < c->L.size(); ++i) {
+                LayerState& l = c->L[i];
+                const size_t e = (size_t)l.d.n * l.mk_pad;
+                for (int s = 0; s < 2; ++s) ZF_CTRY(c->dalloc(&l.dacc[s], e * sizeof(float), false));
+                ZF_CUDA(cudaHostAlloc(&l.acc_sealed_h, std::max<size_t>((size_t)l.d.n * l.mk * sizeof(float), 64),
+                                      cudaHostAllocDefault));
+                c->host_pinned.push_back(l.acc_sealed_h);
+                h[i].src = l.stage_dev[0];
+                h[i].acc0 = l.dacc[0];
+                h[i].acc1 = l.dacc[1];
+                h[i].vec_begin = c->acc_vecs;
+                c->acc_vecs += (int64_t)(e / 8);
+            }
+            ZF_CTRY(c->dalloc(&c->d_acc_tab, h.size() * sizeof(AccLayer)));
+            ZF_CUDA(cudaMemcpy(c->d_acc_tab, h.data(), h.size() * sizeof(AccLayer), cudaMemcpyHostToDevice));
+            for (auto& e : c->acc_d2h_ev) ZF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            ZF_CUDA(cudaEventCreateWithFlags(&c->k7_done, cudaEventDisableTiming));
+        }
+        if (cfg->host_accumulate && !c->devacc) {
             for (auto& l : c->L) {
                 for (int s = 0; s < 2; ++s) {
                     const size_t bytes = std::max<size_t>((size_t)l.d.n * l.mk * sizeof(float), 64);
@@ -1235,7 +1270,9 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
                     l.acc[s] = p;
                 }
             }
-            if (cfg->cpu_update) {
+        }
+        if (cfg->host_accumulate && cfg->cpu_update) {
+            {
                 for (auto& l : c->L) {
                     const size_t nm = (size_t)l.d.n * l.d.m;
                     for (float** pp : {&l.master, &l.mh, &l.vh}) {
@@ -1255,10 +1292,12 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
                     ZF_CTRY(c->dalloc(&l.unsel_dev, (l.mk + 16) * sizeof(int32_t)));
                 }
             }
+        }
+        if (cfg->host_accumulate) {
             int nt = cfg->host_threads > 0 ? cfg->host_threads
                                            : (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
             c->pool = new Pool(nt);
-            c->h1 = std::thread([c] { c->h1_loop(); });
+            if (!c->devacc) c->h1 = std::thread([c] { c->h1_loop(); });
         }
     }
     // ---- NCCL (collective across ranks)
@@ -1383,7 +1422,9 @@ zf_status f1_refresh(zf_ctx* c, void* const* params, cudaStream_t s) {
 // the window's average gradient acc/S on the fp32 master of the unselected columns; the
 // rounded results are uploaded and scattered into the parameters.
 zf_status f1_window_end(zf_ctx* c, int64_t t, int buf, int64_t len, void* const* params, cudaStream_t s) {
-    {
+    if (c->devacc) {
+        ZF_CUDA(cudaEventSynchronize(c->acc_d2h_ev[buf]));  // the sealed window's host copy
+    } else {
         std::unique_lock<std::mutex> lk(c->mu);
         c->cv.wait(lk, [&] { return c->h1_done >= t; });
     }
@@ -1398,7 +1439,7 @@ zf_status f1_window_end(zf_ctx* c, int64_t t, int buf, int64_t len, void* const*
         LayerState& l = c->L[i];
         const int64_t m = l.d.m, n = l.d.n, mk = l.mk;
         if (mk == 0) continue;
-        const float* acc = l.acc[buf];
+        const float* acc = c->devacc ? l.acc_sealed_h : l.acc[buf];
         std::vector<float> ss(mk), bc2s(mk);
         for (int64_t u = 0; u < mk; ++u) {
             const double tt = (double)(l.th[l.unsel_host[u]] + 1);
@@ -1513,7 +1554,7 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
         // (K3 counts per-layer completions only when offloading; see build_tables)
         // the device staging buffer sb is free once the D2H copies issued two steps ago finished
         if (c->d2h_issued[sb]) ZF_CUDA(cudaStreamWaitEvent(s, c->d2h_all[sb], 0));
-        if (c->cfg.host_accumulate) {
+        if (c->cfg.host_accumulate && !c->devacc) {
             // host staging buffer sb is free once H1 consumed step t-2
             std::unique_lock<std::mutex> lk(c->mu);
             c->cv.wait(lk, [&] { return c->h1_done >= t - 2 || c->last_t < t - 2; });
@@ -1576,6 +1617,16 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
         c->cur ^= 1;
         c->have_sel = true;
     }
+    if (c->devacc) {
+        // K7: add this step's compact block into the window's device accumulator (before K6,
+        // which decides whether this step ends the window); a window's first step overwrites
+        // the buffer, so it waits for that buffer's last D2H (two windows ago)
+        const int b = (int)(c->mw % 2);
+        if (c->mw_len == 0) ZF_CUDA(cudaStreamWaitEvent(s, c->acc_d2h_ev[b], 0));
+        ZF_CUDA(launch_accumulate(c->d_acc_tab, nl, c->acc_vecs, c->gdt, c->mw_len == 0 ? 1 : 0, b,
+                                  c->autoz ? c->auto_state : nullptr, s));
+        c->launches++;
+    }
     if (c->autoz) {
         // K6: the step's Zen-auto decision from its norms and the (new) current selection
         const int slot = (int)(t % zf_ctx::AUTO_RING);
@@ -1589,7 +1640,7 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
     c->last_step = t0;
     ZF_CUDA(cudaEventRecord(c->step_done, s));
 
-    if (c->cfg.offload) {
+    if (c->cfg.offload && !c->devacc) {
         // X1: per-layer D2H as soon as the layer's last unit finished (cyclic counter)
         if (!c->wait_value) ZF_CUDA(cudaStreamWaitEvent(c->copy_stream, c->step_done, 0));
         for (int i = 0; i < nl; ++i) {
@@ -1625,14 +1676,41 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
         // CPU update of an ended window (synchronous, reading R18)
         c->mw_len += 1;
         bool end = (t + 1) % c->cfg.accum_interval == 0;
-        if (c->autoz && c->cfg.cpu_update) {
+        double rA = NAN, ri = NAN, ru = NAN;
+        if (c->autoz && (c->cfg.cpu_update || c->devacc)) {
             const int slot = (int)(t % zf_ctx::AUTO_RING);
             ZF_CUDA(cudaEventSynchronize(c->auto_ev[slot]));
-            end = static_cast<const volatile AutoRecord*>(c->auto_rec_h + slot)->end != 0;
+            const volatile AutoRecord* r = c->auto_rec_h + slot;
+            end = r->end != 0;
+            rA = r->A;
+            ri = r->imp;
+            ru = r->unimp;
         } else if (c->autoz) {
             end = false;  // not needed on this thread without f1 (H1 tracks the windows)
         }
-        if (c->cfg.cpu_update && end) ZF_TRY(f1_window_end(c, t, (int)(c->mw % 2), c->mw_len, params, s));
+        const int b = (int)(c->mw % 2);
+        if (c->devacc) {
+            // this thread plays H1's bookkeeping role; a sealed window goes to the host once
+            if (end) {
+                ZF_CUDA(cudaEventRecord(c->k7_done, s));
+                ZF_CUDA(cudaStreamWaitEvent(c->copy_stream, c->k7_done, 0));
+                for (auto& l : c->L)
+                    if (l.mk && l.d.n)
+                        ZF_CUDA(cudaMemcpy2DAsync(l.acc_sealed_h, l.mk * sizeof(float), l.dacc[b],
+                                                  l.mk_pad * sizeof(float), l.mk * sizeof(float), l.d.n,
+                                                  cudaMemcpyDeviceToHost, c->copy_stream));
+                ZF_CUDA(cudaEventRecord(c->acc_d2h_ev[b], c->copy_stream));
+            }
+            std::lock_guard<std::mutex> lk(c->mu);
+            c->h1_last_buf = b;
+            if (end) c->h1_sealed_buf = b;
+            c->log_t.push_back(t0);
+            c->log_end.push_back(end ? 1 : 0);
+            c->log_A.push_back(rA);
+            c->log_i.push_back(ri);
+            c->log_u.push_back(ru);
+        }
+        if (c->cfg.cpu_update && end) ZF_TRY(f1_window_end(c, t, b, c->mw_len, params, s));
         if (end) {
             c->mw += 1;
             c->mw_len = 0;
@@ -1705,7 +1783,7 @@ extern "C" zf_status zf_compact_buffer(zf_ctx* c, int32_t layer, const void** de
     const int sb = (int)(c->last_t % c->n_stage);
     if (dev) *dev = c->L[layer].stage_dev[sb];
     if (dev_ld) *dev_ld = c->L[layer].mk_pad;
-    if (host) *host = c->cfg.offload ? c->L[layer].stage_host[sb] : nullptr;
+    if (host) *host = c->cfg.offload && !c->devacc ? c->L[layer].stage_host[sb] : nullptr;
     return ZF_OK;
 }
 
@@ -1719,11 +1797,27 @@ extern "C" zf_status zf_host_accumulator(zf_ctx* c, int32_t layer, int32_t which
         // windows as the host accumulation processed them (fixed S or Zen-auto)
         std::lock_guard<std::mutex> lk(c->mu);
         const int b = which == 0 ? c->h1_last_buf : c->h1_sealed_buf;
-        if (b >= 0) p = l.acc[b];
+        if (c->devacc) {
+            if (which == 1 && b >= 0) p = l.acc_sealed_h;  // the active window lives on the device
+        } else if (b >= 0) {
+            p = l.acc[b];
+        }
     }
     if (host) *host = p;
     if (rows) *rows = l.d.n;
     if (cols) *cols = l.mk;
+    return ZF_OK;
+}
+
+extern "C" zf_status zf_device_accumulator(zf_ctx* c, int32_t layer, int32_t which, const float** dev,
+                                           int64_t* ld) {
+    if (!c || layer < 0 || layer >= (int)c->L.size()) return fail(ZF_EINVAL, "bad ctx/layer");
+    if (!c->devacc) return fail(ZF_ESTATE, "device accumulation is off");
+    const LayerState& l = c->L[layer];
+    std::lock_guard<std::mutex> lk(c->mu);
+    const int b = which == 0 ? c->h1_last_buf : c->h1_sealed_buf;
+    if (dev) *dev = b >= 0 ? l.dacc[b] : nullptr;
+    if (ld) *ld = l.mk_pad;
     return ZF_OK;
 }
 

@@ -20,7 +20,7 @@ ZF_FP32, ZF_BF16 = 0, 1
 
 SYMBOLS = ["zf_status_string", "zf_last_error", "zf_version", "zf_k_for", "zf_column_norms", "zf_topk_columns",
            "zf_selective_adam", "zf_compact_unselected", "zf_nccl_unique_id", "zf_create", "zf_step", "zf_sync",
-           "zf_selected", "zf_norms", "zf_optimizer_state", "zf_compact_buffer", "zf_host_accumulator", "zf_window_log", "zf_set_lr",
+           "zf_selected", "zf_norms", "zf_optimizer_state", "zf_compact_buffer", "zf_host_accumulator", "zf_device_accumulator", "zf_window_log", "zf_set_lr",
            "zf_kernel_launches", "zf_profile", "zf_profile_read", "zf_destroy"]
 
 
@@ -45,7 +45,8 @@ class Config(ctypes.Structure):
                 ("refresh_interval", ctypes.c_int32), ("accum_interval", ctypes.c_int32), ("adam", AdamParams),
                 ("offload", ctypes.c_int32), ("host_accumulate", ctypes.c_int32), ("host_threads", ctypes.c_int32),
                 ("cpu_update", ctypes.c_int32), ("warmup_steps", ctypes.c_int32),
-                ("auto_gamma", ctypes.c_float), ("state_offload", ctypes.c_int32)]
+                ("auto_gamma", ctypes.c_float), ("state_offload", ctypes.c_int32),
+                ("device_accumulate", ctypes.c_int32)]
 
 
 if not os.path.exists(_LIB_PATH):
@@ -85,6 +86,8 @@ _pd = ctypes.POINTER(ctypes.c_double)
 lib.zf_window_log.argtypes = [_vp, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_i32), _pd, _pd, _pd,
                               ctypes.POINTER(_i64)]
 lib.zf_window_log.restype = _st
+lib.zf_device_accumulator.argtypes = [_vp, _i32, _i32, ctypes.POINTER(_vp), ctypes.POINTER(_i64)]
+lib.zf_device_accumulator.restype = _st
 lib.zf_set_lr.argtypes = [_vp, ctypes.c_double]; lib.zf_set_lr.restype = _st
 lib.zf_kernel_launches.argtypes = [_vp]; lib.zf_kernel_launches.restype = _i64
 lib.zf_destroy.argtypes = [_vp]; lib.zf_destroy.restype = _st
@@ -202,7 +205,7 @@ class Context:
                  refresh_interval=4, accum_interval=4, adam: AdamParams | None = None, offload=False,
                  host_accumulate=False, host_threads=0, world=1, rank=0, nccl_id: bytes | None = None,
                  device: int | None = None, cpu_update=False, warmup_steps=0, auto_gamma=0.0,
-                 state_offload=False):
+                 state_offload=False, device_accumulate=False):
         self.layers = [l if isinstance(l, LayerShape) else LayerShape(*l) for l in layers]
         descs = (LayerDesc * len(self.layers))()
         for d, l in zip(descs, self.layers):
@@ -224,6 +227,7 @@ class Context:
         cfg.warmup_steps = int(warmup_steps)
         cfg.auto_gamma = float(auto_gamma)
         cfg.state_offload = int(state_offload)
+        cfg.device_accumulate = int(device_accumulate)
         self.cfg = cfg
         self.device = torch.cuda.current_device() if device is None else device
         h = ctypes.c_void_p()
@@ -316,6 +320,16 @@ class Context:
             return None
         arr = (ctypes.c_float * (r.value * c.value)).from_address(p.value)
         return np.ctypeslib.as_array(arr).reshape(r.value, c.value)
+
+    def device_accumulator(self, layer: int, which: int = 0):
+        """device_accumulate: the fp32 device accumulator [n, m-k] (strided view), or None."""
+        p, ld = ctypes.c_void_p(), ctypes.c_int64()
+        _check(lib.zf_device_accumulator(self._h, layer, which, ctypes.byref(p), ctypes.byref(ld)),
+               "zf_device_accumulator")
+        if not p.value:
+            return None
+        n, mk = self.layers[layer].n, self.layers[layer].m - self.k[layer]
+        return _view(p.value, (n, ld.value), torch.float32)[:, :mk]
 
     def window_log(self):
         """Accumulation-window log after sync(): list of (t, ended, A, imp, unimp) per regular

@@ -165,12 +165,12 @@ def test_compact_bitexact(zf, orc, gpu, n, m, dt, ld, ppm):
 
 # ------------------------------------------------------------------ zf_step vs oracle, multi-step
 def _run_stateful(zf, orc, gpu, shapes, gdt, pdt, ppm, N, S, steps, offload, lr=1e-3, wd=0.0, check_every=1,
-                  tie=False, ld_pad=0, cpu_update=False, warmup=0, state_offload=False):
+                  tie=False, ld_pad=0, cpu_update=False, warmup=0, state_offload=False, devacc=False):
     hp_o = orc.AdamHP(lr=lr, weight_decay=wd)
     ctx = zf.Context([zf.LayerShape(n, m, m + ld_pad, m + ld_pad) for n, m in shapes], grad_dtype=TDT[gdt],
                      param_dtype=TDT[pdt], topk_ratio_ppm=ppm, refresh_interval=N, accum_interval=S,
                      adam=zf.adam_params(lr=lr, weight_decay=wd), offload=offload, host_accumulate=offload, cpu_update=cpu_update,
-                     warmup_steps=warmup, state_offload=state_offload)
+                     warmup_steps=warmup, state_offload=state_offload, device_accumulate=devacc)
     scales = [gpu.ColScale(m, li) for li, (n, m) in enumerate(shapes)]
     Gs = [torch.empty(n, m + ld_pad, dtype=TDT[gdt], device="cuda")[:, :m] for n, m in shapes]
     Ps = [torch.empty(n, m + ld_pad, dtype=TDT[pdt], device="cuda")[:, :m] for n, m in shapes]
@@ -212,9 +212,14 @@ def _run_stateful(zf, orc, gpu, shapes, gdt, pdt, ppm, N, S, steps, offload, lr=
                 assert out.shape == (n, 0)
                 continue
             assert_bits_equal(to_np(ctx.compact_buffer(li)), out, f"compact t={t} l={li}")
-            if offload:
+            if offload and devacc:
+                assert ctx.compact_host(li) is None and ctx.host_accumulator(li, 0) is None
+                assert_bits_equal(to_np(ctx.device_accumulator(li, 0)), L.acc[((t - warmup) // S) % 2],
+                                  f"device acc t={t} l={li}")
+            elif offload:
                 assert_bits_equal(ctx.compact_host(li).copy(), out, f"compact host t={t} l={li}")
                 assert_bits_equal(ctx.host_accumulator(li, 0).copy(), L.acc[((t - warmup) // S) % 2], f"acc t={t} l={li}")
+            if offload:
                 sealed = ctx.host_accumulator(li, 1)
                 osealed = L.sealed(t)
                 assert (sealed is None) == (osealed is None)
@@ -274,6 +279,17 @@ def test_step_layers_without_rows(zf, orc, gpu, cpu):
     zero norms, the same selection rule, nothing else -- while the others stay bit-exact."""
     shapes = [(0, 512), (37, 1001), (0, 4096), (64, 512), (0, 77)]
     _run_stateful(zf, orc, gpu, shapes, "bf16", "bf16", 100000, 2, 2, 5, offload=True, cpu_update=cpu)
+
+
+@pytest.mark.parametrize("shapes,gdt,NS,tau,cpu", [([(256, 512)], "fp32", 2, 0, False),
+                                                  ([(64, 512), (37, 1001), (0, 96), (16, 4096)], "bf16", 2, 1, True),
+                                                  ([(513, 768), (64, 4096)], "bf16", 4, 0, True),
+                                                  ([(130, 257), (5, 20000)], "fp32", 1, 0, False)])
+def test_step_device_accumulate(zf, orc, gpu, shapes, gdt, NS, tau, cpu):
+    """K7 (device_accumulate): the window accumulators live in HBM and only sealed windows go
+    to the host; device active accumulator, host sealed copy, f1 updates bit-exact."""
+    _run_stateful(zf, orc, gpu, shapes, gdt, gdt, 100000, NS, NS, tau + 7, offload=True, cpu_update=cpu,
+                  warmup=tau, devacc=True)
 
 
 def test_cpu_update_needs_aligned_windows(zf):
@@ -394,7 +410,8 @@ def test_llama2_13b_rank0_shard_offload_sampled(zf, orc, gpu):
 
 
 # ------------------------------------------------------------------ f2: Zen-auto (reading R21)
-def _run_auto(zf, orc, gpu, shapes, gdt, pdt, ppm, N, smax, gamma, steps, cpu_update=False, warmup=0, lr=1e-3):
+def _run_auto(zf, orc, gpu, shapes, gdt, pdt, ppm, N, smax, gamma, steps, cpu_update=False, warmup=0, lr=1e-3,
+              devacc=False):
     """zf_step with auto_gamma against OracleModel: per step the window decision and its
     inputs (A, mean important / unimportant channel norm), and bit for bit the selection,
     moments, parameters (incl. f1 updates with the window's length), compact blocks and
@@ -403,7 +420,7 @@ def _run_auto(zf, orc, gpu, shapes, gdt, pdt, ppm, N, smax, gamma, steps, cpu_up
     ctx = zf.Context([zf.LayerShape(n, m) for n, m in shapes], grad_dtype=TDT[gdt], param_dtype=TDT[pdt],
                      topk_ratio_ppm=ppm, refresh_interval=N, accum_interval=smax, adam=zf.adam_params(lr=lr),
                      offload=True, host_accumulate=True, cpu_update=cpu_update, warmup_steps=warmup,
-                     auto_gamma=gamma)
+                     auto_gamma=gamma, device_accumulate=devacc)
     scales = [gpu.ColScale(m, li) for li, (n, m) in enumerate(shapes)]
     Gs = [torch.empty(n, m, dtype=TDT[gdt], device="cuda") for n, m in shapes]
     Ps = [torch.empty(n, m, dtype=TDT[pdt], device="cuda") for n, m in shapes]
@@ -449,7 +466,8 @@ def _run_auto(zf, orc, gpu, shapes, gdt, pdt, ppm, N, smax, gamma, steps, cpu_up
         for got, want, what in ((lA, oA, "A"), (li_, oi, "imp"), (lu, ou, "unimp")):
             assert abs(got - want) <= 1e-5 * abs(want), (t, what, got, want)
         for li, L in enumerate(model.layers):
-            assert_bits_equal(ctx.host_accumulator(li, 0).copy(), L.acc[w_before % 2], f"acc t={t} l={li}")
+            got = to_np(ctx.device_accumulator(li, 0)) if devacc else ctx.host_accumulator(li, 0).copy()
+            assert_bits_equal(got, L.acc[w_before % 2], f"acc t={t} l={li}")
         if lend:
             sealed_buf = w_before % 2
         for li, L in enumerate(model.layers):
@@ -466,13 +484,14 @@ def _run_auto(zf, orc, gpu, shapes, gdt, pdt, ppm, N, smax, gamma, steps, cpu_up
 AUTO_SHAPES = [(64, 256), (96, 200), (128, 320)]
 
 
-@pytest.mark.parametrize("gamma,cpu,pdt", [(0.15, False, "bf16"), (0.15, True, "bf16"), (0.25, True, "fp32"),
-                                           (0.1, False, "fp32")])
-def test_step_zen_auto(zf, orc, gpu, gamma, cpu, pdt):
+@pytest.mark.parametrize("gamma,cpu,pdt,devacc", [(0.15, False, "bf16", False), (0.15, True, "bf16", False),
+                                                  (0.25, True, "fp32", False), (0.1, False, "fp32", False),
+                                                  (0.15, False, "bf16", True), (0.25, True, "bf16", True)])
+def test_step_zen_auto(zf, orc, gpu, gamma, cpu, pdt, devacc):
     """Zen-auto (f2, reading R21) on column-concentrated synthetic gradients: intervals vary
     (not all equal to S_max), windows cut at the refresh every 8 steps."""
     gdt = "bf16" if pdt == "bf16" else "fp32"
-    iv = _run_auto(zf, orc, gpu, AUTO_SHAPES, gdt, pdt, 100000, 8, 8, gamma, 16, cpu_update=cpu)
+    iv = _run_auto(zf, orc, gpu, AUTO_SHAPES, gdt, pdt, 100000, 8, 8, gamma, 16, cpu_update=cpu, devacc=devacc)
     assert sum(iv) == 16 and min(iv) < 8, iv
 
 
