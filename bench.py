@@ -55,6 +55,9 @@ def parse():
                     help="also time Zen-auto (f2) with this gamma (K1 every step + K6 decision; offload + H1)")
     ap.add_argument("--partition", default="rows", choices=["rows", "flat"],
                     help="N>1 data layout: every matrix split by rows (R13), or a row-snapped flat ZeRO partition (f3)")
+    ap.add_argument("--shard-of", type=int, default=1, metavar="P",
+                    help="time rank 0's row shard of a P-GPU data-parallel run on this one GPU (no all-reduce): "
+                         "per-rank evidence for the multi-GPU configs on a one-GPU box")
     ap.add_argument("--json-out", default=None)
     return ap.parse_args()
 
@@ -204,10 +207,11 @@ def run_zenflow(args, rank, world):
     names = synth.MODELS[args.model]()
     full_shapes = [(n, m) for _, n, m in names]
 
+    sim = args.shard_of if (args.shard_of > 1 and world == 1) else 1
     if args.partition == "flat":
-        spans = flat_partition(full_shapes, world, rank)
+        spans = flat_partition(full_shapes, max(world, sim), rank)
     else:
-        spans = [shard_rows(n, world, rank) for n, _ in full_shapes]
+        spans = [shard_rows(n, max(world, sim), rank) for n, _ in full_shapes]
     shapes = [(b - a, m) for (a, b), (_, m) in zip(spans, full_shapes)]
     row0s = [a for a, _ in spans]
     ks = [zf.k_for(m, args.ratio_ppm) for _, m in shapes]
@@ -302,7 +306,9 @@ def run_zenflow(args, rank, world):
         "data": "synthetic (seeded column-concentrated bf16 gradients, bf16 params, fp32 AdamW state)",
         "config": {"workload": f"{args.model}-all-linear-k{args.ratio_ppm // 10000}pct", "model": args.model,
                    "linears": nl, "elements": sum(n * m for n, m in full_shapes), "ratio_ppm": args.ratio_ppm,
-                   "refresh_interval": args.refresh, "parallelism": f"dp{world} ({'flat ZeRO partition' if args.partition == 'flat' else 'row shards'}, norm all-reduce)",
+                   "refresh_interval": args.refresh, "parallelism": (f"dp{world} ({'flat ZeRO partition' if args.partition == 'flat' else 'row shards'}, norm all-reduce)"
+                                   if sim == 1 else f"rank 0 of dp{sim} ({args.partition}) timed alone on 1 GPU, "
+                                   "no all-reduce"),
                    "l2": "inputs larger than L2 (working set > 100 GB vs 126 MB L2); no flush needed",
                    "lr": args.lr},
         "phases_ms_per_launch": {"k3_update": k3_avg, "k1_norms": k1_ms / max(1, n_k1),
