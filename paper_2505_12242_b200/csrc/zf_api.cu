@@ -230,18 +230,47 @@ K3Geom k3_geom(int64_t n, int64_t m, int64_t k, int gsz, int psz, bool p_dense, 
     K3Geom g{};
     // moments staged unless even one row's old moments cannot fit next to a minimal tile
     g.mv_ok = adam && k3_unit_bytes(1, std::min<int64_t>(m, 128), k, gsz, psz, p_dense, true) <= A;
-    g.R = 1;
-    if (k3_unit_bytes(1, m, k, gsz, psz, p_dense, g.mv_ok) <= A) {
-        g.seg_cols = m;
-        g.nseg = 1;
-        int64_t R = 1;
-        while (R < std::min<int64_t>(n, 127) && k3_unit_bytes(R + 1, m, k, gsz, psz, p_dense, g.mv_ok) <= A) ++R;
-        g.R = (int32_t)R;
-    } else {
-        int64_t c = 128;  // segments start 16-byte aligned in the mask/prefix words
-        while (c + 128 < m && k3_unit_bytes(1, c + 128, k, gsz, psz, p_dense, g.mv_ok) <= A) c += 128;
-        g.seg_cols = c;
-        g.nseg = (int32_t)((m + c - 1) / c);
+    // Units are R rows x c columns (c = m, or a multiple of 128 so segments start 16-byte
+    // aligned in the mask/prefix words): the shape with the fewest units per matrix (the most
+    // bytes per stage), ties to full rows / wider segments.  ZF_K3_GEOM=rows keeps the older
+    // rule (full rows when one fits, else single-row segments).
+    // Measured (tools/k3_geom_ab.sh): the search wins with a staged p tile (Llama-2-13B K3
+    // 23.90 -> 22.76 ms: m = 5120 rows go from 1-row units to 3 rows x 2688 columns) but
+    // loses without one (k = 1%: 6.92 -> 7.27 ms, more exposed p loads per unit), so
+    // unstaged-p layers keep the row rule.
+    static const bool rows_env = getenv("ZF_K3_GEOM") && std::string(getenv("ZF_K3_GEOM")) == "rows";
+    const bool rows_only = rows_env || !p_dense;
+    auto rmax = [&](int64_t c) {
+        int64_t R = 0;
+        while (R < std::min<int64_t>(n, 127) && k3_unit_bytes(R + 1, c, k, gsz, psz, p_dense, g.mv_ok) <= A) ++R;
+        return R;
+    };
+    int64_t best_units = -1;
+    std::vector<int64_t> cands;
+    cands.push_back(m);
+    for (int64_t c = ((m - 1) / 128) * 128; c >= 128; c -= 128) cands.push_back(c);
+    for (int64_t c : cands) {
+        const int64_t R = rmax(c);
+        if (R < 1) continue;
+        const int64_t nseg = (m + c - 1) / c;
+        if (rows_only && best_units >= 0) break;
+        if (rows_only && nseg > 1) {  // older rule: widest single-row segment
+            const int64_t u = n * nseg;
+            g.seg_cols = c; g.nseg = (int32_t)nseg; g.R = 1; best_units = u;
+            break;
+        }
+        const int64_t u = ((n + R - 1) / R) * nseg;
+        if (best_units < 0 || u < best_units) {
+            best_units = u;
+            g.seg_cols = c;
+            g.nseg = (int32_t)nseg;
+            g.R = (int32_t)R;
+        }
+    }
+    if (best_units < 0) {  // nothing fits (tiny arena): single-row minimal segments
+        g.seg_cols = 128;
+        g.nseg = (int32_t)((m + 127) / 128);
+        g.R = 1;
     }
     g.units = ((n + g.R - 1) / g.R) * g.nseg;
     return g;
