@@ -163,6 +163,21 @@ def test_compact_bitexact(zf, orc, gpu, n, m, dt, ld, ppm):
     assert_bits_equal(to_np(out)[: n * (m - k)].reshape(n, m - k), want, "compact")
 
 
+@pytest.mark.parametrize("n,m,dt", [(512, 4096, "bf16"), (33, 1000, "fp32")])
+def test_compact_into_pinned_host(zf, orc, gpu, n, m, dt):
+    """Row 6/7 through the stateless primitive: K3 writes the compact block straight into
+    pinned host memory (zero-copy over the host link, include/zf.h)."""
+    rng = np.random.default_rng(n)
+    G = _grad(gpu, n, m, dt, layer=4)
+    k = orc.k_for(m, 100000)
+    idx_np = np.sort(rng.choice(m, k, replace=False)).astype(np.int32)
+    out = torch.full((n * (m - k),), 3, dtype=TDT[dt]).pin_memory()
+    zf.zf_compact_unselected(G, from_np(idx_np), out)
+    torch.cuda.synchronize()
+    want = orc.compact(np.ascontiguousarray(to_np(G)), idx_np)
+    assert_bits_equal(to_np(out).reshape(n, m - k), want, "compact (pinned host)")
+
+
 # ------------------------------------------------------------------ zf_step vs oracle, multi-step
 def _run_stateful(zf, orc, gpu, shapes, gdt, pdt, ppm, N, S, steps, offload, lr=1e-3, wd=0.0, check_every=1,
                   tie=False, ld_pad=0, cpu_update=False, warmup=0, state_offload=False, devacc=False):
