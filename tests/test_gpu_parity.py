@@ -307,6 +307,35 @@ def test_step_device_accumulate(zf, orc, gpu, shapes, gdt, NS, tau, cpu):
                   warmup=tau, devacc=True)
 
 
+@pytest.mark.parametrize("ppm", [1000000, 1])
+def test_step_degenerate_k(zf, orc, gpu, ppm):
+    """k = m (every column important: plain AdamW, empty compact block) and k = 1."""
+    shapes = [(64, 512), (37, 1001)]
+    _run_stateful(zf, orc, gpu, shapes, "bf16", "bf16", ppm, 2, 2, 4, offload=True, cpu_update=True)
+    _run_stateful(zf, orc, gpu, shapes, "fp32", "fp32", ppm, 2, 2, 3, offload=True, devacc=True)
+
+
+def test_zen_auto_gpu_spec_worked_example(zf):
+    """SPEC S:434 on the GPU, against the closed form (not the oracle): a constant stream whose
+    unimportant per-channel norm is 0.25 x the important one triggers the window end at the
+    4th step with gamma = 1 (windows of 4 steps; refresh every 16)."""
+    n, m = 64, 256
+    k = zf.k_for(m, 100000)
+    G = torch.full((n, m), 0.25, dtype=torch.bfloat16, device="cuda")
+    G[:, :k] = 1.0
+    P = torch.zeros(n, m, dtype=torch.bfloat16, device="cuda")
+    ctx = zf.Context([zf.LayerShape(n, m)], topk_ratio_ppm=100000, refresh_interval=16, accum_interval=16,
+                     offload=True, host_accumulate=True, auto_gamma=1.0)
+    for t in range(16):
+        ctx.step(t, [G], [P])
+    ctx.sync()
+    log = ctx.window_log()
+    ctx.close()
+    assert [t for (t, e, *_r) in log if e] == [3, 7, 11, 15]
+    for t, e, A, i, u in log:
+        assert abs(u / i - 0.25) < 1e-6 and abs(A - ((t % 4) + 1) * u) <= 1e-9 * A
+
+
 def test_cpu_update_needs_aligned_windows(zf):
     with pytest.raises(zf.ZFError):
         zf.Context([zf.LayerShape(8, 64)], refresh_interval=2, accum_interval=4, offload=True, host_accumulate=True,
