@@ -367,7 +367,7 @@ def run_zenflow(args, rank, world):
         ctx.close()
         del ctx
         ends = [t for (t, e, *_r) in log if e]
-        dev_ms = sum(v[0] for v in profa.values()) / args.steps
+        dev_ms = sum(profa[p][0] for p in ("k1_norms", "k2_topk", "k3_update", "k7_accumulate")) / args.steps
         result["zen_auto"] = {"gamma": args.also_auto, "kernel_ms_per_step": dev_ms,
                               "wall_ms_per_step": msa / args.steps,
                               "k1_launches": profa["k1_norms"][1], "gpu_launches": la,
@@ -386,7 +386,29 @@ def run_zenflow(args, rank, world):
         host_g.copy_(_g0)
         h2d = host_g.numel() * 2
         gpp = (ctypes.c_void_p * nl)(*[g.data_ptr() for g in G0])
+        d2h_host = sum(n * (m - k) * 2 for (n, m), k in zip(shapes, ks))
+        d2h_dev = sum(n * (m - k) * 4 for (n, m), k in zip(shapes, ks)) / args.refresh  # one fp32 window per S
         K = args.e2e_steps
+
+        # host-link peaks on this box: 1 GiB pinned <-> device copies, CUDA events
+        def link_peak(d2h):
+            nb = 1 << 30
+            hb = torch.empty(nb, dtype=torch.uint8, pin_memory=True)
+            db = torch.empty(nb, dtype=torch.uint8, device="cuda")
+            for _ in range(2):
+                (hb.copy_(db, non_blocking=True) if d2h else db.copy_(hb, non_blocking=True))
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(4):
+                (hb.copy_(db, non_blocking=True) if d2h else db.copy_(hb, non_blocking=True))
+            e1.record()
+            torch.cuda.synchronize()
+            del hb, db
+            return 4 * nb / (e0.elapsed_time(e1) * 1e-3) / 1e9
+
+        link = {"d2h_peak_GBs": link_peak(True), "h2d_peak_GBs": link_peak(False),
+                "peak_source": "measured in this run: 1 GiB pinned <-> device cudaMemcpyAsync, CUDA events"}
 
         def e2e_run(devacc):
             ctx = make_ctx(args.ratio_ppm, True, device_accumulate=devacc)
@@ -394,6 +416,8 @@ def run_zenflow(args, rank, world):
                 _g0.copy_(host_g, non_blocking=True)
                 ctx.step_ptrs(t, gpp, pp, stream)
             ctx.sync()
+            ctx.profile_read()
+            ctx.profile(True)
             if world > 1:
                 dist.barrier()
             t0 = time.perf_counter()
@@ -402,6 +426,18 @@ def run_zenflow(args, rank, world):
                 ctx.step_ptrs(t, gpp, pp, stream)
             ctx.sync()
             e2e_s = time.perf_counter() - t0
+            prof_e = ctx.profile_read()
+            ctx.profile(False)
+            if devacc:
+                ms_w, n_w = prof_e["d2h_window"]
+                wbytes = sum(n * (m - k) * 4 for (n, m), k in zip(shapes, ks))
+                link["window_d2h_GBs"] = wbytes / (ms_w / n_w * 1e-3) / 1e9 if n_w else None
+                link["window_d2h_ms"] = ms_w / n_w if n_w else None
+                link["k7_ms"] = prof_e["k7_accumulate"][0] / max(1, prof_e["k7_accumulate"][1])
+            else:
+                ms_s, n_s = prof_e["d2h_step"]
+                link["x1_d2h_GBs"] = d2h_host / (ms_s / n_s * 1e-3) / 1e9 if n_s else None
+                link["x1_d2h_ms_per_step"] = ms_s / n_s if n_s else None
             e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
             if world > 1:
                 dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
@@ -410,10 +446,12 @@ def run_zenflow(args, rank, world):
             torch.cuda.empty_cache()
             return e2e_t.item() * 1e3 / K
 
-        d2h_host = sum(n * (m - k) * 2 for (n, m), k in zip(shapes, ks))
-        d2h_dev = sum(n * (m - k) * 4 for (n, m), k in zip(shapes, ks)) / args.refresh  # one fp32 window per S
         ms_dev = e2e_run(True)
         ms_host = e2e_run(False)
+        for key in ("x1_d2h_GBs", "window_d2h_GBs"):
+            if link.get(key):
+                link[key.replace("_GBs", "_frac")] = link[key] / link["d2h_peak_GBs"]
+        result["host_link"] = link
         result["e2e"] = {"value": ms_dev, "unit": UNIT, "h2d_bytes_per_step": h2d,
                          "d2h_bytes_per_step": int(d2h_dev), "steps": K,
                          "path": "pinned host G -> H2D -> zf_step (offload, device_accumulate: K7 fp32 window "

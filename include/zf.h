@@ -263,11 +263,14 @@ zf_status zf_window_log(zf_ctx* ctx, int64_t cap, int64_t* t, int32_t* end, doub
                         int64_t* count);
 /* Change the learning rate used from the next zf_step on (schedules). */
 zf_status zf_set_lr(zf_ctx* ctx, double lr);
-/* Per-phase device timing: when enabled, zf_step records CUDA events on its
- * launch stream around each phase (0: K1 column norms, 1: NCCL norm all-reduce,
- * 2: K2 top-k, 3: K3 fused selective AdamW + compaction).  zf_profile_read waits
- * for the recorded events, writes the summed milliseconds ms[4] and occurrence
- * counts count[4] [host] since the previous read, and resets them. */
+/* Per-phase device timing: when enabled, zf_step records CUDA events around each
+ * phase on the stream it runs on (0: K1 column norms, 1: NCCL norm all-reduce,
+ * 2: K2 top-k, 3: K3 fused selective AdamW + compaction, 4: a step's per-layer D2H
+ * of the compact blocks on the copy stream -- first copy start to last copy end,
+ * 5: a sealed window's D2H (device_accumulate), 6: K7 device accumulation).
+ * zf_profile_read waits for the recorded events, writes the summed milliseconds
+ * ms[7] and occurrence counts count[7] [host] since the previous read, and resets
+ * them. */
 zf_status zf_profile(zf_ctx* ctx, int32_t enable);
 zf_status zf_profile_read(zf_ctx* ctx, double* ms, int64_t* count);
 /* Number of this library's kernel launches issued so far by the context. */

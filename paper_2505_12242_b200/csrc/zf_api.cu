@@ -678,8 +678,9 @@ struct zf_ctx {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
     struct Pending { int phase; cudaEvent_t a, b; };
     std::vector<Pending> pending;
-    double prof_ms[4] = {0, 0, 0, 0};
-    int64_t prof_n[4] = {0, 0, 0, 0};
+    static constexpr int NPHASE = 7;
+    double prof_ms[NPHASE] = {};
+    int64_t prof_n[NPHASE] = {};
 
     ~zf_ctx();
     zf_status prof_begin(int phase, cudaStream_t s, Pending* p) {
@@ -1652,8 +1653,11 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
         // the buffer, so it waits for that buffer's last D2H (two windows ago)
         const int b = (int)(c->mw % 2);
         if (c->mw_len == 0) ZF_CUDA(cudaStreamWaitEvent(s, c->acc_d2h_ev[b], 0));
+        zf_ctx::Pending pe6;
+        ZF_TRY(c->prof_begin(6, s, &pe6));
         ZF_CUDA(launch_accumulate(c->d_acc_tab, nl, c->acc_vecs, c->gdt, c->mw_len == 0 ? 1 : 0, b,
                                   c->autoz ? c->auto_state : nullptr, s));
+        ZF_TRY(c->prof_end(&pe6, s));
         c->launches++;
     }
     if (c->autoz) {
@@ -1672,6 +1676,8 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
     if (c->cfg.offload && !c->devacc) {
         // X1: per-layer D2H as soon as the layer's last unit finished (cyclic counter)
         if (!c->wait_value) ZF_CUDA(cudaStreamWaitEvent(c->copy_stream, c->step_done, 0));
+        zf_ctx::Pending pe4;
+        bool pe4_open = false;
         for (int i = 0; i < nl; ++i) {
             LayerState& l = c->L[i];
             if (c->wait_value) {
@@ -1685,10 +1691,17 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
                 }
             }
             // one flat copy of the pitched block (H1 reads the rows at the same pitch)
-            if (l.mk && l.d.n) ZF_CUDA(cudaMemcpyAsync(l.stage_host[sb], l.stage_dev[sb], (size_t)l.d.n * l.mk_pad * c->gsz,
-                                              cudaMemcpyDeviceToHost, c->copy_stream));
+            if (l.mk && l.d.n) {
+                if (!pe4_open) {  // phase 4: the step's D2H span, from the first copy's start
+                    ZF_TRY(c->prof_begin(4, c->copy_stream, &pe4));
+                    pe4_open = true;
+                }
+                ZF_CUDA(cudaMemcpyAsync(l.stage_host[sb], l.stage_dev[sb], (size_t)l.d.n * l.mk_pad * c->gsz,
+                                        cudaMemcpyDeviceToHost, c->copy_stream));
+            }
             ZF_CUDA(cudaEventRecord(l.d2h_ev[sb], c->copy_stream));
         }
+        if (pe4_open) ZF_TRY(c->prof_end(&pe4, c->copy_stream));
         ZF_CUDA(cudaEventRecord(c->d2h_all[sb], c->copy_stream));
         c->d2h_issued[sb] = true;
         if (c->cfg.host_accumulate) {
@@ -1723,11 +1736,14 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
             if (end) {
                 ZF_CUDA(cudaEventRecord(c->k7_done, s));
                 ZF_CUDA(cudaStreamWaitEvent(c->copy_stream, c->k7_done, 0));
+                zf_ctx::Pending pe5;
+                ZF_TRY(c->prof_begin(5, c->copy_stream, &pe5));  // phase 5: the sealed window's D2H
                 for (auto& l : c->L)
                     if (l.mk && l.d.n)
                         ZF_CUDA(cudaMemcpy2DAsync(l.acc_sealed_h, l.mk * sizeof(float), l.dacc[b],
                                                   l.mk_pad * sizeof(float), l.mk * sizeof(float), l.d.n,
                                                   cudaMemcpyDeviceToHost, c->copy_stream));
+                ZF_TRY(c->prof_end(&pe5, c->copy_stream));
                 ZF_CUDA(cudaEventRecord(c->acc_d2h_ev[b], c->copy_stream));
             }
             std::lock_guard<std::mutex> lk(c->mu);
@@ -1893,7 +1909,7 @@ extern "C" zf_status zf_profile_read(zf_ctx* c, double* ms, int64_t* count) {
         c->ev_pool.push_back({p.a, p.b});
     }
     c->pending.clear();
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < zf_ctx::NPHASE; ++i) {
         if (ms) ms[i] = c->prof_ms[i];
         if (count) count[i] = c->prof_n[i];
         c->prof_ms[i] = 0;

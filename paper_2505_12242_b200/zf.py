@@ -259,12 +259,12 @@ class Context:
     def profile(self, enable: bool = True):
         _check(lib.zf_profile(self._h, int(enable)), "zf_profile")
 
-    PHASES = ("k1_norms", "allreduce", "k2_topk", "k3_update")
+    PHASES = ("k1_norms", "allreduce", "k2_topk", "k3_update", "d2h_step", "d2h_window", "k7_accumulate")
 
     def profile_read(self):
         """{phase: (summed ms, count)} since the last read (waits for the recorded events)."""
-        ms = (ctypes.c_double * 4)()
-        n = (ctypes.c_int64 * 4)()
+        ms = (ctypes.c_double * len(self.PHASES))()
+        n = (ctypes.c_int64 * len(self.PHASES))()
         _check(lib.zf_profile_read(self._h, ms, n), "zf_profile_read")
         return {p: (ms[i], n[i]) for i, p in enumerate(self.PHASES)}
 
