@@ -208,8 +208,9 @@ typedef struct zf_ctx zf_ctx;
 zf_status zf_nccl_unique_id(void* out128 /* [host] 128 bytes */);
 
 /* Create a context on CUDA device `device`.  layers [host] [n_layers].
- * world/rank: data-parallel group; nccl_id128 [host] is required iff world > 1
- * (collective call: every rank must call zf_create).  Each rank passes the
+ * world/rank: data-parallel group; with world > 1, nccl_id128 [host] makes zf_create
+ * a collective call that joins an NCCL communicator (every rank must call it); NULL
+ * selects the host all-reduce callback (zf_set_host_allreduce).  Each rank passes the
  * row shard it owns (reading R13: rows [r*n/P, (r+1)*n/P) of every matrix). */
 zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, const zf_config* cfg, int32_t world,
                     int32_t rank, const void* nccl_id128, int32_t device, zf_ctx** out);
@@ -261,6 +262,15 @@ zf_status zf_device_accumulator(zf_ctx* ctx, int32_t layer, int32_t which, const
  * [host] arrays that are not NULL; *count = the number of entries so far. */
 zf_status zf_window_log(zf_ctx* ctx, int64_t cap, int64_t* t, int32_t* end, double* A, double* imp, double* unimp,
                         int64_t* count);
+/* Row a2 without NCCL: a context created with world > 1 and nccl_id128 == NULL sums the
+ * ranks' partial norm vectors through this callback instead of ncclAllReduce -- zf_step
+ * copies the flat fp32 norm vector [count] to a pinned host buffer, calls fn(buf, count,
+ * user), which must replace it in place by the element-wise sum over all ranks (and
+ * return 0; nonzero -> ZF_ENCCL), and copies it back.  Stream-synchronous; meant for
+ * host-side process groups (e.g. torch.distributed over gloo) and for running several
+ * ranks on one GPU.  Must be set before the first zf_step of such a context. */
+typedef int32_t (*zf_host_allreduce_fn)(float* buf, int64_t count, void* user);
+zf_status zf_set_host_allreduce(zf_ctx* ctx, zf_host_allreduce_fn fn, void* user);
 /* Change the learning rate used from the next zf_step on (schedules). */
 zf_status zf_set_lr(zf_ctx* ctx, double lr);
 /* Per-phase device timing: when enabled, zf_step records CUDA events around each

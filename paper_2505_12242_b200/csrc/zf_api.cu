@@ -583,6 +583,9 @@ struct zf_ctx {
     zf_config cfg{};
     int world = 1, rank = 0;
     ncclComm_t comm = nullptr;
+    zf_host_allreduce_fn host_allreduce = nullptr;  // world > 1 without NCCL
+    void* host_allreduce_user = nullptr;
+    float* norms_host = nullptr;
     int gdt = 0, pdt = 0, gsz = 2, psz = 2;
     std::vector<LayerState> L;
     int64_t total_m = 0, max_m = 0, k1_units = 0, k3_units = 0;
@@ -1086,7 +1089,8 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
         return fail(ZF_EINVAL, "device_accumulate requires host_accumulate (it moves that accumulation onto the GPU)");
     ZF_TRY(check_hp(&cfg->adam));
     if (world < 1 || rank < 0 || rank >= world) return fail(ZF_EINVAL, "bad world/rank");
-    if (world > 1 && !nccl_id128) return fail(ZF_EINVAL, "nccl_id128 required when world > 1");
+    // world > 1 without an NCCL id: the norm exchange goes through a host all-reduce callback
+    // registered with zf_set_host_allreduce before the first step
     for (int i = 0; i < n_layers; ++i) {
         const zf_layer_desc& d = layers[i];
         if (d.n < 0 || d.m < 1 || d.m > 0x7fffffffLL || d.ld_grad < d.m || d.ld_param < d.m)
@@ -1330,8 +1334,12 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
             if (!c->devacc) c->h1 = std::thread([c] { c->h1_loop(); });
         }
     }
-    // ---- NCCL (collective across ranks)
-    if (world > 1) {
+    // ---- NCCL (collective across ranks), or a pinned host buffer for the host all-reduce
+    if (world > 1 && !nccl_id128) {
+        ZF_CUDA(cudaHostAlloc(&c->norms_host, std::max<size_t>(c->total_m * sizeof(float), 64), cudaHostAllocDefault));
+        c->host_pinned.push_back(c->norms_host);
+    }
+    if (world > 1 && nccl_id128) {
         ncclUniqueId id;
         std::memcpy(&id, nccl_id128, sizeof id);
         ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
@@ -1566,6 +1574,8 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
     } else if (t0 % N != 0) {
         return fail(ZF_ESTATE, "first step must be a refresh step (t %% N == 0)");
     }
+    if (c->world > 1 && !c->comm && !c->host_allreduce)
+        return fail(ZF_ESTATE, "world > 1 needs an NCCL id at zf_create or zf_set_host_allreduce");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     ZF_CUDA(cudaSetDevice(c->device));
     if (t0 < tau) return warmup_step(c, t0, grads, params, s);
@@ -1603,7 +1613,16 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
         c->launches++;
         if (c->world > 1) {
             ZF_TRY(c->prof_begin(1, s, &pe));
-            ZF_NCCL(ncclAllReduce(c->norms, c->norms, (size_t)c->total_m, ncclFloat32, ncclSum, c->comm, s));
+            if (c->comm) {
+                ZF_NCCL(ncclAllReduce(c->norms, c->norms, (size_t)c->total_m, ncclFloat32, ncclSum, c->comm, s));
+            } else {
+                // host all-reduce (e.g. torch.distributed gloo): stream-synchronous round trip
+                ZF_CUDA(cudaMemcpyAsync(c->norms_host, c->norms, c->total_m * sizeof(float), cudaMemcpyDeviceToHost, s));
+                ZF_CUDA(cudaStreamSynchronize(s));
+                if (c->host_allreduce(c->norms_host, c->total_m, c->host_allreduce_user) != 0)
+                    return fail(ZF_ENCCL, "host all-reduce callback failed");
+                ZF_CUDA(cudaMemcpyAsync(c->norms, c->norms_host, c->total_m * sizeof(float), cudaMemcpyHostToDevice, s));
+            }
             ZF_TRY(c->prof_end(&pe, s));
         }
     }
@@ -1880,6 +1899,14 @@ extern "C" zf_status zf_window_log(zf_ctx* c, int64_t cap, int64_t* t, int32_t* 
         if (unimp) unimp[i] = c->log_u[i];
     }
     if (count) *count = n;
+    return ZF_OK;
+}
+
+extern "C" zf_status zf_set_host_allreduce(zf_ctx* c, zf_host_allreduce_fn fn, void* user) {
+    if (!c) return fail(ZF_EINVAL, "ctx is NULL");
+    if (c->world < 2 || c->comm) return fail(ZF_ESTATE, "host all-reduce needs world > 1 created without an NCCL id");
+    c->host_allreduce = fn;
+    c->host_allreduce_user = user;
     return ZF_OK;
 }
 

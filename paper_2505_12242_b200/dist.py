@@ -86,3 +86,15 @@ def segment_map(shapes, spans, idx_per_matrix):
                 out.append((li, sid, base + int(c), m, rows))
         base += rows * m
     return out
+
+
+def gloo_allreduce(group=None):
+    """A ``host_allreduce`` for ``zf.Context`` over a torch.distributed process group (e.g.
+    gloo): sums the flat fp32 norm vector in place across the ranks (row a2 without NCCL)."""
+    import torch
+    import torch.distributed as dist
+
+    def fn(buf):
+        t = torch.from_numpy(buf)          # shares memory with the library's pinned buffer
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return fn

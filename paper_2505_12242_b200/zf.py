@@ -20,7 +20,7 @@ ZF_FP32, ZF_BF16 = 0, 1
 
 SYMBOLS = ["zf_status_string", "zf_last_error", "zf_version", "zf_k_for", "zf_column_norms", "zf_topk_columns",
            "zf_selective_adam", "zf_compact_unselected", "zf_nccl_unique_id", "zf_create", "zf_step", "zf_sync",
-           "zf_selected", "zf_norms", "zf_optimizer_state", "zf_compact_buffer", "zf_host_accumulator", "zf_device_accumulator", "zf_window_log", "zf_set_lr",
+           "zf_selected", "zf_norms", "zf_optimizer_state", "zf_compact_buffer", "zf_host_accumulator", "zf_device_accumulator", "zf_window_log", "zf_set_host_allreduce", "zf_set_lr",
            "zf_kernel_launches", "zf_profile", "zf_profile_read", "zf_destroy"]
 
 
@@ -88,6 +88,9 @@ lib.zf_window_log.argtypes = [_vp, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_i
 lib.zf_window_log.restype = _st
 lib.zf_device_accumulator.argtypes = [_vp, _i32, _i32, ctypes.POINTER(_vp), ctypes.POINTER(_i64)]
 lib.zf_device_accumulator.restype = _st
+HOST_ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.POINTER(ctypes.c_float), ctypes.c_int64, ctypes.c_void_p)
+lib.zf_set_host_allreduce.argtypes = [_vp, HOST_ALLREDUCE_FN, _vp]
+lib.zf_set_host_allreduce.restype = _st
 lib.zf_set_lr.argtypes = [_vp, ctypes.c_double]; lib.zf_set_lr.restype = _st
 lib.zf_kernel_launches.argtypes = [_vp]; lib.zf_kernel_launches.restype = _i64
 lib.zf_destroy.argtypes = [_vp]; lib.zf_destroy.restype = _st
@@ -205,7 +208,7 @@ class Context:
                  refresh_interval=4, accum_interval=4, adam: AdamParams | None = None, offload=False,
                  host_accumulate=False, host_threads=0, world=1, rank=0, nccl_id: bytes | None = None,
                  device: int | None = None, cpu_update=False, warmup_steps=0, auto_gamma=0.0,
-                 state_offload=False, device_accumulate=False):
+                 state_offload=False, device_accumulate=False, host_allreduce=None):
         self.layers = [l if isinstance(l, LayerShape) else LayerShape(*l) for l in layers]
         descs = (LayerDesc * len(self.layers))()
         for d, l in zip(descs, self.layers):
@@ -236,6 +239,19 @@ class Context:
                              ctypes.byref(h)), "zf_create")
         self._h = h
         self.k = [k_for(l.m, topk_ratio_ppm) for l in self.layers]
+        self._ar = None
+        if host_allreduce is not None:
+            # host_allreduce(np.ndarray float32 [count]) sums in place over the ranks (e.g. gloo)
+            import numpy as np
+
+            def _cb(buf, count, user):
+                try:
+                    host_allreduce(np.ctypeslib.as_array(buf, shape=(count,)))
+                    return 0
+                except Exception:  # noqa: BLE001 -- reported as ZF_ENCCL by zf_step
+                    return 1
+            self._ar = HOST_ALLREDUCE_FN(_cb)
+            _check(lib.zf_set_host_allreduce(h, self._ar, None), "zf_set_host_allreduce")
         n = len(self.layers)
         self._gp = (ctypes.c_void_p * n)()
         self._pp = (ctypes.c_void_p * n)()

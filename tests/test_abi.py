@@ -94,7 +94,7 @@ def test_create_validation(zf):
     cfg.offload, cfg.refresh_interval, cfg.accum_interval = 1, 6, 4                  # N % S != 0
     assert L.zf_create(descs, 1, ctypes.byref(cfg), 1, 0, None, 0, ctypes.byref(h)) == zf.ZF_EINVAL
     cfg.refresh_interval = 4
-    assert L.zf_create(descs, 1, ctypes.byref(cfg), 2, 0, None, 0, ctypes.byref(h)) == zf.ZF_EINVAL  # no nccl id
+    assert L.zf_create(descs, 1, ctypes.byref(cfg), 2, 2, None, 0, ctypes.byref(h)) == zf.ZF_EINVAL  # rank >= world
     cfg.auto_gamma = -1.0                                                              # Zen-auto gamma < 0
     assert L.zf_create(descs, 1, ctypes.byref(cfg), 1, 0, None, 0, ctypes.byref(h)) == zf.ZF_EINVAL
     cfg.auto_gamma, cfg.host_accumulate = 1.0, 0                                       # Zen-auto needs H1

@@ -1,0 +1,100 @@
+"""Two data-parallel ranks through the real library on one GPU (row a2 / §8(e)): two
+processes, each with its row shard of every matrix (reading R13), exchange their partial
+column norms through ``zf_set_host_allreduce`` over a gloo process group (NCCL cannot put
+two ranks on one device), select the same columns, and each rank's rows of the parameters,
+moments, compact blocks and host accumulators are bit-exact against the CPU oracle run on
+the FULL matrices (the oracle's rows do not depend on the other rows; downstream of a
+refresh it uses the GPU's selection, protocol O10)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(256, 512), (130, 257), (64, 4096), (5, 2000)]
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, steps, N, cpu_update, partition):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    sys.path.insert(0, os.path.join(root, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import synth
+    from gpu_util import assert_bits_equal, assert_close_rel, selection_ok, to_np
+    from oracle import oracle as orc
+    from paper_2505_12242_b200 import zf
+    from paper_2505_12242_b200.dist import flat_partition, gloo_allreduce, shard_rows
+    from synth import gpu
+
+    torch.cuda.set_device(0)
+    spans = (flat_partition(SHAPES, world, rank) if partition == "flat"
+             else [shard_rows(n, world, rank) for n, _ in SHAPES])
+    local = [(b - a, m) for (a, b), (_, m) in zip(spans, SHAPES)]
+    ctx = zf.Context([zf.LayerShape(n, m) for n, m in local], topk_ratio_ppm=100000, refresh_interval=N,
+                     accum_interval=N, adam=zf.adam_params(lr=1e-3), offload=True, host_accumulate=True,
+                     cpu_update=cpu_update, world=world, rank=rank, host_allreduce=gloo_allreduce())
+    scales = [gpu.ColScale(m, li) for li, (_, m) in enumerate(SHAPES)]
+    Gs = [torch.empty(n, m, dtype=torch.bfloat16, device="cuda") for n, m in local]
+    Ps = [torch.empty(n, m, dtype=torch.bfloat16, device="cuda") for n, m in local]
+    for li, P in enumerate(Ps):
+        gpu.fill_param(P, li, row0=spans[li][0])
+    oracle = [orc.OracleLayer(n=n, m=m, ratio_ppm=100000, refresh_interval=N, accum_interval=N,
+                              hp=orc.AdamHP(lr=1e-3), cpu_update=cpu_update) for n, m in SHAPES]
+    Po = [synth.param(n, m, li) for li, (n, m) in enumerate(SHAPES)]
+    for t in range(steps):
+        for li in range(len(SHAPES)):
+            scales[li].advance_to(t)
+            gpu.fill_grad(Gs[li], li, t, scales[li], row0=spans[li][0])
+        ctx.step(t, Gs, Ps)
+        ctx.sync()
+        refresh = t % N == 0
+        for li, ((n, m), (a, b)) in enumerate(zip(SHAPES, spans)):
+            L = oracle[li]
+            Gfull = synth.grad(n, m, li, t, synth.col_scale_at(m, t, li))
+            gidx = to_np(ctx.selected(li))
+            if refresh:
+                onorms = orc.column_norms(Gfull)
+                assert_close_rel(to_np(ctx.norms(li)), onorms, 1e-5, f"rank {rank} norms t={t} l={li}")
+                selection_ok(gidx, orc.topk(onorms, L.k), onorms)
+            out = L.step(t, Gfull, Po[li], idx_override=gidx if refresh else None)
+            assert_bits_equal(gidx, L.idx, f"rank {rank} idx t={t} l={li}")
+            if b == a:
+                continue
+            M, V, st = ctx.optimizer_state(li)
+            assert_bits_equal(to_np(M), L.M[a:b], f"rank {rank} exp_avg t={t} l={li}")
+            assert_bits_equal(to_np(V), L.V[a:b], f"rank {rank} exp_avg_sq t={t} l={li}")
+            assert_bits_equal(to_np(st), L.steps, f"rank {rank} steps t={t} l={li}")
+            assert_bits_equal(to_np(Ps[li]), Po[li][a:b], f"rank {rank} params t={t} l={li}")
+            assert_bits_equal(ctx.compact_host(li).copy(), out[a:b], f"rank {rank} compact t={t} l={li}")
+            assert_bits_equal(ctx.host_accumulator(li, 0).copy(), L.acc[(t // N) % 2][a:b],
+                              f"rank {rank} acc t={t} l={li}")
+    # every rank made the same selection
+    sel = torch.from_numpy(np.concatenate([to_np(ctx.selected(li)) for li in range(len(SHAPES))]).astype(np.int64))
+    gathered = [torch.empty_like(sel) for _ in range(world)]
+    dist.all_gather(gathered, sel)
+    assert all(torch.equal(g, gathered[0]) for g in gathered)
+    ctx.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cpu_update,partition", [(False, "rows"), (True, "rows"), (False, "flat")])
+def test_two_ranks_one_gpu_host_allreduce(cpu_update, partition):
+    from paper_2505_12242_b200 import _build
+    _build.build()
+    mp.spawn(_worker, args=(2, _free_port(), 5, 2, cpu_update, partition), nprocs=2, join=True)
