@@ -49,7 +49,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not os.path.exists(stamp) or open(stamp).read() != flags:
         force = True
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
-    hdrs = sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(ROOT, "include", "zf.h")]
+    hdrs = sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))) + [os.path.join(ROOT, "include", "zf.h")]
     objs = []
     jobs = []
     for s in srcs:

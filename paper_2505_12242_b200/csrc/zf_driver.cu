@@ -1,877 +1,8 @@
-// zf_api.cu -- the C-ABI of libzf.so (include/zf.h) and the host runtime of the
-// stateful driver: argument validation, the per-layer state in HBM, launch
-// tables, the NCCL norm all-reduce, D2H staging on a copy stream gated per layer,
-// and the host accumulation thread pool.  See DESIGN.md §5-§6.
-#include <cuda.h>
-#include <cuda_runtime.h>
-#include <nccl.h>
-
-#include <algorithm>
-#include <atomic>
-#include <cmath>
-#include <condition_variable>
-#include <cstdarg>
-#include <cstdio>
-#include <cstdlib>
-#include <cstring>
-#include <deque>
-#include <functional>
-#include <tuple>
-#include <map>
-#include <mutex>
-#include <string>
-#include <thread>
-#include <vector>
-
-#include "../../include/zf.h"
-#include "zf_internal.cuh"
-
-using namespace zf;
-
-// ============================================================ errors
-namespace {
-thread_local std::string g_last_error;
-
-zf_status fail(zf_status st, const char* fmt, ...) {
-    char buf[512];
-    va_list ap;
-    va_start(ap, fmt);
-    vsnprintf(buf, sizeof buf, fmt, ap);
-    va_end(ap);
-    g_last_error = buf;
-    return st;
-}
-
-#define ZF_CUDA(call)                                                                                       \
-    do {                                                                                                    \
-        cudaError_t e_ = (call);                                                                            \
-        if (e_ != cudaSuccess) return fail(ZF_ECUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call,             \
-                                            cudaGetErrorString(e_));                                        \
-    } while (0)
-
-#define ZF_NCCL(call)                                                                                       \
-    do {                                                                                                    \
-        ncclResult_t r_ = (call);                                                                           \
-        if (r_ != ncclSuccess) return fail(ZF_ENCCL, "%s:%d %s: %s", __FILE__, __LINE__, #call,             \
-                                            ncclGetErrorString(r_));                                        \
-    } while (0)
-
-#define ZF_TRY(expr)                \
-    do {                            \
-        zf_status s_ = (expr);      \
-        if (s_ != ZF_OK) return s_; \
-    } while (0)
-
-int esize(zf_dtype d) { return d == ZF_BF16 ? 2 : 4; }
-bool dtype_ok(int d) { return d == ZF_FP32 || d == ZF_BF16; }
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
-
-// ============================================================ AdamW constants
-// bias-correction tables computed on the host in double, one rounding to fp32
-// (DESIGN.md §2 O6): ss[t] = f32(lr / (1 - b1^t)), bc2s[t] = f32(sqrt(1 - b2^t)).
-// Both are monotone in t and reach their limits (f32(lr), 1.0f) at a finite t;
-// the tables stop there and the kernel uses the limit beyond.
-constexpr int64_t MAX_TAB = 1 << 24;
-constexpr int64_t SS_CAP = 1 << 16;  // ss table capacity of a context (beta1 <= 0.999)
-
-std::vector<float> make_ss(double lr, double b1) {
-    std::vector<float> t(1, 0.0f);
-    const float lim = (float)lr;
-    for (int64_t i = 1; i < MAX_TAB; ++i) {
-        const float v = (float)(lr / (1.0 - std::pow(b1, (double)i)));
-        if (v == lim) break;
-        t.push_back(v);
-    }
-    return t;
-}
-
-std::vector<float> make_bc2(double b2) {
-    std::vector<float> t(1, 0.0f);
-    for (int64_t i = 1; i < MAX_TAB; ++i) {
-        const float v = (float)std::sqrt(1.0 - std::pow(b2, (double)i));
-        if (v == 1.0f) break;
-        t.push_back(v);
-    }
-    return t;
-}
-
-// {ss[t], bc2s[t]} interleaved over the longer of the two tables, the shorter one's limit
-// filled in beyond its end (one 8-byte load per slot in K3).
-std::vector<float> make_sb(const std::vector<float>& ss, const std::vector<float>& bc2, double lr) {
-    const size_t n = std::max(ss.size(), bc2.size());
-    std::vector<float> t(2 * n);
-    for (size_t i = 0; i < n; ++i) {
-        t[2 * i] = i < ss.size() ? ss[i] : (float)lr;
-        t[2 * i + 1] = i < bc2.size() ? bc2[i] : 1.0f;
-    }
-    return t;
-}
-
-zf_status check_hp(const zf_adam_params* hp) {
-    if (!hp) return fail(ZF_EINVAL, "hp is NULL");
-    if (!(hp->lr >= 0.0f) || !std::isfinite(hp->lr)) return fail(ZF_EINVAL, "lr must be finite and >= 0");
-    if (!(hp->beta1 >= 0.0f && hp->beta1 < 1.0f)) return fail(ZF_EINVAL, "beta1 must be in [0, 1)");
-    if (!(hp->beta2 >= 0.0f && hp->beta2 < 1.0f)) return fail(ZF_EINVAL, "beta2 must be in [0, 1)");
-    if (!(hp->eps > 0.0f) || !std::isfinite(hp->eps)) return fail(ZF_EINVAL, "eps must be > 0");
-    if (!(hp->weight_decay >= 0.0f) || !std::isfinite(hp->weight_decay)) return fail(ZF_EINVAL, "weight_decay must be >= 0");
-    return ZF_OK;
-}
-
-// Scalars of AdamK (the tables are attached by the caller).
-AdamK adam_scalars(const zf_adam_params& hp) {
-    const double lr = hp.lr, b1 = hp.beta1, b2 = hp.beta2, eps = hp.eps, wd = hp.weight_decay;
-    AdamK a{};
-    a.b1 = (float)b1;
-    a.b2 = (float)b2;
-    a.omb1 = (float)(1.0 - b1);
-    a.omb2 = (float)(1.0 - b2);
-    a.eps = (float)eps;
-    a.decay = (float)(1.0 - lr * wd);
-    a.wd = (float)wd;
-    a.wd_mode = wd == 0.0 ? 0 : (hp.decoupled ? 1 : 2);
-    a.ss_inf = (float)lr;
-    return a;
-}
-
-// Process-wide cache of device tables for the stateless primitive (never freed).
-struct TabCache {
-    std::mutex mu;
-    std::map<std::tuple<int, uint64_t, uint64_t>, std::pair<float*, int>> ss;  // (dev, lr, b1)
-    std::map<std::pair<int, uint64_t>, std::pair<float*, int>> bc2;              // (dev, b2)
-    std::map<std::tuple<int, uint64_t, uint64_t, uint64_t>, std::pair<float*, int>> sb;  // (dev, lr, b1, b2)
-};
-TabCache& tab_cache() {
-    static TabCache* c = new TabCache();
-    return *c;
-}
-
-uint64_t dbits(double x) {
-    uint64_t u;
-    std::memcpy(&u, &x, 8);
-    return u;
-}
-
-zf_status upload_table(const std::vector<float>& h, float** d, cudaStream_t s) {
-    float* pinned = nullptr;
-    ZF_CUDA(cudaMallocHost(&pinned, h.size() * sizeof(float)));  // kept alive with the table
-    std::memcpy(pinned, h.data(), h.size() * sizeof(float));
-    ZF_CUDA(cudaMalloc(d, h.size() * sizeof(float)));
-    ZF_CUDA(cudaMemcpyAsync(*d, pinned, h.size() * sizeof(float), cudaMemcpyHostToDevice, s));
-    return ZF_OK;
-}
-
-zf_status cached_tables(const zf_adam_params& hp, cudaStream_t s, AdamK* a) {
-    int dev = 0;
-    ZF_CUDA(cudaGetDevice(&dev));
-    TabCache& c = tab_cache();
-    std::lock_guard<std::mutex> lk(c.mu);
-    auto ks = std::make_tuple(dev, dbits(hp.lr), dbits(hp.beta1));
-    auto it = c.ss.find(ks);
-    if (it == c.ss.end()) {
-        auto h = make_ss(hp.lr, hp.beta1);
-        float* d = nullptr;
-        ZF_TRY(upload_table(h, &d, s));
-        it = c.ss.emplace(ks, std::make_pair(d, (int)h.size())).first;
-    }
-    auto kb = std::make_pair(dev, dbits(hp.beta2));
-    auto jt = c.bc2.find(kb);
-    if (jt == c.bc2.end()) {
-        auto h = make_bc2(hp.beta2);
-        float* d = nullptr;
-        ZF_TRY(upload_table(h, &d, s));
-        jt = c.bc2.emplace(kb, std::make_pair(d, (int)h.size())).first;
-    }
-    auto kq = std::make_tuple(dev, dbits(hp.lr), dbits(hp.beta1), dbits(hp.beta2));
-    auto qt = c.sb.find(kq);
-    if (qt == c.sb.end()) {
-        auto h = make_sb(make_ss(hp.lr, hp.beta1), make_bc2(hp.beta2), hp.lr);
-        float* d = nullptr;
-        ZF_TRY(upload_table(h, &d, s));
-        qt = c.sb.emplace(kq, std::make_pair(d, (int)(h.size() / 2))).first;
-    }
-    a->ss_tab = it->second.first;
-    a->ss_len = it->second.second;
-    a->bc2_tab = jt->second.first;
-    a->bc2_len = jt->second.second;
-    a->sb_tab = reinterpret_cast<const float2*>(qt->second.first);
-    a->sb_len = qt->second.second;
-    return ZF_OK;
-}
-
-// ============================================================ geometry
-struct K3Geom {
-    int64_t seg_cols;
-    int32_t nseg, R;
-    int64_t units;
-    bool mv_ok;
-};
-
-// p tile staging pays off when most 32-byte sectors of a row hold a selected column
-bool k3_p_dense(int64_t m, int64_t k, int psz) {
-    const double frac = (double)k / (double)m;
-    return 1.0 - std::pow(1.0 - frac, 32.0 / psz) >= 0.5;
-}
-
-// Worst-case bytes one K3 unit stages (R rows x c columns): G tile, p tile (if dense),
-// mask words, the unselected-column list, moment slabs (R*k: also covers the old rows of a refresh),
-// step counts and remap sources; each as a 16-byte-granular superset.
-int64_t k3_unit_bytes(int64_t R, int64_t c, int64_t k, int gsz, int psz, bool p_dense, bool mv) {
-    auto a16 = [](int64_t b) { return (b + 15) & ~int64_t(15); };
-    int64_t b = a16(R * c * gsz) + 2 * ((c + 31) / 32 + 8) * 4;
-    if (p_dense) b += a16(R * c * psz);
-    if (mv) b += 2 * (R * k + 8) * 4 + 3 * (std::min(c, k) + 8) * 4;  // moments; steps, sources, idx
-    b += a16((c + 8) * 2);                                              // unselected-column offsets
-    return b;
-}
-
-K3Geom k3_geom(int64_t n, int64_t m, int64_t k, int gsz, int psz, bool p_dense, bool adam = true) {
-    const UpdLimits lim = update_limits();
-    const int64_t A = lim.arena_bytes;
-    K3Geom g{};
-    // moments staged unless even one row's old moments cannot fit next to a minimal tile
-    g.mv_ok = adam && k3_unit_bytes(1, std::min<int64_t>(m, 128), k, gsz, psz, p_dense, true) <= A;
-    // Units are R rows x c columns (c = m, or a multiple of 128 so segments start 16-byte
-    // aligned in the mask/prefix words): the shape with the fewest units per matrix (the most
-    // bytes per stage), ties to full rows / wider segments.  ZF_K3_GEOM=rows keeps the older
-    // rule (full rows when one fits, else single-row segments).
-    // Measured (tools/k3_geom_ab.sh): the search wins with a staged p tile (Llama-2-13B K3
-    // 23.90 -> 22.76 ms: m = 5120 rows go from 1-row units to 3 rows x 2688 columns) but
-    // loses without one (k = 1%: 6.92 -> 7.27 ms, more exposed p loads per unit), so
-    // unstaged-p layers keep the row rule.
-    static const bool rows_env = getenv("ZF_K3_GEOM") && std::string(getenv("ZF_K3_GEOM")) == "rows";
-    const bool rows_only = rows_env || !p_dense;
-    auto rmax = [&](int64_t c) {
-        int64_t R = 0;
-        while (R < std::min<int64_t>(n, 127) && k3_unit_bytes(R + 1, c, k, gsz, psz, p_dense, g.mv_ok) <= A) ++R;
-        return R;
-    };
-    int64_t best_units = -1;
-    std::vector<int64_t> cands;
-    cands.push_back(m);
-    for (int64_t c = ((m - 1) / 128) * 128; c >= 128; c -= 128) cands.push_back(c);
-    for (int64_t c : cands) {
-        const int64_t R = rmax(c);
-        if (R < 1) continue;
-        const int64_t nseg = (m + c - 1) / c;
-        if (rows_only && best_units >= 0) break;
-        if (rows_only && nseg > 1) {  // older rule: widest single-row segment
-            const int64_t u = n * nseg;
-            g.seg_cols = c; g.nseg = (int32_t)nseg; g.R = 1; best_units = u;
-            break;
-        }
-        const int64_t u = ((n + R - 1) / R) * nseg;
-        if (best_units < 0 || u < best_units) {
-            best_units = u;
-            g.seg_cols = c;
-            g.nseg = (int32_t)nseg;
-            g.R = (int32_t)R;
-        }
-    }
-    if (best_units < 0) {  // nothing fits (tiny arena): single-row minimal segments
-        g.seg_cols = 128;
-        g.nseg = (int32_t)((m + 127) / 128);
-        g.R = 1;
-    }
-    g.units = ((n + g.R - 1) / g.R) * g.nseg;
-    return g;
-}
-
-bool k3_tma_ok(const void* G, int64_t ldg, int64_t m, int gsz) {
-    return aligned16(G) && ((ldg * gsz) % 16 == 0) && ((m * gsz) % 16 == 0);
-}
-
-// Stream-ordered scratch (freed asynchronously on the same stream).
-struct Scratch {
-    cudaStream_t s;
-    std::vector<void*> ptrs;
-    explicit Scratch(cudaStream_t st) : s(st) {}
-    template <typename T>
-    zf_status get(T** p, size_t bytes, bool zero) {
-        void* q = nullptr;
-        ZF_CUDA(cudaMallocAsync(&q, std::max<size_t>(bytes, 16), s));
-        ptrs.push_back(q);
-        if (zero) ZF_CUDA(cudaMemsetAsync(q, 0, std::max<size_t>(bytes, 16), s));
-        *p = static_cast<T*>(q);
-        return ZF_OK;
-    }
-    ~Scratch() {
-        for (void* q : ptrs) cudaFreeAsync(q, s);
-    }
-};
-
-zf_status check_matrix(const void* G, int gdt, int64_t n, int64_t m, int64_t ld, const char* what) {
-    if (!G) return fail(ZF_EINVAL, "%s is NULL", what);
-    if (!dtype_ok(gdt)) return fail(ZF_EINVAL, "%s: unsupported dtype %d", what, gdt);
-    if (n < 1 || m < 1) return fail(ZF_EINVAL, "%s: need n >= 1 and m >= 1 (got n=%lld m=%lld)", what, (long long)n,
-                                    (long long)m);
-    if (m > 0x7fffffffLL) return fail(ZF_EINVAL, "%s: m too large", what);
-    if (ld < m) return fail(ZF_EINVAL, "%s: ld (%lld) < m (%lld)", what, (long long)ld, (long long)m);
-    return ZF_OK;
-}
-
-}  // namespace
-
-// ============================================================ basic API
-extern "C" const char* zf_status_string(int32_t s) {
-    switch (s) {
-        case ZF_OK: return "ZF_OK";
-        case ZF_EINVAL: return "ZF_EINVAL: invalid argument";
-        case ZF_ENONFINITE: return "ZF_ENONFINITE: non-finite gradient";
-        case ZF_ECUDA: return "ZF_ECUDA: CUDA error";
-        case ZF_ENCCL: return "ZF_ENCCL: NCCL error";
-        case ZF_ENOMEM: return "ZF_ENOMEM: out of memory";
-        case ZF_ESTATE: return "ZF_ESTATE: invalid state";
-        default: return "unknown zf_status";
-    }
-}
-
-extern "C" const char* zf_last_error(void) { return g_last_error.c_str(); }
-
-extern "C" int32_t zf_version(void) { return 100; }
-
-extern "C" int64_t zf_k_for(int64_t m, int32_t ppm) {
-    if (m < 1 || ppm <= 0 || ppm > 1000000) return -1;
-    int64_t k = (m * (int64_t)ppm + 999999) / 1000000;
-    return std::min<int64_t>(std::max<int64_t>(k, 1), m);
-}
-
-// ============================================================ stateless primitives
-extern "C" zf_status zf_column_norms(const void* G, zf_dtype gdt, int64_t n, int64_t m, int64_t ld, float* norms,
-                                     int32_t* nonfinite, zf_stream_t stream) {
-    g_last_error.clear();
-    ZF_TRY(check_matrix(G, gdt, n, m, ld, "G"));
-    if (!norms) return fail(ZF_EINVAL, "norms is NULL");
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    const int gsz = esize(gdt);
-    Table<NormLayer> t{};
-    NormLayer& L = t.one;
-    t.dev = nullptr;
-    t.n = 1;
-    L.G = G;
-    L.n = n;
-    L.m = m;
-    L.ld = ld;
-    L.out = norms;
-    L.nrb = (int32_t)((n + norms_rows_per_block() - 1) / norms_rows_per_block());
-    L.ncb = (int32_t)((m + norms_cols_per_block(gdt) - 1) / norms_cols_per_block(gdt));
-    L.unit_begin = 0;
-    L.vec_ok = aligned16(G) && ((ld * gsz) % 16 == 0);
-    Scratch sc(s);
-    if (L.nrb > 1) {
-        ZF_TRY(sc.get(&L.partial, (size_t)L.nrb * m * sizeof(float), false));
-        ZF_TRY(sc.get(&L.counter, (size_t)L.ncb * sizeof(uint32_t), true));
-    }
-    ZF_CUDA(launch_norms(t, (int64_t)L.nrb * L.ncb, gdt, nonfinite, s));
-    return ZF_OK;
-}
-
-extern "C" zf_status zf_topk_columns(const float* norms, int64_t m, int64_t k, int32_t* idx, zf_stream_t stream) {
-    g_last_error.clear();
-    if (!norms || !idx) return fail(ZF_EINVAL, "norms/idx is NULL");
-    if (m < 1) return fail(ZF_EINVAL, "empty norms vector (m=%lld)", (long long)m);
-    if (m > 0x7fffffffLL) return fail(ZF_EINVAL, "m too large");
-    if (k < 1 || k > m) return fail(ZF_EINVAL, "need 1 <= k <= m (k=%lld m=%lld)", (long long)k, (long long)m);
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    Scratch sc(s);
-    Table<TopkLayer> t{};
-    t.dev = nullptr;
-    t.n = 1;
-    TopkLayer& L = t.one;
-    L.norms = norms;
-    L.m = m;
-    L.k = k;
-    L.idx = idx;
-    const int64_t W = (m + 31) / 32;
-    ZF_TRY(sc.get(&L.mask, W * sizeof(uint32_t), false));
-    ZF_TRY(sc.get(&L.prefix, W * sizeof(int32_t), false));
-    ZF_CUDA(launch_topk(t, m, 0, nullptr, s));
-    return ZF_OK;
-}
-
-extern "C" zf_status zf_selective_adam(void* p, zf_dtype pdt, int64_t ldp, const void* G, zf_dtype gdt, int64_t ldg,
-                                       int64_t n, int64_t m, const int32_t* idx, int64_t k, float* exp_avg,
-                                       float* exp_avg_sq, int32_t* step, const zf_adam_params* hp,
-                                       zf_stream_t stream) {
-    g_last_error.clear();
-    ZF_TRY(check_matrix(G, gdt, n, m, ldg, "G"));
-    ZF_TRY(check_matrix(p, pdt, n, m, ldp, "p"));
-    if (!idx || !exp_avg || !exp_avg_sq || !step) return fail(ZF_EINVAL, "idx/exp_avg/exp_avg_sq/step is NULL");
-    if (k < 1 || k > m) return fail(ZF_EINVAL, "need 1 <= k <= m");
-    ZF_TRY(check_hp(hp));
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    AdamK a = adam_scalars(*hp);
-    ZF_TRY(cached_tables(*hp, s, &a));
-    Scratch sc(s);
-    uint32_t* counter = nullptr;
-    ZF_TRY(sc.get(&counter, sizeof(uint32_t), true));
-    ZF_CUDA(launch_adam_only(G, gdt, ldg, p, pdt, ldp, n, idx, k, exp_avg, exp_avg_sq, step, counter, a, s));
-    return ZF_OK;
-}
-
-extern "C" zf_status zf_compact_unselected(const void* G, zf_dtype gdt, int64_t n, int64_t m, int64_t ld,
-                                           const int32_t* idx, int64_t k, void* out, zf_stream_t stream) {
-    g_last_error.clear();
-    ZF_TRY(check_matrix(G, gdt, n, m, ld, "G"));
-    if (!idx || !out) return fail(ZF_EINVAL, "idx/out is NULL");
-    if (k < 1 || k > m) return fail(ZF_EINVAL, "need 1 <= k <= m");
-    if (!aligned16(out)) return fail(ZF_EINVAL, "out must be 16-byte aligned");
-    if (k == m) return ZF_OK;  // empty output
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    const int gsz = esize(gdt);
-    Scratch sc(s);
-    UpdParams prm{};
-    prm.layers.dev = nullptr;
-    prm.layers.n = 1;
-    UpdLayer& L = prm.layers.one;
-    const int64_t W = (m + 31) / 32;
-    uint32_t* mask = nullptr;
-    int32_t* prefix = nullptr;
-    int32_t* bad = nullptr;
-    uint16_t* ucol = nullptr;
-    ZF_TRY(sc.get(&mask, (W + 8) * sizeof(uint32_t), true));    // padded: K3 stages words in 16-byte groups
-    ZF_TRY(sc.get(&prefix, (W + 8) * sizeof(int32_t), true));
-    ZF_TRY(sc.get(&ucol, (m - k + 16) * sizeof(uint16_t), true));
-    ZF_TRY(sc.get(&bad, sizeof(int32_t), true));
-    ZF_TRY(sc.get(&prm.claim, sizeof(uint32_t), true));
-    const K3Geom geo = k3_geom(n, m, k, gsz, gsz, false, false);
-    ZF_CUDA(launch_build_mask(idx, k, m, mask, prefix, ucol, geo.seg_cols, gsz, bad, s));
-    L.G = G;
-    L.n = n;
-    L.m = m;
-    L.ldg = ld;
-    L.k = k;
-    L.idx = idx;
-    L.mask = mask;
-    L.prefix = prefix;
-    L.ucol = ucol;
-    L.out = out;
-    L.out_ld = m - k;
-    L.seg_cols = geo.seg_cols;
-    L.nseg = geo.nseg;
-    L.R = geo.R;
-    L.units = geo.units;
-    L.unit_begin = 0;
-    L.tma_ok = k3_tma_ok(G, ld, m, gsz);
-    prm.total_units = geo.units;
-    prm.claim_base = 0;
-    prm.do_adam = 0;
-    prm.do_compact = 1;
-    ZF_CUDA(launch_update(prm, gdt, gdt, update_grid(gdt, gdt), s));
-    return ZF_OK;
-}
-
-// ============================================================ stateful driver
-namespace {
-
-typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-
-struct LayerState {
-    zf_layer_desc d{};
-    int64_t k = 0, W = 0, mk = 0;
-    int64_t mk_pad = 0;               // device compact block row pitch (16-byte rows)
-    // K1
-    int32_t nrb = 0, ncb = 0;
-    int64_t norm_off = 0, norm_unit_begin = 0;
-    float* partial = nullptr;
-    uint32_t* k1_counter = nullptr;
-    // selection sets (double-buffered for the refresh remap)
-    int32_t* idx[2] = {nullptr, nullptr};
-    uint32_t* mask[2] = {nullptr, nullptr};
-    int32_t* prefix[2] = {nullptr, nullptr};
-    uint16_t* ucol[2] = {nullptr, nullptr};
-    int32_t* steps[2] = {nullptr, nullptr};
-    int32_t* slot_src = nullptr;
-    float* mom[2] = {nullptr, nullptr};
-    float* vel[2] = {nullptr, nullptr};
-    void* stage_dev[2] = {nullptr, nullptr};
-    void* stage_host[2] = {nullptr, nullptr};
-    float* acc[2] = {nullptr, nullptr};
-    float* dacc[2] = {nullptr, nullptr};  // device_accumulate: [n, mk_pad] fp32 window accumulators
-    float* acc_sealed_h = nullptr;        // device_accumulate: pinned dense [n, mk] copy of the sealed window
-    // K3 geometry
-    K3Geom geo{};
-    int64_t unit_begin = 0;
-    cudaEvent_t d2h_ev[2] = {nullptr, nullptr};
-    // f1: deferred CPU AdamW (reading R18)
-    float* master = nullptr;          // [n, m] fp32 host master (valid on CPU-updated columns)
-    float* mh = nullptr;              // [n, m] host moments
-    float* vh = nullptr;
-    std::vector<int32_t> th;          // [m] host step count per column
-    std::vector<int32_t> idx_host;    // current selection (ascending), host copy
-    std::vector<int32_t> unsel_host;  // its complement (ascending)
-    void* p_mirror = nullptr;         // pinned [n, m] copy of p at a refresh
-    void* p_up = nullptr;             // pinned [n, m-k] updated unselected params
-    void* p_up_dev = nullptr;         // device [n, m-k]
-    int32_t* unsel_dev = nullptr;     // device [m-k]
-    // f2: warm-up selection set (all m columns; reading R20)
-    int32_t* idx_w = nullptr;
-    uint32_t* mask_w = nullptr;
-    int32_t* prefix_w = nullptr;
-    int32_t* steps_w = nullptr;
-    float* mom_w = nullptr;           // [n, m]
-    float* vel_w = nullptr;
-    K3Geom geo_w{};
-    int64_t unit_begin_w = 0;
-};
-
-// Simple pool for the host accumulation (row 8, H1).
-class Pool {
-   public:
-    explicit Pool(int n) : n_(n) {
-        for (int i = 0; i < n_; ++i) th_.emplace_back([this, i] { run(i); });
-    }
-    ~Pool() {
-        {
-            std::lock_guard<std::mutex> lk(mu_);
-            stop_ = true;
-            ++gen_;
-        }
-        cv_.notify_all();
-        for (auto& t : th_) t.join();
-    }
-    // fn(begin, end) over [0, count) split into n_ contiguous slices; callers from several
-    // threads (H1 and the f1 host update) are serialised.
-    template <typename F>
-    void parallel_for(int64_t count, F&& fn) {
-        std::lock_guard<std::mutex> call(call_mu_);
-        std::unique_lock<std::mutex> lk(mu_);
-        job_ = [&](int i) {
-            const int64_t per = (count + n_ - 1) / n_;
-            const int64_t b = std::min<int64_t>(count, per * i), e = std::min<int64_t>(count, b + per);
-            if (b < e) fn(b, e);
-        };
-        pending_ = n_;
-        ++gen_;
-        cv_.notify_all();
-        done_cv_.wait(lk, [&] { return pending_ == 0; });
-        job_ = nullptr;
-    }
-
-   private:
-    void run(int i) {
-        uint64_t seen = 0;
-        for (;;) {
-            std::function<void(int)> job;
-            {
-                std::unique_lock<std::mutex> lk(mu_);
-                cv_.wait(lk, [&] { return gen_ != seen; });
-                seen = gen_;
-                if (stop_) return;
-                job = job_;
-            }
-            if (job) job(i);
-            {
-                std::lock_guard<std::mutex> lk(mu_);
-                if (--pending_ == 0) done_cv_.notify_all();
-            }
-        }
-    }
-    int n_;
-    std::vector<std::thread> th_;
-    std::mutex mu_, call_mu_;
-    std::condition_variable cv_, done_cv_;
-    std::function<void(int)> job_;
-    uint64_t gen_ = 0;
-    int pending_ = 0;
-    bool stop_ = false;
-};
-
-}  // namespace
-
-struct zf_ctx {
-    int device = 0;
-    zf_config cfg{};
-    int world = 1, rank = 0;
-    ncclComm_t comm = nullptr;
-    zf_host_allreduce_fn host_allreduce = nullptr;  // world > 1 without NCCL
-    void* host_allreduce_user = nullptr;
-    float* norms_host = nullptr;
-    int gdt = 0, pdt = 0, gsz = 2, psz = 2;
-    std::vector<LayerState> L;
-    int64_t total_m = 0, max_m = 0, k1_units = 0, k3_units = 0;
-    bool has_empty = false;       // some layer has n = 0 rows on this rank
-    int n_stage = 1;
-    float* norms = nullptr;
-    std::vector<void*> dev_allocs, host_pinned;
-    std::vector<float*> host_plain;
-    int32_t* nonfinite_h = nullptr;  // mapped pinned
-    int32_t* nonfinite_d = nullptr;
-    uint32_t* claim = nullptr;
-    uint32_t* done = nullptr;  // [n_layers]
-    uint32_t claim_base = 0;
-    int32_t since = 0;            // K3 launches since the last refresh (step-count delta)
-    std::vector<uint32_t> done_target;  // expected per-layer completion count after the last step
-    cudaStream_t aux = nullptr;   // inspection copies (zf_optimizer_state)
-    std::vector<int32_t*> steps_view;
-    int grid = 148;
-    // launch tables
-    NormLayer* d_norm_tab = nullptr;
-    std::vector<NormLayer> h_norm_tab, up_norm_tab;
-    TopkLayer* d_topk_tab[3] = {nullptr, nullptr, nullptr};  // [new set 0 | new set 1 | first (new 1, no old)]
-    UpdLayer* d_upd_tab[8] = {};                              // [(cur)*4 + refresh*2 + stage]
-    std::vector<UpdLayer> h_upd_tab[8], up_upd_tab[8];
-    // f2 warm-up (reading R20): K3 table of the all-columns set, K2 table of the first
-    // regular refresh (old = warm-up set) and K3 tables of that step (remap from [n, m])
-    int64_t tau = 0, k3_units_w = 0;
-    UpdLayer* d_upd_w = nullptr;
-    std::vector<UpdLayer> h_upd_w, up_upd_w;
-    TopkLayer* d_topk_w = nullptr;
-    UpdLayer* d_upd_x[2] = {};
-    std::vector<UpdLayer> h_upd_x[2], up_upd_x[2];
-    int64_t last_step = -1;       // t of the last zf_step call (warm-up included)
-    // table uploads through a small pinned ring
-    std::vector<unsigned char*> ring;
-    std::vector<cudaEvent_t> ring_ev;
-    size_t ring_bytes = 0;
-    int ring_pos = 0;
-    // AdamW tables (ss depends on lr; may change via zf_set_lr)
-    AdamK adam{};
-    float* d_ss = nullptr;
-    float* d_bc2 = nullptr;
-    float* d_sb = nullptr;
-    std::vector<float> bc2_host;
-    double lr_cur = 0.0, lr_uploaded = -1.0;
-    // step state
-    int cur = 0;
-    bool have_sel = false;
-    int64_t last_t = -1;          // regular-schedule index (t - tau) of the last regular step
-    int64_t launches = 0;
-    cudaEvent_t step_done = nullptr, k3_done = nullptr;
-    // offload
-    cudaStream_t copy_stream = nullptr;
-    cudaEvent_t d2h_all[2] = {nullptr, nullptr};
-    bool d2h_issued[2] = {false, false};
-    PFN_waitValue32 wait_value = nullptr;
-    // host accumulation
-    Pool* pool = nullptr;
-    std::thread h1;
-    std::mutex mu;
-    std::condition_variable cv;
-    std::deque<int64_t> jobs;
-    int64_t h1_done = -1;
-    bool stopping = false;
-    // accumulation windows as H1 sees them (fixed S, or Zen-auto decisions), and the log
-    int64_t h1_win = 0;           // index of the window the next processed step belongs to
-    bool h1_first = true;         // the next processed step starts a window
-    int h1_last_buf = -1;         // buffer the last processed step accumulated into
-    int h1_sealed_buf = -1;       // buffer of the last ended window
-    std::vector<int64_t> log_t;
-    std::vector<int32_t> log_end;
-    std::vector<double> log_A, log_i, log_u;
-    // the same windows as zf_step sees them (f1 updates at window ends)
-    int64_t mw = 0, mw_len = 0;
-    // f2 Zen-auto (reading R21): K6 tables per current set, device state, decision records
-    bool autoz = false;
-    AutoLayer* d_auto_tab[2] = {nullptr, nullptr};
-    double* auto_sums = nullptr;
-    uint32_t* auto_counter = nullptr;
-    AutoState* auto_state = nullptr;
-    AutoRecord* auto_rec_h = nullptr;   // mapped pinned ring [AUTO_RING]
-    AutoRecord* auto_rec_d = nullptr;
-    cudaEvent_t auto_ev[8] = {};
-    static constexpr int AUTO_RING = 8;
-    // device-side window accumulation (K7; device_accumulate)
-    bool devacc = false;
-    AccLayer* d_acc_tab = nullptr;
-    int64_t acc_vecs = 0;
-    cudaEvent_t acc_d2h_ev[2] = {nullptr, nullptr};
-    cudaEvent_t k7_done = nullptr;
-    // per-phase timing (zf_profile)
-    bool profiling = false;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
-    struct Pending { int phase; cudaEvent_t a, b; };
-    std::vector<Pending> pending;
-    static constexpr int NPHASE = 7;
-    double prof_ms[NPHASE] = {};
-    int64_t prof_n[NPHASE] = {};
-
-    ~zf_ctx();
-    zf_status prof_begin(int phase, cudaStream_t s, Pending* p) {
-        p->phase = phase;
-        p->a = p->b = nullptr;
-        if (!profiling) return ZF_OK;
-        if (ev_pool.empty()) {
-            cudaEvent_t a, b;
-            ZF_CUDA(cudaEventCreate(&a));
-            ZF_CUDA(cudaEventCreate(&b));
-            ev_pool.push_back({a, b});
-        }
-        p->a = ev_pool.back().first;
-        p->b = ev_pool.back().second;
-        ev_pool.pop_back();
-        ZF_CUDA(cudaEventRecord(p->a, s));
-        return ZF_OK;
-    }
-    zf_status prof_end(Pending* p, cudaStream_t s) {
-        if (!p->a) return ZF_OK;
-        ZF_CUDA(cudaEventRecord(p->b, s));
-        pending.push_back(*p);
-        return ZF_OK;
-    }
-    zf_status dev_alloc(void** p, size_t bytes) {
-        void* q = nullptr;
-        ZF_CUDA(cudaMalloc(&q, std::max<size_t>(bytes, 256)));
-        dev_allocs.push_back(q);
-        *p = q;
-        return ZF_OK;
-    }
-    template <typename T>
-    zf_status dalloc(T** p, size_t bytes, bool zero = true) {
-        void* q = nullptr;
-        ZF_TRY(dev_alloc(&q, bytes));
-        if (zero) ZF_CUDA(cudaMemset(q, 0, std::max<size_t>(bytes, 256)));
-        *p = static_cast<T*>(q);
-        return ZF_OK;
-    }
-    zf_status upload(void* dst, const void* src, size_t bytes, cudaStream_t s) {
-        if (bytes > ring_bytes) return fail(ZF_ESTATE, "table upload larger than ring slot");
-        unsigned char* buf = ring[ring_pos];
-        ZF_CUDA(cudaEventSynchronize(ring_ev[ring_pos]));  // slot free once its last copy finished
-        std::memcpy(buf, src, bytes);
-        ZF_CUDA(cudaMemcpyAsync(dst, buf, bytes, cudaMemcpyHostToDevice, s));
-        ZF_CUDA(cudaEventRecord(ring_ev[ring_pos], s));
-        ring_pos = (ring_pos + 1) % (int)ring.size();
-        return ZF_OK;
-    }
-    // optimizer-state storage: HBM, or mapped pinned host memory (state_offload, row f3)
-    zf_status state_alloc(float** p, size_t elems) {
-        if (!cfg.state_offload) return dalloc(p, elems * sizeof(float));
-        void* h = nullptr;
-        ZF_CUDA(cudaHostAlloc(&h, std::max<size_t>(elems * sizeof(float), 256), cudaHostAllocMapped));
-        host_pinned.push_back(h);
-        std::memset(h, 0, std::max<size_t>(elems * sizeof(float), 256));
-        void* d = nullptr;
-        ZF_CUDA(cudaHostGetDevicePointer(&d, h, 0));
-        *p = static_cast<float*>(d);
-        return ZF_OK;
-    }
-    void h1_loop();
-};
-
-zf_ctx::~zf_ctx() {
-    if (h1.joinable()) {
-        {
-            std::lock_guard<std::mutex> lk(mu);
-            stopping = true;
-        }
-        cv.notify_all();
-        h1.join();
-    }
-    delete pool;
-    cudaSetDevice(device);
-    cudaDeviceSynchronize();
-    if (comm) ncclCommDestroy(comm);
-    for (void* p : dev_allocs) cudaFree(p);
-    for (void* p : host_pinned) cudaFreeHost(p);
-    for (float* p : host_plain) std::free(p);
-    for (auto& l : L)
-        for (int i = 0; i < 2; ++i)
-            if (l.d2h_ev[i]) cudaEventDestroy(l.d2h_ev[i]);
-    for (auto e : ring_ev) cudaEventDestroy(e);
-    for (auto e : d2h_all)
-        if (e) cudaEventDestroy(e);
-    for (auto e : auto_ev)
-        if (e) cudaEventDestroy(e);
-    for (auto e : acc_d2h_ev)
-        if (e) cudaEventDestroy(e);
-    if (k7_done) cudaEventDestroy(k7_done);
-    for (auto& e : ev_pool) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
-    for (auto& e : pending) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
-    if (step_done) cudaEventDestroy(step_done);
-    if (k3_done) cudaEventDestroy(k3_done);
-    if (copy_stream) cudaStreamDestroy(copy_stream);
-    if (aux) cudaStreamDestroy(aux);
-}
-
-// One row of H1 (fp32 adds in step order; a window's first step writes 0 + x).  Cloned for
-// the host's vector ISA; -ffp-contract=off keeps every add a single IEEE operation.
-__attribute__((target_clones("avx512f", "avx2", "default")))
-void acc_row_bf16(float* __restrict__ acc, const uint16_t* __restrict__ src, int64_t n, bool first) {
-    if (first) {
-        for (int64_t i = 0; i < n; ++i) {
-            uint32_t u = (uint32_t)src[i] << 16;
-            float x;
-            std::memcpy(&x, &u, 4);
-            acc[i] = 0.0f + x;
-        }
-    } else {
-        for (int64_t i = 0; i < n; ++i) {
-            uint32_t u = (uint32_t)src[i] << 16;
-            float x;
-            std::memcpy(&x, &u, 4);
-            acc[i] = acc[i] + x;
-        }
-    }
-}
-__attribute__((target_clones("avx512f", "avx2", "default")))
-void acc_row_f32(float* __restrict__ acc, const float* __restrict__ src, int64_t n, bool first) {
-    if (first) {
-        for (int64_t i = 0; i < n; ++i) acc[i] = 0.0f + src[i];
-    } else {
-        for (int64_t i = 0; i < n; ++i) acc[i] = acc[i] + src[i];
-    }
-}
-
-// H1: accumulate each layer's staged compact block into the window's fp32 buffer
-// as soon as its D2H copy completed (DESIGN.md §2 O8).
-void zf_ctx::h1_loop() {
-    cudaSetDevice(device);
-    const int S = cfg.accum_interval;
-    for (;;) {
-        int64_t t;
-        {
-            std::unique_lock<std::mutex> lk(mu);
-            cv.wait(lk, [&] { return stopping || !jobs.empty(); });
-            if (jobs.empty()) return;
-            t = jobs.front();
-        }
-        const int a = (int)(h1_win % 2);
-        const bool first = h1_first;
-        const int sb = (int)(t % n_stage);
-        for (auto& l : L) {
-            cudaEventSynchronize(l.d2h_ev[sb]);
-            const int64_t mk = l.mk, ld = l.mk_pad;
-            float* acc = l.acc[a];
-            const void* stage = l.stage_host[sb];
-            const bool bf = gdt == ZF_BF16;
-            pool->parallel_for(l.d.n, [&](int64_t b, int64_t e) {
-                for (int64_t r = b; r < e; ++r) {
-                    if (bf) acc_row_bf16(acc + r * mk, static_cast<const uint16_t*>(stage) + r * ld, mk, first);
-                    else acc_row_f32(acc + r * mk, static_cast<const float*>(stage) + r * ld, mk, first);
-                }
-            });
-        }
-        // the window decision of step t: fixed S, or K6's record (Zen-auto, reading R21)
-        bool end = (t + 1) % S == 0;
-        double rA = NAN, ri = NAN, ru = NAN;
-        if (autoz) {
-            const int slot = (int)(t % AUTO_RING);
-            cudaEventSynchronize(auto_ev[slot]);
-            const volatile AutoRecord* r = auto_rec_h + slot;
-            end = r->end != 0;
-            rA = r->A;
-            ri = r->imp;
-            ru = r->unimp;
-        }
-        {
-            std::lock_guard<std::mutex> lk(mu);
-            h1_last_buf = a;
-            if (end) {
-                h1_sealed_buf = a;
-                ++h1_win;
-            }
-            h1_first = end;
-            log_t.push_back(t + tau);
-            log_end.push_back(end ? 1 : 0);
-            log_A.push_back(rA);
-            log_i.push_back(ri);
-            log_u.push_back(ru);
-            jobs.pop_front();
-            h1_done = t;
-        }
-        cv.notify_all();
-    }
-}
+// zf_driver.cu -- the stateful driver of the C-ABI (include/zf.h): zf_create (per-layer
+// state in HBM, launch tables, NCCL communicator, offload buffers), zf_step (K1 -> norm
+// all-reduce -> K2 -> K3 -> K7/K6, per-layer D2H, window bookkeeping, f1), zf_sync and
+// the views of library-owned state.  See DESIGN.md §5-§6.
+#include "zf_host.h"
 
 extern "C" zf_status zf_nccl_unique_id(void* out128) {
     g_last_error.clear();
@@ -1388,139 +519,7 @@ zf_status refresh_pointer_tables(zf_ctx* c, int variant, bool refresh, void* con
 
 }  // namespace
 
-// ============================================================ f1: deferred CPU AdamW (reading R18)
 namespace {
-
-uint16_t host_bf16_rne(float x) {
-    uint32_t u;
-    std::memcpy(&u, &x, 4);
-    if ((u & 0x7fffffffu) > 0x7f800000u) return (uint16_t)((u >> 16) | 0x40u);
-    u += 0x7fffu + ((u >> 16) & 1u);
-    return (uint16_t)(u >> 16);
-}
-
-float host_widen(const void* p, int dt, size_t i) {
-    if (dt == ZF_BF16) {
-        uint32_t u = (uint32_t) static_cast<const uint16_t*>(p)[i] << 16;
-        float f;
-        std::memcpy(&f, &u, 4);
-        return f;
-    }
-    return static_cast<const float*>(p)[i];
-}
-
-// At a refresh: columns entering the CPU-updated set take the parameter's current value as
-// their fp32 master with zero host moments/step count; then the new selection is recorded.
-zf_status f1_refresh(zf_ctx* c, void* const* params, cudaStream_t s) {
-    const int nl = (int)c->L.size();
-    std::vector<std::vector<int32_t>> nidx(nl);
-    for (int i = 0; i < nl; ++i) {
-        LayerState& l = c->L[i];
-        nidx[i].resize(l.k);
-        ZF_CUDA(cudaMemcpyAsync(nidx[i].data(), l.idx[c->cur], l.k * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-        if (l.d.n > 0)
-        ZF_CUDA(cudaMemcpy2DAsync(l.p_mirror, l.d.m * c->psz, params[i], l.d.ld_param * c->psz, l.d.m * c->psz, l.d.n,
-                                  cudaMemcpyDeviceToHost, s));
-    }
-    ZF_CUDA(cudaStreamSynchronize(s));
-    for (int i = 0; i < nl; ++i) {
-        LayerState& l = c->L[i];
-        const int64_t m = l.d.m, n = l.d.n;
-        std::vector<char> was_cpu(m, 0), now_cpu(m, 1);
-        if (!l.idx_host.empty()) {
-            std::fill(was_cpu.begin(), was_cpu.end(), 1);
-            for (int32_t col : l.idx_host) was_cpu[col] = 0;
-        }
-        for (int32_t col : nidx[i]) now_cpu[col] = 0;
-        std::vector<int32_t> entering;
-        for (int64_t col = 0; col < m; ++col)
-            if (now_cpu[col] && !was_cpu[col]) entering.push_back((int32_t)col);
-        const int pdt = c->pdt;
-        c->pool->parallel_for(n, [&](int64_t b, int64_t e) {
-            for (int64_t r = b; r < e; ++r)
-                for (int32_t col : entering) {
-                    l.master[r * m + col] = host_widen(l.p_mirror, pdt, (size_t)(r * m + col));
-                    l.mh[r * m + col] = 0.0f;
-                    l.vh[r * m + col] = 0.0f;
-                }
-        });
-        for (int32_t col : entering) l.th[col] = 0;
-        l.idx_host = nidx[i];
-        l.unsel_host.clear();
-        for (int64_t col = 0; col < m; ++col)
-            if (now_cpu[col]) l.unsel_host.push_back((int32_t)col);
-        if (!l.unsel_host.empty())
-            ZF_CUDA(cudaMemcpy(l.unsel_dev, l.unsel_host.data(), l.unsel_host.size() * sizeof(int32_t),
-                               cudaMemcpyHostToDevice));
-    }
-    return ZF_OK;
-}
-
-// At a window end: one AdamW step (O6 op order, double-derived constants rounded once) with
-// the window's average gradient acc/S on the fp32 master of the unselected columns; the
-// rounded results are uploaded and scattered into the parameters.
-zf_status f1_window_end(zf_ctx* c, int64_t t, int buf, int64_t len, void* const* params, cudaStream_t s) {
-    if (c->devacc) {
-        ZF_CUDA(cudaEventSynchronize(c->acc_d2h_ev[buf]));  // the sealed window's host copy
-    } else {
-        std::unique_lock<std::mutex> lk(c->mu);
-        c->cv.wait(lk, [&] { return c->h1_done >= t; });
-    }
-    const zf_adam_params& hp = c->cfg.adam;
-    const double lr = c->lr_cur, b1d = hp.beta1, b2d = hp.beta2;
-    const float b1 = (float)b1d, b2 = (float)b2d, omb1 = (float)(1.0 - b1d), omb2 = (float)(1.0 - b2d);
-    const float eps = (float)hp.eps, wd_f = (float)hp.weight_decay, decay = (float)(1.0 - lr * hp.weight_decay);
-    const int wd_mode = hp.weight_decay == 0.0 ? 0 : (hp.decoupled ? 1 : 2);
-    const float Sf = (float)len;  // the window's length: S, or Zen-auto's interval (R21)
-    const int nl = (int)c->L.size();
-    for (int i = 0; i < nl; ++i) {
-        LayerState& l = c->L[i];
-        const int64_t m = l.d.m, n = l.d.n, mk = l.mk;
-        if (mk == 0) continue;
-        const float* acc = c->devacc ? l.acc_sealed_h : l.acc[buf];
-        std::vector<float> ss(mk), bc2s(mk);
-        for (int64_t u = 0; u < mk; ++u) {
-            const double tt = (double)(l.th[l.unsel_host[u]] + 1);
-            ss[u] = (float)(lr / (1.0 - std::pow(b1d, tt)));
-            bc2s[u] = (float)std::sqrt(1.0 - std::pow(b2d, tt));
-        }
-        const int pdt = c->pdt;
-        c->pool->parallel_for(n, [&](int64_t b, int64_t e) {
-            for (int64_t r = b; r < e; ++r) {
-                for (int64_t u = 0; u < mk; ++u) {
-                    const int64_t col = l.unsel_host[u];
-                    float g = acc[r * mk + u] / Sf;
-                    float p = l.master[r * m + col];
-                    float mm = l.mh[r * m + col], vv = l.vh[r * m + col];
-                    if (wd_mode == 1) p = p * decay;
-                    else if (wd_mode == 2) {
-                        const float wp = wd_f * p;
-                        g = g + wp;
-                    }
-                    const float a1 = b1 * mm, a2 = omb1 * g;
-                    mm = a1 + a2;
-                    const float c1 = b2 * vv, c2 = omb2 * g, c3 = c2 * g;
-                    vv = c1 + c3;
-                    const float den = std::sqrt(vv) / bc2s[u] + eps;
-                    const float upd = mm / den;
-                    const float delta = ss[u] * upd;
-                    p = p - delta;
-                    l.master[r * m + col] = p;
-                    l.mh[r * m + col] = mm;
-                    l.vh[r * m + col] = vv;
-                    if (pdt == ZF_BF16) static_cast<uint16_t*>(l.p_up)[r * mk + u] = host_bf16_rne(p);
-                    else static_cast<float*>(l.p_up)[r * mk + u] = p;
-                }
-            }
-        });
-        for (int64_t u = 0; u < mk; ++u) l.th[l.unsel_host[u]] += 1;
-        ZF_CUDA(cudaMemcpyAsync(l.p_up_dev, l.p_up, (size_t)n * mk * c->psz, cudaMemcpyHostToDevice, s));
-        ZF_CUDA(launch_scatter_unselected(params[i], pdt, l.d.ld_param, n, mk, l.unsel_dev, l.p_up_dev, s));
-        c->launches++;
-    }
-    ZF_CUDA(cudaStreamSynchronize(s));  // pinned upload buffers are reused next window
-    return ZF_OK;
-}
 
 // f2 warm-up step (reading R20): every column selected, moments [n, m] updated in place by
 // K3 (no compaction, nothing offloaded).  K3 launches since the set was made = t.
