@@ -31,6 +31,8 @@
 //  - with offload, each consumer warp bumps a per-layer counter after its share of
 //    a unit (red.release); the copy stream waits on it (cuStreamWaitValue32) to
 //    start the layer's device->host copy.
+#include <cstdlib>
+
 #include "zf_internal.cuh"
 
 namespace zf {
@@ -681,6 +683,9 @@ UpdLimits update_limits() {
 int update_grid(int, int) {
     int dev = 0, sms = NUM_SMS_B200;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // ZF_K3_GRID: experiment knob (fewer persistent CTAs than SMs: is K3 bound per SM or globally?)
+    static const int env = getenv("ZF_K3_GRID") ? atoi(getenv("ZF_K3_GRID")) : 0;
+    if (env > 0 && env < sms) return env;
     return sms;
 }
 
