@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--shard-of", type=int, default=1, metavar="P",
                     help="time rank 0's row shard of a P-GPU data-parallel run on this one GPU (no all-reduce): "
                          "per-rank evidence for the multi-GPU configs on a one-GPU box")
+    ap.add_argument("--also-cpu-update", action="store_true",
+                    help="also time e2e with the deferred CPU AdamW (f1), synchronous vs overlapped (R23)")
     ap.add_argument("--json-out", default=None)
     return ap.parse_args()
 
@@ -410,8 +412,8 @@ def run_zenflow(args, rank, world):
         link = {"d2h_peak_GBs": link_peak(True), "h2d_peak_GBs": link_peak(False),
                 "peak_source": "measured in this run: 1 GiB pinned <-> device cudaMemcpyAsync, CUDA events"}
 
-        def e2e_run(devacc):
-            ctx = make_ctx(args.ratio_ppm, True, device_accumulate=devacc)
+        def e2e_run(devacc, **kw):
+            ctx = make_ctx(args.ratio_ppm, True, device_accumulate=devacc, **kw)
             for t in range(2):  # warm-up
                 _g0.copy_(host_g, non_blocking=True)
                 ctx.step_ptrs(t, gpp, pp, stream)
@@ -448,6 +450,13 @@ def run_zenflow(args, rank, world):
 
         ms_dev = e2e_run(True)
         ms_host = e2e_run(False)
+        if args.also_cpu_update:
+            # f1 at every window end: synchronous (R18) vs overlapped with the next step's H2D (R23)
+            result["e2e_cpu_update"] = {
+                "sync_ms_per_step": e2e_run(True, cpu_update=True),
+                "async_ms_per_step": e2e_run(True, cpu_update=True, cpu_update_async=True),
+                "note": "device_accumulate + deferred CPU AdamW of the unselected columns every S steps; "
+                        "async overlaps it with the caller's next H2D of G"}
         for key in ("x1_d2h_GBs", "window_d2h_GBs"):
             if link.get(key):
                 link[key.replace("_GBs", "_frac")] = link[key] / link["d2h_peak_GBs"]

@@ -200,6 +200,17 @@ typedef struct {
                                          traffic).  Requires host_accumulate; with offload
                                          the per-step compact D2H is replaced by the
                                          per-window one.  Bit-identical sums.           */
+    int32_t cpu_update_async;         /* 1 (with cpu_update): the window-end CPU AdamW runs
+                                         on a worker thread while the caller goes on (its
+                                         next forward/backward), and lands at the start
+                                         of the next zf_step or in zf_sync (reading R23,
+                                         the paper's overlapped "zero-stall" update,
+                                         P:437-441).  Every zf_step / zf_sync leaves the
+                                         same state as the synchronous mode; between a
+                                         window's last zf_step and the next call the
+                                         unselected columns are one window stale.  The
+                                         parameter buffers of that last step must stay
+                                         valid until then.                              */
 } zf_config;
 
 typedef struct zf_ctx zf_ctx;

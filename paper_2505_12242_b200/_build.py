@@ -41,7 +41,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     nccl = _nccl_dir()
     extra = os.environ.get("ZF_NVCC_EXTRA", "").split()
-    common = ARCH + extra + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-ffp-contract=off", "-Xptxas", "-v" if verbose else "-O3",
+    common = ARCH + extra + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-ffp-contract=off,-fno-math-errno", "-Xptxas", "-v" if verbose else "-O3",
                      "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nccl, "include")]
     # a change of compile flags (e.g. ZF_NVCC_EXTRA experiments) forces a rebuild
     stamp = os.path.join(BUILD, "flags.txt")

@@ -210,6 +210,7 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
     if (cfg->host_accumulate && (cfg->refresh_interval % cfg->accum_interval) != 0)
         return fail(ZF_EINVAL, "host_accumulate requires refresh_interval %% accum_interval == 0");
     if (cfg->cpu_update && !cfg->host_accumulate) return fail(ZF_EINVAL, "cpu_update requires host_accumulate");
+    if (cfg->cpu_update_async && !cfg->cpu_update) return fail(ZF_EINVAL, "cpu_update_async requires cpu_update");
     if (cfg->cpu_update && cfg->refresh_interval % cfg->accum_interval != 0)
         return fail(ZF_EINVAL, "cpu_update requires refresh_interval to be a multiple of accum_interval");
     if (cfg->warmup_steps < 0) return fail(ZF_EINVAL, "warmup_steps must be >= 0");
@@ -439,15 +440,15 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
         if (cfg->host_accumulate && cfg->cpu_update) {
             {
                 for (auto& l : c->L) {
-                    const size_t nm = (size_t)l.d.n * l.d.m;
+                    const size_t nm = (size_t)l.d.n * l.d.m, nmk = std::max<size_t>((size_t)l.d.n * l.mk, 16);
                     for (float** pp : {&l.master, &l.mh, &l.vh}) {
-                        float* q = static_cast<float*>(std::aligned_alloc(64, (nm * sizeof(float) + 63) / 64 * 64));
+                        float* q = static_cast<float*>(std::aligned_alloc(64, (nmk * sizeof(float) + 63) / 64 * 64));
                         if (!q) return bail(fail(ZF_ENOMEM, "host optimizer state allocation failed"));
-                        std::memset(q, 0, nm * sizeof(float));
+                        std::memset(q, 0, nmk * sizeof(float));
                         c->host_plain.push_back(q);
                         *pp = q;
                     }
-                    l.th.assign(l.d.m, 0);
+                    l.th.assign(l.mk, 0);
                     ZF_CUDA(cudaHostAlloc(&l.p_mirror, std::max<size_t>(nm * c->psz, 64), cudaHostAllocDefault));
                     c->host_pinned.push_back(l.p_mirror);
                     ZF_CUDA(cudaHostAlloc(&l.p_up, std::max<size_t>((size_t)l.d.n * l.mk * c->psz, 64),
@@ -577,6 +578,9 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
         return fail(ZF_ESTATE, "world > 1 needs an NCCL id at zf_create or zf_set_host_allreduce");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     ZF_CUDA(cudaSetDevice(c->device));
+    // R23: the previous window's CPU update (computed while the caller ran its next forward /
+    // backward) lands before this step touches any parameter
+    ZF_TRY(f1_finish(c, s));
     if (t0 < tau) return warmup_step(c, t0, grads, params, s);
     // the regular schedule (refreshes, windows, offload stages) counts from step tau (R20)
     const int64_t t = t0 - tau;
@@ -773,7 +777,10 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
             c->log_i.push_back(ri);
             c->log_u.push_back(ru);
         }
-        if (c->cfg.cpu_update && end) ZF_TRY(f1_window_end(c, t, b, c->mw_len, params, s));
+        if (c->cfg.cpu_update && end) {
+            if (c->cfg.cpu_update_async) ZF_TRY(f1_launch(c, t, b, c->mw_len, params));
+            else ZF_TRY(f1_window_end(c, t, b, c->mw_len, params, s));
+        }
         if (end) {
             c->mw += 1;
             c->mw_len = 0;
@@ -787,6 +794,10 @@ extern "C" zf_status zf_sync(zf_ctx* c) {
     if (!c) return fail(ZF_EINVAL, "ctx is NULL");
     ZF_CUDA(cudaSetDevice(c->device));
     ZF_CUDA(cudaEventSynchronize(c->step_done));
+    if (c->f1_pending) {  // R23: land the pending CPU update so the state is complete
+        ZF_TRY(f1_finish(c, c->aux));
+        ZF_CUDA(cudaStreamSynchronize(c->aux));
+    }
     if (c->copy_stream) ZF_CUDA(cudaStreamSynchronize(c->copy_stream));
     if (c->cfg.host_accumulate) {
         std::unique_lock<std::mutex> lk(c->mu);

@@ -4,6 +4,7 @@
 #include "zf_host.h"
 
 zf_ctx::~zf_ctx() {
+    if (f1_worker.joinable()) f1_worker.join();
     if (h1.joinable()) {
         {
             std::lock_guard<std::mutex> lk(mu);
@@ -165,30 +166,52 @@ zf_status f1_refresh(zf_ctx* c, void* const* params, cudaStream_t s) {
     ZF_CUDA(cudaStreamSynchronize(s));
     for (int i = 0; i < nl; ++i) {
         LayerState& l = c->L[i];
-        const int64_t m = l.d.m, n = l.d.n;
-        std::vector<char> was_cpu(m, 0), now_cpu(m, 1);
-        if (!l.idx_host.empty()) {
-            std::fill(was_cpu.begin(), was_cpu.end(), 1);
-            for (int32_t col : l.idx_host) was_cpu[col] = 0;
-        }
+        const int64_t m = l.d.m, n = l.d.n, mk = l.mk;
+        std::vector<char> now_cpu(m, 1);
         for (int32_t col : nidx[i]) now_cpu[col] = 0;
-        std::vector<int32_t> entering;
+        std::vector<int32_t> unew;
+        unew.reserve(mk);
         for (int64_t col = 0; col < m; ++col)
-            if (now_cpu[col] && !was_cpu[col]) entering.push_back((int32_t)col);
+            if (now_cpu[col]) unew.push_back((int32_t)col);
+        // src[u] = position of column unew[u] in the old unselected list (retained), or -1
+        // (entering: was selected, or the first refresh) -- both lists ascending
+        const std::vector<int32_t>& uold = l.unsel_host;
+        std::vector<int32_t> src(mk, -1);
+        for (size_t u = 0, v = 0; u < unew.size(); ++u) {
+            while (v < uold.size() && uold[v] < unew[u]) ++v;
+            if (v < uold.size() && uold[v] == unew[u]) src[u] = (int32_t)v;
+        }
         const int pdt = c->pdt;
-        c->pool->parallel_for(n, [&](int64_t b, int64_t e) {
-            for (int64_t r = b; r < e; ++r)
-                for (int32_t col : entering) {
-                    l.master[r * m + col] = host_widen(l.p_mirror, pdt, (size_t)(r * m + col));
-                    l.mh[r * m + col] = 0.0f;
-                    l.vh[r * m + col] = 0.0f;
+        if (mk > 0)
+            c->pool->parallel_for(n, [&](int64_t b, int64_t e) {
+                std::vector<float> tmp(3 * (size_t)mk);
+                for (int64_t r = b; r < e; ++r) {
+                    float* M = l.master + r * mk;
+                    float* Mh = l.mh + r * mk;
+                    float* Vh = l.vh + r * mk;
+                    std::memcpy(tmp.data(), M, mk * sizeof(float));
+                    std::memcpy(tmp.data() + mk, Mh, mk * sizeof(float));
+                    std::memcpy(tmp.data() + 2 * mk, Vh, mk * sizeof(float));
+                    for (int64_t u = 0; u < mk; ++u) {
+                        const int32_t v = src[u];
+                        if (v >= 0) {  // retained: keeps its master, moments
+                            M[u] = tmp[v];
+                            Mh[u] = tmp[mk + v];
+                            Vh[u] = tmp[2 * mk + v];
+                        } else {       // entering: the parameter's current value, zero moments
+                            M[u] = host_widen(l.p_mirror, pdt, (size_t)(r * m + unew[u]));
+                            Mh[u] = 0.0f;
+                            Vh[u] = 0.0f;
+                        }
+                    }
                 }
-        });
-        for (int32_t col : entering) l.th[col] = 0;
+            });
+        std::vector<int32_t> thn(mk, 0);
+        for (int64_t u = 0; u < mk; ++u)
+            if (src[u] >= 0) thn[u] = l.th[src[u]];
+        l.th.swap(thn);
         l.idx_host = nidx[i];
-        l.unsel_host.clear();
-        for (int64_t col = 0; col < m; ++col)
-            if (now_cpu[col]) l.unsel_host.push_back((int32_t)col);
+        l.unsel_host.swap(unew);
         if (!l.unsel_host.empty())
             ZF_CUDA(cudaMemcpy(l.unsel_dev, l.unsel_host.data(), l.unsel_host.size() * sizeof(int32_t),
                                cudaMemcpyHostToDevice));
@@ -196,10 +219,69 @@ zf_status f1_refresh(zf_ctx* c, void* const* params, cudaStream_t s) {
     return ZF_OK;
 }
 
-// At a window end: one AdamW step (O6 op order, double-derived constants rounded once) with
-// the window's average gradient acc/S on the fp32 master of the unselected columns; the
-// rounded results are uploaded and scattered into the parameters.
-zf_status f1_window_end(zf_ctx* c, int64_t t, int buf, int64_t len, void* const* params, cudaStream_t s) {
+// One row of the window update (O6 op order, every operation one IEEE fp32 op; the host
+// build uses -ffp-contract=off, so the vectorised clones keep the rounding of the scalar
+// code: vdivps / vsqrtps are correctly rounded).
+template <int WD, bool BF>
+static inline void f1_row_impl(float* __restrict__ M, float* __restrict__ Mh, float* __restrict__ Vh,
+                               const float* __restrict__ acc, const float* __restrict__ ss,
+                               const float* __restrict__ bc2s, void* __restrict__ out, int64_t mk, float Sf,
+                               float b1, float b2, float omb1, float omb2, float eps, float wd_f, float decay) {
+    for (int64_t u = 0; u < mk; ++u) {
+        float g = acc[u] / Sf;
+        float p = M[u];
+        float mm = Mh[u], vv = Vh[u];
+        if (WD == 1) p = p * decay;
+        if (WD == 2) {
+            const float wp = wd_f * p;
+            g = g + wp;
+        }
+        const float a1 = b1 * mm, a2 = omb1 * g;
+        mm = a1 + a2;
+        const float c1 = b2 * vv, c2 = omb2 * g, c3 = c2 * g;
+        vv = c1 + c3;
+        const float den = std::sqrt(vv) / bc2s[u] + eps;
+        const float upd = mm / den;
+        const float delta = ss[u] * upd;
+        p = p - delta;
+        M[u] = p;
+        Mh[u] = mm;
+        Vh[u] = vv;
+        if (BF) {
+            uint32_t x;
+            std::memcpy(&x, &p, 4);
+            const uint32_t rne = (x + 0x7fffu + ((x >> 16) & 1u)) >> 16;
+            const uint32_t nan = (x >> 16) | 0x40u;
+            static_cast<uint16_t*>(out)[u] = (uint16_t)(((x & 0x7fffffffu) > 0x7f800000u) ? nan : rne);
+        } else {
+            static_cast<float*>(out)[u] = p;
+        }
+    }
+}
+
+__attribute__((target_clones("avx512f", "avx2", "default")))
+void f1_row(int wd_mode, bool bf, float* M, float* Mh, float* Vh, const float* acc, const float* ss,
+            const float* bc2s, void* out, int64_t mk, float Sf, float b1, float b2, float omb1, float omb2, float eps,
+            float wd_f, float decay) {
+#define ZF_F1_ROW(W, B) f1_row_impl<W, B>(M, Mh, Vh, acc, ss, bc2s, out, mk, Sf, b1, b2, omb1, omb2, eps, wd_f, decay)
+    if (bf) {
+        if (wd_mode == 0) ZF_F1_ROW(0, true);
+        else if (wd_mode == 1) ZF_F1_ROW(1, true);
+        else ZF_F1_ROW(2, true);
+    } else {
+        if (wd_mode == 0) ZF_F1_ROW(0, false);
+        else if (wd_mode == 1) ZF_F1_ROW(1, false);
+        else ZF_F1_ROW(2, false);
+    }
+#undef ZF_F1_ROW
+}
+
+// The host half: one AdamW step of every unselected column from the sealed window `buf` of
+// `len` steps (waits for that window's accumulation first); results in the pinned p_up
+// blocks and the host master/moments.  Runs on the caller's thread (sync) or on the f1
+// worker thread (cpu_update_async, reading R23).
+zf_status f1_compute(zf_ctx* c, int64_t t, int buf, int64_t len, double lr) {
+    if (c->f1_up_ev) ZF_CUDA(cudaEventSynchronize(c->f1_up_ev));  // the previous upload read p_up
     if (c->devacc) {
         ZF_CUDA(cudaEventSynchronize(c->acc_d2h_ev[buf]));  // the sealed window's host copy
     } else {
@@ -207,7 +289,7 @@ zf_status f1_window_end(zf_ctx* c, int64_t t, int buf, int64_t len, void* const*
         c->cv.wait(lk, [&] { return c->h1_done >= t; });
     }
     const zf_adam_params& hp = c->cfg.adam;
-    const double lr = c->lr_cur, b1d = hp.beta1, b2d = hp.beta2;
+    const double b1d = hp.beta1, b2d = hp.beta2;
     const float b1 = (float)b1d, b2 = (float)b2d, omb1 = (float)(1.0 - b1d), omb2 = (float)(1.0 - b2d);
     const float eps = (float)hp.eps, wd_f = (float)hp.weight_decay, decay = (float)(1.0 - lr * hp.weight_decay);
     const int wd_mode = hp.weight_decay == 0.0 ? 0 : (hp.decoupled ? 1 : 2);
@@ -220,46 +302,68 @@ zf_status f1_window_end(zf_ctx* c, int64_t t, int buf, int64_t len, void* const*
         const float* acc = c->devacc ? l.acc_sealed_h : l.acc[buf];
         std::vector<float> ss(mk), bc2s(mk);
         for (int64_t u = 0; u < mk; ++u) {
-            const double tt = (double)(l.th[l.unsel_host[u]] + 1);
+            const double tt = (double)(l.th[u] + 1);
             ss[u] = (float)(lr / (1.0 - std::pow(b1d, tt)));
             bc2s[u] = (float)std::sqrt(1.0 - std::pow(b2d, tt));
         }
-        const int pdt = c->pdt;
+        const bool bf = c->pdt == ZF_BF16;
         c->pool->parallel_for(n, [&](int64_t b, int64_t e) {
-            for (int64_t r = b; r < e; ++r) {
-                for (int64_t u = 0; u < mk; ++u) {
-                    const int64_t col = l.unsel_host[u];
-                    float g = acc[r * mk + u] / Sf;
-                    float p = l.master[r * m + col];
-                    float mm = l.mh[r * m + col], vv = l.vh[r * m + col];
-                    if (wd_mode == 1) p = p * decay;
-                    else if (wd_mode == 2) {
-                        const float wp = wd_f * p;
-                        g = g + wp;
-                    }
-                    const float a1 = b1 * mm, a2 = omb1 * g;
-                    mm = a1 + a2;
-                    const float c1 = b2 * vv, c2 = omb2 * g, c3 = c2 * g;
-                    vv = c1 + c3;
-                    const float den = std::sqrt(vv) / bc2s[u] + eps;
-                    const float upd = mm / den;
-                    const float delta = ss[u] * upd;
-                    p = p - delta;
-                    l.master[r * m + col] = p;
-                    l.mh[r * m + col] = mm;
-                    l.vh[r * m + col] = vv;
-                    if (pdt == ZF_BF16) static_cast<uint16_t*>(l.p_up)[r * mk + u] = host_bf16_rne(p);
-                    else static_cast<float*>(l.p_up)[r * mk + u] = p;
-                }
-            }
+            for (int64_t r = b; r < e; ++r)
+                f1_row(wd_mode, bf, l.master + r * mk, l.mh + r * mk, l.vh + r * mk, acc + r * mk, ss.data(),
+                       bc2s.data(), static_cast<unsigned char*>(l.p_up) + (size_t)r * mk * c->psz, mk, Sf, b1, b2, omb1,
+                       omb2, eps, wd_f, decay);
         });
-        for (int64_t u = 0; u < mk; ++u) l.th[l.unsel_host[u]] += 1;
+        for (int64_t u = 0; u < mk; ++u) l.th[u] += 1;
+    }
+    return ZF_OK;
+}
+
+// The device half: upload every layer's p_up block and scatter it into the parameter's
+// unselected columns (K5), on stream s; f1_up_ev marks when p_up may be rewritten.
+zf_status f1_apply(zf_ctx* c, void* const* params, cudaStream_t s) {
+    for (size_t i = 0; i < c->L.size(); ++i) {
+        LayerState& l = c->L[i];
+        const int64_t n = l.d.n, mk = l.mk;
+        if (mk == 0 || n == 0) continue;
         ZF_CUDA(cudaMemcpyAsync(l.p_up_dev, l.p_up, (size_t)n * mk * c->psz, cudaMemcpyHostToDevice, s));
-        ZF_CUDA(launch_scatter_unselected(params[i], pdt, l.d.ld_param, n, mk, l.unsel_dev, l.p_up_dev, s));
+        ZF_CUDA(launch_scatter_unselected(params[i], c->pdt, l.d.ld_param, n, mk, l.unsel_dev, l.p_up_dev, s));
         c->launches++;
     }
-    ZF_CUDA(cudaStreamSynchronize(s));  // pinned upload buffers are reused next window
+    if (!c->f1_up_ev) ZF_CUDA(cudaEventCreateWithFlags(&c->f1_up_ev, cudaEventDisableTiming));
+    ZF_CUDA(cudaEventRecord(c->f1_up_ev, s));
     return ZF_OK;
+}
+
+// Synchronous window end (reading R18): compute, apply, and wait.
+zf_status f1_window_end(zf_ctx* c, int64_t t, int buf, int64_t len, void* const* params, cudaStream_t s) {
+    ZF_TRY(f1_compute(c, t, buf, len, c->lr_cur));
+    ZF_TRY(f1_apply(c, params, s));
+    ZF_CUDA(cudaStreamSynchronize(s));
+    return ZF_OK;
+}
+
+// cpu_update_async (reading R23): start the host half on the worker thread and return; the
+// update is applied by f1_finish at the start of the next zf_step (or in zf_sync).
+zf_status f1_launch(zf_ctx* c, int64_t t, int buf, int64_t len, void* const* params) {
+    c->f1_params.assign(params, params + c->L.size());
+    c->f1_status = ZF_OK;
+    const double lr = c->lr_cur;
+    c->f1_worker = std::thread([c, t, buf, len, lr] {
+        cudaSetDevice(c->device);
+        const zf_status st = f1_compute(c, t, buf, len, lr);
+        c->f1_status = st;
+        if (st != ZF_OK) c->f1_error = g_last_error;
+    });
+    c->f1_pending = true;
+    return ZF_OK;
+}
+
+zf_status f1_finish(zf_ctx* c, cudaStream_t s) {
+    if (!c->f1_pending) return ZF_OK;
+    c->f1_worker.join();
+    c->f1_pending = false;
+    if (c->f1_status != ZF_OK) return fail(c->f1_status, "deferred CPU update: %s", c->f1_error.c_str());
+    return f1_apply(c, c->f1_params.data(), s);
 }
 
 }  // namespace zfh

@@ -344,10 +344,12 @@ struct LayerState {
     int64_t unit_begin = 0;
     cudaEvent_t d2h_ev[2] = {nullptr, nullptr};
     // f1: deferred CPU AdamW (reading R18)
-    float* master = nullptr;          // [n, m] fp32 host master (valid on CPU-updated columns)
-    float* mh = nullptr;              // [n, m] host moments
+    // dense over the current unselected columns (position u = column unsel_host[u]), remapped
+    // at every refresh: the window update is then a contiguous, vectorised row loop
+    float* master = nullptr;          // [n, m-k] fp32 host master of the CPU-updated columns
+    float* mh = nullptr;              // [n, m-k] host moments
     float* vh = nullptr;
-    std::vector<int32_t> th;          // [m] host step count per column
+    std::vector<int32_t> th;          // [m-k] host step count per unselected column
     std::vector<int32_t> idx_host;    // current selection (ascending), host copy
     std::vector<int32_t> unsel_host;  // its complement (ascending)
     void* p_mirror = nullptr;         // pinned [n, m] copy of p at a refresh
@@ -514,6 +516,13 @@ struct zf_ctx {
     std::vector<double> log_A, log_i, log_u;
     // the same windows as zf_step sees them (f1 updates at window ends)
     int64_t mw = 0, mw_len = 0;
+    // f1 host update: upload-done event; cpu_update_async worker (reading R23)
+    cudaEvent_t f1_up_ev = nullptr;
+    std::thread f1_worker;
+    bool f1_pending = false;
+    zf_status f1_status = ZF_OK;
+    std::string f1_error;
+    std::vector<void*> f1_params;
     // f2 Zen-auto (reading R21): K6 tables per current set, device state, decision records
     bool autoz = false;
     AutoLayer* d_auto_tab[2] = {nullptr, nullptr};
@@ -609,4 +618,6 @@ void acc_row_bf16(float* acc, const uint16_t* src, int64_t n, bool first);
 void acc_row_f32(float* acc, const float* src, int64_t n, bool first);
 zf_status f1_refresh(zf_ctx* c, void* const* params, cudaStream_t s);
 zf_status f1_window_end(zf_ctx* c, int64_t t, int buf, int64_t len, void* const* params, cudaStream_t s);
+zf_status f1_launch(zf_ctx* c, int64_t t, int buf, int64_t len, void* const* params);
+zf_status f1_finish(zf_ctx* c, cudaStream_t s);
 }  // namespace zfh

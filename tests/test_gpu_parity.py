@@ -180,12 +180,14 @@ def test_compact_into_pinned_host(zf, orc, gpu, n, m, dt):
 
 # ------------------------------------------------------------------ zf_step vs oracle, multi-step
 def _run_stateful(zf, orc, gpu, shapes, gdt, pdt, ppm, N, S, steps, offload, lr=1e-3, wd=0.0, check_every=1,
-                  tie=False, ld_pad=0, cpu_update=False, warmup=0, state_offload=False, devacc=False):
+                  tie=False, ld_pad=0, cpu_update=False, warmup=0, state_offload=False, devacc=False,
+                  cpu_async=False):
     hp_o = orc.AdamHP(lr=lr, weight_decay=wd)
     ctx = zf.Context([zf.LayerShape(n, m, m + ld_pad, m + ld_pad) for n, m in shapes], grad_dtype=TDT[gdt],
                      param_dtype=TDT[pdt], topk_ratio_ppm=ppm, refresh_interval=N, accum_interval=S,
                      adam=zf.adam_params(lr=lr, weight_decay=wd), offload=offload, host_accumulate=offload, cpu_update=cpu_update,
-                     warmup_steps=warmup, state_offload=state_offload, device_accumulate=devacc)
+                     warmup_steps=warmup, state_offload=state_offload, device_accumulate=devacc,
+                     cpu_update_async=cpu_async)
     scales = [gpu.ColScale(m, li) for li, (n, m) in enumerate(shapes)]
     Gs = [torch.empty(n, m + ld_pad, dtype=TDT[gdt], device="cuda")[:, :m] for n, m in shapes]
     Ps = [torch.empty(n, m + ld_pad, dtype=TDT[pdt], device="cuda")[:, :m] for n, m in shapes]
@@ -334,6 +336,35 @@ def test_zen_auto_gpu_spec_worked_example(zf):
     assert [t for (t, e, *_r) in log if e] == [3, 7, 11, 15]
     for t, e, A, i, u in log:
         assert abs(u / i - 0.25) < 1e-6 and abs(A - ((t % 4) + 1) * u) <= 1e-9 * A
+
+
+@pytest.mark.parametrize("NS,pdt,devacc", [(2, "bf16", False), (4, "fp32", True), (1, "bf16", True)])
+def test_step_cpu_update_async(zf, orc, gpu, NS, pdt, devacc):
+    """R23: the window-end CPU AdamW runs on a worker thread and lands at the next zf_step /
+    zf_sync -- after every zf_sync the state is bit-exact with the oracle's synchronous f1."""
+    gdt = "bf16" if pdt == "bf16" else "fp32"
+    _run_stateful(zf, orc, gpu, [(256, 512), (37, 1001)], gdt, pdt, 100000, NS, NS, 9, offload=True,
+                  cpu_update=True, cpu_async=True, devacc=devacc)
+
+
+def test_cpu_update_async_is_stale_until_the_next_call(zf, gpu):
+    """Between a window's last zf_step and the next call, the unselected columns still hold
+    their pre-update values (the one-window staleness of the overlapped update); the next
+    zf_step applies the update before anything else."""
+    n, m = 64, 512
+    ctx = zf.Context([zf.LayerShape(n, m)], topk_ratio_ppm=100000, refresh_interval=2, accum_interval=2,
+                     offload=True, host_accumulate=True, cpu_update=True, cpu_update_async=True)
+    G = _grad(gpu, n, m, "bf16")
+    P = torch.zeros(n, m, dtype=torch.bfloat16, device="cuda")
+    ctx.step(0, [G], [P])
+    ctx.step(1, [G], [P])                      # window end: CPU update launched, not applied
+    torch.cuda.synchronize()
+    unsel = torch.ones(m, dtype=torch.bool, device="cuda")
+    unsel[ctx.selected(0).long()] = False
+    assert torch.all(P[:, unsel] == 0)
+    ctx.sync()                                 # lands the update
+    assert torch.count_nonzero(P[:, unsel]) > 0
+    ctx.close()
 
 
 def test_cpu_update_needs_aligned_windows(zf):
