@@ -17,7 +17,34 @@ __global__ void k_scatter(B* __restrict__ P, int64_t ldp, int64_t n, int64_t mk,
     }
 }
 
+// K5': the gather the other way (f1 refresh): buf[i][e] = P[i][cols[e]], the columns
+// entering the CPU-updated set, so only they cross the host link.
+template <typename B>
+__global__ void k_gather(const B* __restrict__ P, int64_t ldp, int64_t n, int64_t nc, const int32_t* __restrict__ cols,
+                         B* __restrict__ buf) {
+    const int64_t total = n * nc;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = q / nc, e = q - i * nc;
+        buf[q] = P[i * ldp + __ldg(cols + e)];
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_gather_columns(const void* P, int pdt, int64_t ldp, int64_t n, int64_t nc, const int32_t* cols,
+                                  void* buf, cudaStream_t s) {
+    const int64_t total = n * nc;
+    if (total <= 0) return cudaSuccess;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > NUM_SMS_B200 * 16) blocks = NUM_SMS_B200 * 16;
+    if (pdt == DT_BF16)
+        k_gather<uint16_t><<<(unsigned)blocks, 256, 0, s>>>(static_cast<const uint16_t*>(P), ldp, n, nc, cols,
+                                                            static_cast<uint16_t*>(buf));
+    else
+        k_gather<uint32_t><<<(unsigned)blocks, 256, 0, s>>>(static_cast<const uint32_t*>(P), ldp, n, nc, cols,
+                                                            static_cast<uint32_t*>(buf));
+    return cudaGetLastError();
+}
 
 cudaError_t launch_scatter_unselected(void* P, int pdt, int64_t ldp, int64_t n, int64_t mk, const int32_t* unsel,
                                       const void* buf, cudaStream_t s) {

@@ -449,7 +449,8 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
                         *pp = q;
                     }
                     l.th.assign(l.mk, 0);
-                    ZF_CUDA(cudaHostAlloc(&l.p_mirror, std::max<size_t>(nm * c->psz, 64), cudaHostAllocDefault));
+                    (void)nm;
+                    ZF_CUDA(cudaHostAlloc(&l.p_mirror, std::max<size_t>(nmk * c->psz, 64), cudaHostAllocDefault));
                     c->host_pinned.push_back(l.p_mirror);
                     ZF_CUDA(cudaHostAlloc(&l.p_up, std::max<size_t>((size_t)l.d.n * l.mk * c->psz, 64),
                                           cudaHostAllocDefault));

@@ -159,28 +159,45 @@ zf_status f1_refresh(zf_ctx* c, void* const* params, cudaStream_t s) {
         LayerState& l = c->L[i];
         nidx[i].resize(l.k);
         ZF_CUDA(cudaMemcpyAsync(nidx[i].data(), l.idx[c->cur], l.k * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-        if (l.d.n > 0)
-        ZF_CUDA(cudaMemcpy2DAsync(l.p_mirror, l.d.m * c->psz, params[i], l.d.ld_param * c->psz, l.d.m * c->psz, l.d.n,
-                                  cudaMemcpyDeviceToHost, s));
     }
     ZF_CUDA(cudaStreamSynchronize(s));
+    // new unselected lists, the retained columns' old positions, and the entering columns,
+    // whose current parameter values are gathered on the device and read back (K5')
+    std::vector<std::vector<int32_t>> unew(nl), src(nl), ent(nl);
     for (int i = 0; i < nl; ++i) {
         LayerState& l = c->L[i];
-        const int64_t m = l.d.m, n = l.d.n, mk = l.mk;
+        const int64_t m = l.d.m, mk = l.mk;
         std::vector<char> now_cpu(m, 1);
         for (int32_t col : nidx[i]) now_cpu[col] = 0;
-        std::vector<int32_t> unew;
-        unew.reserve(mk);
+        unew[i].reserve(mk);
         for (int64_t col = 0; col < m; ++col)
-            if (now_cpu[col]) unew.push_back((int32_t)col);
-        // src[u] = position of column unew[u] in the old unselected list (retained), or -1
-        // (entering: was selected, or the first refresh) -- both lists ascending
+            if (now_cpu[col]) unew[i].push_back((int32_t)col);
+        // src[u] = position of column unew[u] in the old unselected list (retained), or
+        // -(1 + e) for the e-th entering column (was selected, or the first refresh)
         const std::vector<int32_t>& uold = l.unsel_host;
-        std::vector<int32_t> src(mk, -1);
-        for (size_t u = 0, v = 0; u < unew.size(); ++u) {
-            while (v < uold.size() && uold[v] < unew[u]) ++v;
-            if (v < uold.size() && uold[v] == unew[u]) src[u] = (int32_t)v;
+        src[i].assign(mk, 0);
+        for (size_t u = 0, v = 0; u < unew[i].size(); ++u) {
+            while (v < uold.size() && uold[v] < unew[i][u]) ++v;
+            if (v < uold.size() && uold[v] == unew[i][u]) {
+                src[i][u] = (int32_t)v;
+            } else {
+                src[i][u] = -1 - (int32_t)ent[i].size();
+                ent[i].push_back(unew[i][u]);
+            }
         }
+        const int64_t ne = (int64_t)ent[i].size();
+        if (ne > 0 && l.d.n > 0) {
+            ZF_CUDA(cudaMemcpy(l.unsel_dev, ent[i].data(), ne * sizeof(int32_t), cudaMemcpyHostToDevice));
+            ZF_CUDA(launch_gather_columns(params[i], c->pdt, l.d.ld_param, l.d.n, ne, l.unsel_dev, l.p_up_dev, s));
+            c->launches++;
+            ZF_CUDA(cudaMemcpyAsync(l.p_mirror, l.p_up_dev, (size_t)l.d.n * ne * c->psz, cudaMemcpyDeviceToHost, s));
+            ZF_CUDA(cudaStreamSynchronize(s));  // unsel_dev / p_up_dev are reused by the next layer
+        }
+    }
+    for (int i = 0; i < nl; ++i) {
+        LayerState& l = c->L[i];
+        const int64_t n = l.d.n, mk = l.mk, ne = (int64_t)ent[i].size();
+        const std::vector<int32_t>& sr = src[i];
         const int pdt = c->pdt;
         if (mk > 0)
             c->pool->parallel_for(n, [&](int64_t b, int64_t e) {
@@ -193,13 +210,13 @@ zf_status f1_refresh(zf_ctx* c, void* const* params, cudaStream_t s) {
                     std::memcpy(tmp.data() + mk, Mh, mk * sizeof(float));
                     std::memcpy(tmp.data() + 2 * mk, Vh, mk * sizeof(float));
                     for (int64_t u = 0; u < mk; ++u) {
-                        const int32_t v = src[u];
+                        const int32_t v = sr[u];
                         if (v >= 0) {  // retained: keeps its master, moments
                             M[u] = tmp[v];
                             Mh[u] = tmp[mk + v];
                             Vh[u] = tmp[2 * mk + v];
                         } else {       // entering: the parameter's current value, zero moments
-                            M[u] = host_widen(l.p_mirror, pdt, (size_t)(r * m + unew[u]));
+                            M[u] = host_widen(l.p_mirror, pdt, (size_t)(r * ne + (-1 - v)));
                             Mh[u] = 0.0f;
                             Vh[u] = 0.0f;
                         }
@@ -208,10 +225,10 @@ zf_status f1_refresh(zf_ctx* c, void* const* params, cudaStream_t s) {
             });
         std::vector<int32_t> thn(mk, 0);
         for (int64_t u = 0; u < mk; ++u)
-            if (src[u] >= 0) thn[u] = l.th[src[u]];
+            if (sr[u] >= 0) thn[u] = l.th[sr[u]];
         l.th.swap(thn);
         l.idx_host = nidx[i];
-        l.unsel_host.swap(unew);
+        l.unsel_host.swap(unew[i]);
         if (!l.unsel_host.empty())
             ZF_CUDA(cudaMemcpy(l.unsel_dev, l.unsel_host.data(), l.unsel_host.size() * sizeof(int32_t),
                                cudaMemcpyHostToDevice));

@@ -352,7 +352,7 @@ struct LayerState {
     std::vector<int32_t> th;          // [m-k] host step count per unselected column
     std::vector<int32_t> idx_host;    // current selection (ascending), host copy
     std::vector<int32_t> unsel_host;  // its complement (ascending)
-    void* p_mirror = nullptr;         // pinned [n, m] copy of p at a refresh
+    void* p_mirror = nullptr;         // pinned [n, <= m-k]: the entering columns of p at a refresh
     void* p_up = nullptr;             // pinned [n, m-k] updated unselected params
     void* p_up_dev = nullptr;         // device [n, m-k]
     int32_t* unsel_dev = nullptr;     // device [m-k]
