@@ -199,27 +199,44 @@ zf_status f1_refresh(zf_ctx* c, void* const* params, cudaStream_t s) {
         const int64_t n = l.d.n, mk = l.mk, ne = (int64_t)ent[i].size();
         const std::vector<int32_t>& sr = src[i];
         const int pdt = c->pdt;
+        // runs of consecutive retained positions (u0, v0, len) move with memmove; entering
+        // positions are filled from the gathered parameter values
+        struct Run { int64_t u0, v0, len; };
+        std::vector<Run> runs;
+        std::vector<int64_t> enter_pos;
+        for (int64_t u = 0; u < mk; ++u) {
+            const int32_t v = sr[u];
+            if (v < 0) {
+                enter_pos.push_back(u);
+            } else if (!runs.empty() && runs.back().u0 + runs.back().len == u && runs.back().v0 + runs.back().len == v) {
+                ++runs.back().len;
+            } else {
+                runs.push_back({u, (int64_t)v, 1});
+            }
+        }
+        // retained columns only move toward lower positions or stay (both lists ascending,
+        // the new one drops old columns before adding), so an in-place forward pass is safe
+        // for runs with u0 <= v0; runs moving up are copied from a row snapshot
+        bool all_down = true;
+        for (const Run& q : runs) all_down = all_down && q.u0 <= q.v0;
         if (mk > 0)
             c->pool->parallel_for(n, [&](int64_t b, int64_t e) {
-                std::vector<float> tmp(3 * (size_t)mk);
+                std::vector<float> tmp(all_down ? 0 : 3 * (size_t)mk);
                 for (int64_t r = b; r < e; ++r) {
-                    float* M = l.master + r * mk;
-                    float* Mh = l.mh + r * mk;
-                    float* Vh = l.vh + r * mk;
-                    std::memcpy(tmp.data(), M, mk * sizeof(float));
-                    std::memcpy(tmp.data() + mk, Mh, mk * sizeof(float));
-                    std::memcpy(tmp.data() + 2 * mk, Vh, mk * sizeof(float));
-                    for (int64_t u = 0; u < mk; ++u) {
-                        const int32_t v = sr[u];
-                        if (v >= 0) {  // retained: keeps its master, moments
-                            M[u] = tmp[v];
-                            Mh[u] = tmp[mk + v];
-                            Vh[u] = tmp[2 * mk + v];
-                        } else {       // entering: the parameter's current value, zero moments
-                            M[u] = host_widen(l.p_mirror, pdt, (size_t)(r * ne + (-1 - v)));
-                            Mh[u] = 0.0f;
-                            Vh[u] = 0.0f;
-                        }
+                    float* A3[3] = {l.master + r * mk, l.mh + r * mk, l.vh + r * mk};
+                    if (all_down) {
+                        for (const Run& q : runs)
+                            for (float* A : A3) std::memmove(A + q.u0, A + q.v0, q.len * sizeof(float));
+                    } else {
+                        for (int a = 0; a < 3; ++a) std::memcpy(tmp.data() + a * mk, A3[a], mk * sizeof(float));
+                        for (const Run& q : runs)
+                            for (int a = 0; a < 3; ++a)
+                                std::memcpy(A3[a] + q.u0, tmp.data() + a * mk + q.v0, q.len * sizeof(float));
+                    }
+                    for (int64_t u : enter_pos) {  // entering: the parameter's value, zero moments
+                        A3[0][u] = host_widen(l.p_mirror, pdt, (size_t)(r * ne + (-1 - sr[u])));
+                        A3[1][u] = 0.0f;
+                        A3[2][u] = 0.0f;
                     }
                 }
             });
