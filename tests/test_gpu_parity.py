@@ -368,6 +368,64 @@ def test_cpu_update_async_is_stale_until_the_next_call(zf, gpu):
     ctx.close()
 
 
+def test_step_lr_schedule(zf, orc, gpu):
+    """zf_set_lr (a schedule): the bias-corrected step size of the next step uses the
+    new lr, on the GPU (K3) and in the deferred CPU update; bit-exact vs the oracle run with
+    the same per-step lr (decoupled weight decay uses it too)."""
+    shapes = [(64, 512), (37, 1001)]
+    hp = orc.AdamHP(lr=1e-3, weight_decay=0.01)
+    ctx = zf.Context([zf.LayerShape(n, m) for n, m in shapes], grad_dtype=torch.bfloat16, param_dtype=torch.float32,
+                     topk_ratio_ppm=100000, refresh_interval=2, accum_interval=2,
+                     adam=zf.adam_params(lr=1e-3, weight_decay=0.01), offload=True, host_accumulate=True,
+                     cpu_update=True)
+    scales = [gpu.ColScale(m, li) for li, (n, m) in enumerate(shapes)]
+    Gs = [torch.empty(n, m, dtype=torch.bfloat16, device="cuda") for n, m in shapes]
+    Ps = [torch.empty(n, m, dtype=torch.float32, device="cuda") for n, m in shapes]
+    for li, P in enumerate(Ps):
+        gpu.fill_param(P, li)
+    layers = [orc.OracleLayer(n=n, m=m, ratio_ppm=100000, refresh_interval=2, accum_interval=2, hp=hp,
+                              cpu_update=True) for n, m in shapes]
+    Po = [to_np(P) for P in Ps]
+    for t in range(6):
+        lr = 1e-3 * (0.5 ** t)
+        ctx.set_lr(lr)
+        hp.lr = lr
+        for li, (G, sc) in enumerate(zip(Gs, scales)):
+            sc.advance_to(t)
+            gpu.fill_grad(G, li, t, sc)
+        ctx.step(t, Gs, Ps)
+        ctx.sync()
+        for li, L in enumerate(layers):
+            gidx = to_np(ctx.selected(li))
+            L.step(t, to_np(Gs[li]), Po[li], idx_override=gidx if t % 2 == 0 else None)
+            assert_bits_equal(to_np(Ps[li]), Po[li], f"params t={t} l={li}")
+    ctx.close()
+
+
+def test_profile_phases(zf, gpu):
+    """zf_profile / zf_profile_read: per-phase event timings and counts (K1 and K2 on refresh
+    steps, K3 every step, the per-step D2H span with offload; K7 and the window D2H with
+    device accumulation)."""
+    G = _grad(gpu, 256, 512, "bf16")
+    P = torch.zeros(256, 512, dtype=torch.bfloat16, device="cuda")
+    for devacc in (False, True):
+        ctx = zf.Context([zf.LayerShape(256, 512)], topk_ratio_ppm=100000, refresh_interval=2, accum_interval=2,
+                         offload=True, host_accumulate=True, device_accumulate=devacc)
+        ctx.profile(True)
+        for t in range(4):
+            ctx.step(t, [G], [P])
+        ctx.sync()
+        prof = ctx.profile_read()
+        ctx.close()
+        assert prof["k1_norms"][1] == 2 and prof["k2_topk"][1] == 2 and prof["k3_update"][1] == 4
+        assert prof["allreduce"][1] == 0
+        if devacc:
+            assert prof["k7_accumulate"][1] == 4 and prof["d2h_window"][1] == 2 and prof["d2h_step"][1] == 0
+        else:
+            assert prof["d2h_step"][1] == 4 and prof["k7_accumulate"][1] == 0
+        assert all(ms >= 0.0 for ms, _n in prof.values()) and prof["k3_update"][0] > 0.0
+
+
 def test_cpu_update_needs_aligned_windows(zf):
     with pytest.raises(zf.ZFError):
         zf.Context([zf.LayerShape(8, 64)], refresh_interval=2, accum_interval=4, offload=True, host_accumulate=True,
