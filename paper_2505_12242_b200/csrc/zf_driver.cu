@@ -479,6 +479,15 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
         if (r != ncclSuccess) return bail(fail(ZF_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r)));
     }
     ZF_CUDA(cudaDeviceSynchronize());
+    {
+        // leave room for kernel launches (local memory, launch resources): a context that
+        // fills HBM to the brim would fail at its first zf_step instead of here
+        size_t fr = 0, tot = 0;
+        ZF_CUDA(cudaMemGetInfo(&fr, &tot));
+        if (fr < ((size_t)256 << 20))
+            return bail(fail(ZF_ENOMEM, "device memory nearly exhausted after allocating the context (%zu MB free)",
+                             fr >> 20));
+    }
     *out = c;
     return ZF_OK;
 #undef ZF_CTRY

@@ -45,11 +45,16 @@ inline zf_status fail(zf_status st, const char* fmt, ...) {
     return st;
 }
 
+// A failed runtime call is reported once: the thread's last-error state is reset so a
+// later launch check (cudaGetLastError) does not report it again (e.g. an out-of-memory
+// zf_create followed by a successful one).
 #define ZF_CUDA(call)                                                                                       \
     do {                                                                                                    \
         cudaError_t e_ = (call);                                                                            \
-        if (e_ != cudaSuccess) return fail(ZF_ECUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call,             \
-                                            cudaGetErrorString(e_));                                        \
+        if (e_ != cudaSuccess) {                                                                            \
+            (void)cudaGetLastError();                                                                       \
+            return fail(ZF_ECUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_));       \
+        }                                                                                                   \
     } while (0)
 
 #define ZF_NCCL(call)                                                                                       \
