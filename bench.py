@@ -320,6 +320,14 @@ def run_zenflow(args, rank, world):
         "gpu_launches": launches,
         "clocks": clk,
     }
+    if world > 1 and prof["allreduce"][1]:
+        # row a2 on NVLink: the flat fp32 norm vector, once per refresh (nccl-tests conventions)
+        ar_bytes = 4 * sum(m for _n, m in full_shapes)
+        ar_avg = ar_ms / prof["allreduce"][1]
+        algbw = ar_bytes / (ar_avg * 1e-3) / 1e9
+        result["nvlink_allreduce"] = {"bytes": ar_bytes, "ms": ar_avg, "algbw_GBs": algbw,
+                                      "busbw_GBs": algbw * 2 * (world - 1) / world,
+                                      "peak_GBs_per_direction": 900.0}
     achieved = alg / (k3_avg * 1e-3) / 1e9
     result["roofline"] = {"bound": "hbm", "kernel": "k_update (K3 fused selective AdamW + compaction)",
                           "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
