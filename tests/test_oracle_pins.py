@@ -386,6 +386,31 @@ def test_remap_retained_entering_leaving(orc):
     assert M.tolist() == [[2, 0], [4, 0]] and V.tolist() == [[20, 0], [40, 0]] and st.tolist() == [7, 0]
 
 
+def test_remap_entering_column_restarts_from_the_step1_closed_form(orc):
+    """R7 on whole steps, against closed forms: a column that enters the selection at a
+    refresh starts AdamW from zero moments and step count, so its first GPU update is the
+    bias-corrected step-1 move p - lr*g/(|g|+eps); a column that leaves and re-enters later
+    restarts the same way; a retained column continues its sequence (step 2 from a constant
+    g is again -lr*g/(|g|+eps), m_hat = g, v_hat = g^2)."""
+    n, m, lr, eps = 3, 10, 1e-3, 1e-8
+    L = orc.OracleLayer(n=n, m=m, ratio_ppm=100000, refresh_interval=2, accum_interval=2, hp=orc.AdamHP(lr=lr))
+    P = np.zeros((n, m), np.float32)
+
+    def G_top(col, g=0.5):
+        G = np.full((n, m), 0.01, np.float32)
+        G[:, col] = g
+        return G
+
+    for t, top in enumerate([2, 2, 7, 7, 2, 2]):   # column 2, then 7 (entering), then 2 again (re-entering)
+        before = P.copy()
+        L.step(t, G_top(top), P)
+        assert L.idx.tolist() == [top]
+        d = P[:, top] - before[:, top]
+        want = -lr * 0.5 / (0.5 + eps)
+        assert np.allclose(d, want, rtol=1e-6), (t, d, want)    # step 1 (entering) and step 2 (retained)
+        assert L.steps.tolist() == [1 + t % 2]                   # the step count restarts at each entry
+
+
 # ------------------------------------------------------------------ O8  accumulation
 def test_accumulate_constant_dyadic_stream(orc):
     # dyadic values: fp32 sums are exact, so after S steps acc = S * g exactly
