@@ -163,10 +163,12 @@ void oracle_column_map(const int32_t* idx, int64_t k, int64_t m, int32_t* slot, 
         if (slot[j] < 0) upos[j] = u++;
 }
 
-/* O5  Refresh remap [R7] (paper silent, S:329 -- parity unpinned beyond
- * internal consistency): a column kept across the refresh carries its moments
- * and step count to its new slot; an entering column starts from zero; a
- * leaving column's state is dropped.  M/V are [n, k] row-major. */
+/* O5  Refresh remap [R7] (paper silent): a column kept across the refresh
+ * carries its moments and step count to its new slot; an entering column starts
+ * from zero; a leaving column's state is dropped.  M/V are [n, k] row-major.
+ * Pinned on whole steps by the AdamW closed forms (entering -> step-1 move,
+ * retained -> continued sequence; tests/test_oracle_pins.py); the carry/zero/drop
+ * choice itself is the reading. */
 void oracle_remap(int64_t n,
                   const int32_t* idx_old, int64_t k_old, const float* m_old, const float* v_old,
                   const int32_t* step_old,
