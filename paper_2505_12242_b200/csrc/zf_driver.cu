@@ -587,6 +587,7 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
     if (c->world > 1 && !c->comm && !c->host_allreduce)
         return fail(ZF_ESTATE, "world > 1 needs an NCCL id at zf_create or zf_set_host_allreduce");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    c->last_stream = s;
     ZF_CUDA(cudaSetDevice(c->device));
     // R23: the previous window's CPU update (computed while the caller ran its next forward /
     // backward) lands before this step touches any parameter
@@ -805,8 +806,9 @@ extern "C" zf_status zf_sync(zf_ctx* c) {
     ZF_CUDA(cudaSetDevice(c->device));
     ZF_CUDA(cudaEventSynchronize(c->step_done));
     if (c->f1_pending) {  // R23: land the pending CPU update so the state is complete
-        ZF_TRY(f1_finish(c, c->aux));
-        ZF_CUDA(cudaStreamSynchronize(c->aux));
+        // on the stream of the last zf_step: after whatever the caller queued there since
+        ZF_TRY(f1_finish(c, c->last_stream));
+        ZF_CUDA(cudaStreamSynchronize(c->last_stream));
     }
     if (c->copy_stream) ZF_CUDA(cudaStreamSynchronize(c->copy_stream));
     if (c->cfg.host_accumulate) {

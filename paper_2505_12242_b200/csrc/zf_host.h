@@ -528,6 +528,7 @@ struct zf_ctx {
     zf_status f1_status = ZF_OK;
     std::string f1_error;
     std::vector<void*> f1_params;
+    cudaStream_t last_stream = nullptr;  // stream of the last zf_step
     // f2 Zen-auto (reading R21): K6 tables per current set, device state, decision records
     bool autoz = false;
     AutoLayer* d_auto_tab[2] = {nullptr, nullptr};
