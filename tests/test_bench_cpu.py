@@ -30,3 +30,14 @@ def test_algorithmic_and_sector_bytes():
     import numpy as np
     s = bench.sector_bytes([(8, 64)], [np.arange(0, 64, 16)])   # one column per bf16 sector
     assert s == 8 * 64 * 2 + 8 * 60 * 2 + 8 * 4 * 16 + 8 * 4 * 32 * 2
+
+
+def test_reference_arm_nonzero_rank_exits_quietly():
+    """Under torchrun (N > 1) only rank 0 runs the reference arm; the others exit 0 with no
+    output and no rendezvous."""
+    env = dict(os.environ, RANK="1", WORLD_SIZE="2", LOCAL_RANK="1")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=300, cwd=ROOT,
+                       env=env)
+    assert r.returncode == 0, r.stderr
+    assert r.stdout.strip() == ""
