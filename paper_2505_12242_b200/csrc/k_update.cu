@@ -233,6 +233,7 @@ __device__ __forceinline__ void adam_unit(const StageInfo& si, unsigned char* A,
     PB* gP = static_cast<PB*>(si.P);
     const int64_t ldp = si.ldp;
     const int tdelta = prm.step_delta + 1;
+    uint32_t dbg_sink = 0;
     int sl, rg, nrg;
     if (ns >= NCT) {
         sl = ctid; rg = 0; nrg = 1;
@@ -289,10 +290,15 @@ __device__ __forceinline__ void adam_unit(const StageInfo& si, unsigned char* A,
             }
             adamw_elem_t(GE::to_f(gb), p, mm, vv, sb.x, sb.y, prm.adam);
             *pp = PE::from_f(p);
-            __stcs(mo + r * k, mm);
-            __stcs(vo + r * k, vv);
+            if (prm.debug_mode != 7) {
+                __stcs(mo + r * k, mm);
+                __stcs(vo + r * k, vv);
+            } else {
+                dbg_sink ^= __float_as_uint(mm) ^ __float_as_uint(vv);
+            }
         }
     }
+    asm volatile("" ::"r"(dbg_sink));  // debug mode 7 keeps the moment math live
 }
 
 template <int GDT, int PDT>
@@ -457,6 +463,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
     const int grp = cwa / K3_GW;               // consumer group
     const int cw = cwa - grp * K3_GW;          // warp index within the group
     const int ctid = cw * 32 + lane;
+    uint32_t dbg_sink = 0;             // debug mode 7 keeps the gathers live
     uint32_t nfacc = 0;                // non-finite detector (exponent all-ones -> carry into the top bit)
     __nv_bfloat162 nf2 = __float2bfloat162_rn(0.0f);  // bf16: NaN-propagating max of |x|
     uint32_t finished = 0, phase = 0;  // per stage: end sentinel seen / mbarrier parity
@@ -554,7 +561,8 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
                                 nfacc |= ((o.x & 0x7f800000u) + 0x00800000u) | ((o.y & 0x7f800000u) + 0x00800000u) |
                                          ((o.z & 0x7f800000u) + 0x00800000u) | ((o.w & 0x7f800000u) + 0x00800000u);
                             }
-                            st_cs_v4(out + r * old + q, o);
+                            if (prm.debug_mode != 7) st_cs_v4(out + r * old + q, o);
+                            else dbg_sink ^= o.x ^ o.y ^ o.z ^ o.w;  // keep the gather live
                         }
                         w += K3_GW;
                         while (w >= nwin) { w -= nwin; ++r; }
@@ -604,7 +612,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
                 const int cl = (w * 32 + lane) * VP;
                 if (cl < sw) {
                     const uint32_t bits = (smask[cl >> 5] >> (cl & 31)) & ((1u << VP) - 1u);
-                    if (bits) st_v4(gP + r * ldp + cl, lds128(sP + r * sw + cl));
+                    if (bits && prm.debug_mode != 7) st_v4(gP + r * ldp + cl, lds128(sP + r * sw + cl));
                 }
                 w += K3_GW;
                 while (w >= nwin) { w -= nwin; ++r; }
@@ -618,6 +626,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
             if (done) red_release_add(done, 1u);  // per-warp completion count (offload only)
         }
     }
+    asm volatile("" ::"r"(dbg_sink));
     if (prm.nonfinite) {
         uint32_t hit = GSZ == 2 ? (nfacc & 0x80008000u) : (nfacc & 0x80000000u);
         if constexpr (GSZ == 2) {
