@@ -59,6 +59,7 @@ constexpr int K3_ARENA = ZF_K3_ARENA_KB * 1024;   // bytes per stage arena
 constexpr int K3_SMEM = K3_STAGES * K3_ARENA;
 static_assert(K3_ARENA % 128 == 0, "alignment");
 static_assert(K3_SMEM <= 227 * 1024 - 512, "shared memory budget");
+static_assert(K3_STAGES % K3_GROUPS == 0 && K3_NCW % K3_GROUPS == 0, "stages and warps split evenly over groups");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -475,10 +476,26 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
         return m;
     }();
     const uint32_t mine = kMine << grp;  // the stages of my group
+#ifdef ZF_K3_PROF
+    // per-warp cycle accounting (lane 0): wait full, AdamW, compaction, group wait, write-back+release
+    unsigned long long pc[6] = {0, 0, 0, 0, 0, 0};
+    long long tq = clock64();
+#define ZF_TICK(i)                         \
+    do {                                   \
+        const long long tn_ = clock64();   \
+        pc[i] += (unsigned long long)(tn_ - tq); \
+        tq = tn_;                          \
+    } while (0)
+#else
+#define ZF_TICK(i) \
+    do {           \
+    } while (0)
+#endif
     for (int it = grp;; it += K3_GROUPS) {
         const int st = it % K3_STAGES;
         if ((finished >> st) & 1u) continue;
         mbar_wait(&full[st], (phase >> st) & 1u);
+        ZF_TICK(0);
         phase ^= 1u << st;
         const StageInfo& si = info[st];
         if (si.u < 0) {  // this stage's producer ran out of units; others may still hold some
@@ -517,6 +534,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
             if (lane == 0) mbar_arrive(&gbar[grp]);  // release: this warp's tile updates
         }
 
+        ZF_TICK(1);
         // ---------------- (2) compaction by gather ----------------
         const int nk = si.nkeep;
         if (prm.do_compact && nk > 0 && prm.debug_mode != 3) {
@@ -541,7 +559,9 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
                             const int q = qa + OPL * g;
                             const uint32_t rowa = sGa + (uint32_t)(r * sw * GSZ);
                             uint4 o;
-                            if constexpr (GSZ == 2) {
+                            if (prm.debug_mode == 8) {  // experiment: compaction stores without its shared-memory gathers
+                                o = make_uint4(q, r, 0u, 0u);
+                            } else if constexpr (GSZ == 2) {
                                 const uint4 u = lds128(sU + q);
                                 o.x = lds_u16(rowa + (u.x & 0xffffu)) | (lds_u16(rowa + (u.x >> 16)) << 16);
                                 o.y = lds_u16(rowa + (u.y & 0xffffu)) | (lds_u16(rowa + (u.y >> 16)) << 16);
@@ -596,10 +616,12 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
             }
         }
 
+        ZF_TICK(2);
         // ---------------- (3) p write-back of the touched 16-byte chunks ----------------
         if (pwb) {
             mbar_wait(&gbar[grp], gphase);  // acquire: every warp of the group finished its AdamW
             gphase ^= 1u;
+            ZF_TICK(3);
             constexpr int VP = 16 / PSZ;    // p columns per chunk
             const uint32_t* smask = reinterpret_cast<const uint32_t*>(A + si.oMask) + si.eMask;
             const PB* sP = reinterpret_cast<const PB*>(A + si.oP);
@@ -625,7 +647,16 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
             mbar_arrive(&empty[st]);
             if (done) red_release_add(done, 1u);  // per-warp completion count (offload only)
         }
+        ZF_TICK(4);
+#ifdef ZF_K3_PROF
+        pc[5] += 1;  // units
+#endif
     }
+#ifdef ZF_K3_PROF
+    if (lane == 0 && prm.prof)
+        for (int i = 0; i < 6; ++i) atomicAdd(prm.prof + i, pc[i]);
+#endif
+#undef ZF_TICK
     asm volatile("" ::"r"(dbg_sink));
     if (prm.nonfinite) {
         uint32_t hit = GSZ == 2 ? (nfacc & 0x80008000u) : (nfacc & 0x80000000u);

@@ -667,6 +667,18 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
         static const int dbg = getenv("ZF_K3_DEBUG_MODE") ? atoi(getenv("ZF_K3_DEBUG_MODE")) : 0;
         prm.debug_mode = dbg;
     }
+#ifdef ZF_K3_PROF
+    {
+        // experiment builds: K3 consumer cycle breakdown, printed to stderr by zf_sync
+        static unsigned long long* prof = nullptr;
+        if (!prof) {
+            cudaMalloc(&prof, 8 * sizeof(unsigned long long));
+            cudaMemset(prof, 0, 8 * sizeof(unsigned long long));
+        }
+        prm.prof = prof;
+        c->k3_prof = prof;
+    }
+#endif
     const int grid = (int)std::min<int64_t>(c->grid, c->k3_units);
     zf_ctx::Pending pe3;
     ZF_TRY(c->prof_begin(3, s, &pe3));
@@ -814,6 +826,15 @@ extern "C" zf_status zf_sync(zf_ctx* c) {
     if (c->cfg.host_accumulate) {
         std::unique_lock<std::mutex> lk(c->mu);
         c->cv.wait(lk, [&] { return c->jobs.empty(); });
+    }
+    if (c->k3_prof && getenv("ZF_K3_PROF_PRINT")) {
+        unsigned long long h[6];
+        ZF_CUDA(cudaMemcpy(h, c->k3_prof, sizeof h, cudaMemcpyDeviceToHost));
+        ZF_CUDA(cudaMemset(c->k3_prof, 0, 8 * sizeof(unsigned long long)));
+        const double u = h[5] ? (double)h[5] : 1.0;
+        fprintf(stderr, "[k3 prof] per warp-unit cycles: wait_full %.0f adam %.0f compact %.0f gbar_wait %.0f "
+                        "writeback+release %.0f (warp-units %llu)\n",
+                h[0] / u, h[1] / u, h[2] / u, h[3] / u, h[4] / u, h[5]);
     }
     volatile int32_t* f = c->nonfinite_h;
     if (*f) {

@@ -529,6 +529,7 @@ struct zf_ctx {
     std::string f1_error;
     std::vector<void*> f1_params;
     cudaStream_t last_stream = nullptr;  // stream of the last zf_step
+    unsigned long long* k3_prof = nullptr;  // -DZF_K3_PROF builds only
     // f2 Zen-auto (reading R21): K6 tables per current set, device state, decision records
     bool autoz = false;
     AutoLayer* d_auto_tab[2] = {nullptr, nullptr};
