@@ -39,7 +39,7 @@ namespace zf {
 namespace {
 
 #ifndef ZF_K3_NCW
-#define ZF_K3_NCW 16
+#define ZF_K3_NCW 20
 #endif
 constexpr int K3_NCW = ZF_K3_NCW;                 // consumer warps
 #ifndef ZF_K3_GROUPS
