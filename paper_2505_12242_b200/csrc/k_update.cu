@@ -38,6 +38,12 @@
 namespace zf {
 namespace {
 
+// p updates go straight from the AdamW phase to HBM (only values whose bits changed);
+// -DZF_K3_TILE_WRITEBACK restores the round-1 scheme (update the staged tile, then write back
+// every 16-byte chunk holding a selected column after a group barrier).
+#ifndef ZF_K3_TILE_WRITEBACK
+#define ZF_K3_PDIRECT 1
+#endif
 #ifndef ZF_K3_NCW
 #define ZF_K3_NCW 20
 #endif
@@ -269,7 +275,8 @@ __device__ __forceinline__ void adam_unit(const StageInfo& si, unsigned char* A,
             if constexpr (GE::SIZE == 2) nfacc |= ((uint32_t)gb & 0x7f80u) + 0x0080u;
             else nfacc |= ((uint32_t)gb & 0x7f800000u) + 0x00800000u;
             PB* pp = PST ? p_ + r * pstride : p_ + r * ldp;
-            float p = PE::to_f(*pp);
+            const PB pold = *pp;
+            float p = PE::to_f(pold);
             float mm, vv;
             if constexpr (MST) {
                 if constexpr (REMAP) {
@@ -290,7 +297,16 @@ __device__ __forceinline__ void adam_unit(const StageInfo& si, unsigned char* A,
                 }
             }
             adamw_elem_t(GE::to_f(gb), p, mm, vv, sb.x, sb.y, prm.adam);
+#ifdef ZF_K3_PDIRECT
+            {
+                // p read from the staged tile, a changed value stored straight to HBM: no tile
+                // write-back phase and no group barrier (same memory state)
+                const PB pnew = PE::from_f(p);
+                if (pnew != pold) gP[r * ldp + c] = pnew;
+            }
+#else
             *pp = PE::from_f(p);
+#endif
             if (prm.debug_mode != 7) {
                 __stcs(mo + r * k, mm);
                 __stcs(vo + r * k, vv);
@@ -513,7 +529,11 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
         const GB* sG = reinterpret_cast<const GB*>(A + si.oG);
         const int ns = si.s1 - si.s0;
         const bool adam = prm.do_adam && (prm.debug_mode == 0 || prm.debug_mode >= 3) && ns > 0;
+#ifdef ZF_K3_PDIRECT
+        const bool pwb = false;
+#else
         const bool pwb = adam && si.pstaged;
+#endif
 
         // ---------------- (1) AdamW ----------------
         if (adam) {
