@@ -44,6 +44,11 @@ namespace {
 #ifndef ZF_K3_TILE_WRITEBACK
 #define ZF_K3_PDIRECT 1
 #endif
+// producers prefetch a claimed unit's G / p rows into L2 while its arena is still busy
+// (-DZF_K3_NO_L2PF disables)
+#ifndef ZF_K3_NO_L2PF
+#define ZF_K3_L2PF 1
+#endif
 #ifndef ZF_K3_NCW
 #define ZF_K3_NCW 20
 #endif
@@ -106,6 +111,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
             smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
+}
+// L2 prefetch of a global range by the TMA engine (no shared memory, no completion):
+// lets a producer start a claimed unit's DRAM reads while its arena is still busy.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, int64_t bytes) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15);
+    const uintptr_t b = (reinterpret_cast<uintptr_t>(src) + (uintptr_t)bytes + 15) & ~uintptr_t(15);
+    for (uintptr_t q = a; q < b;) {
+        const uint32_t n = (uint32_t)((b - q) < (uintptr_t)(1u << 20) ? (b - q) : (uintptr_t)(1u << 20));
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(q), "r"(n) : "memory");
+        q += n;
+    }
 }
 __device__ __forceinline__ uint64_t evict_first_policy() {
     uint64_t p;
@@ -365,6 +381,27 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
                 si.s0 = g.c0 == 0 ? 0 : (g.c0 >= Lp->m ? (int32_t)Lp->k : __ldg(Lp->prefix + (g.c0 >> 5)));
                 si.s1 = g.c1 >= Lp->m ? (int32_t)Lp->k : __ldg(Lp->prefix + (g.c1 >> 5));
             }
+#ifdef ZF_K3_L2PF
+            if (si.u >= 0 && it > 0 && lane == 0) {
+                // the arena is still being consumed: pull this unit's G and p rows toward L2 now
+                const UpdLayer& L = *Lp;
+                const int sw = (int)(g.c1 - g.c0);
+                if (L.tma_ok) {
+                    const unsigned char* G = static_cast<const unsigned char*>(L.G);
+                    if (L.nseg == 1 && L.ldg == L.m) bulk_prefetch_l2(G + g.r0 * L.m * GSZ, (int64_t)g.Rr * sw * GSZ);
+                    else
+                        for (int r = 0; r < g.Rr; ++r)
+                            bulk_prefetch_l2(G + ((g.r0 + r) * L.ldg + g.c0) * GSZ, (int64_t)sw * GSZ);
+                }
+                if (prm.do_adam && si.s1 > si.s0 && L.p_tma) {
+                    const unsigned char* P = static_cast<const unsigned char*>(L.P);
+                    if (L.nseg == 1 && L.ldp == L.m) bulk_prefetch_l2(P + g.r0 * L.m * PSZ, (int64_t)g.Rr * sw * PSZ);
+                    else
+                        for (int r = 0; r < g.Rr; ++r)
+                            bulk_prefetch_l2(P + ((g.r0 + r) * L.ldp + g.c0) * PSZ, (int64_t)sw * PSZ);
+                }
+            }
+#endif
             if (it > 0) mbar_wait(&empty[st], (it - 1) & 1);
             unsigned char* A = smem + st * K3_ARENA;
             if (si.u < 0) {
