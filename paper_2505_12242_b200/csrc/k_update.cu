@@ -44,7 +44,8 @@ namespace {
 #ifndef ZF_K3_TILE_WRITEBACK
 #define ZF_K3_PDIRECT 1
 #endif
-// producers prefetch a claimed unit's G / p rows into L2 while its arena is still busy
+// producers prefetch a claimed unit's G / p rows and moment slabs into L2 while its arena is
+// still busy
 // (-DZF_K3_NO_L2PF disables)
 #ifndef ZF_K3_NO_L2PF
 #define ZF_K3_L2PF 1
@@ -399,6 +400,18 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
                     else
                         for (int r = 0; r < g.Rr; ++r)
                             bulk_prefetch_l2(P + ((g.r0 + r) * L.ldp + g.c0) * PSZ, (int64_t)sw * PSZ);
+                }
+                if (prm.do_adam && si.s1 > si.s0 && L.mv_tma) {  // and the moment slabs
+                    int64_t e0, e1;
+                    if (L.slot_src) {
+                        e0 = g.r0 * L.k_in;
+                        e1 = (g.r0 + g.Rr) * L.k_in;
+                    } else {
+                        e0 = g.r0 * L.k + si.s0;
+                        e1 = (g.r0 + g.Rr - 1) * L.k + si.s1;
+                    }
+                    bulk_prefetch_l2(L.m_in + e0, (e1 - e0) * 4);
+                    bulk_prefetch_l2(L.v_in + e0, (e1 - e0) * 4);
                 }
             }
 #endif
