@@ -21,10 +21,19 @@
 namespace zf {
 namespace {
 
-constexpr int K1_THREADS = 256;
+#ifndef ZF_K1_THREADS
+#define ZF_K1_THREADS 256
+#endif
+#ifndef ZF_K1_RB
+#define ZF_K1_RB 1024
+#endif
+#ifndef ZF_K1_UNROLL
+#define ZF_K1_UNROLL 4
+#endif
+constexpr int K1_THREADS = ZF_K1_THREADS;
 constexpr int K1_WARPS = K1_THREADS / 32;
-constexpr int K1_RB = 128;      // rows per row block
-constexpr int K1_UNROLL = 4;    // rows in flight per thread
+constexpr int K1_RB = ZF_K1_RB;          // rows per row block (1024: 7B K1 2.41 -> 1.91 ms, tools/k1_cfg.sh)
+constexpr int K1_UNROLL = ZF_K1_UNROLL;  // rows in flight per thread
 
 __device__ __forceinline__ int find_layer(const Table<NormLayer>& t, int64_t u) {
     int lo = 0, hi = t.n - 1;
