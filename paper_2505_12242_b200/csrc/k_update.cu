@@ -13,21 +13,22 @@
 // G, 2(1-κ) B of compact output, and for the selected columns the read-modify-
 // write of p (in 32-byte sectors) and of the fp32 moments.
 //  - persistent grid, one CTA per SM, warp-specialised: 4 producer warps (one
-//    thread each, one stage arena each) and 16 consumer warps in two groups of 8.
-//    Work units (R whole rows, or a 128-aligned column segment of one row) are
-//    claimed dynamically, one atomic per unit.
-//  - a producer stages EVERYTHING a unit needs into its 56 KB arena with bulk copies
-//    (cp.async.bulk, the TMA engine) completing on one mbarrier: the G tile, the p
-//    tile (when the selection touches most of p's 32-byte sectors), the moment slabs
-//    (or the old rows on a refresh), the slot step counts, column indices and remap
-//    sources, the mask words and the segment's list of unselected-column byte
-//    offsets (written by K2).  Consumers issue no global loads; waits are
-//    hardware-suspended (mbarrier.try_wait).
-//  - consumers: slot-major AdamW in shared memory (a slot's column, step count and
-//    bias corrections read once for all its rows; explicit round-to-nearest
-//    intrinsics in the oracle's op order), compaction by gather (4 outputs per
-//    thread per vector store, coalesced across the warp), then every 16-byte chunk
-//    of the p tile holding a selected column is written back with one vector store.
+//    thread each, one stage arena each) and 20 consumer warps in two groups of 10.
+//    Work units (R rows x c columns, c = m or a 128-aligned segment) are claimed
+//    dynamically, one atomic per unit.
+//  - a producer prefetches the claimed unit's G / p rows and moment slabs into L2
+//    while its arena is still being consumed, then stages EVERYTHING the unit needs
+//    into its 56 KB arena with bulk copies (cp.async.bulk, the TMA engine) completing
+//    on one mbarrier: the G tile, the p tile (when the selection touches most of p's
+//    32-byte sectors), the moment slabs (or the old rows on a refresh), the slot step
+//    counts, column indices and remap sources, the mask words and the segment's list
+//    of unselected-column byte offsets (written by K2).  Consumers issue no global
+//    loads; waits are hardware-suspended (mbarrier.try_wait).
+//  - consumers: slot-major AdamW (a slot's column, step count and bias corrections
+//    read once for all its rows; explicit round-to-nearest intrinsics in the
+//    oracle's op order), p read from the staged tile and each changed value stored
+//    straight to HBM; then compaction by gather (8 bf16 outputs per thread per vector
+//    store, coalesced across the warp).
 //  - with offload, each consumer warp bumps a per-layer counter after its share of
 //    a unit (red.release); the copy stream waits on it (cuStreamWaitValue32) to
 //    start the layer's device->host copy.
