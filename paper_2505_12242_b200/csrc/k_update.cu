@@ -55,6 +55,10 @@ namespace {
 #define ZF_K3_NCW 20
 #endif
 constexpr int K3_NCW = ZF_K3_NCW;                 // consumer warps
+#ifndef ZF_K3_ROW_UNROLL
+#define ZF_K3_ROW_UNROLL 2
+#endif
+constexpr int K3_ROW_UNROLL = ZF_K3_ROW_UNROLL;   // rows of one slot in flight per AdamW thread
 #ifndef ZF_K3_GROUPS
 #define ZF_K3_GROUPS 2
 #endif
@@ -287,7 +291,7 @@ __device__ __forceinline__ void adam_unit(const StageInfo& si, unsigned char* A,
         const int pstride = PST ? sw : (int)0;
         float* mo = si.m_out + s;
         float* vo = si.v_out + s;
-#pragma unroll 2
+#pragma unroll K3_ROW_UNROLL
         for (int r = rg; r < Rr; r += nrg) {
             const GB gb = g_[r * sw];
             if constexpr (GE::SIZE == 2) nfacc |= ((uint32_t)gb & 0x7f80u) + 0x0080u;
