@@ -426,6 +426,15 @@ def test_profile_phases(zf, gpu):
         assert all(ms >= 0.0 for ms, _n in prof.values()) and prof["k3_update"][0] > 0.0
 
 
+def test_step_paper_lr_most_values_unchanged(zf, orc, gpu):
+    """At the paper's lr 1e-5 most bf16 parameters keep their bits in a step; K3 stores only
+    changed values (reading the staged tile) -- parameters, moments, compaction and
+    accumulators must still be bit-exact (staged-p and unstaged-p layers, f1 on)."""
+    shapes = [(64, 4096), (130, 257), (33, 1000)]
+    _run_stateful(zf, orc, gpu, shapes, "bf16", "bf16", 100000, 2, 2, 5, offload=True, lr=1e-5, cpu_update=True)
+    _run_stateful(zf, orc, gpu, shapes, "bf16", "bf16", 10000, 2, 2, 4, offload=True, lr=1e-5)
+
+
 def test_cpu_update_needs_aligned_windows(zf):
     with pytest.raises(zf.ZFError):
         zf.Context([zf.LayerShape(8, 64)], refresh_interval=2, accum_interval=4, offload=True, host_accumulate=True,
