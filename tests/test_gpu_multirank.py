@@ -98,3 +98,65 @@ def test_two_ranks_one_gpu_host_allreduce(cpu_update, partition):
     from paper_2505_12242_b200 import _build
     _build.build()
     mp.spawn(_worker, args=(2, _free_port(), 5, 2, cpu_update, partition), nprocs=2, join=True)
+
+
+AUTO_SHAPES = [(64, 256), (96, 200), (128, 320)]
+
+
+def _worker_auto(rank, world, port, steps, gamma):
+    """Zen-auto (R21) on two ranks: K1 every step, the partial norms summed through the host
+    all-reduce, the same window decision on both ranks, equal to the oracle's on the full
+    matrices; each rank's parameter rows bit-exact."""
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    sys.path.insert(0, os.path.join(root, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import synth
+    from gpu_util import assert_bits_equal, to_np
+    from oracle import oracle as orc
+    from paper_2505_12242_b200 import zf
+    from paper_2505_12242_b200.dist import gloo_allreduce, shard_rows
+    from synth import gpu
+
+    torch.cuda.set_device(0)
+    spans = [shard_rows(n, world, rank) for n, _ in AUTO_SHAPES]
+    local = [(b - a, m) for (a, b), (_, m) in zip(spans, AUTO_SHAPES)]
+    N = 8
+    ctx = zf.Context([zf.LayerShape(n, m) for n, m in local], topk_ratio_ppm=100000, refresh_interval=N,
+                     accum_interval=N, adam=zf.adam_params(lr=1e-3), offload=True, host_accumulate=True,
+                     world=world, rank=rank, host_allreduce=gloo_allreduce(), auto_gamma=gamma)
+    scales = [gpu.ColScale(m, li) for li, (_, m) in enumerate(AUTO_SHAPES)]
+    Gs = [torch.empty(n, m, dtype=torch.bfloat16, device="cuda") for n, m in local]
+    Ps = [torch.empty(n, m, dtype=torch.bfloat16, device="cuda") for n, m in local]
+    for li, P in enumerate(Ps):
+        gpu.fill_param(P, li, row0=spans[li][0])
+    model = orc.OracleModel([orc.OracleLayer(n=n, m=m, ratio_ppm=100000, refresh_interval=N, accum_interval=N,
+                                             hp=orc.AdamHP(lr=1e-3)) for n, m in AUTO_SHAPES], auto_gamma=gamma)
+    Po = [synth.param(n, m, li) for li, (n, m) in enumerate(AUTO_SHAPES)]
+    for t in range(steps):
+        for li in range(len(AUTO_SHAPES)):
+            scales[li].advance_to(t)
+            gpu.fill_grad(Gs[li], li, t, scales[li], row0=spans[li][0])
+        ctx.step(t, Gs, Ps)
+        ctx.sync()
+        Gfull = [synth.grad(n, m, li, t, synth.col_scale_at(m, t, li)) for li, (n, m) in enumerate(AUTO_SHAPES)]
+        ov = [to_np(ctx.selected(li)) for li in range(len(AUTO_SHAPES))] if t % N == 0 else None
+        model.step(t, Gfull, Po, idx_overrides=ov)
+        oA, oi, _ou = model.stats[-1]
+        assert abs(oA - gamma * oi) > 1e-4 * gamma * oi, "decision too close to call"
+        for li, (a, b) in enumerate(spans):
+            assert_bits_equal(to_np(Ps[li]), Po[li][a:b], f"rank {rank} params t={t} l={li}")
+    ends = [t for (t, e, *_r) in ctx.window_log() if e]
+    assert ends == model.ends, (rank, ends, model.ends)
+    assert min(model.intervals()) < N
+    ctx.close()
+    dist.destroy_process_group()
+
+
+def test_two_ranks_zen_auto():
+    from paper_2505_12242_b200 import _build
+    _build.build()
+    mp.spawn(_worker_auto, args=(2, _free_port(), 16, 0.15), nprocs=2, join=True)
