@@ -717,3 +717,28 @@ def test_zen_auto_cpu_update_uses_the_window_length(orc):
     assert M.ends == [3]
     assert np.allclose(P[:, k:], -1e-3 * 0.25 / (0.25 + 1e-8), rtol=1e-6)
     assert M.layers[0].th[k:].tolist() == [1] * (m - k)
+
+
+def test_zen_auto_pools_channels_over_the_model(orc):
+    """R21: the important / unimportant means are over every column of the model (pooled),
+    not averages of per-layer means.  Layer A: 16x40 with 4 important columns of 1.0 and 36
+    unimportant of 0.5; layer B: 16x10 with 1 important column of 1.0 and 9 unimportant of
+    0.0625.  Per-channel L2 norms: important 4, unimportant 2 (A) and 0.25 (B); pooled
+    unimportant mean u = (36*2 + 9*0.25)/45 = 1.65, i = 4: with gamma = 1 the window ends
+    when A = s*u >= 4, i.e. at s = 3 (s*u = 4.95; s = 2 gives 3.3).  (Averaging the two
+    layers' means instead would give u = 1.125 -> s = 4.)"""
+    n = 16
+    LA = orc.OracleLayer(n=n, m=40, ratio_ppm=100000, refresh_interval=16, accum_interval=16)
+    LB = orc.OracleLayer(n=n, m=10, ratio_ppm=100000, refresh_interval=16, accum_interval=16)
+    assert LA.k == 4 and LB.k == 1
+    M = orc.OracleModel([LA, LB], auto_gamma=1.0)
+    GA = np.full((n, 40), 0.5, np.float32)
+    GA[:, :4] = 1.0
+    GB = np.full((n, 10), 0.0625, np.float32)
+    GB[:, 0] = 1.0
+    PA, PB = np.zeros((n, 40), np.float32), np.zeros((n, 10), np.float32)
+    for t in range(9):
+        M.step(t, [GA, GB], [PA, PB])
+    assert M.intervals() == [3, 3, 3]
+    A, i, u = M.stats[0]
+    assert abs(u - (36 * 2 + 9 * 0.25) / 45) < 1e-12 and abs(i - 4.0) < 1e-12
