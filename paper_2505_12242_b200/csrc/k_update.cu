@@ -454,7 +454,12 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
             off = (g.Rr * sw * GSZ + 15) & ~15;
             // mask words of the segment (p write-back) and the segment's unselected-column list
             const int64_t w0 = g.c0 >> 5, nwm = (sw + 31) >> 5;
+#ifndef ZF_K3_PDIRECT
             si.eMask = stage_elems<4>(A, &off, L.mask, w0, w0 + nwm, &full[st], &tx, &si.oMask);
+#else
+            (void)w0;
+            (void)nwm;  // the mask words served the tile write-back only
+#endif
             si.j0 = (int32_t)(g.c0 - si.s0);
             si.nkeep = sw - ns;
             if (prm.do_compact && si.nkeep > 0)
