@@ -701,10 +701,11 @@ def test_zen_auto_huge_gamma_is_the_fixed_schedule(orc):
 
 
 def test_zen_auto_cpu_update_uses_the_window_length(orc):
-    """f1 under Zen-auto: a window of L steps updates theta^(c) once with acc / L (P:527 with
-    S = L).  Constant dyadic stream, ratio 0.25, gamma = 1 -> L = 4; at the first flush
-    every unimportant column moves by -lr*g/(|g|+eps) (bias-corrected step 1 with the
-    exact window average g)."""
+    """f1 under Zen-auto: the CPU update happens exactly at the window end Zen-auto picks
+    (ratio 0.25, gamma = 1 -> L = 4), once, and moves every unimportant column by the
+    bias-corrected step-1 amount -lr*g/(|g|+eps).  At g = 0.25 >> eps that move is
+    scale-invariant, so this pins WHEN the update lands and the step count, not the 1/L
+    factor; ``test_f1_zen_auto_window_length_factor_in_the_eps_regime`` pins the factor."""
     n, m = 16, 64
     M = _auto_model(orc, n, m, 100000, N=8, smax=8, gamma=1.0, cpu_update=True)
     k = M.layers[0].k
@@ -742,3 +743,75 @@ def test_zen_auto_pools_channels_over_the_model(orc):
     assert M.intervals() == [3, 3, 3]
     A, i, u = M.stats[0]
     assert abs(u - (36 * 2 + 9 * 0.25) / 45) < 1e-12 and abs(i - 4.0) < 1e-12
+
+
+# ------------------------------------------------------------------ f1: the 1/S factor of P:527
+# AdamW is invariant to the scale of its gradient except through eps (and through an L2
+# weight-decay term), so the factor 1/S of P:527 (theta^(c) -= alpha * (1/S) * sum over the
+# window) is only visible where |g| is comparable to eps or where wd*p is added to g.  These
+# pins sit in those regimes, with closed forms evaluated in double.
+_TINY = 2.0 ** -27          # ~7.45e-9, comparable to eps = 1e-8; dyadic, so window sums are exact
+
+
+def _step1_move(g, lr=1e-3, eps=1e-8):
+    """Bias-corrected first AdamW step from zero moments: -lr * g / (|g| + eps)."""
+    return -lr * g / (abs(g) + eps)
+
+
+def test_f1_window_average_in_the_eps_regime(orc):
+    """Fixed S = 2, constant unselected gradient g = 2^-27 ~ eps: the flush uses acc / S = g,
+    so the move is -lr*g/(g+eps) = -4.27e-4; using the window SUM (2g) would move by
+    -lr*2g/(2g+eps) = -5.98e-4 (reading R18)."""
+    n, m = 4, 10
+    G = np.full((n, m), _TINY, np.float32)
+    G[:, 0] = 9.0                                      # column 0 selected (k = 1)
+    P = np.zeros((n, m), np.float32)
+    L = orc.OracleLayer(n=n, m=m, ratio_ppm=100000, refresh_interval=2, accum_interval=2, cpu_update=True)
+    L.step(0, G, P)
+    L.step(1, G, P)
+    want = _step1_move(_TINY)
+    assert abs(want - _step1_move(2 * _TINY)) > 0.3 * abs(want)     # the regime separates the two
+    assert np.allclose(P[:, 1:], want, rtol=1e-5, atol=0)
+
+
+def test_f1_window_average_with_l2_weight_decay(orc):
+    """Non-decoupled weight decay adds wd*p to the window average (O6 with g = acc/S):
+    g' = 0.25 + 0.5 * (-0.75) = -0.125, so the first flush moves p UP by lr; with the window
+    sum (0.5) g' = +0.125 and p would move down (P:527 + R8's L2 mode)."""
+    n, m = 3, 8
+    G = np.full((n, m), 0.25, np.float32)
+    G[:, 0] = 9.0
+    P = np.full((n, m), -0.75, np.float32)
+    hp = orc.AdamHP(lr=1e-3, weight_decay=0.5, decoupled=0)
+    L = orc.OracleLayer(n=n, m=m, ratio_ppm=125000, refresh_interval=2, accum_interval=2, hp=hp, cpu_update=True)
+    L.step(0, G, P)
+    assert np.all(P[:, 1:] == np.float32(-0.75))
+    L.step(1, G, P)
+    want = -0.75 + _step1_move(0.25 + 0.5 * -0.75)     # = -0.75 + lr (to 1e-7 relative)
+    assert np.allclose(P[:, 1:], want, rtol=1e-6, atol=0)
+    assert np.all(P[:, 1:] > -0.75)
+
+
+def test_f1_zen_auto_window_length_factor_in_the_eps_regime(orc):
+    """Zen-auto with N = S_max = 8, gamma = 0.75 on a constant stream of tiny gradients
+    (important 4*2^-27, unimportant 2^-27: per-channel ratio 0.25).  The decision ends a
+    window after L = 3 steps (3 * 0.25 >= 0.75); windows are t = 0..2, 3..5, and 6..7, the
+    last cut to L = 2 by the refresh at t = 8.  Each flush averages with its OWN length
+    (P:527 with S = L, reading R21), so every flush sees g = 2^-27 and, with constant g, every
+    AdamW step moves by -lr*g/(|g|+eps) (m_hat = g, v_hat = g^2).  Dividing by S_max would
+    feed 3g/8, 3g/8, g/4; not dividing would feed 3g, 3g, 2g -- both change P."""
+    n, m = 16, 64
+    M = _auto_model(orc, n, m, 100000, N=8, smax=8, gamma=0.75, cpu_update=True)
+    k = M.layers[0].k
+    G = _two_level(n, m, k, 4 * _TINY, _TINY)
+    P = np.zeros((n, m), np.float32)
+    step = _step1_move(_TINY)
+    for t in range(3):
+        M.step(t, [G], [P])
+    assert M.ends == [2]
+    assert np.allclose(P[:, k:], step, rtol=1e-5, atol=0)
+    for t in range(3, 8):
+        M.step(t, [G], [P])
+    assert M.intervals() == [3, 3, 2]
+    assert np.allclose(P[:, k:], 3 * step, rtol=1e-5, atol=0)
+    assert M.layers[0].th[k:].tolist() == [3] * (m - k)
