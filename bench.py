@@ -48,7 +48,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--also-k1pct", action="store_true", help="also time k = 1% (reported as an extra field)")
+    ap.add_argument("--no-k1pct", action="store_true", help="skip the k = 1%% line (reported as the k1pct field)")
+    ap.add_argument("--no-lr1e3", action="store_true",
+                    help="skip timing the main config at lr 1e-3 (nearly every bf16 value changes; field lr_1e-3)")
     ap.add_argument("--also-state-offload", action="store_true",
                     help="also time the f3 state swap-out mode (moments in mapped pinned host memory)")
     ap.add_argument("--also-auto", type=float, default=0.0, metavar="GAMMA",
@@ -60,6 +62,10 @@ def parse():
                          "per-rank evidence for the multi-GPU configs on a one-GPU box")
     ap.add_argument("--also-cpu-update", action="store_true",
                     help="also time e2e with the deferred CPU AdamW (f1), synchronous vs overlapped (R23)")
+    ap.add_argument("--colocate", action="store_true",
+                    help="N > 1 ranks share the visible GPU(s) (rank r on cuda:r %% device_count): gloo process group "
+                         "and the library's host all-reduce instead of NCCL -- runs the multi-rank path (launcher, "
+                         "sharding, norm exchange, max-over-ranks timing) on a one-GPU box; not a scaling number")
     ap.add_argument("--json-out", default=None)
     return ap.parse_args()
 
@@ -136,59 +142,130 @@ def sector_bytes(shapes, idxs, gsz=2, psz=2):
 
 
 # ------------------------------------------------------------ CPU oracle timing (baseline)
-def oracle_sample_ms_per_step(model, ratio_ppm, refresh, steps, budget_s=25.0):
-    """Time the oracle (single thread, as it stands) on a bounded sample of the
-    workload -- one matrix of each distinct shape of the model -- and scale its
-    time per element-step to the whole model.  Returns (ms_per_step, sample)."""
-    import synth
+def _oracle_worker(wid, core, mats, ratio_ppm, refresh, lr, steps, barrier, q):
+    """One process of the oracle timing: pinned to `core`, owns the matrices `mats`
+    [(layer, n, m)], generates their inputs (host C twin of the generator), then runs the
+    oracle's step sequence on them in lock step with the other workers (a barrier after
+    every step), so each step's wall time is the slowest worker's."""
+    try:
+        os.sched_setaffinity(0, {core})
+    except (AttributeError, OSError):
+        pass
     from oracle import oracle as orc
-    shapes_all = [(n, m) for _, n, m in synth.MODELS[model]()]
-    total = sum(n * m for n, m in shapes_all)
-    uniq = []
-    for s in shapes_all:
-        if s not in uniq:
-            uniq.append(s)
-    uniq = [s for s in uniq if s[0] * s[1] <= 50_000_000][:3]  # bounded sample
-    layers, Ps, scales = [], [], []
-    for li, (n, m) in enumerate(uniq):
-        layers.append(orc.OracleLayer(n=n, m=m, ratio_ppm=ratio_ppm, refresh_interval=refresh,
-                                      accum_interval=refresh, hp=orc.AdamHP(lr=1e-5)))
-        Ps.append(synth.param(n, m, li))
-        scales.append(synth.col_scale_init(m, li))
-    Gs = [synth.grad(n, m, li, 0, scales[li]) for li, (n, m) in enumerate(uniq)]
-    sample_elems = sum(n * m for n, m in uniq)
+    from synth import host
+    hp = orc.AdamHP(lr=lr)
+    st = []
+    for li, n, m in mats:
+        G = host.grad(n, m, li, 0, host.col_scale_at(m, 0, li))
+        st.append({"n": n, "G": G, "P": host.param(n, m, li), "k": orc.k_for(m, ratio_ppm), "idx": None})
     times = []
-    t_begin = time.perf_counter()
+    barrier.wait()
     for t in range(steps):
         t0 = time.perf_counter()
-        for L, G, P in zip(layers, Gs, Ps):
-            L.step(t, G, P)
+        for s_ in st:
+            if t % refresh == 0:         # O1 norms -> O3 top-k -> O5 remap (P:486, P:505-508)
+                idx = orc.topk(orc.column_norms(s_["G"]), s_["k"])
+                if s_["idx"] is None:
+                    s_["M"] = np.zeros((s_["n"], s_["k"]), np.float32)
+                    s_["V"] = np.zeros((s_["n"], s_["k"]), np.float32)
+                    s_["steps"] = np.zeros(s_["k"], np.int32)
+                else:
+                    s_["M"], s_["V"], s_["steps"] = orc.remap(s_["n"], s_["idx"], s_["M"], s_["V"], s_["steps"], idx)
+                s_["idx"] = idx
+            orc.selective_adamw(s_["P"], s_["G"], s_["idx"], s_["M"], s_["V"], s_["steps"], hp)   # O6
+            orc.compact(s_["G"], s_["idx"])                                                        # O7
+        barrier.wait()
         times.append(time.perf_counter() - t0)
-        if time.perf_counter() - t_begin > budget_s and (t + 1) % refresh == 0:
-            break
-    per_elem = sum(times) / len(times) / sample_elems
-    desc = (f"{len(times)} oracle steps (refresh every {refresh}) over {len(uniq)} matrices "
-            f"{'+'.join(f'{n}x{m}' for n, m in uniq)} = {sample_elems / 1e6:.1f}M elements; "
-            f"time/element-step scaled to the model's {total / 1e9:.3f}G elements")
-    return per_elem * total * 1e3, desc, len(times)
+    if wid == 0:
+        q.put(times)
+
+
+def oracle_ms_per_step(model, ratio_ppm, refresh, steps, warmup, lr=1e-5, max_frac_mem=0.6):
+    """Time the CPU oracle (as it stands: oracle/zf_oracle.cpp through oracle.py, one thread
+    per process) on the FULL model, one process per host core (pinned), matrices balanced
+    over the processes by element count; the GPU arm's step sequence (refresh every N, then
+    selective AdamW + compaction; no host accumulation, which the GPU line does not run
+    either).  If the host cannot hold the model's state, a stated prefix of the matrices is
+    timed and scaled by element count.  Returns (ms_per_step, sample, cores)."""
+    import multiprocessing as mp
+
+    import synth
+    names = synth.MODELS[model]()
+    mats = [(li, n, m) for li, (_nm, n, m) in enumerate(names)]
+    total = sum(n * m for _, n, m in mats)
+    cores = sorted(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else list(range(os.cpu_count()))
+    k_frac = ratio_ppm / 1e6
+    need = lambda elems: elems * (2 + 2 + 8 * k_frac + 2 * 2 + 2)   # G, P, M+V, compact + temporaries (bytes)
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:  # noqa: BLE001
+        avail = 1 << 62
+    frac = 1.0
+    if need(total) > max_frac_mem * avail:
+        keep, acc = [], 0
+        for x in mats:
+            if need(acc + x[1] * x[2]) > max_frac_mem * avail:
+                break
+            keep.append(x)
+            acc += x[1] * x[2]
+        mats, frac = keep, acc / total
+    nw = max(1, min(len(cores), len(mats)))
+    bins = [[] for _ in range(nw)]
+    load = [0] * nw
+    for x in sorted(mats, key=lambda x: -x[1] * x[2]):   # longest-processing-time first
+        w = load.index(min(load))
+        bins[w].append(x)
+        load[w] += x[1] * x[2]
+    ctx = mp.get_context("spawn")
+    barrier, q = ctx.Barrier(nw), ctx.Queue()
+    procs = [ctx.Process(target=_oracle_worker, args=(w, cores[w], bins[w], ratio_ppm, refresh, lr,
+                                                      warmup + steps, barrier, q)) for w in range(nw)]
+    for p in procs:
+        p.start()
+    times = q.get()
+    for p in procs:
+        p.join()
+    timed = times[warmup:] or times
+    ms = sum(timed) / len(timed) * 1e3 / frac
+    elems = sum(n * m for _, n, m in mats)
+    desc = (f"{'full model' if frac == 1.0 else f'first {len(mats)} of {len(names)} matrices'}: "
+            f"{len(mats)} matrices, {elems / 1e9:.3f} G elements ({frac:.1%} of the model"
+            f"{'' if frac == 1.0 else ', time scaled by element count'}); {len(timed)} timed steps after "
+            f"{min(warmup, len(times) - len(timed)) if len(times) > len(timed) else 0} warm-up (refresh every "
+            f"{refresh}); {nw} single-threaded oracle processes pinned one per core, lock-stepped per step")
+    return ms, desc, nw
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    ms, desc, n = oracle_sample_ms_per_step(args.model, args.ratio_ppm, args.refresh,
-                                            max(1, args.steps + args.warmup), budget_s=150.0)
+    ms, desc, cores = oracle_ms_per_step(args.model, args.ratio_ppm, args.refresh, max(1, args.steps),
+                                         args.warmup, lr=args.lr)
     line = {"impl": "reference", "metric": METRIC, "value": ms, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": f"{args.model}-all-linear-k{args.ratio_ppm // 10000}pct", "model": args.model,
-                       "ratio_ppm": args.ratio_ppm, "refresh_interval": args.refresh},
-            "cpu_baseline": {"value": ms, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
+                       "ratio_ppm": args.ratio_ppm, "refresh_interval": args.refresh, "lr": args.lr},
+            "cpu_baseline": {"value": ms, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
+                             "host_cores": os.cpu_count()},
             "e2e": {"value": ms, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------ GPU arm
+def max_over_ranks(vals, world):
+    """Element-wise max over ranks (CPU tensor: works for the nccl and the gloo group)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, dtype=torch.float64)
+    if world > 1:
+        if dist.get_backend() == "nccl":
+            t = t.cuda()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.cpu().tolist()
+
+
 def run_zenflow(args, rank, world):
     import torch
     import torch.distributed as dist
@@ -204,6 +281,8 @@ def run_zenflow(args, rank, world):
     from paper_2505_12242_b200.dist import flat_partition, shard_rows
 
     dev = int(os.environ.get("LOCAL_RANK", 0))
+    if args.colocate:
+        dev %= torch.cuda.device_count()
     torch.cuda.set_device(dev)
     hbm_peak, peak_src = peaks()
     names = synth.MODELS[args.model]()
@@ -239,16 +318,19 @@ def run_zenflow(args, rank, world):
         sgpu.fill_param(Ps[li], li, row0=row0s[li])
         del sc
     torch.cuda.synchronize()
-    nccl_id = None
-    if world > 1:
+    nccl_id, host_ar = None, None
+    if world > 1 and not args.colocate:
         from paper_2505_12242_b200.dist import broadcast_nccl_id
         nccl_id = broadcast_nccl_id()
+    elif world > 1:
+        from paper_2505_12242_b200.dist import gloo_allreduce
+        host_ar = gloo_allreduce()
 
     def make_ctx(ratio_ppm, offload, **kw):
         return zf.Context([zf.LayerShape(n, m) for n, m in shapes], topk_ratio_ppm=ratio_ppm,
                           refresh_interval=args.refresh, accum_interval=args.refresh,
                           adam=zf.adam_params(lr=args.lr), offload=offload, host_accumulate=offload,
-                          world=world, rank=rank, nccl_id=nccl_id, device=dev, **kw)
+                          world=world, rank=rank, nccl_id=nccl_id, device=dev, host_allreduce=host_ar, **kw)
 
     import ctypes
     nl = len(shapes)
@@ -289,11 +371,16 @@ def run_zenflow(args, rank, world):
     idxs = [ctx.selected(li).cpu().numpy() for li in range(nl)]
     ctx.close()
     del ctx
-    t_ms = torch.tensor([ms_total, prof["k3_update"][0], prof["k1_norms"][0], prof["k2_topk"][0],
-                         prof["allreduce"][0]], dtype=torch.float64, device="cuda")
+    mine = {"rank": rank, "device": dev, "k3_ms": prof["k3_update"][0] / max(1, prof["k3_update"][1]),
+            "k3_alg_GBs": algorithmic_bytes(shapes, ks) / (prof["k3_update"][0] / max(1, prof["k3_update"][1]) * 1e-3)
+            / 1e9 if prof["k3_update"][1] else None, "ms_per_step": ms_total / args.steps,
+            "elements": sum(n * m for n, m in shapes)}
+    per_rank = [mine]
     if world > 1:
-        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
-    ms_total, k3_ms, k1_ms, k2_ms, ar_ms = t_ms.tolist()
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, mine)
+    ms_total, k3_ms, k1_ms, k2_ms, ar_ms = max_over_ranks(
+        [ms_total, prof["k3_update"][0], prof["k1_norms"][0], prof["k2_topk"][0], prof["allreduce"][0]], world)
     ms_per_step = ms_total / args.steps
     n_k3 = prof["k3_update"][1]
     n_k1 = prof["k1_norms"][1]
@@ -309,7 +396,9 @@ def run_zenflow(args, rank, world):
         "config": {"workload": f"{args.model}-all-linear-k{args.ratio_ppm // 10000}pct"
                                + (f"-rank0-of-dp{sim}" if sim > 1 else ""), "model": args.model,
                    "linears": nl, "elements": sum(n * m for n, m in full_shapes), "ratio_ppm": args.ratio_ppm,
-                   "refresh_interval": args.refresh, "parallelism": (f"dp{world} ({'flat ZeRO partition' if args.partition == 'flat' else 'row shards'}, norm all-reduce)"
+                   "refresh_interval": args.refresh, "parallelism": (f"dp{world} ({'flat ZeRO partition' if args.partition == 'flat' else 'row shards'}, "
+                                   + ("norm all-reduce over gloo via the host callback, ranks co-located on "
+                                      f"{torch.cuda.device_count()} GPU(s))" if args.colocate else "NCCL norm all-reduce)")
                                    if sim == 1 else f"rank 0 of dp{sim} ({args.partition}) timed alone on 1 GPU, "
                                    "no all-reduce"),
                    "l2": "inputs larger than L2 (working set > 100 GB vs 126 MB L2); no flush needed",
@@ -318,6 +407,7 @@ def run_zenflow(args, rank, world):
                                  "k2_topk": k2_ms / max(1, prof["k2_topk"][1]),
                                  "allreduce": (ar_ms / max(1, prof["allreduce"][1])) if world > 1 else None},
         "gpu_launches": launches,
+        "per_rank": per_rank if world > 1 else None,
         "clocks": clk,
     }
     if world > 1 and prof["allreduce"][1]:
@@ -350,13 +440,34 @@ def run_zenflow(args, rank, world):
         result["k1_roofline"] = {"bound": "hbm", "achieved": g_bytes / (k1_avg * 1e-3) / 1e9, "peak": hbm_peak,
                                  "unit": "GB/s", "frac": g_bytes / (k1_avg * 1e-3) / 1e9 / hbm_peak}
 
-    # ---- k = 1% (extra field)
-    if args.also_k1pct:
-        ctx = make_ctx(10000, False)
-        ms1, prof1, _ = timed_run(ctx, args.steps, args.warmup, "k1pct")
+    def k3_line(ctx_ppm, lr=None, tag=""):
+        ctx = make_ctx(ctx_ppm, False) if lr is None else zf.Context(
+            [zf.LayerShape(n, m) for n, m in shapes], topk_ratio_ppm=ctx_ppm, refresh_interval=args.refresh,
+            accum_interval=args.refresh, adam=zf.adam_params(lr=lr), world=world, rank=rank, nccl_id=nccl_id,
+            device=dev, host_allreduce=host_ar)
+        msx, profx, _ = timed_run(ctx, args.steps, args.warmup, tag)
+        idxx = [ctx.selected(li).cpu().numpy() for li in range(nl)]
         ctx.close()
         del ctx
-        result["k1pct_ms_per_step"] = ms1 / args.steps
+        ksx = [zf.k_for(m, ctx_ppm) for _, m in shapes]
+        msx, k3x, k1x = max_over_ranks([msx, profx["k3_update"][0], profx["k1_norms"][0]], world)
+        k3a = k3x / max(1, profx["k3_update"][1])
+        algx = algorithmic_bytes(shapes, ksx)
+        secx = sector_bytes(shapes, idxx)
+        return {"ms_per_step": msx / args.steps, "k3_ms": k3a, "k1_ms": k1x / max(1, profx["k1_norms"][1]),
+                "roofline": {"bound": "hbm", "kernel": "k_update", "achieved": algx / (k3a * 1e-3) / 1e9,
+                             "peak": hbm_peak, "unit": "GB/s", "frac": algx / (k3a * 1e-3) / 1e9 / hbm_peak,
+                             "algorithmic_bytes_per_launch": algx, "sector_compulsory_bytes_per_launch": secx,
+                             "frac_sector": secx / (k3a * 1e-3) / 1e9 / hbm_peak}}
+
+    # ---- k = 1% (config 3's second ratio) with its own K3 roofline
+    if not args.no_k1pct and args.ratio_ppm != 10000:
+        result["k1pct"] = k3_line(10000, tag="k1pct")
+        result["k1pct"]["workload"] = f"{args.model}-all-linear-k1pct"
+    # ---- the main config at lr 1e-3: nearly every selected bf16 value changes, so K3 stores
+    #      (and read-modify-writes) the p sectors the lr 1e-5 headline mostly skips
+    if not args.no_lr1e3 and args.lr != 1e-3:
+        result["lr_1e-3"] = k3_line(args.ratio_ppm, lr=1e-3, tag="lr1e3")
 
     # ---- f3 state swap-out: moments in mapped pinned host memory (extra field)
     if args.also_state_offload:
@@ -495,10 +606,7 @@ def run_zenflow(args, rank, world):
                 ms_s, n_s = prof_e["d2h_step"]
                 link["x1_d2h_GBs"] = d2h_host / (ms_s / n_s * 1e-3) / 1e9 if n_s else None
                 link["x1_d2h_ms_per_step"] = ms_s / n_s if n_s else None
-            e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-            if world > 1:
-                dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-            return e2e_t.item() * 1e3 / K
+            return max_over_ranks([e2e_s], world)[0] * 1e3 / K
 
         try:
             ms_dev = e2e_run(True)
@@ -537,8 +645,8 @@ def run_zenflow(args, rank, world):
 
     # ---- CPU oracle baseline (rank 0, N=1 only)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        ms, desc, _ = oracle_sample_ms_per_step(args.model, args.ratio_ppm, args.refresh, 8, budget_s=25.0)
-        result["cpu_baseline"] = {"value": ms, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
+        ms, desc, cores = oracle_ms_per_step(args.model, args.ratio_ppm, args.refresh, args.refresh, 0, lr=args.lr)
+        result["cpu_baseline"] = {"value": ms, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
                                   "host_cores": os.cpu_count()}
     if rank == 0:
         line = json.dumps(result)
@@ -547,10 +655,44 @@ def run_zenflow(args, rank, world):
             open(args.json_out, "w").write(line + "\n")
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def self_launch(args) -> int:
+    """`bench.py --gpus N` (N > 1) without a torchrun environment: re-run this script as N
+    ranks under torch.distributed.run on 127.0.0.1 (one process per GPU, or per rank with
+    --colocate) and return its exit code.  Only rank 0 prints the JSON line."""
+    if args.impl == "zenflow" and not args.colocate:
+        import torch
+        nd = torch.cuda.device_count()
+        if nd < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} but {nd} CUDA device(s) visible; use --colocate to run "
+                  f"{args.gpus} ranks on the visible GPU(s)", file=sys.stderr)
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    if not args.colocate:
+        env.setdefault("NCCL_DEBUG", "INFO")        # communicator lines (nranks) on stderr
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", 1))
     rank = int(os.environ.get("RANK", 0))
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "zenflow":
+        sys.exit(self_launch(args))
+    if os.environ.get("ZF_BENCH_LAUNCH_PROBE"):
+        # launcher test hook (tests/test_bench_cpu.py): report the rank layout, do no work
+        print(json.dumps({"rank": rank, "world": world, "local_rank": int(os.environ.get("LOCAL_RANK", 0))}),
+              flush=True)
+        return
     if world != args.gpus and "WORLD_SIZE" in os.environ:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
     if args.impl == "reference":
@@ -561,8 +703,17 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl")
+        if args.colocate:
+            dist.init_process_group("gloo")
+        else:
+            if torch.cuda.device_count() < world:
+                print(f"bench.py: WORLD_SIZE={world} but {torch.cuda.device_count()} CUDA device(s); "
+                      "use --colocate", file=sys.stderr)
+                sys.exit(2)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+            dist.init_process_group("nccl")
     run_zenflow(args, rank, world)
     if world > 1:
         import torch.distributed as dist

@@ -121,7 +121,10 @@ zf_status zf_selective_adam(void* p, zf_dtype pdt, int64_t ldp, const void* G, z
  * CPU".  out[i][u] = G[i][j] where j is the u-th column NOT in idx (ascending):
  * a bit copy into a dense row-major [n, m-k] buffer of dtype gdt (reading R12).
  *   out      device memory, or mapped pinned host memory; 16-byte aligned for the
- *            vector path.  k == m gives an empty output (nothing written). */
+ *            vector path.  k == m gives an empty output (nothing written).
+ *   idx      [k] int32 device data, strictly ascending, each in [0, m).  Its contents
+ *            are NOT validated (that would need a host round trip): an idx violating
+ *            this leaves out unspecified, without any out-of-bounds access. */
 zf_status zf_compact_unselected(const void* G, zf_dtype gdt, int64_t n, int64_t m, int64_t ld,
                                 const int32_t* idx, int64_t k, void* out, zf_stream_t stream);
 

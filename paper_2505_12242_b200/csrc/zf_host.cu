@@ -187,7 +187,8 @@ zf_status f1_refresh(zf_ctx* c, void* const* params, cudaStream_t s) {
         }
         const int64_t ne = (int64_t)ent[i].size();
         if (ne > 0 && l.d.n > 0) {
-            ZF_CUDA(cudaMemcpy(l.unsel_dev, ent[i].data(), ne * sizeof(int32_t), cudaMemcpyHostToDevice));
+            // ordered on s (a caller's non-blocking stream too); ent[i] outlives the sync below
+            ZF_CUDA(cudaMemcpyAsync(l.unsel_dev, ent[i].data(), ne * sizeof(int32_t), cudaMemcpyHostToDevice, s));
             ZF_CUDA(launch_gather_columns(params[i], c->pdt, l.d.ld_param, l.d.n, ne, l.unsel_dev, l.p_up_dev, s));
             c->launches++;
             ZF_CUDA(cudaMemcpyAsync(l.p_mirror, l.p_up_dev, (size_t)l.d.n * ne * c->psz, cudaMemcpyDeviceToHost, s));
@@ -247,8 +248,8 @@ zf_status f1_refresh(zf_ctx* c, void* const* params, cudaStream_t s) {
         l.idx_host = nidx[i];
         l.unsel_host.swap(unew[i]);
         if (!l.unsel_host.empty())
-            ZF_CUDA(cudaMemcpy(l.unsel_dev, l.unsel_host.data(), l.unsel_host.size() * sizeof(int32_t),
-                               cudaMemcpyHostToDevice));
+            ZF_CUDA(cudaMemcpyAsync(l.unsel_dev, l.unsel_host.data(), l.unsel_host.size() * sizeof(int32_t),
+                                    cudaMemcpyHostToDevice, s));  // ordered before the K5 scatter on s
     }
     return ZF_OK;
 }

@@ -15,7 +15,7 @@ def test_reference_arm_json_line():
     assert r.returncode == 0, r.stderr
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["unit"] == "ms/step" and line["higher_is_better"] is False
-    assert line["value"] > 0 and line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] == 1
+    assert line["value"] > 0 and line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
 
 
@@ -41,3 +41,26 @@ def test_reference_arm_nonzero_rank_exits_quietly():
                        env=env)
     assert r.returncode == 0, r.stderr
     assert r.stdout.strip() == ""
+
+
+def test_gpus_n_self_launches_n_ranks():
+    """`bench.py --gpus 2` without a torchrun environment re-runs itself as 2 ranks under
+    torch.distributed.run (127.0.0.1); the probe hook makes each rank print its layout."""
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR",
+                                                             "MASTER_PORT")}
+    env["ZF_BENCH_LAUNCH_PROBE"] = "1"
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--colocate", "--steps", "1",
+                        "--warmup", "0"], capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr
+    lines = [json.loads(x) for x in r.stdout.strip().splitlines() if x.startswith("{")]
+    assert sorted(x["rank"] for x in lines) == [0, 1] and all(x["world"] == 2 for x in lines)
+
+
+def test_gpus_n_refuses_more_ranks_than_devices():
+    """Without --colocate, asking for more ranks than visible GPUs is an error (exit 2), not a
+    silent single-GPU run labelled as multi-GPU."""
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1",
+                        "--warmup", "0"], capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert r.returncode == 2 and "--colocate" in r.stderr

@@ -160,3 +160,91 @@ def test_two_ranks_zen_auto():
     from paper_2505_12242_b200 import _build
     _build.build()
     mp.spawn(_worker_auto, args=(2, _free_port(), 16, 0.15), nprocs=2, join=True)
+
+
+def _worker_fullsize(rank, world, port, steps, sample):
+    """BASELINE config 4 on one GPU: rank `rank` of a `world`-way row-sharded Llama-2-7B (all
+    225 linears, n/world rows each, k = 10%, N = 4), the norm exchange through the host
+    all-reduce; on the sampled layers every rank's rows of the parameters, moments, step
+    counts and compact block are bit-exact against the oracle on the FULL matrices
+    (P:481 the 4-way [1024, 4096] shard; S:219 sharding never changes the selection)."""
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    sys.path.insert(0, os.path.join(root, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import synth
+    from gpu_util import assert_bits_equal, assert_close_rel, selection_ok, to_np
+    from oracle import oracle as orc
+    from paper_2505_12242_b200 import zf
+    from paper_2505_12242_b200.dist import gloo_allreduce, shard_rows
+    from synth import gpu
+
+    torch.cuda.set_device(0)
+    full = [(n, m) for _, n, m in synth.llama2_7b_linears()]
+    spans = [shard_rows(n, world, rank) for n, _ in full]
+    local = [(b - a, m) for (a, b), (_, m) in zip(spans, full)]
+    ctx = zf.Context([zf.LayerShape(n, m) for n, m in local], topk_ratio_ppm=100000, refresh_interval=4,
+                     accum_interval=4, adam=zf.adam_params(lr=1e-3), world=world, rank=rank,
+                     host_allreduce=gloo_allreduce())
+    tot = sum(n * m for n, m in local)
+    gbuf = torch.empty(tot, dtype=torch.bfloat16, device="cuda")
+    pbuf = torch.empty(tot, dtype=torch.bfloat16, device="cuda")
+    Gs, Ps, off = [], [], 0
+    for n, m in local:
+        Gs.append(gbuf[off:off + n * m].view(n, m))
+        Ps.append(pbuf[off:off + n * m].view(n, m))
+        off += n * m
+    scales = [gpu.ColScale(m, li) for li, (_, m) in enumerate(full)]
+    for li, P in enumerate(Ps):
+        gpu.fill_param(P, li, row0=spans[li][0])
+    oracle = {li: orc.OracleLayer(n=full[li][0], m=full[li][1], ratio_ppm=100000, refresh_interval=4,
+                                  accum_interval=4, hp=orc.AdamHP(lr=1e-3)) for li in sample}
+    Po = {}
+    for li in sample:
+        Pf = torch.empty(full[li], dtype=torch.bfloat16, device="cuda")
+        gpu.fill_param(Pf, li)
+        Po[li] = to_np(Pf)
+        del Pf
+    for t in range(steps):
+        for li in range(len(full)):
+            scales[li].advance_to(t)
+            gpu.fill_grad(Gs[li], li, t, scales[li], row0=spans[li][0])
+        ctx.step(t, Gs, Ps)
+        ctx.sync()
+        for li in sample:
+            (n, m), (a, b), L = full[li], spans[li], oracle[li]
+            Gf = torch.empty(n, m, dtype=torch.bfloat16, device="cuda")
+            gpu.fill_grad(Gf, li, t, scales[li])        # the full matrix (GPU twin of synth.grad)
+            Gn = to_np(Gf)
+            del Gf
+            gidx = to_np(ctx.selected(li))
+            if t % 4 == 0:
+                onorms = orc.column_norms(Gn)
+                assert_close_rel(to_np(ctx.norms(li)), onorms, 1e-5, f"rank {rank} norms t={t} l={li}")
+                selection_ok(gidx, orc.topk(onorms, L.k), onorms)
+            out = L.step(t, Gn, Po[li], idx_override=gidx if t % 4 == 0 else None)
+            M, V, st = ctx.optimizer_state(li)
+            assert_bits_equal(to_np(st), L.steps, f"rank {rank} steps t={t} l={li}")
+            assert_bits_equal(to_np(M), L.M[a:b], f"rank {rank} exp_avg t={t} l={li}")
+            assert_bits_equal(to_np(V), L.V[a:b], f"rank {rank} exp_avg_sq t={t} l={li}")
+            assert_bits_equal(to_np(Ps[li]), Po[li][a:b], f"rank {rank} params t={t} l={li}")
+            assert_bits_equal(to_np(ctx.compact_buffer(li)), out[a:b], f"rank {rank} compact t={t} l={li}")
+    sel = torch.from_numpy(np.concatenate([to_np(ctx.selected(li)) for li in range(len(full))]).astype(np.int64))
+    gathered = [torch.empty_like(sel) for _ in range(world)]
+    dist.all_gather(gathered, sel)
+    assert all(torch.equal(g, gathered[0]) for g in gathered)
+    ctx.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.slow
+def test_llama2_7b_four_row_shards_one_gpu():
+    """Config 4 at P = 4 (all 225 Llama-2-7B linears, 1/4 of the rows per process, four
+    processes on one GPU): q_proj, down_proj of block 0 and lm_head checked on every rank
+    over two refresh periods' worth of steps."""
+    from paper_2505_12242_b200 import _build
+    _build.build()
+    mp.spawn(_worker_fullsize, args=(4, _free_port(), 5, [0, 6, 224]), nprocs=4, join=True)

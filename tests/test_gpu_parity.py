@@ -181,7 +181,7 @@ def test_compact_into_pinned_host(zf, orc, gpu, n, m, dt):
 # ------------------------------------------------------------------ zf_step vs oracle, multi-step
 def _run_stateful(zf, orc, gpu, shapes, gdt, pdt, ppm, N, S, steps, offload, lr=1e-3, wd=0.0, check_every=1,
                   tie=False, ld_pad=0, cpu_update=False, warmup=0, state_offload=False, devacc=False,
-                  cpu_async=False):
+                  cpu_async=False, side_stream=False):
     hp_o = orc.AdamHP(lr=lr, weight_decay=wd)
     ctx = zf.Context([zf.LayerShape(n, m, m + ld_pad, m + ld_pad) for n, m in shapes], grad_dtype=TDT[gdt],
                      param_dtype=TDT[pdt], topk_ratio_ppm=ppm, refresh_interval=N, accum_interval=S,
@@ -205,8 +205,17 @@ def _run_stateful(zf, orc, gpu, shapes, gdt, pdt, ppm, N, S, steps, offload, lr=
                 sc.advance_to(t)
                 gpu.fill_grad(G, li, t, sc)
         Gn = [np.ascontiguousarray(to_np(G)) for G in Gs]
-        ctx.step(t, Gs, Ps)
-        ctx.sync()
+        if side_stream:
+            # a caller's non-blocking stream (every torch side stream is one): the library's
+            # host->device uploads must be ordered on it, not on the legacy default stream
+            ss = torch.cuda.Stream()
+            ss.wait_stream(torch.cuda.current_stream())
+            ctx.step(t, Gs, Ps, stream=ss)
+            ctx.sync()
+            ss.synchronize()
+        else:
+            ctx.step(t, Gs, Ps)
+            ctx.sync()
         warm = t < warmup
         refresh = not warm and (t - warmup) % N == 0
         for li, (n, m) in enumerate(shapes):
@@ -346,6 +355,14 @@ def test_step_cpu_update_async(zf, orc, gpu, NS, pdt, devacc):
     gdt = "bf16" if pdt == "bf16" else "fp32"
     _run_stateful(zf, orc, gpu, [(256, 512), (37, 1001)], gdt, pdt, 100000, NS, NS, 9, offload=True,
                   cpu_update=True, cpu_async=True, devacc=devacc)
+
+
+@pytest.mark.parametrize("cpu_async", [False, True])
+def test_step_cpu_update_on_a_side_stream(zf, orc, gpu, cpu_async):
+    """f1 with zf_step on a non-blocking torch stream: the refresh's column-list uploads and
+    the K5 scatter are ordered on the caller's stream (bit-exact vs the oracle)."""
+    _run_stateful(zf, orc, gpu, [(96, 300), (64, 128)], "bf16", "bf16", 100000, 2, 2, 7, offload=True,
+                  cpu_update=True, cpu_async=cpu_async, side_stream=True)
 
 
 def test_cpu_update_async_is_stale_until_the_next_call(zf, gpu):
@@ -543,6 +560,14 @@ def test_llama2_7b_fullsize_sampled(zf, orc, gpu):
     """BASELINE config 3 at full size (225 linears, 6.6 G elements, k=10%), refresh at
     t=0 then a steady step; q_proj, gate_proj, down_proj of layer 0 and lm_head checked."""
     _run_fullsize(zf, orc, gpu, synth.llama2_7b_linears(), 100000, 2, [0, 4, 6, 224], offload=False)
+
+
+@pytest.mark.slow
+def test_llama2_7b_fullsize_k1pct_sampled(zf, orc, gpu):
+    """BASELINE config 3 at k = 1% (225 linears, 6.6 G elements; k = 41 / 111 per matrix), in
+    the bench's launch configuration, over two refreshes (t = 0 and 4) and the steady steps
+    between them; q_proj, gate_proj, down_proj of layer 0 and lm_head checked."""
+    _run_fullsize(zf, orc, gpu, synth.llama2_7b_linears(), 10000, 5, [0, 4, 6, 224], offload=False)
 
 
 @pytest.mark.slow

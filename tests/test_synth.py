@@ -82,3 +82,16 @@ def test_gpu_generator_bit_identical():
         want = synth.grad_tie(n, m, layer, 2, dtype=dt)
         got = out.cpu().view(torch.int16).numpy().view(np.uint16) if dt == "bf16" else out.cpu().numpy()
         assert np.array_equal(got.view(np.uint8), want.view(np.uint8)), dt
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_host_c_twin_bit_identical(dtype):
+    """synth/synth_host.c (used to generate full-size inputs for the CPU-oracle timing) is
+    bit-identical to the numpy recipe: scales over several steps, gradients, params, shards."""
+    from synth import host
+    for m, layer, step in ((300, 3, 0), (4096, 7, 5), (257, 1, 12)):
+        e = synth.col_scale_at(m, step, layer)
+        assert np.array_equal(host.col_scale_at(m, step, layer), e)
+        assert np.array_equal(host.grad(9, m, layer, step, e, dtype, row0=13),
+                              synth.grad(9, m, layer, step, e, dtype, row0=13))
+        assert np.array_equal(host.param(5, m, layer, dtype, row0=2), synth.param(5, m, layer, dtype, row0=2))
