@@ -214,6 +214,22 @@ typedef struct {
                                          unselected columns are one window stale.  The
                                          parameter buffers of that last step must stay
                                          valid until then.                              */
+    int32_t param_subset;             /* 1: the selective optimizer keeps its parameter
+                                         subset p[:, idx] as a dense [n, k] block in HBM
+                                         ("a selective-optimizer, initialized only
+                                         with the corresponding parameter subset"): every
+                                         refresh step re-reads the selected columns from
+                                         p and rewrites the block; steady steps read p's
+                                         current value from the block instead of p's
+                                         row-major sectors (2 B per selected element
+                                         instead of most of p: a selected column touches
+                                         ~83% of p's 32-byte sectors at k = 10%), and
+                                         store an updated value to both p and the block
+                                         when its bits change.  Results are bit-identical.
+                                         Contract: between refreshes the library is the
+                                         only writer of the selected columns of p; a
+                                         caller that writes them calls zf_params_changed
+                                         before the next zf_step.  0: read p itself.    */
 } zf_config;
 
 typedef struct zf_ctx zf_ctx;
@@ -297,6 +313,10 @@ zf_status zf_set_lr(zf_ctx* ctx, double lr);
  * them. */
 zf_status zf_profile(zf_ctx* ctx, int32_t enable);
 zf_status zf_profile_read(zf_ctx* ctx, double* ms, int64_t* count);
+/* param_subset: the caller wrote p (e.g. loaded a checkpoint) outside zf_step; the next
+ * zf_step re-reads the selected columns from p (as a refresh does) before using them. */
+zf_status zf_params_changed(zf_ctx* c);
+
 /* Number of this library's kernel launches issued so far by the context. */
 int64_t zf_kernel_launches(zf_ctx* ctx);
 zf_status zf_destroy(zf_ctx* ctx);

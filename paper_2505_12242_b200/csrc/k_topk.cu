@@ -26,19 +26,20 @@ constexpr int K2_THREADS = 1024;
 constexpr int K2_WARPS = K2_THREADS / 32;
 constexpr int64_t K2_SMEM_KEYS_MAX = 48 * 1024;  // keys held in shared memory up to this m
 
-// Unselected columns of one mask word, in order: ucol[j] = byte offset of the column in
-// its K3 segment's tile row.  j0 = index of the word's first unselected column.
+// Unselected columns of one mask word, in order: ucol[j] = the column's byte offset in the
+// row, modulo 2^16 (K3 subtracts its tile's first byte offset modulo 2^16, so the list serves
+// every unit shape whose tile rows are shorter than 64 KB).  j0 = index of the word's first
+// unselected column.
 __device__ __forceinline__ void emit_ucol(uint16_t* ucol, uint32_t word, int64_t w, int64_t m, int64_t j0,
-                                          int64_t seg_cols, int gsz) {
+                                          int64_t /*seg_cols*/, int gsz) {
     uint32_t keep = ~word;
     const int64_t cbase = w * 32;
     if (cbase + 32 > m) keep &= (1u << (m - cbase)) - 1u;
-    const int64_t segoff = cbase % seg_cols;  // seg_cols is m or a multiple of 32
     int64_t j = j0;
     while (keep) {
         const int b = __ffs(keep) - 1;
         keep &= keep - 1u;
-        ucol[j++] = (uint16_t)((segoff + b) * gsz);
+        ucol[j++] = (uint16_t)(((cbase + b) * gsz) & 0xffff);
     }
 }
 

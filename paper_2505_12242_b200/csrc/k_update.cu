@@ -10,25 +10,26 @@
 // gradients to the CPU".  Moment carry-over across a refresh: reading R7.
 //
 // B200 design (DESIGN.md §5 K3).  HBM-bound: per element of G it moves 2 B of
-// G, 2(1-κ) B of compact output, and for the selected columns the read-modify-
-// write of p (in 32-byte sectors) and of the fp32 moments.
+// G, 2(1-κ) B of compact output, and for the selected columns p (the dense
+// parameter-subset slab on steady steps, p's 32-byte sectors on refreshes) and
+// the fp32 moments.
 //  - persistent grid, one CTA per SM, warp-specialised: 4 producer warps (one
 //    thread each, one stage arena each) and 20 consumer warps in two groups of 10.
-//    Work units (R rows x c columns, c = m or a 128-aligned segment) are claimed
-//    dynamically, one atomic per unit.
-//  - a producer prefetches the claimed unit's G / p rows and moment slabs into L2
-//    while its arena is still being consumed, then stages EVERYTHING the unit needs
-//    into its 56 KB arena with bulk copies (cp.async.bulk, the TMA engine) completing
-//    on one mbarrier: the G tile, the p tile (when the selection touches most of p's
-//    32-byte sectors), the moment slabs (or the old rows on a refresh), the slot step
-//    counts, column indices and remap sources, the mask words and the segment's list
-//    of unselected-column byte offsets (written by K2).  Consumers issue no global
-//    loads; waits are hardware-suspended (mbarrier.try_wait).
-//  - consumers: slot-major AdamW (a slot's column, step count and bias corrections
-//    read once for all its rows; explicit round-to-nearest intrinsics in the
-//    oracle's op order), p read from the staged tile and each changed value stored
-//    straight to HBM; then compaction by gather (8 bf16 outputs per thread per vector
-//    store, coalesced across the warp).
+//    Work units (R rows x c columns) are claimed dynamically, one atomic per unit;
+//    refresh and steady steps use their own unit shapes (a steady unit holds no p tile).
+//  - a producer prefetches the claimed unit's G rows / slabs into L2 while its arena is
+//    still being consumed, then stages the unit's DATA into its arena with bulk copies
+//    (cp.async.bulk, the TMA engine) completing on one mbarrier: the G tile, the p tile
+//    (refresh, when the selection touches most of p's 32-byte sectors) or the dense
+//    parameter-subset slab (steady), and the moment slabs (or the old rows on a refresh).
+//    The layer's selection METADATA (selected columns, per-slot bias corrections, remap
+//    sources, the unselected-column list) is not staged: every unit of a layer reads the
+//    same arrays, so the consumers read them through L1 and the arenas carry only data
+//    (more bytes in flight per SM).  Waits are hardware-suspended (mbarrier.try_wait).
+//  - consumers: slot-major AdamW (a slot's column and bias corrections read once for all
+//    its rows; explicit round-to-nearest intrinsics in the oracle's op order), each
+//    changed p value stored straight to HBM; then compaction by gather (8 bf16 outputs per
+//    thread per vector store, coalesced across the warp).
 //  - with offload, each consumer warp bumps a per-layer counter after its share of
 //    a unit (red.release); the copy stream waits on it (cuStreamWaitValue32) to
 //    start the layer's device->host copy.
@@ -39,12 +40,6 @@
 namespace zf {
 namespace {
 
-// p updates go straight from the AdamW phase to HBM (only values whose bits changed);
-// -DZF_K3_TILE_WRITEBACK restores the round-1 scheme (update the staged tile, then write back
-// every 16-byte chunk holding a selected column after a group barrier).
-#ifndef ZF_K3_TILE_WRITEBACK
-#define ZF_K3_PDIRECT 1
-#endif
 // producers prefetch a claimed unit's G / p rows and moment slabs into L2 while its arena is
 // still busy
 // (-DZF_K3_NO_L2PF disables)
@@ -52,7 +47,7 @@ namespace {
 #define ZF_K3_L2PF 1
 #endif
 #ifndef ZF_K3_NCW
-#define ZF_K3_NCW 20
+#define ZF_K3_NCW 28   // 2 groups of 14 (64 registers per thread); measured best of 16-28 (tools/k3_flags.sh)
 #endif
 constexpr int K3_NCW = ZF_K3_NCW;                 // consumer warps
 #ifndef ZF_K3_ROW_UNROLL
@@ -64,11 +59,21 @@ constexpr int K3_ROW_UNROLL = ZF_K3_ROW_UNROLL;   // rows of one slot in flight 
 #endif
 constexpr int K3_GROUPS = ZF_K3_GROUPS;           // independent consumer groups; group g owns stages g, g+G, ...
 constexpr int K3_GW = K3_NCW / K3_GROUPS;         // warps per group
+#ifndef ZF_K3_AW
+#define ZF_K3_AW 0
+#endif
+// role split inside a group: warps [0, K3_AW) run the unit's AdamW while warps [K3_AW, K3_GW)
+// run its compaction, concurrently (0: every warp runs both phases, one after the other)
+constexpr int K3_AW = ZF_K3_AW;
+constexpr int K3_AWARPS = K3_AW > 0 ? K3_AW : K3_GW;   // warps that run AdamW
+constexpr int K3_CW0 = K3_AW > 0 ? K3_AW : 0;          // first compaction warp of a group
+constexpr int K3_CWARPS = K3_GW - K3_CW0;              // warps that run the compaction
+static_assert(K3_AW >= 0 && K3_AW < K3_GW, "role split");
 #ifndef ZF_K3_STAGES
 #define ZF_K3_STAGES 4
 #endif
 #ifndef ZF_K3_ARENA_KB
-#define ZF_K3_ARENA_KB 56
+#define ZF_K3_ARENA_KB 48   // 4 x 48 KB of stages leaves ~60 KB of L1 for the layers' metadata
 #endif
 constexpr int K3_STAGES = ZF_K3_STAGES;           // stage arenas = producer warps (one chain per stage)
 constexpr int K3_THREADS = 32 * (K3_NCW + K3_STAGES);
@@ -147,12 +152,7 @@ __device__ __forceinline__ void st_cs_v4(void* p, uint4 v) {
                  : "memory");
 }
 
-__device__ __forceinline__ uint4 lds128(const void* p) {
-    uint4 v;
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "r"(smem_u32(p)) : "memory");
-    return v;
-}
+
 // Bulk-copy the ESZ-byte elements [e0, e1) of `src` to arena offset *off as an aligned
 // superset (16-byte granules; the source arrays are padded).  Returns the element
 // offset of e0 within the copy; advances *off.
@@ -181,10 +181,7 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
     return v;
 }
-__device__ __forceinline__ void st_v4(void* p, uint4 v) {
-    asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-                 : "memory");
-}
+
 
 __device__ __forceinline__ int find_layer_from(const Table<UpdLayer>& t, int64_t u, int hint) {
     int li = hint;
@@ -215,9 +212,9 @@ struct StageInfo {
     int64_t u;        // unit (-1: no more work)
     int32_t li;       // layer
     int32_t s0, s1;   // selected-slot range of the segment
-    int32_t oG, oP, oM, oV, oS, oSrc, oMask, oIdx, oU;
-    int32_t eM, eV, eS, eSrc, eMask, eIdx, eU;
-    int32_t pstaged, mstaged, remap;
+    int32_t oG, oP, oM, oV, oPs;
+    int32_t eM, eV, ePs;
+    int32_t pstaged, mstaged, remap, psub_mode;
     int32_t j0, nkeep;          // segment's first output index within a row / outputs per row
     uint32_t mg_ns;             // ceil(2^24 / ns): x / ns == (x * mg_ns) >> 24 for x <= 512
     // unit geometry and layer fields, so consumers never touch the global layer table
@@ -228,38 +225,44 @@ struct StageInfo {
     void* out;                  // compact block of the layer
     float* m_out;               // + r0*k
     float* v_out;
+    void* psub;                 // param_subset block + r0*k (NULL: none)
     const float* m_in;          // layer base (non-staged path)
     const float* v_in;
-    const int32_t* steps;       // layer base (non-staged path)
-    const int32_t* slot_src;
-    const int32_t* idx;
+    // per-layer selection metadata, read by the consumers through L1 (every unit of a layer
+    // reads the same arrays, so they stay cache-resident instead of taking stage bytes)
+    const int32_t* steps;       // [k] step counts at the last refresh (used when sbv is NULL)
+    const float2* sbv;          // [k] per-slot {ss, bc2s} of this launch (K3 prologue), or NULL
+    const int32_t* slot_src;    // [k] remap sources (refresh)
+    const int32_t* idx;         // [k] selected columns
+    const uint16_t* ucol;       // [m-k] byte offsets (mod 2^16) of the unselected columns
     uint32_t* done;
 };
 
 // AdamW over one unit's (row, slot) pairs by the K3_GW*32 threads of a consumer group,
-// slot-major: a slot's column, step count and bias corrections are read once for all of
-// its rows.  PST: p tile staged (updated there, written back later); MST: moments, step
-// counts, column indices (and remap sources) staged; REMAP: refresh step (moments come from
-// the old slots).  Without MST the remap flag is read at run time (global-load path).
-template <int GDT, int PDT, bool PST, bool MST, bool REMAP>
+// slot-major: a slot's column, bias corrections (and remap source) are read once for all of
+// its rows.  PST: p tile staged; MST: moment slabs staged; REMAP: refresh step (moments come
+// from the old slots); PSUB: p's current values from the staged subset slab (steady step with
+// param_subset).  Without MST the remap flag is read at run time (global-load path).  Every
+// changed p value is stored straight to HBM (and to the subset block).
+template <int GDT, int PDT, bool PST, bool MST, bool REMAP, bool PSUB = false, int NCT = K3_AWARPS * 32>
 __device__ __forceinline__ void adam_unit(const StageInfo& si, unsigned char* A, const UpdParams& prm, int ctid,
                                           uint32_t& nfacc) {
+    static_assert(!PSUB || (MST && !REMAP && !PST), "the subset slab is staged on steady steps only");
     using GE = Elt<GDT>;
     using PE = Elt<PDT>;
     using GB = typename GE::bits;
     using PB = typename PE::bits;
-    constexpr int NCT = K3_GW * 32;
     const int sw = si.sw, Rr = si.Rr, ns = si.s1 - si.s0;
     const int k = si.k, kin = si.kin, s0 = si.s0, c0 = (int)si.c0;
     const bool remap = MST ? REMAP : (si.remap != 0);
     const GB* sG = reinterpret_cast<const GB*>(A + si.oG);
-    PB* sP = reinterpret_cast<PB*>(A + si.oP);
+    const PB* sP = reinterpret_cast<const PB*>(A + si.oP);
     const float* sM = reinterpret_cast<const float*>(A + si.oM) + si.eM;
     const float* sV = reinterpret_cast<const float*>(A + si.oV) + si.eV;
-    const int32_t* sS = reinterpret_cast<const int32_t*>(A + si.oS) + si.eS;
-    const int32_t* sSrc = reinterpret_cast<const int32_t*>(A + si.oSrc) + si.eSrc;
-    const int32_t* sIdx = reinterpret_cast<const int32_t*>(A + si.oIdx) + si.eIdx;
+    const PB* sPs = reinterpret_cast<const PB*>(A + si.oPs) + si.ePs;   // PSUB: staged [R, s0:s1) subset slab
     PB* gP = static_cast<PB*>(si.P);
+    PB* gS = static_cast<PB*>(si.psub);                                  // subset block rows of the unit
+    const int pmode = si.psub_mode;
     const int64_t ldp = si.ldp;
     const int tdelta = prm.step_delta + 1;
     uint32_t dbg_sink = 0;
@@ -274,21 +277,12 @@ __device__ __forceinline__ void adam_unit(const StageInfo& si, unsigned char* A,
     }
     for (; sl < ns; sl += NCT) {
         const int s = s0 + sl;
-        int c, stp, src = 0;
-        if constexpr (MST) {
-            c = sIdx[sl];
-            stp = sS[sl];
-            if constexpr (REMAP) src = sSrc[sl];
-        } else {
-            c = __ldg(si.idx + s);
-            stp = __ldg(si.steps + s);
-            if (remap) src = __ldg(si.slot_src + s);
-        }
-        const float2 sb = adam_sb(stp + tdelta, prm.adam);
+        const int c = __ldg(si.idx + s);
+        // {ss, bc2s} of the slot's step count: the prologue's per-slot array, else the tables
+        const float2 sb = si.sbv ? __ldg(si.sbv + s) : adam_sb(__ldg(si.steps + s) + tdelta, prm.adam);
+        const int src = remap ? __ldg(si.slot_src + s) : 0;
         const int cl = c - c0;
         const GB* g_ = sG + cl;
-        PB* p_ = PST ? sP + cl : gP + c;
-        const int pstride = PST ? sw : (int)0;
         float* mo = si.m_out + s;
         float* vo = si.v_out + s;
 #pragma unroll K3_ROW_UNROLL
@@ -296,8 +290,10 @@ __device__ __forceinline__ void adam_unit(const StageInfo& si, unsigned char* A,
             const GB gb = g_[r * sw];
             if constexpr (GE::SIZE == 2) nfacc |= ((uint32_t)gb & 0x7f80u) + 0x0080u;
             else nfacc |= ((uint32_t)gb & 0x7f800000u) + 0x00800000u;
-            PB* pp = PST ? p_ + r * pstride : p_ + r * ldp;
-            const PB pold = *pp;
+            PB pold;
+            if constexpr (PSUB) pold = sPs[r * k + sl];
+            else if constexpr (PST) pold = sP[r * sw + cl];
+            else pold = pmode == 2 ? gS[r * k + s] : gP[r * ldp + c];
             float p = PE::to_f(pold);
             float mm, vv;
             if constexpr (MST) {
@@ -319,16 +315,14 @@ __device__ __forceinline__ void adam_unit(const StageInfo& si, unsigned char* A,
                 }
             }
             adamw_elem_t(GE::to_f(gb), p, mm, vv, sb.x, sb.y, prm.adam);
-#ifdef ZF_K3_PDIRECT
             {
-                // p read from the staged tile, a changed value stored straight to HBM: no tile
-                // write-back phase and no group barrier (same memory state)
+                // a changed value is stored straight to HBM (the memory state is that of storing
+                // every value; at lr 1e-5 most bf16 values do not change); param_subset: mode 1
+                // (re)builds the block, mode 2 keeps it equal to p
                 const PB pnew = PE::from_f(p);
                 if (pnew != pold) gP[r * ldp + c] = pnew;
+                if (pmode == 1 || (pmode == 2 && pnew != pold)) gS[r * k + s] = pnew;
             }
-#else
-            *pp = PE::from_f(p);
-#endif
             if (prm.debug_mode != 7) {
                 __stcs(mo + r * k, mm);
                 __stcs(vo + r * k, vv);
@@ -340,6 +334,128 @@ __device__ __forceinline__ void adam_unit(const StageInfo& si, unsigned char* A,
     asm volatile("" ::"r"(dbg_sink));  // debug mode 7 keeps the moment math live
 }
 
+#ifndef ZF_K3_NB
+#define ZF_K3_NB 1
+#endif
+// Staged-moment AdamW (MST) in batches: each thread takes NB (row, slot) pairs at a time --
+// pair q = row * ns + slot, q = ctid, ctid + NCT, ... (row-major, so the warp's 32 lanes hold
+// 32 consecutive slots of one row: conflict-free slab reads and coalesced moment stores) --
+// and issues every load of the batch (the slots' columns and {ss, bc2s} through L1, then g, p,
+// m, v from the stage) before any arithmetic: NB independent chains per thread instead of one
+// latency-bound chain per slot.
+template <int GDT, int PDT, bool PST, bool REMAP, bool PSUB, int NCT = K3_AWARPS * 32, int NB = ZF_K3_NB>
+__device__ __forceinline__ void adam_unit_b(const StageInfo& si, unsigned char* A, const UpdParams& prm, int ctid,
+                                            uint32_t& nfacc) {
+    static_assert(!PSUB || (!REMAP && !PST), "the subset slab is staged on steady steps only");
+    using GE = Elt<GDT>;
+    using PE = Elt<PDT>;
+    using GB = typename GE::bits;
+    using PB = typename PE::bits;
+    const int sw = si.sw, Rr = si.Rr, ns = si.s1 - si.s0;
+    const int k = si.k, kin = si.kin, s0 = si.s0, c0 = (int)si.c0;
+    const GB* sG = reinterpret_cast<const GB*>(A + si.oG);
+    const PB* sP = reinterpret_cast<const PB*>(A + si.oP);
+    const float* sM = reinterpret_cast<const float*>(A + si.oM) + si.eM;
+    const float* sV = reinterpret_cast<const float*>(A + si.oV) + si.eV;
+    const PB* sPs = reinterpret_cast<const PB*>(A + si.oPs) + si.ePs;
+    PB* gP = static_cast<PB*>(si.P);
+    PB* gS = static_cast<PB*>(si.psub);
+    const int pmode = si.psub_mode;
+    const int ldp = (int)si.ldp;       // < 2^31 / Rr: unit-relative offsets fit 32 bits
+    const int tdelta = prm.step_delta + 1;
+    const int total = Rr * ns;
+    // (row, slot) of pair ctid and the per-NCT step, by the exact multiply-shift ns reciprocal
+    int r = (int)(((uint64_t)ctid * si.mg_ns) >> 24), sl = ctid - r * ns;
+    const int dr = (int)(((uint64_t)NCT * si.mg_ns) >> 24), dsl = NCT - dr * ns;
+    uint32_t dbg_sink = 0;
+    for (int q = ctid; q < total; q += NCT * NB) {
+        int so[NB], pa[NB], cc[NB], src[NB], rr[NB];
+        float2 sb[NB];
+        GB gb[NB];
+        PB po[NB];
+        float mm[NB], vv[NB];
+        // (A) the batch's pairs: per-slot loads through L1
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+            rr[j] = r;
+            so[j] = r * k + s0 + sl;                 // [row, slot] offset in the unit's slab rows
+            pa[j] = r * ldp - c0;                    // row offset in p, minus the tile's first column
+            if (q + j * NCT < total) {
+                const int s = s0 + sl;
+                cc[j] = __ldg(si.idx + s);
+                sb[j] = si.sbv ? __ldg(si.sbv + s) : adam_sb(__ldg(si.steps + s) + tdelta, prm.adam);
+                if constexpr (REMAP) src[j] = __ldg(si.slot_src + s) + r * kin;
+            }
+            r += dr;
+            sl += dsl;
+            if (sl >= ns) { sl -= ns; ++r; }
+        }
+        // (B) stage reads (g, p, m, v) of every pair of the batch
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+            if (q + j * NCT < total) {
+                const int row = rr[j];
+                const int cl = cc[j] - c0;
+                gb[j] = sG[row * sw + cl];
+                if constexpr (PSUB) po[j] = sPs[so[j] - s0];
+                else if constexpr (PST) po[j] = sP[row * sw + cl];
+                else po[j] = pmode == 2 ? gS[so[j]] : gP[pa[j] + c0 + cc[j]];
+                if constexpr (REMAP) {
+                    const bool ok = src[j] >= row * kin;
+                    mm[j] = ok ? sM[src[j]] : 0.0f;
+                    vv[j] = ok ? sV[src[j]] : 0.0f;
+                } else {
+                    mm[j] = sM[so[j] - s0];
+                    vv[j] = sV[so[j] - s0];
+                }
+                pa[j] += c0 + cc[j];
+            }
+        }
+        // (C) arithmetic and stores
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+            if (q + j * NCT < total) {
+                if constexpr (GE::SIZE == 2) nfacc |= ((uint32_t)gb[j] & 0x7f80u) + 0x0080u;
+                else nfacc |= ((uint32_t)gb[j] & 0x7f800000u) + 0x00800000u;
+                float p = PE::to_f(po[j]);
+                adamw_elem_t(GE::to_f(gb[j]), p, mm[j], vv[j], sb[j].x, sb[j].y, prm.adam);
+                const PB pnew = PE::from_f(p);
+                if (prm.debug_mode < 9 || prm.debug_mode > 14) {
+                    if (pnew != po[j]) gP[pa[j]] = pnew;
+                    if (pmode == 1 || (pmode == 2 && pnew != po[j])) gS[so[j]] = pnew;
+                } else if (prm.debug_mode == 12) {   // experiments: 9 no p / subset stores; 12 no subset stores
+                    if (pnew != po[j]) gP[pa[j]] = pnew;
+                } else if (prm.debug_mode == 13) {   // 13 no p stores
+                    if (pmode == 1 || (pmode == 2 && pnew != po[j])) gS[so[j]] = pnew;
+                } else if (prm.debug_mode == 14) {   // 14 every p / subset value stored (no branch)
+                    gP[pa[j]] = pnew;
+                    gS[so[j]] = pnew;
+                } else {
+                    dbg_sink ^= pnew;
+                }
+                if (prm.debug_mode != 7 && prm.debug_mode != 10) {   // (10: no moment stores)
+                    __stcs(si.m_out + so[j], mm[j]);
+                    __stcs(si.v_out + so[j], vv[j]);
+                } else {
+                    dbg_sink ^= __float_as_uint(mm[j]) ^ __float_as_uint(vv[j]);
+                }
+            }
+        }
+    }
+    asm volatile("" ::"r"(dbg_sink));
+}
+
+__device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint2 ldg_nc_v2(const void* p) {
+    uint2 v;
+    asm volatile("ld.global.nc.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+}
+
 template <int GDT, int PDT>
 __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant__ UpdParams prm) {
     using GE = Elt<GDT>;
@@ -349,7 +465,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
     constexpr int GSZ = GE::SIZE, PSZ = PE::SIZE;
 
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t full[K3_STAGES], empty[K3_STAGES], gbar[K3_GROUPS];
+    __shared__ __align__(8) uint64_t full[K3_STAGES], empty[K3_STAGES];
     __shared__ StageInfo info[K3_STAGES];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -360,7 +476,6 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
             mbar_init(&full[st], 1);
             mbar_init(&empty[st], K3_GW);
         }
-        for (int g = 0; g < K3_GROUPS; ++g) mbar_init(&gbar[g], K3_GW);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -388,8 +503,8 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
                 si.s1 = g.c1 >= Lp->m ? (int32_t)Lp->k : __ldg(Lp->prefix + (g.c1 >> 5));
             }
 #ifdef ZF_K3_L2PF
-            if (si.u >= 0 && it > 0 && lane == 0) {
-                // the arena is still being consumed: pull this unit's G and p rows toward L2 now
+            if (si.u >= 0 && it > 0) {
+                // the arena is still being consumed: pull this unit's rows and slabs toward L2 now
                 const UpdLayer& L = *Lp;
                 const int sw = (int)(g.c1 - g.c0);
                 if (L.tma_ok) {
@@ -399,6 +514,9 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
                         for (int r = 0; r < g.Rr; ++r)
                             bulk_prefetch_l2(G + ((g.r0 + r) * L.ldg + g.c0) * GSZ, (int64_t)sw * GSZ);
                 }
+                if (prm.do_adam && si.s1 > si.s0 && L.psub_mode == 2 && L.mv_tma)
+                    bulk_prefetch_l2(static_cast<const unsigned char*>(L.psub) + (g.r0 * L.k + si.s0) * PSZ,
+                                     ((g.Rr - 1) * L.k + si.s1 - si.s0) * PSZ);
                 if (prm.do_adam && si.s1 > si.s0 && L.p_tma) {
                     const unsigned char* P = static_cast<const unsigned char*>(L.P);
                     if (L.nseg == 1 && L.ldp == L.m) bulk_prefetch_l2(P + g.r0 * L.m * PSZ, (int64_t)g.Rr * sw * PSZ);
@@ -452,35 +570,30 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
                     for (int c = 0; c < sw; ++c) sG[r * sw + c] = G[(g.r0 + r) * L.ldg + g.c0 + c];
             }
             off = (g.Rr * sw * GSZ + 15) & ~15;
-            // mask words of the segment (p write-back) and the segment's unselected-column list
-            const int64_t w0 = g.c0 >> 5, nwm = (sw + 31) >> 5;
-#ifndef ZF_K3_PDIRECT
-            si.eMask = stage_elems<4>(A, &off, L.mask, w0, w0 + nwm, &full[st], &tx, &si.oMask);
-#else
-            (void)w0;
-            (void)nwm;  // the mask words served the tile write-back only
-#endif
             si.j0 = (int32_t)(g.c0 - si.s0);
             si.nkeep = sw - ns;
-            if (prm.do_compact && si.nkeep > 0)
-                si.eU = stage_elems<2>(A, &off, L.ucol, si.j0, si.j0 + si.nkeep, &full[st], &tx, &si.oU);
             if (prm.do_adam && ns > 0) {
                 si.mg_ns = (uint32_t)(((1u << 24) + (uint32_t)ns - 1u) / (uint32_t)ns);
                 si.pstaged = L.p_tma;
                 si.mstaged = L.mv_tma;
+                si.psub_mode = L.psub_mode;
+                if (si.psub_mode == 2 && si.mstaged) {
+                    // steady step: p's current selected values from the dense subset block,
+                    // the [R, s0:s1) slab (same layout as the moment slab)
+                    const int64_t e0 = g.r0 * L.k + si.s0, e1 = (g.r0 + g.Rr - 1) * L.k + si.s1;
+                    si.ePs = stage_elems<PSZ>(A, &off, L.psub, e0, e1, &full[st], &tx, &si.oPs);
+                }
                 if (si.pstaged) {
                     const unsigned char* P = static_cast<const unsigned char*>(L.P);
                     si.oP = off;
-                    if (prm.debug_mode == 4) {
-                        // traffic experiment: write back touched p chunks without reading p
-                    } else if (L.nseg == 1 && L.ldp == L.m) {
+                    if (L.nseg == 1 && L.ldp == L.m) {
                         bulk_g2s(A + off, P + g.r0 * L.m * PSZ, (uint32_t)(g.Rr * sw * PSZ), &full[st], pol_last);
                     } else {
                         for (int r = 0; r < g.Rr; ++r)
                             bulk_g2s(A + off + r * sw * PSZ, P + ((g.r0 + r) * L.ldp + g.c0) * PSZ,
                                      (uint32_t)(sw * PSZ), &full[st], pol_last);
                     }
-                    if (prm.debug_mode != 4) tx += (uint32_t)(g.Rr * sw * PSZ);
+                    tx += (uint32_t)(g.Rr * sw * PSZ);
                     off += (g.Rr * sw * PSZ + 15) & ~15;
                 }
                 if (si.mstaged) {
@@ -488,16 +601,12 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
                     if (L.slot_src) {  // refresh: the old moments of the unit's rows (full old rows)
                         e0 = g.r0 * L.k_in;
                         e1 = (g.r0 + g.Rr) * L.k_in;
-                    } else {           // steady: the [R, s0:s1) slab (contiguous: full rows, or R == 1)
+                    } else {           // steady: the [R, s0:s1) slab (a superset when R > 1 and segmented)
                         e0 = g.r0 * L.k + si.s0;
                         e1 = (g.r0 + g.Rr - 1) * L.k + si.s1;
                     }
                     si.eM = stage_elems<4>(A, &off, L.m_in, e0, e1, &full[st], &tx, &si.oM);
                     si.eV = stage_elems<4>(A, &off, L.v_in, e0, e1, &full[st], &tx, &si.oV);
-                    si.eS = stage_elems<4>(A, &off, L.steps, si.s0, si.s1, &full[st], &tx, &si.oS);
-                    si.eIdx = stage_elems<4>(A, &off, L.idx, si.s0, si.s1, &full[st], &tx, &si.oIdx);
-                    if (L.slot_src)
-                        si.eSrc = stage_elems<4>(A, &off, L.slot_src, si.s0, si.s1, &full[st], &tx, &si.oSrc);
                 }
             }
             si.Rr = g.Rr;
@@ -513,11 +622,14 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
             si.out = L.out;
             si.m_out = L.m_out + g.r0 * L.k;
             si.v_out = L.v_out + g.r0 * L.k;
+            si.psub = L.psub ? static_cast<PB*>(L.psub) + g.r0 * L.k : nullptr;
             si.m_in = L.m_in;
             si.v_in = L.v_in;
             si.steps = L.steps;
+            si.sbv = L.sbv;
             si.slot_src = L.slot_src;
             si.idx = L.idx;
+            si.ucol = L.ucol;
             si.done = L.done;
             info[st] = si;
             mbar_expect_tx(&full[st], tx);  // the single arrival of this phase
@@ -528,14 +640,12 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
     // ===================== consumer warps =====================
     // Two groups of K3_GW warps; group g consumes stages g, g+2, ...  Per unit:
     //  (1) AdamW on the unit's (row, slot) pairs by all threads of the group, slot-major
-    //      (a slot's column, step count and bias corrections read once for all its rows);
-    //      p is updated in the staged tile (or in place in HBM when it was not staged);
-    //      each warp then arrives on the group's mbarrier (split phase: no waiting yet);
+    //      (a slot's column and bias corrections read once for all its rows); each changed p
+    //      value is stored straight to HBM;
     //  (2) compaction by gather, warp-wide windows of one row: lane l writes outputs
     //      8l..8l+7 (bf16; 4 for fp32) of the window with one 16-byte store, reading the
-    //      staged tile at the listed unselected-column offsets;
-    //  (3) wait for the group's AdamW, then write back every 16-byte chunk of the p tile
-    //      holding a selected column (warp-wide windows, one chunk per lane).
+    //      staged tile at the unselected-column offsets (the layer's list, through L1);
+    //  then each warp releases the stage.
     const int cwa = warp - K3_STAGES;          // consumer warp index
     const int grp = cwa / K3_GW;               // consumer group
     const int cw = cwa - grp * K3_GW;          // warp index within the group
@@ -544,7 +654,6 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
     uint32_t nfacc = 0;                // non-finite detector (exponent all-ones -> carry into the top bit)
     __nv_bfloat162 nf2 = __float2bfloat162_rn(0.0f);  // bf16: NaN-propagating max of |x|
     uint32_t finished = 0, phase = 0;  // per stage: end sentinel seen / mbarrier parity
-    uint32_t gphase = 0;               // parity of this group's AdamW-done barrier
 
     constexpr uint32_t kMine = [] {
         uint32_t m = 0;
@@ -553,7 +662,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
     }();
     const uint32_t mine = kMine << grp;  // the stages of my group
 #ifdef ZF_K3_PROF
-    // per-warp cycle accounting (lane 0): wait full, AdamW, compaction, group wait, write-back+release
+    // per-warp cycle accounting (lane 0): wait full, AdamW, compaction, -, release
     unsigned long long pc[6] = {0, 0, 0, 0, 0, 0};
     long long tq = clock64();
 #define ZF_TICK(i)                         \
@@ -589,39 +698,48 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
         const GB* sG = reinterpret_cast<const GB*>(A + si.oG);
         const int ns = si.s1 - si.s0;
         const bool adam = prm.do_adam && (prm.debug_mode == 0 || prm.debug_mode >= 3) && ns > 0;
-#ifdef ZF_K3_PDIRECT
-        const bool pwb = false;
-#else
-        const bool pwb = adam && si.pstaged;
-#endif
 
         // ---------------- (1) AdamW ----------------
-        if (adam) {
-            if (si.pstaged && si.mstaged) {
+        if (adam && cw < K3_AWARPS) {
+#ifndef ZF_K3_SLOTMAJOR
+            if (si.psub_mode == 2 && si.mstaged) {
+                adam_unit_b<GDT, PDT, false, false, true>(si, A, prm, ctid, nfacc);
+            } else if (si.pstaged && si.mstaged) {
+                if (si.remap) adam_unit_b<GDT, PDT, true, true, false>(si, A, prm, ctid, nfacc);
+                else adam_unit_b<GDT, PDT, true, false, false>(si, A, prm, ctid, nfacc);
+            } else if (si.mstaged) {
+                if (si.remap) adam_unit_b<GDT, PDT, false, true, false>(si, A, prm, ctid, nfacc);
+                else adam_unit_b<GDT, PDT, false, false, false>(si, A, prm, ctid, nfacc);
+            } else if (si.pstaged) {
+#else
+            if (si.psub_mode == 2 && si.mstaged) {
+                adam_unit<GDT, PDT, false, true, false, true>(si, A, prm, ctid, nfacc);
+            } else if (si.pstaged && si.mstaged) {
                 if (si.remap) adam_unit<GDT, PDT, true, true, true>(si, A, prm, ctid, nfacc);
                 else adam_unit<GDT, PDT, true, true, false>(si, A, prm, ctid, nfacc);
-            } else if (si.pstaged) {
-                adam_unit<GDT, PDT, true, false, false>(si, A, prm, ctid, nfacc);
             } else if (si.mstaged) {
                 if (si.remap) adam_unit<GDT, PDT, false, true, true>(si, A, prm, ctid, nfacc);
                 else adam_unit<GDT, PDT, false, true, false>(si, A, prm, ctid, nfacc);
+            } else if (si.pstaged) {
+#endif
+                adam_unit<GDT, PDT, true, false, false>(si, A, prm, ctid, nfacc);
             } else {
                 adam_unit<GDT, PDT, false, false, false>(si, A, prm, ctid, nfacc);
             }
-        }
-        if (pwb) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&gbar[grp]);  // release: this warp's tile updates
         }
 
         ZF_TICK(1);
         // ---------------- (2) compaction by gather ----------------
         const int nk = si.nkeep;
-        if (prm.do_compact && nk > 0 && prm.debug_mode != 3) {
+        const int cc = cw - K3_CW0;                // compaction warp index (role split)
+        const int cct = cc * 32 + lane;
+        if (prm.do_compact && nk > 0 && prm.debug_mode != 3 && cc >= 0) {
             constexpr int OPL = 16 / GSZ;              // outputs per lane (one 16-byte store)
             const int j0 = si.j0;
             const int old = (int)si.out_ld;
-            const uint16_t* sU = reinterpret_cast<const uint16_t*>(A + si.oU) + si.eU;
+            const uint16_t* gU = si.ucol + j0;         // the segment's unselected columns (byte offsets mod 2^16)
+            const uint32_t base = (uint32_t)((si.c0 * GSZ) & 0xffff);  // the tile's first byte offset
+            const uint32_t base2 = base | (base << 16);
             const uint32_t sGa = smem_u32(sG);
             GB* out = static_cast<GB*>(si.out) + si.r0 * si.out_ld + j0;   // row 0, output 0 of the unit
             if (old % OPL == 0) {
@@ -631,18 +749,41 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
                 const int tail = nk - qa - OPL * ng;
                 const int nwin = (ng + 31) >> 5;       // 32-group windows per row
                 if (nwin > 0) {
-                    int r = 0, w = cw;
-                    while (w >= nwin) { w -= nwin; ++r; }
-                    for (; r < Rr;) {
+                    // (window, row) pairs, window-major, in one contiguous share per warp: a
+                    // window's offset vector is loaded once for all its rows, and the next
+                    // window's is prefetched while the current one's rows are gathered
+                    const int npair = nwin * Rr;
+                    const int per = (npair + K3_CWARPS - 1) / K3_CWARPS;
+                    int f = cc * per;
+                    const int f1 = min(npair, f + per);
+                    int w = f / Rr, r = f - w * Rr;
+                    auto load_u = [&](int ww) {
+                        const int g = (ww << 5) + lane;
+                        uint4 u = make_uint4(0u, 0u, 0u, 0u);
+                        if (ww < nwin && g < ng) {
+                            if constexpr (GSZ == 2) u = ldg_nc_v4(gU + qa + OPL * g);
+                            else {
+                                const uint2 u2 = ldg_nc_v2(gU + qa + OPL * g);
+                                u.x = u2.x;
+                                u.y = u2.y;
+                            }
+                        }
+                        u.x = __vsub2(u.x, base2);    // per-halfword: offsets within the tile row
+                        u.y = __vsub2(u.y, base2);
+                        u.z = __vsub2(u.z, base2);
+                        u.w = __vsub2(u.w, base2);
+                        return u;
+                    };
+                    uint4 u = f < f1 ? load_u(w) : make_uint4(0u, 0u, 0u, 0u);
+                    uint4 un = u;
+                    for (; f < f1; ++f) {
+                        if (r == Rr - 1 && f + 1 < f1) un = load_u(w + 1);   // prefetch the next window
                         const int g = (w << 5) + lane;
                         if (g < ng) {
                             const int q = qa + OPL * g;
                             const uint32_t rowa = sGa + (uint32_t)(r * sw * GSZ);
                             uint4 o;
-                            if (prm.debug_mode == 8) {  // experiment: compaction stores without its shared-memory gathers
-                                o = make_uint4(q, r, 0u, 0u);
-                            } else if constexpr (GSZ == 2) {
-                                const uint4 u = lds128(sU + q);
+                            if constexpr (GSZ == 2) {
                                 o.x = lds_u16(rowa + (u.x & 0xffffu)) | (lds_u16(rowa + (u.x >> 16)) << 16);
                                 o.y = lds_u16(rowa + (u.y & 0xffffu)) | (lds_u16(rowa + (u.y >> 16)) << 16);
                                 o.z = lds_u16(rowa + (u.z & 0xffffu)) | (lds_u16(rowa + (u.z >> 16)) << 16);
@@ -652,24 +793,26 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
                                 nf2 = __hmax2_nan(nf2, __hmax2_nan(__habs2(*reinterpret_cast<const __nv_bfloat162*>(&o.z)),
                                                                    __habs2(*reinterpret_cast<const __nv_bfloat162*>(&o.w))));
                             } else {
-                                // fp32: 4 offsets per lane (the first 8 bytes of u)
-                                const uint2 u2 = *reinterpret_cast<const uint2*>(sU + q);
-                                o.x = lds_u32(rowa + (u2.x & 0xffffu));
-                                o.y = lds_u32(rowa + (u2.x >> 16));
-                                o.z = lds_u32(rowa + (u2.y & 0xffffu));
-                                o.w = lds_u32(rowa + (u2.y >> 16));
+                                // fp32: 4 offsets per lane
+                                o.x = lds_u32(rowa + (u.x & 0xffffu));
+                                o.y = lds_u32(rowa + (u.x >> 16));
+                                o.z = lds_u32(rowa + (u.y & 0xffffu));
+                                o.w = lds_u32(rowa + (u.y >> 16));
                                 nfacc |= ((o.x & 0x7f800000u) + 0x00800000u) | ((o.y & 0x7f800000u) + 0x00800000u) |
                                          ((o.z & 0x7f800000u) + 0x00800000u) | ((o.w & 0x7f800000u) + 0x00800000u);
                             }
-                            if (prm.debug_mode != 7) st_cs_v4(out + r * old + q, o);
+                            if (prm.debug_mode != 7 && prm.debug_mode != 11) st_cs_v4(out + r * old + q, o);  // (11: no compaction stores)
                             else dbg_sink ^= o.x ^ o.y ^ o.z ^ o.w;  // keep the gather live
                         }
-                        w += K3_GW;
-                        while (w >= nwin) { w -= nwin; ++r; }
+                        if (++r == Rr) {
+                            r = 0;
+                            ++w;
+                            u = un;
+                        }
                     }
                 }
                 // per row: the qa head and the tail outputs
-                for (int i = ctid; i < Rr * 2 * OPL; i += K3_GW * 32) {
+                for (int i = cct; i < Rr * 2 * OPL; i += K3_CWARPS * 32) {
                     const int r = i / (2 * OPL), e = i - r * (2 * OPL);
                     int q;
                     if (e < OPL) {
@@ -679,16 +822,18 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
                         if (e - OPL >= tail) continue;
                         q = qa + OPL * ng + (e - OPL);
                     }
-                    const GB x = sG[r * sw + sU[q] / GSZ];
+                    const uint32_t bo = ((uint32_t)__ldg(gU + q) - base) & 0xffffu;
+                    const GB x = sG[r * sw + bo / GSZ];
                     if constexpr (GSZ == 2) nfacc |= ((uint32_t)x & 0x7f80u) + 0x0080u;
                     else nfacc |= ((uint32_t)x & 0x7f800000u) + 0x00800000u;
                     out[r * old + q] = x;
                 }
             } else {
                 // unaligned output rows (stateless primitive with a dense [n, m-k] block)
-                for (int i = ctid; i < Rr * nk; i += K3_GW * 32) {
+                for (int i = cct; i < Rr * nk; i += K3_CWARPS * 32) {
                     const int r = i / nk, q = i - r * nk;
-                    const GB x = sG[r * sw + sU[q] / GSZ];
+                    const uint32_t bo = ((uint32_t)__ldg(gU + q) - base) & 0xffffu;
+                    const GB x = sG[r * sw + bo / GSZ];
                     if constexpr (GSZ == 2) nfacc |= ((uint32_t)x & 0x7f80u) + 0x0080u;
                     else nfacc |= ((uint32_t)x & 0x7f800000u) + 0x00800000u;
                     out[r * old + q] = x;
@@ -697,29 +842,6 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
         }
 
         ZF_TICK(2);
-        // ---------------- (3) p write-back of the touched 16-byte chunks ----------------
-        if (pwb) {
-            mbar_wait(&gbar[grp], gphase);  // acquire: every warp of the group finished its AdamW
-            gphase ^= 1u;
-            ZF_TICK(3);
-            constexpr int VP = 16 / PSZ;    // p columns per chunk
-            const uint32_t* smask = reinterpret_cast<const uint32_t*>(A + si.oMask) + si.eMask;
-            const PB* sP = reinterpret_cast<const PB*>(A + si.oP);
-            PB* gP = static_cast<PB*>(si.P) + si.c0;
-            const int ldp = (int)si.ldp;
-            const int nwin = (sw + 32 * VP - 1) / (32 * VP);
-            int r = 0, w = cw;
-            while (w >= nwin) { w -= nwin; ++r; }
-            for (; r < Rr;) {
-                const int cl = (w * 32 + lane) * VP;
-                if (cl < sw) {
-                    const uint32_t bits = (smask[cl >> 5] >> (cl & 31)) & ((1u << VP) - 1u);
-                    if (bits && prm.debug_mode != 7) st_v4(gP + r * ldp + cl, lds128(sP + r * sw + cl));
-                }
-                w += K3_GW;
-                while (w >= nwin) { w -= nwin; ++r; }
-            }
-        }
         // stage fully consumed by this warp
         __syncwarp();
         if (lane == 0) {
@@ -746,6 +868,16 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
         }
         if (__any_sync(0xffffffffu, hit != 0) && lane == 0) *prm.nonfinite = 1;
     }
+}
+
+// K3 prologue: each slot's bias-correction pair {ss, bc2s} for this launch's step counts
+// (t_s = steps[s] + step_delta + 1), so that K3 stages it with the slot's column index and
+// its AdamW chain has no global table lookup.  One block row per layer.
+__global__ void k_slot_consts(const UpdLayer* __restrict__ layers, int32_t step_delta, AdamK a) {
+    const UpdLayer& L = layers[blockIdx.y];
+    if (!L.sbv) return;
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < L.k; s += (int64_t)gridDim.x * blockDim.x)
+        L.sbv[s] = adam_sb(__ldg(L.steps + s) + step_delta + 1, a);
 }
 
 // Stateless AdamW-only form: (row, slot) pairs, G read at the selected columns only.
@@ -822,6 +954,14 @@ cudaError_t launch_update(const UpdParams& p, int gdt, int pdt, int grid, cudaSt
     else if (gdt == DT_BF16 && pdt == DT_F32) ZF_LAUNCH(DT_BF16, DT_F32);
     else ZF_LAUNCH(DT_F32, DT_BF16);
 #undef ZF_LAUNCH
+    return cudaGetLastError();
+}
+
+cudaError_t launch_slot_consts(const UpdLayer* layers, int32_t nl, int64_t max_k, int32_t step_delta, const AdamK& a,
+                               cudaStream_t s) {
+    if (nl <= 0 || max_k <= 0) return cudaSuccess;
+    const dim3 grid((unsigned)zmin<int64_t>((max_k + 255) / 256, 64), (unsigned)nl);
+    k_slot_consts<<<grid, 256, 0, s>>>(layers, step_delta, a);
     return cudaGetLastError();
 }
 

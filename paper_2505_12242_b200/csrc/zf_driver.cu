@@ -93,12 +93,16 @@ zf_status build_tables(zf_ctx* c) {
             t.out_ld = l.mk_pad;
             t.ucol = l.ucol[nw];
             t.done = c->cfg.offload ? c->done + i : nullptr;
-            t.seg_cols = l.geo.seg_cols;
-            t.nseg = l.geo.nseg;
-            t.R = l.geo.R;
-            t.units = l.geo.units;
-            t.unit_begin = l.unit_begin;
-            t.mv_tma = l.geo.mv_ok ? 1 : 0;
+            const K3Geom& gg = refresh ? l.geo : l.geo_s;
+            t.seg_cols = gg.seg_cols;
+            t.nseg = gg.nseg;
+            t.R = gg.R;
+            t.units = gg.units;
+            t.unit_begin = refresh ? l.unit_begin : l.unit_begin_s;
+            t.mv_tma = gg.mv_ok ? 1 : 0;
+            t.psub = l.psub;
+            t.psub_mode = l.psub ? 1 : 0;   // set per step (refresh_pointer_tables)
+            t.sbv = l.sbv;
         }
         ZF_TRY(c->dalloc(&c->d_upd_tab[v], nl * sizeof(UpdLayer)));
         c->up_upd_tab[v].assign(nl, UpdLayer{});
@@ -128,6 +132,7 @@ zf_status build_tables(zf_ctx* c) {
             t.units = l.geo_w.units;
             t.unit_begin = l.unit_begin_w;
             t.mv_tma = l.geo_w.mv_ok ? 1 : 0;
+            t.sbv = l.sbv;
         }
         ZF_TRY(c->dalloc(&c->d_upd_w, nl * sizeof(UpdLayer)));
         c->up_upd_w.assign(nl, UpdLayer{});
@@ -275,6 +280,11 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
         l.geo = k3_geom(l.d.n, l.d.m, l.k, c->gsz, c->psz, k3_p_dense(l.d.m, l.k, c->psz));
         l.unit_begin = c->k3_units;
         c->k3_units += l.geo.units;
+        // steady steps with param_subset stage the dense subset slab instead of a p tile, so
+        // their units hold more rows (more bytes in flight per stage)
+        l.geo_s = cfg->param_subset ? k3_geom(l.d.n, l.d.m, l.k, c->gsz, c->psz, false, true, true) : l.geo;
+        l.unit_begin_s = c->k3_units_s;
+        c->k3_units_s += l.geo_s.units;
         if (c->tau > 0) {  // warm-up geometry: k = m
             l.geo_w = k3_geom(l.d.n, l.d.m, l.d.m, c->gsz, c->psz, true);
             l.unit_begin_w = c->k3_units_w;
@@ -282,7 +292,8 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
         }
     }
     if (c->k3_units_w > 0x3fffffffLL) return bail(fail(ZF_EINVAL, "model too large"));
-    if (c->k1_units > 0x7fffffffLL || c->k3_units > 0x3fffffffLL) return bail(fail(ZF_EINVAL, "model too large"));
+    if (c->k1_units > 0x7fffffffLL || c->k3_units > 0x3fffffffLL || c->k3_units_s > 0x3fffffffLL)
+        return bail(fail(ZF_EINVAL, "model too large"));
     // ---- device state
     ZF_CTRY(c->dalloc(&c->norms, c->total_m * sizeof(float)));
     ZF_CTRY(c->dalloc(&c->claim, sizeof(uint32_t)));
@@ -302,6 +313,10 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
             ZF_CTRY(c->state_alloc(&l.vel[s], (size_t)n * k + 16));
         }
         ZF_CTRY(c->dalloc(&l.slot_src, (k + 16) * sizeof(int32_t)));
+        // per-slot {ss, bc2s} of the next K3 (prologue), padded for K3's bulk copies
+        ZF_CTRY(c->dalloc(&l.sbv, ((c->tau > 0 ? l.d.m : k) + 16) * sizeof(float2)));
+        if (cfg->param_subset && n > 0)  // padded: K3 stages it with 16-byte-granular bulk copies
+            ZF_CTRY(c->dalloc(&l.psub, ((size_t)n * k + 16) * c->psz, false));
         if (c->tau > 0) {
             // the warm-up set: all m columns selected (slot = column), zero moments and counts
             const int64_t m = l.d.m;
@@ -520,6 +535,14 @@ zf_status refresh_pointer_tables(zf_ctx* c, int variant, bool refresh, void* con
         h[i].tma_ok = k3_tma_ok(grads[i], c->L[i].d.ld_grad, c->L[i].d.m, c->gsz);
         h[i].p_tma = k3_tma_ok(params[i], c->L[i].d.ld_param, c->L[i].d.m, c->psz) &&
                      k3_p_dense(c->L[i].d.m, h[i].k, c->psz);
+        if (h[i].psub) {
+            // param_subset: a steady step with a valid block reads p's selected values from it
+            // (no p tile: steady units are sized without one); refreshes (and the step after
+            // zf_params_changed, which reads p from global memory) rebuild it from p
+            const bool steady = variant >= 0 && ((variant >> 1) & 1) == 0;
+            h[i].psub_mode = steady && c->psub_valid ? 2 : 1;
+            if (steady) h[i].p_tma = 0;
+        }
     }
     if (std::memcmp(h.data(), up.data(), nl * sizeof(UpdLayer)) != 0) {
         ZF_TRY(c->upload(d, h.data(), nl * sizeof(UpdLayer), s));
@@ -552,6 +575,8 @@ zf_status warmup_step(zf_ctx* c, int64_t t, void* const* grads, void* const* par
     const int grid = (int)std::min<int64_t>(c->grid, c->k3_units_w);
     zf_ctx::Pending pe3;
     ZF_TRY(c->prof_begin(3, s, &pe3));
+    ZF_CUDA(launch_slot_consts(c->d_upd_w, nl, c->max_m, prm.step_delta, c->adam, s));
+    c->launches++;
     ZF_CUDA(launch_update(prm, c->gdt, c->pdt, grid, s));
     ZF_TRY(c->prof_end(&pe3, s));
     c->launches++;
@@ -655,7 +680,9 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
     UpdParams prm{};
     prm.layers.dev = from_warmup ? c->d_upd_x[sb & 1] : c->d_upd_tab[variant];
     prm.layers.n = nl;
-    prm.total_units = c->k3_units;
+    const bool steady_geo = !refresh && !from_warmup;  // (a first refresh after warm-up is a refresh)
+    const int64_t units = steady_geo ? c->k3_units_s : c->k3_units;
+    prm.total_units = units;
     prm.claim = c->claim;
     prm.claim_base = c->claim_base;
     prm.step_delta = c->since;
@@ -679,15 +706,21 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
         c->k3_prof = prof;
     }
 #endif
-    const int grid = (int)std::min<int64_t>(c->grid, c->k3_units);
+    const int grid = (int)std::min<int64_t>(c->grid, units);
     zf_ctx::Pending pe3;
     ZF_TRY(c->prof_begin(3, s, &pe3));
+    // prologue: the slots' {ss, bc2s} for this launch (after K2 wrote a refresh's step counts)
+    ZF_CUDA(launch_slot_consts(prm.layers.dev, nl, c->max_m, prm.step_delta, c->adam, s));
+    c->launches++;
     ZF_CUDA(launch_update(prm, c->gdt, c->pdt, grid, s));
     ZF_TRY(c->prof_end(&pe3, s));
     c->launches++;
-    c->claim_base += (uint32_t)(c->k3_units + (int64_t)grid * update_limits().producers);
+    c->claim_base += (uint32_t)(units + (int64_t)grid * update_limits().producers);
     c->since += 1;
-    for (int i = 0; i < nl; ++i) c->done_target[i] += (uint32_t)c->L[i].geo.units * (uint32_t)update_limits().consumer_warps;
+    c->psub_valid = c->cfg.param_subset != 0;  // this K3 (re)built or kept the subset block
+    for (int i = 0; i < nl; ++i)
+        c->done_target[i] += (uint32_t)(steady_geo ? c->L[i].geo_s.units : c->L[i].geo.units) *
+                             (uint32_t)update_limits().consumer_warps;
     if (refresh) {
         c->cur ^= 1;
         c->have_sel = true;
@@ -950,6 +983,13 @@ extern "C" zf_status zf_set_host_allreduce(zf_ctx* c, zf_host_allreduce_fn fn, v
     if (c->world < 2 || c->comm) return fail(ZF_ESTATE, "host all-reduce needs world > 1 created without an NCCL id");
     c->host_allreduce = fn;
     c->host_allreduce_user = user;
+    return ZF_OK;
+}
+
+extern "C" zf_status zf_params_changed(zf_ctx* c) {
+    g_last_error.clear();
+    if (!c) return fail(ZF_EINVAL, "ctx is NULL");
+    c->psub_valid = false;
     return ZF_OK;
 }
 

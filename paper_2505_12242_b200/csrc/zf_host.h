@@ -220,24 +220,27 @@ inline bool k3_p_dense(int64_t m, int64_t k, int psz) {
     return 1.0 - std::pow(1.0 - frac, 32.0 / psz) >= 0.5;
 }
 
-// Worst-case bytes one K3 unit stages (R rows x c columns): G tile, p tile (if dense),
-// mask words, the unselected-column list, moment slabs (R*k: also covers the old rows of a refresh),
-// step counts and remap sources; each as a 16-byte-granular superset.
-inline int64_t k3_unit_bytes(int64_t R, int64_t c, int64_t k, int gsz, int psz, bool p_dense, bool mv) {
+// Worst-case bytes one K3 unit stages (R rows x c columns): the G tile, the p tile (refresh
+// units with a dense selection), the parameter-subset slab (steady units with param_subset)
+// and the moment slabs (R*k: also covers the old rows of a refresh); each a 16-byte-granular
+// superset.  The layer's selection metadata is read through L1, not staged.
+inline int64_t k3_unit_bytes(int64_t R, int64_t c, int64_t k, int gsz, int psz, bool p_tile, bool mv,
+                             bool psub = false) {
     auto a16 = [](int64_t b) { return (b + 15) & ~int64_t(15); };
-    int64_t b = a16(R * c * gsz) + 2 * ((c + 31) / 32 + 8) * 4;
-    if (p_dense) b += a16(R * c * psz);
-    if (mv) b += 2 * (R * k + 8) * 4 + 3 * (std::min(c, k) + 8) * 4;  // moments; steps, sources, idx
-    b += a16((c + 8) * 2);                                              // unselected-column offsets
+    int64_t b = a16(R * c * gsz);
+    if (p_tile) b += a16(R * c * psz);
+    if (psub && mv) b += a16((R * k + 8) * psz) + 16;
+    if (mv) b += 2 * (a16((R * k + 8) * 4) + 16);
     return b;
 }
 
-inline K3Geom k3_geom(int64_t n, int64_t m, int64_t k, int gsz, int psz, bool p_dense, bool adam = true) {
+inline K3Geom k3_geom(int64_t n, int64_t m, int64_t k, int gsz, int psz, bool p_dense, bool adam = true,
+                      bool psub = false) {
     const UpdLimits lim = update_limits();
     const int64_t A = lim.arena_bytes;
     K3Geom g{};
     // moments staged unless even one row's old moments cannot fit next to a minimal tile
-    g.mv_ok = adam && k3_unit_bytes(1, std::min<int64_t>(m, 128), k, gsz, psz, p_dense, true) <= A;
+    g.mv_ok = adam && k3_unit_bytes(1, std::min<int64_t>(m, 128), k, gsz, psz, p_dense, true, psub) <= A;
     // Units are R rows x c columns (c = m, or a multiple of 128 so segments start 16-byte
     // aligned in the mask/prefix words): the shape with the fewest units per matrix (the most
     // bytes per stage), ties to full rows / wider segments.  ZF_K3_GEOM=rows keeps the older
@@ -247,10 +250,11 @@ inline K3Geom k3_geom(int64_t n, int64_t m, int64_t k, int gsz, int psz, bool p_
     // loses without one (k = 1%: 6.92 -> 7.27 ms, more exposed p loads per unit), so
     // unstaged-p layers keep the row rule.
     static const bool rows_env = getenv("ZF_K3_GEOM") && std::string(getenv("ZF_K3_GEOM")) == "rows";
-    const bool rows_only = rows_env || !p_dense;
+    const bool rows_only = rows_env || (!p_dense && !psub);
     auto rmax = [&](int64_t c) {
         int64_t R = 0;
-        while (R < std::min<int64_t>(n, 127) && k3_unit_bytes(R + 1, c, k, gsz, psz, p_dense, g.mv_ok) <= A) ++R;
+        while (R < std::min<int64_t>(n, 127) && k3_unit_bytes(R + 1, c, k, gsz, psz, p_dense, g.mv_ok, psub) <= A)
+            ++R;
         return R;
     };
     int64_t best_units = -1;
@@ -339,14 +343,18 @@ struct LayerState {
     int32_t* slot_src = nullptr;
     float* mom[2] = {nullptr, nullptr};
     float* vel[2] = {nullptr, nullptr};
+    void* psub = nullptr;             // param_subset: [n, k] dense copy of p[:, idx] (HBM)
+    float2* sbv = nullptr;            // [max(k, m during warm-up)] per-slot {ss, bc2s} of the next K3
     void* stage_dev[2] = {nullptr, nullptr};
     void* stage_host[2] = {nullptr, nullptr};
     float* acc[2] = {nullptr, nullptr};
     float* dacc[2] = {nullptr, nullptr};  // device_accumulate: [n, mk_pad] fp32 window accumulators
     float* acc_sealed_h = nullptr;        // device_accumulate: pinned dense [n, mk] copy of the sealed window
     // K3 geometry
-    K3Geom geo{};
+    K3Geom geo{};                     // refresh units (p tile when the selection is dense)
     int64_t unit_begin = 0;
+    K3Geom geo_s{};                   // steady units (param_subset: the subset slab instead of a p tile)
+    int64_t unit_begin_s = 0;
     cudaEvent_t d2h_ev[2] = {nullptr, nullptr};
     // f1: deferred CPU AdamW (reading R18)
     // dense over the current unselected columns (position u = column unsel_host[u]), remapped
@@ -449,7 +457,7 @@ struct zf_ctx {
     float* norms_host = nullptr;
     int gdt = 0, pdt = 0, gsz = 2, psz = 2;
     std::vector<LayerState> L;
-    int64_t total_m = 0, max_m = 0, k1_units = 0, k3_units = 0;
+    int64_t total_m = 0, max_m = 0, k1_units = 0, k3_units = 0, k3_units_s = 0;
     bool has_empty = false;       // some layer has n = 0 rows on this rank
     int n_stage = 1;
     float* norms = nullptr;
@@ -495,6 +503,7 @@ struct zf_ctx {
     // step state
     int cur = 0;
     bool have_sel = false;
+    bool psub_valid = false;      // param_subset: the block holds p[:, idx] (set by a K3 in mode 1)
     int64_t last_t = -1;          // regular-schedule index (t - tau) of the last regular step
     int64_t launches = 0;
     cudaEvent_t step_done = nullptr, k3_done = nullptr;

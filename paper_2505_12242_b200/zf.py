@@ -21,7 +21,7 @@ ZF_FP32, ZF_BF16 = 0, 1
 SYMBOLS = ["zf_status_string", "zf_last_error", "zf_version", "zf_k_for", "zf_column_norms", "zf_topk_columns",
            "zf_selective_adam", "zf_compact_unselected", "zf_nccl_unique_id", "zf_create", "zf_step", "zf_sync",
            "zf_selected", "zf_norms", "zf_optimizer_state", "zf_compact_buffer", "zf_host_accumulator", "zf_device_accumulator", "zf_window_log", "zf_set_host_allreduce", "zf_set_lr",
-           "zf_kernel_launches", "zf_profile", "zf_profile_read", "zf_destroy"]
+           "zf_kernel_launches", "zf_profile", "zf_profile_read", "zf_params_changed", "zf_destroy"]
 
 
 class ZFError(RuntimeError):
@@ -46,7 +46,8 @@ class Config(ctypes.Structure):
                 ("offload", ctypes.c_int32), ("host_accumulate", ctypes.c_int32), ("host_threads", ctypes.c_int32),
                 ("cpu_update", ctypes.c_int32), ("warmup_steps", ctypes.c_int32),
                 ("auto_gamma", ctypes.c_float), ("state_offload", ctypes.c_int32),
-                ("device_accumulate", ctypes.c_int32), ("cpu_update_async", ctypes.c_int32)]
+                ("device_accumulate", ctypes.c_int32), ("cpu_update_async", ctypes.c_int32),
+                ("param_subset", ctypes.c_int32)]
 
 
 if not os.path.exists(_LIB_PATH):
@@ -92,6 +93,7 @@ HOST_ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.POINTER(ctypes.c_flo
 lib.zf_set_host_allreduce.argtypes = [_vp, HOST_ALLREDUCE_FN, _vp]
 lib.zf_set_host_allreduce.restype = _st
 lib.zf_set_lr.argtypes = [_vp, ctypes.c_double]; lib.zf_set_lr.restype = _st
+lib.zf_params_changed.argtypes = [_vp]; lib.zf_params_changed.restype = _st
 lib.zf_kernel_launches.argtypes = [_vp]; lib.zf_kernel_launches.restype = _i64
 lib.zf_destroy.argtypes = [_vp]; lib.zf_destroy.restype = _st
 lib.zf_profile.argtypes = [_vp, _i32]; lib.zf_profile.restype = _st
@@ -208,7 +210,8 @@ class Context:
                  refresh_interval=4, accum_interval=4, adam: AdamParams | None = None, offload=False,
                  host_accumulate=False, host_threads=0, world=1, rank=0, nccl_id: bytes | None = None,
                  device: int | None = None, cpu_update=False, warmup_steps=0, auto_gamma=0.0,
-                 state_offload=False, device_accumulate=False, host_allreduce=None, cpu_update_async=False):
+                 state_offload=False, device_accumulate=False, host_allreduce=None, cpu_update_async=False,
+                 param_subset=True):
         self.layers = [l if isinstance(l, LayerShape) else LayerShape(*l) for l in layers]
         descs = (LayerDesc * len(self.layers))()
         for d, l in zip(descs, self.layers):
@@ -232,6 +235,7 @@ class Context:
         cfg.state_offload = int(state_offload)
         cfg.device_accumulate = int(device_accumulate)
         cfg.cpu_update_async = int(cpu_update_async)
+        cfg.param_subset = int(param_subset)
         self.cfg = cfg
         self.device = torch.cuda.current_device() if device is None else device
         h = ctypes.c_void_p()
@@ -269,6 +273,11 @@ class Context:
 
     def sync(self):
         _check(lib.zf_sync(self._h), "zf_sync")
+
+    def params_changed(self):
+        """param_subset: the caller wrote the parameters outside step(); the next step re-reads
+        the selected columns from them."""
+        _check(lib.zf_params_changed(self._h), "zf_params_changed")
 
     def set_lr(self, lr: float):
         _check(lib.zf_set_lr(self._h, lr), "zf_set_lr")

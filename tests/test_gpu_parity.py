@@ -181,13 +181,13 @@ def test_compact_into_pinned_host(zf, orc, gpu, n, m, dt):
 # ------------------------------------------------------------------ zf_step vs oracle, multi-step
 def _run_stateful(zf, orc, gpu, shapes, gdt, pdt, ppm, N, S, steps, offload, lr=1e-3, wd=0.0, check_every=1,
                   tie=False, ld_pad=0, cpu_update=False, warmup=0, state_offload=False, devacc=False,
-                  cpu_async=False, side_stream=False):
+                  cpu_async=False, side_stream=False, psub=True, poke=None):
     hp_o = orc.AdamHP(lr=lr, weight_decay=wd)
     ctx = zf.Context([zf.LayerShape(n, m, m + ld_pad, m + ld_pad) for n, m in shapes], grad_dtype=TDT[gdt],
                      param_dtype=TDT[pdt], topk_ratio_ppm=ppm, refresh_interval=N, accum_interval=S,
                      adam=zf.adam_params(lr=lr, weight_decay=wd), offload=offload, host_accumulate=offload, cpu_update=cpu_update,
                      warmup_steps=warmup, state_offload=state_offload, device_accumulate=devacc,
-                     cpu_update_async=cpu_async)
+                     cpu_update_async=cpu_async, param_subset=psub)
     scales = [gpu.ColScale(m, li) for li, (n, m) in enumerate(shapes)]
     Gs = [torch.empty(n, m + ld_pad, dtype=TDT[gdt], device="cuda")[:, :m] for n, m in shapes]
     Ps = [torch.empty(n, m + ld_pad, dtype=TDT[pdt], device="cuda")[:, :m] for n, m in shapes]
@@ -205,6 +205,15 @@ def _run_stateful(zf, orc, gpu, shapes, gdt, pdt, ppm, N, S, steps, offload, lr=
                 sc.advance_to(t)
                 gpu.fill_grad(G, li, t, sc)
         Gn = [np.ascontiguousarray(to_np(G)) for G in Gs]
+        if poke is not None and t in poke:
+            # the caller writes the parameters outside zf_step (e.g. a checkpoint load): every
+            # 3rd element of every parameter is negated, on the GPU and in the oracle's copy
+            for li, P in enumerate(Ps):
+                Pc = P.clone()
+                Pc.view(-1)[::3] = -Pc.view(-1)[::3]
+                P.copy_(Pc)
+                Po[li] = np.ascontiguousarray(to_np(P))
+            ctx.params_changed()
         if side_stream:
             # a caller's non-blocking stream (every torch side stream is one): the library's
             # host->device uploads must be ordered on it, not on the legacy default stream
@@ -261,7 +270,7 @@ def test_step_config1_fp32(zf, orc, gpu, NS):
     """BASELINE config 1: one 256x512 fp32 gradient, top-10%, selective AdamW +
     unselected accumulation; N = S in {1, 2, 4}, 8 steps (two windows at S=4)."""
     swaps, launches = _run_stateful(zf, orc, gpu, [(256, 512)], "fp32", "fp32", 100000, NS, NS, 8, offload=True)
-    assert launches == 8 + 2 * (8 // NS)
+    assert launches == 2 * 8 + 2 * (8 // NS)   # per step: K3 prologue + K3; per refresh: K1 + K2
     assert swaps == 0
 
 
@@ -363,6 +372,22 @@ def test_step_cpu_update_on_a_side_stream(zf, orc, gpu, cpu_async):
     the K5 scatter are ordered on the caller's stream (bit-exact vs the oracle)."""
     _run_stateful(zf, orc, gpu, [(96, 300), (64, 128)], "bf16", "bf16", 100000, 2, 2, 7, offload=True,
                   cpu_update=True, cpu_async=cpu_async, side_stream=True)
+
+
+@pytest.mark.parametrize("shapes,gdt,NS,cpu", [([(256, 512)], "fp32", 4, False), ([(300, 4096), (64, 1000)], "bf16", 2, True),
+                                              ([(96, 11008), (40, 4096)], "bf16", 4, False)])
+def test_step_param_subset_off(zf, orc, gpu, shapes, gdt, NS, cpu):
+    """param_subset = 0 (p's selected values read from p on every step) is bit-exact too."""
+    _run_stateful(zf, orc, gpu, shapes, gdt, gdt, 100000, NS, NS, 9, offload=True, cpu_update=cpu, psub=False)
+
+
+@pytest.mark.parametrize("ppm", [100000, 10000])
+def test_params_changed_rereads_the_selected_columns(zf, orc, gpu, ppm):
+    """param_subset: the caller rewrites p between refreshes (t = 2, 5, 6) and calls
+    zf_params_changed; the next steady steps use the new values (bit-exact vs the oracle,
+    which sees the same writes)."""
+    _run_stateful(zf, orc, gpu, [(128, 4096), (96, 700)], "bf16", "bf16", ppm, 4, 4, 9, offload=False,
+                  poke={2, 5, 6})
 
 
 def test_cpu_update_async_is_stale_until_the_next_call(zf, gpu):
