@@ -56,7 +56,7 @@ __global__ void k_scale_init(int8_t* e, int64_t m, uint64_t key) {
 __global__ void k_scale_advance(int8_t* e, int64_t m, uint64_t key_redraw, uint64_t key_scale) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
         uint64_t hr = mix(key_redraw + (uint64_t)j);
-        if ((hr & 0xFFFFFFFFull) < 42949673ull) e[j] = scale_exp(ih4(mix(key_scale + (uint64_t)j)));
+        if ((hr & 0xFFFFFFFFull) < 1288490ull) e[j] = scale_exp(ih4(mix(key_scale + (uint64_t)j)));
     }
 }
 

@@ -59,7 +59,7 @@ void synth_host_col_scale_advance(int8_t* e, int64_t m, int32_t layer, int64_t s
     const uint64_t kr = stream_key(seed, TAG_REDRAW, (uint64_t)layer, (uint64_t)step);
     const uint64_t ks = stream_key(seed, TAG_SCALE, (uint64_t)layer, (uint64_t)step);
     for (int64_t j = 0; j < m; ++j)
-        if ((mix(kr + (uint64_t)j) & 0xFFFFFFFFull) < 42949673ull) e[j] = scale_exp(ih4(mix(ks + (uint64_t)j)));
+        if ((mix(kr + (uint64_t)j) & 0xFFFFFFFFull) < 1288490ull) e[j] = scale_exp(ih4(mix(ks + (uint64_t)j)));
 }
 
 void synth_host_grad(void* out, int dtype, int64_t n, int64_t m, int64_t ld, int64_t row0, int32_t layer,
