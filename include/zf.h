@@ -307,10 +307,11 @@ zf_status zf_set_lr(zf_ctx* ctx, double lr);
  * phase on the stream it runs on (0: K1 column norms, 1: NCCL norm all-reduce,
  * 2: K2 top-k, 3: K3 fused selective AdamW + compaction, 4: a step's per-layer D2H
  * of the compact blocks on the copy stream -- first copy start to last copy end,
- * 5: a sealed window's D2H (device_accumulate), 6: K7 device accumulation).
- * zf_profile_read waits for the recorded events, writes the summed milliseconds
- * ms[7] and occurrence counts count[7] [host] since the previous read, and resets
- * them. */
+ * 5: a sealed window's D2H (device_accumulate), 6: K7 device accumulation,
+ * 7: K3b dense selective AdamW of the split update; phase 3 is then K3a, the
+ * compaction + extraction pass).  zf_profile_read waits for the recorded events,
+ * writes the summed milliseconds ms[8] and occurrence counts count[8] [host] since
+ * the previous read, and resets them. */
 zf_status zf_profile(zf_ctx* ctx, int32_t enable);
 zf_status zf_profile_read(zf_ctx* ctx, double* ms, int64_t* count);
 /* param_subset: the caller wrote p (e.g. loaded a checkpoint) outside zf_step; the next

@@ -226,6 +226,7 @@ struct StageInfo {
     float* m_out;               // + r0*k
     float* v_out;
     void* psub;                 // param_subset block + r0*k (NULL: none)
+    void* gsel;                 // split update: selected-gradient block + r0*k
     const float* m_in;          // layer base (non-staged path)
     const float* v_in;
     // per-layer selection metadata, read by the consumers through L1 (every unit of a layer
@@ -514,9 +515,27 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
                         for (int r = 0; r < g.Rr; ++r)
                             bulk_prefetch_l2(G + ((g.r0 + r) * L.ldg + g.c0) * GSZ, (int64_t)sw * GSZ);
                 }
+                if (prm.do_extract && si.s1 > si.s0 && L.psub_mode == 1 && L.p_tma) {
+                    const unsigned char* P = static_cast<const unsigned char*>(L.P);
+                    if (L.nseg == 1 && L.ldp == L.m) bulk_prefetch_l2(P + g.r0 * L.m * PSZ, (int64_t)g.Rr * sw * PSZ);
+                    else
+                        for (int r = 0; r < g.Rr; ++r)
+                            bulk_prefetch_l2(P + ((g.r0 + r) * L.ldp + g.c0) * PSZ, (int64_t)sw * PSZ);
+                }
                 if (prm.do_adam && si.s1 > si.s0 && L.psub_mode == 2 && L.mv_tma)
                     bulk_prefetch_l2(static_cast<const unsigned char*>(L.psub) + (g.r0 * L.k + si.s0) * PSZ,
                                      ((g.Rr - 1) * L.k + si.s1 - si.s0) * PSZ);
+#ifndef ZF_K3_NO_PSUB_PPF
+                // with the subset slab, still pull the unit's p rows into L2 when the selection
+                // touches most of p's sectors: the changed values' stores then hit cached sectors
+                // instead of each waiting on a partial-sector fill (measured: steady K3 9.48 ->
+                // 9.36 ms at lr 1e-5, 10.33 -> 9.83 ms at lr 1e-3, Llama-2-7B k = 10%)
+                if (prm.do_adam && si.s1 > si.s0 && L.psub_mode == 2 && L.p_dense) {
+                    const unsigned char* P = static_cast<const unsigned char*>(L.P);
+                    for (int r = 0; r < g.Rr; ++r)
+                        bulk_prefetch_l2(P + ((g.r0 + r) * L.ldp + g.c0) * PSZ, (int64_t)sw * PSZ);
+                }
+#endif
                 if (prm.do_adam && si.s1 > si.s0 && L.p_tma) {
                     const unsigned char* P = static_cast<const unsigned char*>(L.P);
                     if (L.nseg == 1 && L.ldp == L.m) bulk_prefetch_l2(P + g.r0 * L.m * PSZ, (int64_t)g.Rr * sw * PSZ);
@@ -572,7 +591,26 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
             off = (g.Rr * sw * GSZ + 15) & ~15;
             si.j0 = (int32_t)(g.c0 - si.s0);
             si.nkeep = sw - ns;
-            if (prm.do_adam && ns > 0) {
+            if (prm.do_extract && ns > 0) {
+                // split update (K3a): the AdamW inputs go to dense blocks; only a psub rebuild
+                // (mode 1) needs p's values, from the p tile when the selection is dense
+                si.mg_ns = (uint32_t)(((1u << 24) + (uint32_t)ns - 1u) / (uint32_t)ns);
+                si.psub_mode = L.psub_mode;
+                si.pstaged = L.psub_mode == 1 && L.p_tma;
+                if (si.pstaged) {
+                    const unsigned char* P = static_cast<const unsigned char*>(L.P);
+                    si.oP = off;
+                    if (L.nseg == 1 && L.ldp == L.m) {
+                        bulk_g2s(A + off, P + g.r0 * L.m * PSZ, (uint32_t)(g.Rr * sw * PSZ), &full[st], pol_last);
+                    } else {
+                        for (int r = 0; r < g.Rr; ++r)
+                            bulk_g2s(A + off + r * sw * PSZ, P + ((g.r0 + r) * L.ldp + g.c0) * PSZ,
+                                     (uint32_t)(sw * PSZ), &full[st], pol_last);
+                    }
+                    tx += (uint32_t)(g.Rr * sw * PSZ);
+                    off += (g.Rr * sw * PSZ + 15) & ~15;
+                }
+            } else if (prm.do_adam && ns > 0) {
                 si.mg_ns = (uint32_t)(((1u << 24) + (uint32_t)ns - 1u) / (uint32_t)ns);
                 si.pstaged = L.p_tma;
                 si.mstaged = L.mv_tma;
@@ -623,6 +661,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
             si.m_out = L.m_out + g.r0 * L.k;
             si.v_out = L.v_out + g.r0 * L.k;
             si.psub = L.psub ? static_cast<PB*>(L.psub) + g.r0 * L.k : nullptr;
+            si.gsel = L.gsel ? static_cast<GB*>(L.gsel) + g.r0 * L.k : nullptr;
             si.m_in = L.m_in;
             si.v_in = L.v_in;
             si.steps = L.steps;
@@ -725,6 +764,33 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
                 adam_unit<GDT, PDT, true, false, false>(si, A, prm, ctid, nfacc);
             } else {
                 adam_unit<GDT, PDT, false, false, false>(si, A, prm, ctid, nfacc);
+            }
+        }
+
+        if (prm.do_extract && ns > 0 && cw < K3_AWARPS) {
+            // split update (K3a): the unit's selected gradients -> gsel [n, k] (and, rebuilding
+            // the parameter subset, p's selected values -> psub), pairs row-major: the warp's
+            // lanes write consecutive slots of one row
+            const GB* sGx = reinterpret_cast<const GB*>(A + si.oG);
+            const PB* sPx = reinterpret_cast<const PB*>(A + si.oP);
+            const PB* gPx = static_cast<const PB*>(si.P);
+            GB* gsel = static_cast<GB*>(si.gsel);
+            PB* psub = static_cast<PB*>(si.psub);
+            const int s0 = si.s0, k = si.k, c0 = (int)si.c0, ldp = (int)si.ldp, total = Rr * ns;
+            constexpr int NCT = K3_AWARPS * 32;
+            int r = (int)(((uint64_t)ctid * si.mg_ns) >> 24), sl = ctid - r * ns;
+            const int dr = (int)(((uint64_t)NCT * si.mg_ns) >> 24), dsl = NCT - dr * ns;
+            for (int q = ctid; q < total; q += NCT) {
+                const int s = s0 + sl;
+                const int c = __ldg(si.idx + s);
+                const GB gb = sGx[r * sw + c - c0];
+                if constexpr (GSZ == 2) nfacc |= ((uint32_t)gb & 0x7f80u) + 0x0080u;
+                else nfacc |= ((uint32_t)gb & 0x7f800000u) + 0x00800000u;
+                gsel[r * k + s] = gb;
+                if (si.psub_mode == 1) psub[r * k + s] = si.pstaged ? sPx[r * sw + c - c0] : gPx[r * ldp + c];
+                r += dr;
+                sl += dsl;
+                if (sl >= ns) { sl -= ns; ++r; }
             }
         }
 

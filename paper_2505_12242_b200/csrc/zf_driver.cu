@@ -103,6 +103,9 @@ zf_status build_tables(zf_ctx* c) {
             t.psub = l.psub;
             t.psub_mode = l.psub ? 1 : 0;   // set per step (refresh_pointer_tables)
             t.sbv = l.sbv;
+            t.gsel = l.gsel;
+            t.adam_row_begin = l.row_begin;
+            if (c->split) t.mv_tma = 0;     // K3a never stages moments
         }
         ZF_TRY(c->dalloc(&c->d_upd_tab[v], nl * sizeof(UpdLayer)));
         c->up_upd_tab[v].assign(nl, UpdLayer{});
@@ -260,6 +263,12 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
     c->lr_cur = cfg->adam.lr;
     c->tau = cfg->warmup_steps;
     c->grid = update_grid(c->gdt, c->pdt);
+    // ZF_K3_SPLIT: the split update (K3a compaction + extraction, K3b dense AdamW, k_adam.cu)
+    // instead of AdamW inside K3's unit pipeline.  Measured slower on Llama-2-7B k = 10% (K3a
+    // 4.65 + K3b 5.7 ms vs 9.4 ms fused): K3b's scattered stores of the changed p values miss
+    // L2 and each waits on a partial-sector fill, 3 ms of its time at lr 1e-5 (3.3 ms without
+    // them), where the fused kernel's stores hit the p rows it pulled into L2
+    c->split = getenv("ZF_K3_SPLIT") != nullptr;
     c->L.resize(n_layers);
     const int rb = norms_rows_per_block(), cb = norms_cols_per_block(c->gdt);
     for (int i = 0; i < n_layers; ++i) {
@@ -277,12 +286,21 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
         c->total_m += l.d.m;
         c->max_m = std::max(c->max_m, l.d.m);
         c->k1_units += (int64_t)l.nrb * l.ncb;
-        l.geo = k3_geom(l.d.n, l.d.m, l.k, c->gsz, c->psz, k3_p_dense(l.d.m, l.k, c->psz));
+        l.row_begin = c->total_rows;   // K3b: the layer's first chunk of adam_dense_vec() elements
+        c->total_rows += (l.d.n * l.k + adam_dense_vec() - 1) / adam_dense_vec();
+        if (c->split) {
+            // split update: K3a stages the G tile (and on refresh steps the p tile, to rebuild the
+            // parameter subset); the moments never enter its stages (K3b streams them)
+            l.geo = k3_geom(l.d.n, l.d.m, l.k, c->gsz, c->psz, k3_p_dense(l.d.m, l.k, c->psz), false);
+            l.geo_s = cfg->param_subset ? k3_geom(l.d.n, l.d.m, l.k, c->gsz, c->psz, false, false) : l.geo;
+        } else {
+            l.geo = k3_geom(l.d.n, l.d.m, l.k, c->gsz, c->psz, k3_p_dense(l.d.m, l.k, c->psz));
+            // steady steps with param_subset stage the dense subset slab instead of a p tile, so
+            // their units hold more rows (more bytes in flight per stage)
+            l.geo_s = cfg->param_subset ? k3_geom(l.d.n, l.d.m, l.k, c->gsz, c->psz, false, true, true) : l.geo;
+        }
         l.unit_begin = c->k3_units;
         c->k3_units += l.geo.units;
-        // steady steps with param_subset stage the dense subset slab instead of a p tile, so
-        // their units hold more rows (more bytes in flight per stage)
-        l.geo_s = cfg->param_subset ? k3_geom(l.d.n, l.d.m, l.k, c->gsz, c->psz, false, true, true) : l.geo;
         l.unit_begin_s = c->k3_units_s;
         c->k3_units_s += l.geo_s.units;
         if (c->tau > 0) {  // warm-up geometry: k = m
@@ -315,8 +333,10 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
         ZF_CTRY(c->dalloc(&l.slot_src, (k + 16) * sizeof(int32_t)));
         // per-slot {ss, bc2s} of the next K3 (prologue), padded for K3's bulk copies
         ZF_CTRY(c->dalloc(&l.sbv, ((c->tau > 0 ? l.d.m : k) + 16) * sizeof(float2)));
-        if (cfg->param_subset && n > 0)  // padded: K3 stages it with 16-byte-granular bulk copies
-            ZF_CTRY(c->dalloc(&l.psub, ((size_t)n * k + 16) * c->psz, false));
+        // padded: K3 stages the subset with 16-byte-granular bulk copies.  The split update keeps
+        // p's selected values in this dense block even without param_subset (rebuilt every step)
+        if ((cfg->param_subset || c->split) && n > 0) ZF_CTRY(c->dalloc(&l.psub, ((size_t)n * k + 16) * c->psz, false));
+        if (c->split && n > 0) ZF_CTRY(c->dalloc(&l.gsel, ((size_t)n * k + 16) * c->gsz, false));
         if (c->tau > 0) {
             // the warm-up set: all m columns selected (slot = column), zero moments and counts
             const int64_t m = l.d.m;
@@ -533,15 +553,16 @@ zf_status refresh_pointer_tables(zf_ctx* c, int variant, bool refresh, void* con
         h[i].G = grads[i];
         h[i].P = params[i];
         h[i].tma_ok = k3_tma_ok(grads[i], c->L[i].d.ld_grad, c->L[i].d.m, c->gsz);
-        h[i].p_tma = k3_tma_ok(params[i], c->L[i].d.ld_param, c->L[i].d.m, c->psz) &&
-                     k3_p_dense(c->L[i].d.m, h[i].k, c->psz);
-        if (h[i].psub) {
+        h[i].p_dense = k3_p_dense(c->L[i].d.m, h[i].k, c->psz) ? 1 : 0;
+        h[i].p_tma = k3_tma_ok(params[i], c->L[i].d.ld_param, c->L[i].d.m, c->psz) && h[i].p_dense;
+        if (h[i].psub && variant != -1) {
             // param_subset: a steady step with a valid block reads p's selected values from it
             // (no p tile: steady units are sized without one); refreshes (and the step after
-            // zf_params_changed, which reads p from global memory) rebuild it from p
+            // zf_params_changed, which reads p from global memory) rebuild it from p.  The split
+            // update without param_subset rebuilds it every step (steady units keep the p tile)
             const bool steady = variant >= 0 && ((variant >> 1) & 1) == 0;
-            h[i].psub_mode = steady && c->psub_valid ? 2 : 1;
-            if (steady) h[i].p_tma = 0;
+            h[i].psub_mode = steady && c->psub_valid && c->cfg.param_subset ? 2 : 1;
+            if (steady && c->cfg.param_subset) h[i].p_tma = 0;
         }
     }
     if (std::memcmp(h.data(), up.data(), nl * sizeof(UpdLayer)) != 0) {
@@ -686,7 +707,8 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
     prm.claim = c->claim;
     prm.claim_base = c->claim_base;
     prm.step_delta = c->since;
-    prm.do_adam = 1;
+    prm.do_adam = c->split ? 0 : 1;
+    prm.do_extract = c->split ? 1 : 0;
     prm.do_compact = 1;
     prm.nonfinite = c->nonfinite_d;
     prm.adam = c->adam;
@@ -715,6 +737,14 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
     ZF_CUDA(launch_update(prm, c->gdt, c->pdt, grid, s));
     ZF_TRY(c->prof_end(&pe3, s));
     c->launches++;
+    if (c->split) {
+        // K3b: AdamW over the dense [n, k] blocks K3a filled (phase 7)
+        zf_ctx::Pending pe7;
+        ZF_TRY(c->prof_begin(7, s, &pe7));
+        ZF_CUDA(launch_adam_dense(prm.layers.dev, nl, c->total_rows, c->gdt, c->pdt, prm.step_delta, c->adam, s));
+        ZF_TRY(c->prof_end(&pe7, s));
+        c->launches++;
+    }
     c->claim_base += (uint32_t)(units + (int64_t)grid * update_limits().producers);
     c->since += 1;
     c->psub_valid = c->cfg.param_subset != 0;  // this K3 (re)built or kept the subset block

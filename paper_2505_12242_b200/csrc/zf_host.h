@@ -345,6 +345,8 @@ struct LayerState {
     float* vel[2] = {nullptr, nullptr};
     void* psub = nullptr;             // param_subset: [n, k] dense copy of p[:, idx] (HBM)
     float2* sbv = nullptr;            // [max(k, m during warm-up)] per-slot {ss, bc2s} of the next K3
+    void* gsel = nullptr;             // split update: [n, k] selected gradients (K3a -> K3b)
+    int64_t row_begin = 0;            // K3b: prefix of ceil(n*k / 8) over layers (its chunks)
     void* stage_dev[2] = {nullptr, nullptr};
     void* stage_host[2] = {nullptr, nullptr};
     float* acc[2] = {nullptr, nullptr};
@@ -504,6 +506,8 @@ struct zf_ctx {
     int cur = 0;
     bool have_sel = false;
     bool psub_valid = false;      // param_subset: the block holds p[:, idx] (set by a K3 in mode 1)
+    bool split = false;           // regular steps run K3a (compaction + extraction) then K3b (dense AdamW)
+    int64_t total_rows = 0;       // K3b chunks over all layers
     int64_t last_t = -1;          // regular-schedule index (t - tau) of the last regular step
     int64_t launches = 0;
     cudaEvent_t step_done = nullptr, k3_done = nullptr;
@@ -560,7 +564,7 @@ struct zf_ctx {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
     struct Pending { int phase; cudaEvent_t a, b; };
     std::vector<Pending> pending;
-    static constexpr int NPHASE = 7;
+    static constexpr int NPHASE = 8;
     double prof_ms[NPHASE] = {};
     int64_t prof_n[NPHASE] = {};
 

@@ -285,7 +285,7 @@ class Context:
     def profile(self, enable: bool = True):
         _check(lib.zf_profile(self._h, int(enable)), "zf_profile")
 
-    PHASES = ("k1_norms", "allreduce", "k2_topk", "k3_update", "d2h_step", "d2h_window", "k7_accumulate")
+    PHASES = ("k1_norms", "allreduce", "k2_topk", "k3_update", "d2h_step", "d2h_window", "k7_accumulate", "k3b_adam")
 
     def profile_read(self):
         """{phase: (summed ms, count)} since the last read (waits for the recorded events)."""

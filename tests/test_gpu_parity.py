@@ -381,6 +381,17 @@ def test_step_param_subset_off(zf, orc, gpu, shapes, gdt, NS, cpu):
     _run_stateful(zf, orc, gpu, shapes, gdt, gdt, 100000, NS, NS, 9, offload=True, cpu_update=cpu, psub=False)
 
 
+@pytest.mark.parametrize("shapes,gdt,pdt,NS,cpu,psub", [([(256, 512)], "fp32", "fp32", 4, False, True),
+                                                   ([(300, 4096), (64, 1000)], "bf16", "bf16", 2, True, True),
+                                                   ([(96, 4096), (40, 700)], "bf16", "fp32", 4, False, False)])
+def test_step_split_update(zf, orc, gpu, monkeypatch, shapes, gdt, pdt, NS, cpu, psub):
+    """The split update (ZF_K3_SPLIT: K3a compaction + extraction, K3b dense AdamW over the
+    [n, k] blocks, incl. the moment remap and the branch-free division/sqrt fast path) is
+    bit-exact vs the oracle as well."""
+    monkeypatch.setenv("ZF_K3_SPLIT", "1")
+    _run_stateful(zf, orc, gpu, shapes, gdt, pdt, 100000, NS, NS, 9, offload=True, cpu_update=cpu, psub=psub)
+
+
 @pytest.mark.parametrize("ppm", [100000, 10000])
 def test_params_changed_rereads_the_selected_columns(zf, orc, gpu, ppm):
     """param_subset: the caller rewrites p between refreshes (t = 2, 5, 6) and calls

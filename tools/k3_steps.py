@@ -48,16 +48,18 @@ if os.environ.get("ZF_OPTS"):
 for o in opts:
     ctx = zf.Context([zf.LayerShape(n, m) for n, m in shapes], topk_ratio_ppm=ppm, refresh_interval=4,
                      accum_interval=4, adam=zf.adam_params(lr=lr), **o)
-    ks = []
+    ks, ka, kb = [], [], []
     for t in range(steps):
         ctx.profile(True)
         ctx.step(t, G0 if t % 2 == 0 else G1, P)
         pr = ctx.profile_read()
-        ks.append(round(pr["k3_update"][0], 3))
+        ks.append(round(pr["k3_update"][0] + pr["k3b_adam"][0], 3))
+        ka.append(round(pr["k3_update"][0], 3))
+        kb.append(round(pr["k3b_adam"][0], 3))
     ctx.sync()
     ctx.close()
     ref = [x for t, x in enumerate(ks) if t % 4 == 0 and t >= 4]
     st = [x for t, x in enumerate(ks) if t % 4 != 0 and t >= 4]
-    print(json.dumps({"opts": o, "ppm": ppm, "lr": lr, "k3_ms": ks, "refresh": sum(ref) / len(ref),
+    print(json.dumps({"opts": o, "ppm": ppm, "lr": lr, "k3_ms": ks, "k3a_ms": ka, "k3b_ms": kb, "refresh": sum(ref) / len(ref),
                       "steady": sum(st) / len(st), "avg": (sum(ref) / len(ref) + 3 * sum(st) / len(st)) / 4}),
           flush=True)
