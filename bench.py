@@ -62,6 +62,9 @@ def parse():
                          "per-rank evidence for the multi-GPU configs on a one-GPU box")
     ap.add_argument("--also-cpu-update", action="store_true",
                     help="also time e2e with the deferred CPU AdamW (f1), synchronous vs overlapped (R23)")
+    ap.add_argument("--no-lagged", action="store_true",
+                    help="skip the f4 (ii) lagged-selection line (device time, and a training-loop proxy "
+                         "with a synthetic compute-bound backward between steps)")
     ap.add_argument("--colocate", action="store_true",
                     help="N > 1 ranks share the visible GPU(s) (rank r on cuda:r %% device_count): gloo process group "
                          "and the library's host all-reduce instead of NCCL -- runs the multi-rank path (launcher, "
@@ -468,6 +471,64 @@ def run_zenflow(args, rank, world):
     #      (and read-modify-writes) the p sectors the lr 1e-5 headline mostly skips
     if not args.no_lr1e3 and args.lr != 1e-3:
         result["lr_1e-3"] = k3_line(args.ratio_ppm, lr=1e-3, tag="lr1e3")
+
+    # ---- f4 (ii) lagged selection: device time of the same loop, and a training-loop proxy in
+    #      which each step is preceded by a compute-bound "backward" (bf16 GEMMs on the caller's
+    #      stream); with the lag, a pre-refresh step's K1 runs on the library's side stream under
+    #      the next backward instead of on the refresh step's critical path
+    if not args.no_lagged and world == 1:
+        def loop_with_backward(lagged, K, W):
+            ctx = zf.Context([zf.LayerShape(n, m) for n, m in shapes], topk_ratio_ppm=args.ratio_ppm,
+                             refresh_interval=args.refresh, accum_interval=args.refresh,
+                             adam=zf.adam_params(lr=args.lr), device=dev, lagged_selection=lagged)
+            a = torch.randn(8192, 8192, dtype=torch.bfloat16, device="cuda")
+            b = torch.randn(8192, 8192, dtype=torch.bfloat16, device="cuda")
+            c_ = torch.empty(8192, 8192, dtype=torch.bfloat16, device="cuda")
+
+            def backward():
+                for _ in range(3):
+                    torch.matmul(a, b, out=c_)
+            for t in range(W):
+                backward()
+                ctx.step_ptrs(t, gp[t % 2], pp, stream)
+            ctx.sync()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for t in range(W, W + K):
+                backward()
+                ctx.step_ptrs(t, gp[t % 2], pp, stream)
+            ctx.sync()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / K
+            ctx.close()
+            e0.record(stream)
+            for _ in range(K):
+                backward()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            bw = e0.elapsed_time(e1) / K
+            del a, b, c_
+            return ms, bw
+        ctxl = zf.Context([zf.LayerShape(n, m) for n, m in shapes], topk_ratio_ppm=args.ratio_ppm,
+                          refresh_interval=args.refresh, accum_interval=args.refresh,
+                          adam=zf.adam_params(lr=args.lr), device=dev, lagged_selection=True)
+        msl, profl, _ = timed_run(ctxl, args.steps, args.warmup, "lagged")
+        ctxl.close()
+        del ctxl
+        Kp = max(8, args.steps)
+        plain_ms, bw_ms = loop_with_backward(False, Kp, 4)
+        lag_ms, _ = loop_with_backward(True, Kp, 4)
+        result["lagged_selection"] = {
+            "ms_per_step": msl / args.steps,
+            "k1_launches": profl["k1_norms"][1],
+            "training_loop_proxy": {"backward_ms": bw_ms, "plain_ms_per_step": plain_ms,
+                                    "lagged_ms_per_step": lag_ms, "steps": Kp,
+                                    "backward": "3 x bf16 GEMM 8192^3 on the caller's stream before every zf_step; "
+                                                "gradient buffers alternate (the lagged K1 reads the other one)"},
+            "note": "device ms/step of the zf_step loop alone is unchanged by the lag (K1 still runs once per N "
+                    "steps); the proxy shows it moving off the optimizer's critical path"}
 
     # ---- f3 state swap-out: moments in mapped pinned host memory (extra field)
     if args.also_state_offload:

@@ -230,6 +230,20 @@ typedef struct {
                                          only writer of the selected columns of p; a
                                          caller that writes them calls zf_params_changed
                                          before the next zf_step.  0: read p itself.    */
+    int32_t lagged_selection;         /* 1: one-step-lagged selection (next row f4 (ii),
+                                         P:505-508 "cache and reuse selected channel
+                                         indices", reading R24): a refresh at regular step
+                                         t > 0 selects by the column norms of step t-1's
+                                         gradient, which K1 (and the norm all-reduce when
+                                         world > 1) computes on the library's side stream
+                                         at the end of step t-1 -- the refresh step makes a
+                                         single pass over G, and the norm pass overlaps
+                                         whatever the caller runs next (its forward /
+                                         backward).  The first refresh uses its own step's
+                                         gradient.  Contract: the gradient buffers of a
+                                         step t with (t+1) % N == 0 must stay valid until
+                                         the next zf_step or zf_sync (e.g. double-buffered
+                                         gradients).  Not with auto_gamma.             */
 } zf_config;
 
 typedef struct zf_ctx zf_ctx;

@@ -226,6 +226,8 @@ class OracleLayer:
     hp: AdamHP = field(default_factory=AdamHP)
     cpu_update: bool = False   # f1: deferred CPU AdamW on the unselected columns (reading R18)
     warmup: int = 0            # f2: tau synchronous warm-up steps with k = m (reading R20)
+    lagged: bool = False       # f4 (ii): a refresh after the first selects by the previous step's norms (R24)
+    lag_norms: np.ndarray | None = None
     idx: np.ndarray | None = None
     M: np.ndarray | None = None
     V: np.ndarray | None = None
@@ -261,7 +263,10 @@ class OracleLayer:
         if self.cpu_update:
             assert self.refresh_interval % self.accum_interval == 0, "R18: refresh only at window starts"
         if t % self.refresh_interval == 0 or self.idx is None:
-            self.last_norms = column_norms(G)
+            # R24 (f4 ii, "cache and reuse selected channel indices"): with a lagged
+            # selection every refresh but the first ranks the columns by the norms of the step
+            # before it; the first (no earlier regular step) by its own gradient's
+            self.last_norms = self.lag_norms if (self.lagged and self.lag_norms is not None) else column_norms(G)
             new_idx = topk(self.last_norms, k) if idx_override is None else np.asarray(idx_override, np.int32)
             old_idx = self.idx
             if self.idx is None:
@@ -275,6 +280,8 @@ class OracleLayer:
                 self._migrate(old_idx, new_idx, P)
         selective_adamw(P, G, self.idx, self.M, self.V, self.steps, self.hp)
         out = compact(G, self.idx)
+        if self.lagged and (t + 1) % self.refresh_interval == 0:
+            self.lag_norms = column_norms(G)            # the next refresh's ranking (R24)
         S = self.accum_interval
         if self.acc is None:
             self.acc = [np.zeros((self.n, self.m - k), np.float32) for _ in range(2)]

@@ -225,6 +225,8 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
     if (!(cfg->auto_gamma >= 0.0f) || !std::isfinite(cfg->auto_gamma))
         return fail(ZF_EINVAL, "auto_gamma must be finite and >= 0");
     if (cfg->auto_gamma > 0.0f && !cfg->host_accumulate) return fail(ZF_EINVAL, "auto_gamma requires host_accumulate");
+    if (cfg->lagged_selection && cfg->auto_gamma > 0.0f)
+        return fail(ZF_EINVAL, "lagged_selection and auto_gamma are exclusive (Zen-auto reads every step's norms)");
     if (cfg->device_accumulate && !cfg->host_accumulate)
         return fail(ZF_EINVAL, "device_accumulate requires host_accumulate (it moves that accumulation onto the GPU)");
     ZF_TRY(check_hp(&cfg->adam));
@@ -414,6 +416,12 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
     }
     c->done_target.assign(n_layers, 0u);
     ZF_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+    c->lagged = cfg->lagged_selection != 0;
+    if (c->lagged) {
+        ZF_CUDA(cudaStreamCreateWithFlags(&c->lag_stream, cudaStreamNonBlocking));
+        ZF_CUDA(cudaEventCreateWithFlags(&c->lag_in, cudaEventDisableTiming));
+        ZF_CUDA(cudaEventCreateWithFlags(&c->norm_ready, cudaEventDisableTiming));
+    }
     for (auto& l : c->L) {
         int32_t* v = nullptr;
         ZF_CTRY(c->dalloc(&v, (c->tau > 0 ? l.d.m : l.k) * sizeof(int32_t)));
@@ -647,8 +655,12 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
     const bool from_warmup = !c->have_sel && tau > 0;
     const int variant = from_warmup ? -2 - (sb & 1) : c->cur * 4 + (refresh ? 2 : 0) + (sb & 1);
     ZF_TRY(upload_ss(c, s));
-    const bool norms_now = refresh || c->autoz;  // Zen-auto reads every step's norms (R21)
-    ZF_TRY(refresh_pointer_tables(c, variant, norms_now, grads, params, s));
+    // f4 (ii), reading R24: a lagged refresh (not the first) takes the norms K1 computed from the
+    // previous step's gradient on the side stream; a pre-refresh step launches that K1
+    const bool lag_refresh = c->lagged && refresh && c->have_sel;
+    const bool lag_pre = c->lagged && (t + 1) % N == 0;
+    const bool norms_now = (refresh && !lag_refresh) || c->autoz;  // Zen-auto reads every step's norms (R21)
+    ZF_TRY(refresh_pointer_tables(c, variant, norms_now || lag_pre, grads, params, s));
 
     if (c->cfg.offload) {
         // (K3 counts per-layer completions only when offloading; see build_tables)
@@ -683,6 +695,21 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
                     return fail(ZF_ENCCL, "host all-reduce callback failed");
                 ZF_CUDA(cudaMemcpyAsync(c->norms, c->norms_host, c->total_m * sizeof(float), cudaMemcpyHostToDevice, s));
             }
+            ZF_TRY(c->prof_end(&pe, s));
+        }
+    }
+    if (lag_refresh) {
+        // the norms of step t-1 (and, with NCCL, their all-reduce) were made on the side stream
+        if (c->lag_pending) ZF_CUDA(cudaStreamWaitEvent(s, c->norm_ready, 0));
+        c->lag_pending = false;
+        if (c->world > 1 && !c->comm) {
+            zf_ctx::Pending pe;
+            ZF_TRY(c->prof_begin(1, s, &pe));
+            ZF_CUDA(cudaMemcpyAsync(c->norms_host, c->norms, c->total_m * sizeof(float), cudaMemcpyDeviceToHost, s));
+            ZF_CUDA(cudaStreamSynchronize(s));
+            if (c->host_allreduce(c->norms_host, c->total_m, c->host_allreduce_user) != 0)
+                return fail(ZF_ENCCL, "host all-reduce callback failed");
+            ZF_CUDA(cudaMemcpyAsync(c->norms, c->norms_host, c->total_m * sizeof(float), cudaMemcpyHostToDevice, s));
             ZF_TRY(c->prof_end(&pe, s));
         }
     }
@@ -729,6 +756,30 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
     }
 #endif
     const int grid = (int)std::min<int64_t>(c->grid, units);
+    if (lag_pre) {
+        // f4 (ii): this step's gradient gives the next refresh's norms: K1 (and the NCCL
+        // all-reduce) on the side stream, ordered after everything above on s (the K1 table
+        // upload, K2's reading of the previous norms), concurrent with K3 and whatever the
+        // caller enqueues next
+        ZF_CUDA(cudaEventRecord(c->lag_in, s));
+        ZF_CUDA(cudaStreamWaitEvent(c->lag_stream, c->lag_in, 0));
+        zf_ctx::Pending pe;
+        if (c->has_empty) ZF_CUDA(cudaMemsetAsync(c->norms, 0, c->total_m * sizeof(float), c->lag_stream));
+        Table<NormLayer> tn{};
+        tn.dev = c->d_norm_tab;
+        tn.n = nl;
+        ZF_TRY(c->prof_begin(0, c->lag_stream, &pe));
+        ZF_CUDA(launch_norms(tn, c->k1_units, c->gdt, c->nonfinite_d, c->lag_stream));
+        ZF_TRY(c->prof_end(&pe, c->lag_stream));
+        c->launches++;
+        if (c->world > 1 && c->comm) {
+            ZF_TRY(c->prof_begin(1, c->lag_stream, &pe));
+            ZF_NCCL(ncclAllReduce(c->norms, c->norms, (size_t)c->total_m, ncclFloat32, ncclSum, c->comm, c->lag_stream));
+            ZF_TRY(c->prof_end(&pe, c->lag_stream));
+        }
+        ZF_CUDA(cudaEventRecord(c->norm_ready, c->lag_stream));
+        c->lag_pending = true;
+    }
     zf_ctx::Pending pe3;
     ZF_TRY(c->prof_begin(3, s, &pe3));
     // prologue: the slots' {ss, bc2s} for this launch (after K2 wrote a refresh's step counts)
@@ -886,6 +937,7 @@ extern "C" zf_status zf_sync(zf_ctx* c) {
         ZF_CUDA(cudaStreamSynchronize(c->last_stream));
     }
     if (c->copy_stream) ZF_CUDA(cudaStreamSynchronize(c->copy_stream));
+    if (c->lag_stream) ZF_CUDA(cudaStreamSynchronize(c->lag_stream));   // a lagged K1 (f4 ii)
     if (c->cfg.host_accumulate) {
         std::unique_lock<std::mutex> lk(c->mu);
         c->cv.wait(lk, [&] { return c->jobs.empty(); });

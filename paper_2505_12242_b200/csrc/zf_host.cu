@@ -37,6 +37,9 @@ zf_ctx::~zf_ctx() {
     if (k3_done) cudaEventDestroy(k3_done);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (aux) cudaStreamDestroy(aux);
+    if (lag_stream) cudaStreamDestroy(lag_stream);
+    if (lag_in) cudaEventDestroy(lag_in);
+    if (norm_ready) cudaEventDestroy(norm_ready);
 }
 
 // One row of H1 (fp32 adds in step order; a window's first step writes 0 + x).  Cloned for

@@ -507,6 +507,10 @@ struct zf_ctx {
     bool have_sel = false;
     bool psub_valid = false;      // param_subset: the block holds p[:, idx] (set by a K3 in mode 1)
     bool split = false;           // regular steps run K3a (compaction + extraction) then K3b (dense AdamW)
+    bool lagged = false;          // f4 (ii): refresh norms from the previous step (K1 on lag_stream)
+    cudaStream_t lag_stream = nullptr;
+    cudaEvent_t lag_in = nullptr, norm_ready = nullptr;
+    bool lag_pending = false;     // a lagged K1 was enqueued and not yet waited for
     int64_t total_rows = 0;       // K3b chunks over all layers
     int64_t last_t = -1;          // regular-schedule index (t - tau) of the last regular step
     int64_t launches = 0;

@@ -181,22 +181,23 @@ def test_compact_into_pinned_host(zf, orc, gpu, n, m, dt):
 # ------------------------------------------------------------------ zf_step vs oracle, multi-step
 def _run_stateful(zf, orc, gpu, shapes, gdt, pdt, ppm, N, S, steps, offload, lr=1e-3, wd=0.0, check_every=1,
                   tie=False, ld_pad=0, cpu_update=False, warmup=0, state_offload=False, devacc=False,
-                  cpu_async=False, side_stream=False, psub=True, poke=None):
+                  cpu_async=False, side_stream=False, psub=True, poke=None, lagged=False):
     hp_o = orc.AdamHP(lr=lr, weight_decay=wd)
     ctx = zf.Context([zf.LayerShape(n, m, m + ld_pad, m + ld_pad) for n, m in shapes], grad_dtype=TDT[gdt],
                      param_dtype=TDT[pdt], topk_ratio_ppm=ppm, refresh_interval=N, accum_interval=S,
                      adam=zf.adam_params(lr=lr, weight_decay=wd), offload=offload, host_accumulate=offload, cpu_update=cpu_update,
                      warmup_steps=warmup, state_offload=state_offload, device_accumulate=devacc,
-                     cpu_update_async=cpu_async, param_subset=psub)
+                     cpu_update_async=cpu_async, param_subset=psub, lagged_selection=lagged)
     scales = [gpu.ColScale(m, li) for li, (n, m) in enumerate(shapes)]
     Gs = [torch.empty(n, m + ld_pad, dtype=TDT[gdt], device="cuda")[:, :m] for n, m in shapes]
     Ps = [torch.empty(n, m + ld_pad, dtype=TDT[pdt], device="cuda")[:, :m] for n, m in shapes]
     for li, P in enumerate(Ps):
         gpu.fill_param(P, li)
     layers = [orc.OracleLayer(n=n, m=m, ratio_ppm=ppm, refresh_interval=N, accum_interval=S, hp=hp_o,
-                              cpu_update=cpu_update, warmup=warmup) for n, m in shapes]
+                              cpu_update=cpu_update, warmup=warmup, lagged=lagged) for n, m in shapes]
     Po = [np.ascontiguousarray(to_np(P)) for P in Ps]
     swaps = 0
+    prevG = None
     for t in range(steps):
         for li, (G, sc) in enumerate(zip(Gs, scales)):
             if tie:
@@ -231,8 +232,14 @@ def _run_stateful(zf, orc, gpu, shapes, gdt, pdt, ppm, N, S, steps, offload, lr=
             L = layers[li]
             gidx = to_np(ctx.selected(li))
             if refresh:
-                onorms = orc.column_norms(Gn[li])
-                assert_close_rel(to_np(ctx.norms(li)), onorms, 1e-5, f"norms t={t} l={li}")
+                # lagged selection (R24): a refresh after the first ranks by the previous step's
+                # norms; after a step that is also a pre-refresh step (N = 1) the norms buffer
+                # already holds this step's
+                lag = lagged and L.lag_norms is not None
+                onorms = orc.column_norms(prevG[li] if lag else Gn[li])
+                pre_now = lagged and (t - warmup + 1) % N == 0
+                if not pre_now:
+                    assert_close_rel(to_np(ctx.norms(li)), onorms, 1e-5, f"norms t={t} l={li}")
                 swaps += selection_ok(gidx, orc.topk(onorms, L.k), onorms)
             out = L.step(t, Gn[li], Po[li], idx_override=gidx if refresh else None)
             if t % check_every and t != steps - 1:
@@ -260,6 +267,7 @@ def _run_stateful(zf, orc, gpu, shapes, gdt, pdt, ppm, N, S, steps, offload, lr=
                 assert (sealed is None) == (osealed is None)
                 if sealed is not None:
                     assert_bits_equal(sealed.copy(), osealed, f"sealed acc t={t} l={li}")
+        prevG = Gn
     launches = ctx.kernel_launches()
     ctx.close()
     return swaps, launches
@@ -390,6 +398,24 @@ def test_step_split_update(zf, orc, gpu, monkeypatch, shapes, gdt, pdt, NS, cpu,
     bit-exact vs the oracle as well."""
     monkeypatch.setenv("ZF_K3_SPLIT", "1")
     _run_stateful(zf, orc, gpu, shapes, gdt, pdt, 100000, NS, NS, 9, offload=True, cpu_update=cpu, psub=psub)
+
+
+@pytest.mark.parametrize("shapes,gdt,NS,cpu,warmup", [([(256, 512)], "fp32", 4, False, 0),
+                                                      ([(300, 4096), (64, 1000)], "bf16", 2, True, 0),
+                                                      ([(96, 700), (40, 256)], "bf16", 1, False, 0),
+                                                      ([(128, 1024)], "bf16", 2, True, 3)])
+def test_step_lagged_selection(zf, orc, gpu, shapes, gdt, NS, cpu, warmup):
+    """f4 (ii), reading R24: a refresh after the first selects by the previous step's norms (K1
+    on the side stream at the end of the pre-refresh step); selection bit-exact on those norms,
+    everything downstream bit-exact vs the oracle's lagged mode (N = S in {1, 2, 4}, f1, warm-up)."""
+    _run_stateful(zf, orc, gpu, shapes, gdt, gdt, 100000, NS, NS, 9 + warmup, offload=True, cpu_update=cpu,
+                  warmup=warmup, lagged=True)
+
+
+def test_lagged_selection_needs_fixed_windows(zf):
+    with pytest.raises(zf.ZFError):
+        zf.Context([zf.LayerShape(8, 64)], offload=True, host_accumulate=True, auto_gamma=0.5,
+                   lagged_selection=True)
 
 
 @pytest.mark.parametrize("ppm", [100000, 10000])

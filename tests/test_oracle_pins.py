@@ -815,3 +815,60 @@ def test_f1_zen_auto_window_length_factor_in_the_eps_regime(orc):
     assert M.intervals() == [3, 3, 2]
     assert np.allclose(P[:, k:], 3 * step, rtol=1e-5, atol=0)
     assert M.layers[0].th[k:].tolist() == [3] * (m - k)
+
+
+# ------------------------------------------------------------------ f4 (ii): lagged selection (reading R24)
+def _spike(n, m, col, big=8.0):
+    G = np.full((n, m), 0.125, np.float32)
+    G[:, col] = big
+    return G
+
+
+def test_lagged_refresh_ranks_by_the_previous_step(orc):
+    """N = 2, k = 1: the step before the refresh at t = 2 has its large column at 5, the
+    refresh step itself at 9.  A lagged selection (R24) picks 5; the plain one picks 9.  The
+    first refresh (t = 0) has no earlier step and picks its own step's column (3)."""
+    n, m = 4, 10
+    seq = [_spike(n, m, 3), _spike(n, m, 5), _spike(n, m, 9), _spike(n, m, 9)]
+    A = orc.OracleLayer(n=n, m=m, ratio_ppm=100000, refresh_interval=2, accum_interval=2, lagged=True)
+    B = orc.OracleLayer(n=n, m=m, ratio_ppm=100000, refresh_interval=2, accum_interval=2)
+    PA, PB = np.zeros((n, m), np.float32), np.zeros((n, m), np.float32)
+    picks = []
+    for t, G in enumerate(seq):
+        A.step(t, G, PA)
+        B.step(t, G, PB)
+        picks.append((A.idx.tolist(), B.idx.tolist()))
+    assert picks[0] == ([3], [3]) and picks[1] == ([3], [3])
+    assert picks[2] == ([5], [9]) and picks[3] == ([5], [9])
+    # column 5 enters at t = 2 and takes two AdamW steps on the constant g = 0.125 of steps 2
+    # and 3 (closed form: each moves by -lr*g/(|g|+eps)); its step count is 2
+    assert np.allclose(PA[:, 5], 2 * (-1e-3 * 0.125 / (0.125 + 1e-8)), rtol=1e-5) and A.steps.tolist() == [2]
+
+
+def test_lagged_equals_plain_on_a_constant_stream(orc):
+    """With G_t = G_{t-1} for all t the lagged ranking is the plain one: selection, moments,
+    parameters, compact blocks and accumulators identical (N = 3, several refreshes)."""
+    import synth
+    n, m = 32, 96
+    e = synth.col_scale_init(m, 0)
+    G = synth.grad(n, m, 0, 0, e, dtype="fp32")
+    A = orc.OracleLayer(n=n, m=m, ratio_ppm=100000, refresh_interval=3, accum_interval=3, lagged=True)
+    B = orc.OracleLayer(n=n, m=m, ratio_ppm=100000, refresh_interval=3, accum_interval=3)
+    PA = synth.param(n, m, 0, dtype="fp32")
+    PB = PA.copy()
+    for t in range(10):
+        assert np.array_equal(A.step(t, G, PA), B.step(t, G, PB))
+        assert np.array_equal(A.idx, B.idx) and np.array_equal(A.M, B.M) and np.array_equal(PA, PB)
+
+
+def test_lagged_N1_uses_the_previous_step_every_step(orc):
+    """N = 1: every step refreshes, each from the previous step's norms (k = 1)."""
+    n, m = 4, 8
+    cols = [1, 6, 2, 7, 0]
+    L = orc.OracleLayer(n=n, m=m, ratio_ppm=125000, refresh_interval=1, accum_interval=1, lagged=True)
+    P = np.zeros((n, m), np.float32)
+    got = []
+    for t, c in enumerate(cols):
+        L.step(t, _spike(n, m, c), P)
+        got.append(int(L.idx[0]))
+    assert got == [1, 1, 6, 2, 7]
