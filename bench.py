@@ -689,6 +689,26 @@ def run_zenflow(args, rank, world):
         for key in ("x1_d2h_GBs", "window_d2h_GBs"):
             if link.get(key):
                 link[key.replace("_GBs", "_frac")] = link[key] / link["d2h_peak_GBs"]
+        # H1's host-memory traffic per step (per unselected element: read the staged bf16 value,
+        # write the fp32 accumulator, and read it back on every step of a window but the first)
+        S_ = args.refresh
+        h1_bytes = sum(n * (m - k) for (n, m), k in zip(shapes, ks)) * (2 + 4 + 4 * (S_ - 1) / S_)
+        link["h1_host_dram_bytes_per_step"] = h1_bytes
+        link["h1_host_dram_GBs"] = h1_bytes / (ms_host * 1e-3) / 1e9
+        link["host_link_floor_ms"] = h2d / (link["h2d_peak_GBs"] * 1e9) * 1e3
+        node = None
+        try:
+            import glob as _glob
+            import subprocess as _sp
+            bid = _sp.run(["nvidia-smi", f"--id={dev}", "--query-gpu=pci.bus_id", "--format=csv,noheader"],
+                          capture_output=True, text=True, timeout=20).stdout.strip().lower()
+            bid = bid[4:] if bid.count(":") == 2 and len(bid.split(":")[0]) == 8 else bid
+            for f in _glob.glob(f"/sys/bus/pci/devices/*{bid[-7:]}/numa_node"):
+                node = int(open(f).read().strip())
+        except Exception:  # noqa: BLE001
+            pass
+        link["gpu_numa_node"] = node
+        link["host_cpus"] = os.cpu_count()
         result["host_link"] = link
         result["e2e"] = {"value": ms_dev if ms_dev is not None else ms_host, "unit": UNIT, "h2d_bytes_per_step": h2d,
                          "d2h_bytes_per_step": int(d2h_dev) if ms_dev is not None else d2h_host, "steps": K,

@@ -429,6 +429,20 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
     }
     ZF_CUDA(cudaEventCreateWithFlags(&c->step_done, cudaEventDisableTiming));
     ZF_CUDA(cudaEventCreateWithFlags(&c->k3_done, cudaEventDisableTiming));
+    // host buffers on the GPU's NUMA node: this thread runs there while it allocates and
+    // first-touches them (pinned staging, accumulators, f1 state), then its affinity returns
+    c->numa_cpus = gpu_numa_cpus(device, &c->numa_node);
+    cpu_set_t saved;
+    const bool pinned_here = !c->numa_cpus.empty() &&
+                             pthread_getaffinity_np(pthread_self(), sizeof saved, &saved) == 0;
+    if (pinned_here) pin_thread_to(c->numa_cpus);
+    struct Restore {
+        bool on;
+        cpu_set_t set;
+        ~Restore() {
+            if (on) pthread_setaffinity_np(pthread_self(), sizeof set, &set);
+        }
+    } restore{pinned_here, saved};
     // ---- offload: copy stream, pinned host staging, per-layer events, host accumulators
     if (cfg->offload) {
         ZF_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
@@ -504,10 +518,12 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
             }
         }
         if (cfg->host_accumulate) {
-            int nt = cfg->host_threads > 0 ? cfg->host_threads
-                                           : (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-            c->pool = new Pool(nt);
-            if (!c->devacc) c->h1 = std::thread([c] { c->h1_loop(); });
+            // H1 / f1 pool: the GPU node's cores (all hardware threads when no node is reported)
+            const int avail = c->numa_cpus.empty() ? (int)std::max(1u, std::thread::hardware_concurrency())
+                                                   : (int)c->numa_cpus.size();
+            int nt = cfg->host_threads > 0 ? cfg->host_threads : std::min(avail, 64);
+            c->pool = new Pool(nt, c->numa_cpus);
+            if (!c->devacc) c->h1 = std::thread([c] { pin_thread_to(c->numa_cpus); c->h1_loop(); });
         }
     }
     // ---- NCCL (collective across ranks), or a pinned host buffer for the host all-reduce

@@ -25,6 +25,10 @@
 #include <thread>
 #include <vector>
 
+#include <pthread.h>
+#include <sched.h>
+#include <cctype>
+
 #include "../../include/zf.h"
 #include "zf_internal.cuh"
 
@@ -382,11 +386,56 @@ struct LayerState {
     int64_t unit_begin_w = 0;
 };
 
-// Simple pool for the host accumulation (row 8, H1).
+// NUMA placement of the host side (rows a7/a8, f1): the CPUs of the NUMA node the GPU hangs
+// off (sysfs numa_node of its PCI function, then that node's cpulist).  Empty when the
+// platform reports no node (-1, e.g. a single-node VM) -- then nothing is pinned.
+inline std::vector<int> gpu_numa_cpus(int device, int* node_out) {
+    std::vector<int> cpus;
+    *node_out = -1;
+    char bus[32] = {0};
+    if (cudaDeviceGetPCIBusId(bus, sizeof bus, device) != cudaSuccess) return cpus;
+    std::string id(bus);
+    for (auto& ch : id) ch = (char)std::tolower((unsigned char)ch);
+    FILE* f = std::fopen(("/sys/bus/pci/devices/" + id + "/numa_node").c_str(), "r");
+    if (!f) return cpus;
+    int node = -1;
+    if (std::fscanf(f, "%d", &node) != 1) node = -1;
+    std::fclose(f);
+    *node_out = node;
+    if (node < 0) return cpus;
+    f = std::fopen(("/sys/devices/system/node/node" + std::to_string(node) + "/cpulist").c_str(), "r");
+    if (!f) return cpus;
+    char buf[4096] = {0};
+    if (std::fgets(buf, sizeof buf, f)) {
+        const char* p = buf;
+        while (*p) {                      // "0-15,32-47"
+            char* e = nullptr;
+            const long a = std::strtol(p, &e, 10);
+            if (e == p) break;
+            long b = a;
+            if (*e == '-') { p = e + 1; b = std::strtol(p, &e, 10); }
+            for (long c = a; c <= b; ++c) cpus.push_back((int)c);
+            p = (*e == ',') ? e + 1 : e;
+            if (*p == '\n') break;
+        }
+    }
+    std::fclose(f);
+    return cpus;
+}
+inline void pin_thread_to(const std::vector<int>& cpus) {
+    if (cpus.empty()) return;
+    cpu_set_t set;
+    CPU_ZERO(&set);
+    for (int c : cpus)
+        if (c < CPU_SETSIZE) CPU_SET(c, &set);
+    pthread_setaffinity_np(pthread_self(), sizeof set, &set);
+}
+
+// Simple pool for the host accumulation (row 8, H1); its threads run on the GPU's NUMA node.
 class Pool {
    public:
-    explicit Pool(int n) : n_(n) {
-        for (int i = 0; i < n_; ++i) th_.emplace_back([this, i] { run(i); });
+    explicit Pool(int n, std::vector<int> cpus = {}) : n_(n), cpus_(std::move(cpus)) {
+        for (int i = 0; i < n_; ++i) th_.emplace_back([this, i] { pin_thread_to(cpus_); run(i); });
     }
     ~Pool() {
         {
@@ -416,6 +465,7 @@ class Pool {
     }
 
    private:
+    std::vector<int> cpus_;
     void run(int i) {
         uint64_t seen = 0;
         for (;;) {
@@ -511,6 +561,8 @@ struct zf_ctx {
     cudaStream_t lag_stream = nullptr;
     cudaEvent_t lag_in = nullptr, norm_ready = nullptr;
     bool lag_pending = false;     // a lagged K1 was enqueued and not yet waited for
+    int numa_node = -1;           // NUMA node of the GPU (-1: not reported)
+    std::vector<int> numa_cpus;   // its CPUs: host threads and first-touch allocations run there
     int64_t total_rows = 0;       // K3b chunks over all layers
     int64_t last_t = -1;          // regular-schedule index (t - tau) of the last regular step
     int64_t launches = 0;
