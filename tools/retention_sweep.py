@@ -15,7 +15,7 @@ Llama-2-7B decoder block, T steps, and reports for each top-k ratio:
 It measures the generator's temporal locality (its calibrated per-step column redraw)
 against the paper's numbers; it is not a benchmark.
 
-usage (GPU box): python tools/retention_sweep.py [--steps 100] [--out profiles/r01c_retention.json]
+usage (GPU box): python tools/retention_sweep.py [--steps 100] [--out profiles/r02_retention.json]
 """
 from __future__ import annotations
 
