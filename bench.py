@@ -46,7 +46,10 @@ def parse():
     ap.add_argument("--refresh", type=int, default=4)
     ap.add_argument("--lr", type=float, default=1e-5)
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--host-stages", type=int, default=0,
+                    help="pinned host staging slots for the host-accumulation e2e line (0: 2*S, capped by "
+                         "the host memory available)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-k1pct", action="store_true", help="skip the k = 1%% line (reported as the k1pct field)")
     ap.add_argument("--no-lr1e3", action="store_true",
@@ -257,6 +260,22 @@ def run_reference(args, rank, world):
 
 
 # ------------------------------------------------------------ GPU arm
+def host_dram_probe():
+    """Host DRAM bandwidth of this box's cores on H1's access patterns (tools/host_membw.c,
+    built here with the host compiler, all cores, 2 GiB fp32 arrays); {} if unavailable."""
+    import subprocess as _sp
+    exe = "/tmp/zf_host_membw"
+    src = os.path.join(ROOT, "tools", "host_membw.c")
+    try:
+        if not os.path.exists(exe) or os.path.getmtime(exe) < os.path.getmtime(src):
+            _sp.run(["gcc", "-O3", "-march=native", "-fopenmp", src, "-o", exe], check=True, capture_output=True,
+                    timeout=120)
+        out = _sp.run([exe, "2", str(os.cpu_count())], capture_output=True, text=True, timeout=300).stdout
+        return json.loads(out.strip().splitlines()[-1])
+    except Exception as ex:  # noqa: BLE001
+        return {"error": str(ex)[-120:]}
+
+
 def max_over_ranks(vals, world):
     """Element-wise max over ranks (CPU tensor: works for the nccl and the gloo group)."""
     import torch
@@ -590,8 +609,34 @@ def run_zenflow(args, rank, world):
             del hb, db
             return 4 * nb / (e0.elapsed_time(e1) * 1e-3) / 1e9
 
+        def link_bidir():
+            # both directions at once (1 GiB each way on two streams): the host link's combined
+            # rate when the H2D of G and the offload D2H overlap
+            nb = 1 << 30
+            hb = [torch.empty(nb, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+            db = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(2)]
+            st = [torch.cuda.Stream(), torch.cuda.Stream()]
+            best = None
+            for rep in range(3):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                with torch.cuda.stream(st[0]):
+                    for _ in range(2):
+                        hb[0].copy_(db[0], non_blocking=True)
+                with torch.cuda.stream(st[1]):
+                    for _ in range(2):
+                        db[1].copy_(hb[1], non_blocking=True)
+                torch.cuda.synchronize()
+                dt = time.perf_counter() - t0
+                if rep and (best is None or dt < best):
+                    best = dt
+            del hb, db
+            return 4 * nb / best / 1e9
+
         link = {"d2h_peak_GBs": link_peak(True), "h2d_peak_GBs": link_peak(False),
-                "peak_source": "measured in this run: 1 GiB pinned <-> device cudaMemcpyAsync, CUDA events"}
+                "bidir_peak_GBs": link_bidir(),
+                "peak_source": "measured in this run: 1 GiB pinned <-> device cudaMemcpyAsync, CUDA events "
+                               "(bidir: 1 GiB each way concurrently on two streams, wall clock)"}
         torch.cuda.empty_cache()  # return the 1 GiB probe to the device before the contexts
 
         # two device gradient buffers: the H2D of step t+1's G (side stream) overlaps step t's
@@ -645,16 +690,22 @@ def run_zenflow(args, rank, world):
                 torch.cuda.empty_cache()
 
         def _e2e_timed(ctx, devacc):
-            e2e_loop(ctx, 0, 2)  # warm-up
+            W2 = args.refresh   # warm-up: one accumulation window
+            e2e_loop(ctx, 0, W2)
             ctx.sync()
+            h1_0 = ctx.host_stats()
             ctx.profile_read()
             ctx.profile(True)
             if world > 1:
                 dist.barrier()
             t0 = time.perf_counter()
-            e2e_loop(ctx, 2, 2 + K)
+            e2e_loop(ctx, W2, W2 + K)
             ctx.sync()
             e2e_s = time.perf_counter() - t0
+            h1_1 = ctx.host_stats()
+            if not devacc:
+                link["h1_passes"] = h1_1[0] - h1_0[0]
+                link["h1_steps"] = h1_1[1] - h1_0[1]
             prof_e = ctx.profile_read()
             ctx.profile(False)
             if devacc:
@@ -675,7 +726,20 @@ def run_zenflow(args, rank, world):
             ms_dev = None
             result["e2e_note"] = f"device_accumulate does not fit in HBM here ({str(ex)[-60:]}); e2e = host accumulation"
             torch.cuda.empty_cache()
-        ms_host = e2e_run(False)
+        # host staging slots for the per-step D2H: H1 accumulates every staged step of a window
+        # in one pass (2*S slots: whole windows, overlapped with the next window's copies),
+        # as many as the host memory holds next to the accumulators and the pinned G
+        S_ = args.refresh
+        acc_bytes = 2 * 4 * sum(n * (m - k) for (n, m), k in zip(shapes, ks))
+        try:
+            avail = int([l.split()[1] for l in open("/proc/meminfo") if l.startswith("MemAvailable")][0]) * 1024
+        except Exception:  # noqa: BLE001
+            avail = 0
+        hstages = args.host_stages or 2 * S_
+        while hstages > 2 and hstages * d2h_host + acc_bytes + h2d > 0.85 * avail:
+            hstages -= 1
+        link["host_stages"] = hstages
+        ms_host = e2e_run(False, host_stages=hstages)
         if not state["double"]:
             result["e2e_note"] = (result.get("e2e_note", "") + "; one device gradient buffer "
                                   "(a second copy does not fit next to the context)").lstrip("; ")
@@ -689,13 +753,25 @@ def run_zenflow(args, rank, world):
         for key in ("x1_d2h_GBs", "window_d2h_GBs"):
             if link.get(key):
                 link[key.replace("_GBs", "_frac")] = link[key] / link["d2h_peak_GBs"]
-        # H1's host-memory traffic per step (per unselected element: read the staged bf16 value,
-        # write the fp32 accumulator, and read it back on every step of a window but the first)
-        S_ = args.refresh
-        h1_bytes = sum(n * (m - k) for (n, m), k in zip(shapes, ks)) * (2 + 4 + 4 * (S_ - 1) / S_)
+        # H1's host-memory traffic per step: per unselected element every staged bf16 value is
+        # read once (2 B); each H1 pass writes the fp32 accumulator once (4 B) and reads it
+        # unless the pass starts its window (4 B); windows = steps / S in the timed region
+        E_ = sum(n * (m - k) for (n, m), k in zip(shapes, ks))
+        p_, s_ = link.get("h1_passes") or K, link.get("h1_steps") or K
+        h1_bytes = E_ * (2 * s_ + 4 * p_ + 4 * max(0, p_ - s_ / S_)) / s_
         link["h1_host_dram_bytes_per_step"] = h1_bytes
         link["h1_host_dram_GBs"] = h1_bytes / (ms_host * 1e-3) / 1e9
         link["host_link_floor_ms"] = h2d / (link["h2d_peak_GBs"] * 1e9) * 1e3
+        # the per-step D2H host-accumulation mode moves G up and the compact block down every
+        # step: its floor is the slower of each direction alone and both through the shared link
+        link["host_link_floor_bidir_ms"] = max(h2d / link["h2d_peak_GBs"], d2h_host / link["d2h_peak_GBs"],
+                                               (h2d + d2h_host) / link["bidir_peak_GBs"]) / 1e9 * 1e3
+        link["host_link_floor_k7_ms"] = max(h2d / link["h2d_peak_GBs"], d2h_dev / link["d2h_peak_GBs"],
+                                            (h2d + d2h_dev) / link["bidir_peak_GBs"]) / 1e9 * 1e3
+        link["host_dram"] = host_dram_probe()
+        if link["host_dram"].get("accB1_GBs"):
+            # H1's floor on this host: its bytes per step at the probe's one-step-pass rate
+            link["h1_floor_ms"] = h1_bytes / (link["host_dram"]["accB1_GBs"] * 1e9) * 1e3
         node = None
         try:
             import glob as _glob

@@ -244,6 +244,16 @@ typedef struct {
                                          step t with (t+1) % N == 0 must stay valid until
                                          the next zf_step or zf_sync (e.g. double-buffered
                                          gradients).  Not with auto_gamma.             */
+    int32_t host_stages;              /* pinned host staging slots of the per-step D2H
+                                         (offload without device_accumulate), each one
+                                         compact block of every layer; 0 = 2.  H1 (row a8)
+                                         accumulates every staged step of the current window
+                                         in ONE pass over the fp32 accumulator (the adds
+                                         stay in step order: bit-identical sums), so more
+                                         slots cut its host-DRAM traffic from ~10 B per
+                                         element and step towards 3 (2·accum_interval slots:
+                                         whole windows, overlapped with the next window's
+                                         copies).  Range [0, 16]; ZF_EINVAL otherwise.   */
 } zf_config;
 
 typedef struct zf_ctx zf_ctx;
@@ -328,9 +338,32 @@ zf_status zf_set_lr(zf_ctx* ctx, double lr);
  * the previous read, and resets them. */
 zf_status zf_profile(zf_ctx* ctx, int32_t enable);
 zf_status zf_profile_read(zf_ctx* ctx, double* ms, int64_t* count);
+/* Row a2 over peer memory (next row f4 (iii), "shares these partial norms with the
+ * other GPUs"): instead of an NCCL all-reduce (or the host callback), the ranks' kernels
+ * sum the partial norm vectors by reading each other's device memory directly -- over
+ * NVLink / NVSwitch between GPUs (CUDA IPC mappings with peer access), or plain device
+ * memory when ranks share a GPU.  Two-shot: each rank sums its 1/world slice of the
+ * columns over the ranks in rank order 0..world-1 (one fixed fp32 order, so every rank
+ * holds the same bits), then every rank gathers the slices; flags in the regions order
+ * the phases and double buffers let the next exchange start while a slow peer still
+ * reads the previous one.  Setup, on every rank of a context created with world > 1 and
+ * no NCCL id (world <= 8):
+ *   zf_peer_handle writes this rank's 64-byte IPC handle [host];
+ *   the caller all-gathers the handles (e.g. torch.distributed) in rank order;
+ *   zf_peer_open(handles [host] world x 64 bytes) maps the others' regions.
+ * A wait that sees no peer for 20 s gives up and zf_sync reports ZF_ENCCL.
+ * ZF_ESTATE: NCCL context, world < 2, zf_peer_open before zf_peer_handle or twice. */
+zf_status zf_peer_handle(zf_ctx* ctx, void* out64);
+zf_status zf_peer_open(zf_ctx* ctx, const void* handles);
+
 /* param_subset: the caller wrote p (e.g. loaded a checkpoint) outside zf_step; the next
  * zf_step re-reads the selected columns from p (as a refresh does) before using them. */
 zf_status zf_params_changed(zf_ctx* c);
+
+/* H1 (row a8) statistics [host]: accumulation passes run and the steps they covered
+ * (steps / passes = the mean batch of window steps one pass accumulated; host_stages).
+ * Counts the passes finished so far (zf_sync first for a complete count). */
+zf_status zf_host_stats(zf_ctx* ctx, int64_t* h1_passes, int64_t* h1_steps);
 
 /* Number of this library's kernel launches issued so far by the context. */
 int64_t zf_kernel_launches(zf_ctx* ctx);

@@ -4,6 +4,8 @@
 // the views of library-owned state.  See DESIGN.md §5-§6.
 #include "zf_host.h"
 
+zf_status peer_allreduce(zf_ctx* c, cudaStream_t s);   // f4 (iii), below
+
 extern "C" zf_status zf_nccl_unique_id(void* out128) {
     g_last_error.clear();
     if (!out128) return fail(ZF_EINVAL, "out is NULL");
@@ -230,6 +232,8 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
     if (cfg->device_accumulate && !cfg->host_accumulate)
         return fail(ZF_EINVAL, "device_accumulate requires host_accumulate (it moves that accumulation onto the GPU)");
     ZF_TRY(check_hp(&cfg->adam));
+    if (cfg->host_stages < 0 || cfg->host_stages > ZF_MAX_HSTAGE)
+        return fail(ZF_EINVAL, "host_stages must be in [0, %d]", ZF_MAX_HSTAGE);
     if (world < 1 || rank < 0 || rank >= world) return fail(ZF_EINVAL, "bad world/rank");
     // world > 1 without an NCCL id: the norm exchange goes through a host all-reduce callback
     // registered with zf_set_host_allreduce before the first step
@@ -262,6 +266,7 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
     c->psz = esize(cfg->param_dtype);
     c->devacc = cfg->device_accumulate != 0;
     c->n_stage = cfg->offload && !c->devacc ? 2 : 1;
+    c->n_hstage = cfg->host_stages > 0 ? cfg->host_stages : 2;
     c->lr_cur = cfg->adam.lr;
     c->tau = cfg->warmup_steps;
     c->grid = update_grid(c->gdt, c->pdt);
@@ -366,6 +371,8 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
         *h = 0;
         c->nonfinite_h = h;
         ZF_CUDA(cudaHostGetDevicePointer(&c->nonfinite_d, h, 0));
+        c->peer_err_h = h + 4;   // f4 (iii): peer-exchange timeout flag, same mapped block
+        *c->peer_err_h = 0;
     }
     // ---- AdamW tables
     c->adam = adam_scalars(cfg->adam);
@@ -448,7 +455,7 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
         ZF_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
         for (int s = 0; s < 2; ++s) ZF_CUDA(cudaEventCreateWithFlags(&c->d2h_all[s], cudaEventDisableTiming));
         for (auto& l : c->L) {
-            for (int s = 0; s < (c->devacc ? 0 : 2); ++s) {  // per-step compact D2H (not with K7)
+            for (int s = 0; s < (c->devacc ? 0 : c->n_hstage); ++s) {  // per-step compact D2H (not with K7)
                 void* h = nullptr;
                 ZF_CUDA(cudaHostAlloc(&h, std::max<size_t>((size_t)l.d.n * l.mk_pad * c->gsz, 64), cudaHostAllocDefault));
                 c->host_pinned.push_back(h);
@@ -654,8 +661,8 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
     } else if (t0 % N != 0) {
         return fail(ZF_ESTATE, "first step must be a refresh step (t %% N == 0)");
     }
-    if (c->world > 1 && !c->comm && !c->host_allreduce)
-        return fail(ZF_ESTATE, "world > 1 needs an NCCL id at zf_create or zf_set_host_allreduce");
+    if (c->world > 1 && !c->comm && !c->host_allreduce && !c->peer)
+        return fail(ZF_ESTATE, "world > 1 needs an NCCL id at zf_create, zf_peer_open or zf_set_host_allreduce");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     c->last_stream = s;
     ZF_CUDA(cudaSetDevice(c->device));
@@ -685,7 +692,13 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
         if (c->cfg.host_accumulate && !c->devacc) {
             // host staging buffer sb is free once H1 consumed step t-2
             std::unique_lock<std::mutex> lk(c->mu);
-            c->cv.wait(lk, [&] { return c->h1_done >= t - 2 || c->last_t < t - 2; });
+            const int64_t need = t - c->n_hstage;
+            if (!(c->h1_done >= need || c->last_t < need)) {
+                ++c->h1_waiters;
+                c->cv.notify_all();
+                c->cv.wait(lk, [&] { return c->h1_done >= need || c->last_t < need; });
+                --c->h1_waiters;
+            }
         }
     }
     if (norms_now) {
@@ -703,6 +716,8 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
             ZF_TRY(c->prof_begin(1, s, &pe));
             if (c->comm) {
                 ZF_NCCL(ncclAllReduce(c->norms, c->norms, (size_t)c->total_m, ncclFloat32, ncclSum, c->comm, s));
+            } else if (c->peer) {
+                ZF_TRY(peer_allreduce(c, s));
             } else {
                 // host all-reduce (e.g. torch.distributed gloo): stream-synchronous round trip
                 ZF_CUDA(cudaMemcpyAsync(c->norms_host, c->norms, c->total_m * sizeof(float), cudaMemcpyDeviceToHost, s));
@@ -718,7 +733,7 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
         // the norms of step t-1 (and, with NCCL, their all-reduce) were made on the side stream
         if (c->lag_pending) ZF_CUDA(cudaStreamWaitEvent(s, c->norm_ready, 0));
         c->lag_pending = false;
-        if (c->world > 1 && !c->comm) {
+        if (c->world > 1 && !c->comm && !c->peer) {
             zf_ctx::Pending pe;
             ZF_TRY(c->prof_begin(1, s, &pe));
             ZF_CUDA(cudaMemcpyAsync(c->norms_host, c->norms, c->total_m * sizeof(float), cudaMemcpyDeviceToHost, s));
@@ -788,9 +803,12 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
         ZF_CUDA(launch_norms(tn, c->k1_units, c->gdt, c->nonfinite_d, c->lag_stream));
         ZF_TRY(c->prof_end(&pe, c->lag_stream));
         c->launches++;
-        if (c->world > 1 && c->comm) {
+        if (c->world > 1 && (c->comm || c->peer)) {
             ZF_TRY(c->prof_begin(1, c->lag_stream, &pe));
-            ZF_NCCL(ncclAllReduce(c->norms, c->norms, (size_t)c->total_m, ncclFloat32, ncclSum, c->comm, c->lag_stream));
+            if (c->comm)
+                ZF_NCCL(ncclAllReduce(c->norms, c->norms, (size_t)c->total_m, ncclFloat32, ncclSum, c->comm, c->lag_stream));
+            else
+                ZF_TRY(peer_allreduce(c, c->lag_stream));
             ZF_TRY(c->prof_end(&pe, c->lag_stream));
         }
         ZF_CUDA(cudaEventRecord(c->norm_ready, c->lag_stream));
@@ -849,7 +867,9 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
     ZF_CUDA(cudaEventRecord(c->step_done, s));
 
     if (c->cfg.offload && !c->devacc) {
-        // X1: per-layer D2H as soon as the layer's last unit finished (cyclic counter)
+        // X1: per-layer D2H as soon as the layer's last unit finished (cyclic counter), into
+        // host staging slot hs
+        const int hs = (int)(t % c->n_hstage);
         if (!c->wait_value) ZF_CUDA(cudaStreamWaitEvent(c->copy_stream, c->step_done, 0));
         zf_ctx::Pending pe4;
         bool pe4_open = false;
@@ -871,10 +891,10 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
                     ZF_TRY(c->prof_begin(4, c->copy_stream, &pe4));
                     pe4_open = true;
                 }
-                ZF_CUDA(cudaMemcpyAsync(l.stage_host[sb], l.stage_dev[sb], (size_t)l.d.n * l.mk_pad * c->gsz,
+                ZF_CUDA(cudaMemcpyAsync(l.stage_host[hs], l.stage_dev[sb], (size_t)l.d.n * l.mk_pad * c->gsz,
                                         cudaMemcpyDeviceToHost, c->copy_stream));
             }
-            ZF_CUDA(cudaEventRecord(l.d2h_ev[sb], c->copy_stream));
+            ZF_CUDA(cudaEventRecord(l.d2h_ev[hs], c->copy_stream));
         }
         if (pe4_open) ZF_TRY(c->prof_end(&pe4, c->copy_stream));
         ZF_CUDA(cudaEventRecord(c->d2h_all[sb], c->copy_stream));
@@ -956,7 +976,10 @@ extern "C" zf_status zf_sync(zf_ctx* c) {
     if (c->lag_stream) ZF_CUDA(cudaStreamSynchronize(c->lag_stream));   // a lagged K1 (f4 ii)
     if (c->cfg.host_accumulate) {
         std::unique_lock<std::mutex> lk(c->mu);
+        ++c->h1_waiters;
+        c->cv.notify_all();
         c->cv.wait(lk, [&] { return c->jobs.empty(); });
+        --c->h1_waiters;
     }
     if (c->k3_prof && getenv("ZF_K3_PROF_PRINT")) {
         unsigned long long h[6];
@@ -966,6 +989,10 @@ extern "C" zf_status zf_sync(zf_ctx* c) {
         fprintf(stderr, "[k3 prof] per warp-unit cycles: wait_full %.0f adam %.0f compact %.0f gbar_wait %.0f "
                         "writeback+release %.0f (warp-units %llu)\n",
                 h[0] / u, h[1] / u, h[2] / u, h[3] / u, h[4] / u, h[5]);
+    }
+    if (c->peer_err_h && *(volatile int32_t*)c->peer_err_h) {
+        *c->peer_err_h = 0;
+        return fail(ZF_ENCCL, "peer-memory norm exchange: a peer did not arrive within the timeout");
     }
     volatile int32_t* f = c->nonfinite_h;
     if (*f) {
@@ -1021,7 +1048,7 @@ extern "C" zf_status zf_compact_buffer(zf_ctx* c, int32_t layer, const void** de
     const int sb = (int)(c->last_t % c->n_stage);
     if (dev) *dev = c->L[layer].stage_dev[sb];
     if (dev_ld) *dev_ld = c->L[layer].mk_pad;
-    if (host) *host = c->cfg.offload && !c->devacc ? c->L[layer].stage_host[sb] : nullptr;
+    if (host) *host = c->cfg.offload && !c->devacc ? c->L[layer].stage_host[c->last_t % c->n_hstage] : nullptr;
     return ZF_OK;
 }
 
@@ -1084,6 +1111,76 @@ extern "C" zf_status zf_set_host_allreduce(zf_ctx* c, zf_host_allreduce_fn fn, v
     return ZF_OK;
 }
 
+// ---- f4 (iii): the norm exchange over peer memory (k_peer.cu)
+static int64_t peer_stride(const zf_ctx* c) { return (c->total_m + 63) / 64 * 64; }
+static size_t peer_region_bytes(const zf_ctx* c) { return 256 + 4 * (size_t)peer_stride(c) * sizeof(float); }
+
+zf_status peer_allreduce(zf_ctx* c, cudaStream_t s) {
+    PeerArgs a = c->peer_args;
+    a.epoch = ++c->peer_epoch;
+    ZF_CUDA(launch_peer_allreduce(a, s));
+    c->launches += 3;
+    return ZF_OK;
+}
+
+extern "C" zf_status zf_peer_handle(zf_ctx* c, void* out64) {
+    g_last_error.clear();
+    if (!c || !out64) return fail(ZF_EINVAL, "ctx/out is NULL");
+    if (c->world < 2 || c->comm) return fail(ZF_ESTATE, "peer exchange needs world > 1 created without an NCCL id");
+    if (c->world > ZF_MAX_PEERS) return fail(ZF_EINVAL, "peer exchange supports world <= %d", ZF_MAX_PEERS);
+    ZF_CUDA(cudaSetDevice(c->device));
+    if (!c->peer_region) {
+        ZF_CUDA(cudaMalloc(&c->peer_region, peer_region_bytes(c)));
+        c->dev_allocs.push_back(c->peer_region);
+        ZF_CUDA(cudaMemset(c->peer_region, 0, peer_region_bytes(c)));
+        ZF_CUDA(cudaDeviceSynchronize());
+    }
+    cudaIpcMemHandle_t h;
+    ZF_CUDA(cudaIpcGetMemHandle(&h, c->peer_region));
+    static_assert(sizeof(h) == 64, "IPC handle size");
+    std::memcpy(out64, &h, 64);
+    return ZF_OK;
+}
+
+extern "C" zf_status zf_peer_open(zf_ctx* c, const void* handles) {
+    g_last_error.clear();
+    if (!c || !handles) return fail(ZF_EINVAL, "ctx/handles is NULL");
+    if (!c->peer_region) return fail(ZF_ESTATE, "zf_peer_handle first");
+    if (c->peer) return fail(ZF_ESTATE, "peer exchange already open");
+    ZF_CUDA(cudaSetDevice(c->device));
+    PeerArgs& a = c->peer_args;
+    a = PeerArgs{};
+    a.world = c->world;
+    a.rank = c->rank;
+    a.M = c->total_m;
+    a.Mp = peer_stride(c);
+    a.norms = c->norms;
+    for (int q = 0; q < c->world; ++q) {
+        unsigned char* base;
+        if (q == c->rank) {
+            base = static_cast<unsigned char*>(c->peer_region);
+        } else {
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, static_cast<const unsigned char*>(handles) + 64 * q, 64);
+            void* p = nullptr;
+            ZF_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+            c->peer_mapped[q] = p;
+            base = static_cast<unsigned char*>(p);
+        }
+        a.flags[q] = reinterpret_cast<unsigned long long*>(base);
+        a.part[q] = reinterpret_cast<float*>(base + 256);
+        a.red[q] = a.part[q] + 2 * a.Mp;
+    }
+    uint32_t* counter = nullptr;
+    ZF_TRY(c->dalloc(&counter, sizeof(uint32_t) * 8, true));
+    a.counter = counter;
+    int32_t* err_d = nullptr;
+    ZF_CUDA(cudaHostGetDevicePointer(&err_d, c->peer_err_h, 0));
+    a.error = err_d;
+    c->peer = true;
+    return ZF_OK;
+}
+
 extern "C" zf_status zf_params_changed(zf_ctx* c) {
     g_last_error.clear();
     if (!c) return fail(ZF_EINVAL, "ctx is NULL");
@@ -1099,6 +1196,15 @@ extern "C" zf_status zf_set_lr(zf_ctx* c, double lr) {
 }
 
 extern "C" int64_t zf_kernel_launches(zf_ctx* c) { return c ? c->launches : -1; }
+
+extern "C" zf_status zf_host_stats(zf_ctx* c, int64_t* passes, int64_t* steps) {
+    g_last_error.clear();
+    if (!c) return fail(ZF_EINVAL, "ctx is NULL");
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (passes) *passes = c->h1_batches;
+    if (steps) *steps = c->h1_batched_steps;
+    return ZF_OK;
+}
 
 extern "C" zf_status zf_profile(zf_ctx* c, int32_t enable) {
     if (!c) return fail(ZF_EINVAL, "ctx is NULL");

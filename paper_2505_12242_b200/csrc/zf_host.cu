@@ -17,11 +17,13 @@ zf_ctx::~zf_ctx() {
     cudaSetDevice(device);
     cudaDeviceSynchronize();
     if (comm) ncclCommDestroy(comm);
+    for (void* p : peer_mapped)
+        if (p) cudaIpcCloseMemHandle(p);
     for (void* p : dev_allocs) cudaFree(p);
     for (void* p : host_pinned) cudaFreeHost(p);
     for (float* p : host_plain) std::free(p);
     for (auto& l : L)
-        for (int i = 0; i < 2; ++i)
+        for (int i = 0; i < ZF_MAX_HSTAGE; ++i)
             if (l.d2h_ev[i]) cudaEventDestroy(l.d2h_ev[i]);
     for (auto e : ring_ev) cudaEventDestroy(e);
     for (auto e : d2h_all)
@@ -71,62 +73,136 @@ void zfh::acc_row_f32(float* __restrict__ acc, const float* __restrict__ src, in
     }
 }
 
-// H1: accumulate each layer's staged compact block into the window's fp32 buffer
-// as soon as its D2H copy completed (DESIGN.md §2 O8).
+// b staged steps of one window in one pass over the accumulator: the host-DRAM traffic of a
+// batch is (first ? 0 : 4) + 2b + 4 bytes per element instead of b x 10 (H1 is host-DRAM
+// bound).  The adds stay in step order per element, so the sums are bit-identical to one
+// step at a time.  Rows are walked in chunks that stay in L1.
+__attribute__((target_clones("avx512f", "avx2", "default")))
+void zfh::acc_row_multi(float* __restrict__ acc, const void* const* src, int b, int64_t n, bool first, bool bf16) {
+    constexpr int64_t CH = 512;
+    float tmp[CH];
+    for (int64_t c0 = 0; c0 < n; c0 += CH) {
+        const int64_t w = n - c0 < CH ? n - c0 : CH;
+        if (first)
+            for (int64_t i = 0; i < w; ++i) tmp[i] = 0.0f;
+        else
+            for (int64_t i = 0; i < w; ++i) tmp[i] = acc[c0 + i];
+        for (int j = 0; j < b; ++j) {
+            if (bf16) {
+                const uint16_t* x = static_cast<const uint16_t*>(src[j]) + c0;
+                for (int64_t i = 0; i < w; ++i) {
+                    uint32_t u = (uint32_t)x[i] << 16;
+                    float f;
+                    std::memcpy(&f, &u, 4);
+                    tmp[i] = tmp[i] + f;
+                }
+            } else {
+                const float* x = static_cast<const float*>(src[j]) + c0;
+                for (int64_t i = 0; i < w; ++i) tmp[i] = tmp[i] + x[i];
+            }
+        }
+        for (int64_t i = 0; i < w; ++i) acc[c0 + i] = tmp[i];
+    }
+}
+
+// H1: accumulate the staged compact blocks into the window's fp32 buffer as their D2H copies
+// complete (DESIGN.md §2 O8).  Steps are taken in batches: every queued
+// step of the current window, up to its last step.  A batch that does not reach the window's
+// end waits for more steps while the producer can still stage them (free host slots) and
+// nobody waits on H1 (zf_step on a slot, zf_sync, f1) -- then it runs with what it has.
 void zf_ctx::h1_loop() {
     cudaSetDevice(device);
     const int S = cfg.accum_interval;
+    std::vector<int64_t> batch;
+    std::vector<char> ends;
     for (;;) {
-        int64_t t;
+        batch.clear();
+        ends.clear();
         {
             std::unique_lock<std::mutex> lk(mu);
             cv.wait(lk, [&] { return stopping || !jobs.empty(); });
             if (jobs.empty()) return;
-            t = jobs.front();
         }
+        // grow the batch: queued steps of the current window, stopping after a window end
+        for (;;) {
+            std::vector<int64_t> q;
+            {
+                std::lock_guard<std::mutex> lk(mu);
+                q.assign(jobs.begin(), jobs.end());
+            }
+            for (size_t i = batch.size(); i < q.size(); ++i) {
+                const int64_t t = q[i];
+                bool end = (t + 1) % S == 0;
+                if (autoz) {
+                    // the window decision of step t: K6's record (Zen-auto, reading R21)
+                    const int slot = (int)(t % AUTO_RING);
+                    cudaEventSynchronize(auto_ev[slot]);
+                    end = auto_rec_h[slot].end != 0;
+                }
+                batch.push_back(t);
+                ends.push_back(end ? 1 : 0);
+                if (end || (int)batch.size() >= n_hstage) break;
+            }
+            if (ends.back() || (int)batch.size() >= n_hstage || n_hstage <= 2) break;
+            // more steps of this window can still be staged: wait for one, unless someone waits on us
+            std::unique_lock<std::mutex> lk(mu);
+            cv.wait(lk, [&] { return stopping || h1_waiters > 0 || jobs.size() > batch.size(); });
+            if (jobs.size() <= batch.size()) break;   // stopping or a waiter: run what we have
+        }
+        const int b = (int)batch.size();
         const int a = (int)(h1_win % 2);
         const bool first = h1_first;
-        const int sb = (int)(t % n_stage);
+        const bool bf = gdt == ZF_BF16;
         for (auto& l : L) {
-            cudaEventSynchronize(l.d2h_ev[sb]);
+            const void* srcs[ZF_MAX_HSTAGE];
+            for (int j = 0; j < b; ++j) {
+                const int hs = (int)(batch[j] % n_hstage);
+                cudaEventSynchronize(l.d2h_ev[hs]);
+                srcs[j] = l.stage_host[hs];
+            }
             const int64_t mk = l.mk, ld = l.mk_pad;
             float* acc = l.acc[a];
-            const void* stage = l.stage_host[sb];
-            const bool bf = gdt == ZF_BF16;
-            pool->parallel_for(l.d.n, [&](int64_t b, int64_t e) {
-                for (int64_t r = b; r < e; ++r) {
-                    if (bf) acc_row_bf16(acc + r * mk, static_cast<const uint16_t*>(stage) + r * ld, mk, first);
-                    else acc_row_f32(acc + r * mk, static_cast<const float*>(stage) + r * ld, mk, first);
+            pool->parallel_for(l.d.n, [&](int64_t rb, int64_t re) {
+                const void* rs[ZF_MAX_HSTAGE];
+                for (int64_t r = rb; r < re; ++r) {
+                    if (b == 1) {
+                        if (bf) acc_row_bf16(acc + r * mk, static_cast<const uint16_t*>(srcs[0]) + r * ld, mk, first);
+                        else acc_row_f32(acc + r * mk, static_cast<const float*>(srcs[0]) + r * ld, mk, first);
+                    } else {
+                        for (int j = 0; j < b; ++j)
+                            rs[j] = static_cast<const unsigned char*>(srcs[j]) + r * ld * (bf ? 2 : 4);
+                        acc_row_multi(acc + r * mk, rs, b, mk, first, bf);
+                    }
                 }
             });
         }
-        // the window decision of step t: fixed S, or K6's record (Zen-auto, reading R21)
-        bool end = (t + 1) % S == 0;
-        double rA = NAN, ri = NAN, ru = NAN;
-        if (autoz) {
-            const int slot = (int)(t % AUTO_RING);
-            cudaEventSynchronize(auto_ev[slot]);
-            const volatile AutoRecord* r = auto_rec_h + slot;
-            end = r->end != 0;
-            rA = r->A;
-            ri = r->imp;
-            ru = r->unimp;
-        }
+        const bool end = ends.back() != 0;
         {
             std::lock_guard<std::mutex> lk(mu);
+            for (int j = 0; j < b; ++j) {
+                double rA = NAN, ri = NAN, ru = NAN;
+                if (autoz) {
+                    const volatile AutoRecord* r = auto_rec_h + (int)(batch[j] % AUTO_RING);
+                    rA = r->A;
+                    ri = r->imp;
+                    ru = r->unimp;
+                }
+                log_t.push_back(batch[j] + tau);
+                log_end.push_back(ends[j]);
+                log_A.push_back(rA);
+                log_i.push_back(ri);
+                log_u.push_back(ru);
+                jobs.pop_front();
+            }
             h1_last_buf = a;
             if (end) {
                 h1_sealed_buf = a;
                 ++h1_win;
             }
             h1_first = end;
-            log_t.push_back(t + tau);
-            log_end.push_back(end ? 1 : 0);
-            log_A.push_back(rA);
-            log_i.push_back(ri);
-            log_u.push_back(ru);
-            jobs.pop_front();
-            h1_done = t;
+            h1_done = batch.back();
+            h1_batches += 1;
+            h1_batched_steps += b;
         }
         cv.notify_all();
     }
@@ -324,7 +400,10 @@ zf_status f1_compute(zf_ctx* c, int64_t t, int buf, int64_t len, double lr) {
         ZF_CUDA(cudaEventSynchronize(c->acc_d2h_ev[buf]));  // the sealed window's host copy
     } else {
         std::unique_lock<std::mutex> lk(c->mu);
+        ++c->h1_waiters;
+        c->cv.notify_all();
         c->cv.wait(lk, [&] { return c->h1_done >= t; });
+        --c->h1_waiters;
     }
     const zf_adam_params& hp = c->cfg.adam;
     const double b1d = hp.beta1, b2d = hp.beta2;

@@ -83,6 +83,7 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 // (DESIGN.md §2 O6): ss[t] = f32(lr / (1 - b1^t)), bc2s[t] = f32(sqrt(1 - b2^t)).
 // Both are monotone in t and reach their limits (f32(lr), 1.0f) at a finite t;
 // the tables stop there and the kernel uses the limit beyond.
+#define ZF_MAX_HSTAGE 16   // host staging slots a context may ask for (zf_config.host_stages)
 constexpr int64_t MAX_TAB = 1 << 24;
 constexpr int64_t SS_CAP = 1 << 16;  // ss table capacity of a context (beta1 <= 0.999)
 
@@ -352,7 +353,7 @@ struct LayerState {
     void* gsel = nullptr;             // split update: [n, k] selected gradients (K3a -> K3b)
     int64_t row_begin = 0;            // K3b: prefix of ceil(n*k / 8) over layers (its chunks)
     void* stage_dev[2] = {nullptr, nullptr};
-    void* stage_host[2] = {nullptr, nullptr};
+    void* stage_host[ZF_MAX_HSTAGE] = {};   // pinned compact blocks, one per host staging slot
     float* acc[2] = {nullptr, nullptr};
     float* dacc[2] = {nullptr, nullptr};  // device_accumulate: [n, mk_pad] fp32 window accumulators
     float* acc_sealed_h = nullptr;        // device_accumulate: pinned dense [n, mk] copy of the sealed window
@@ -361,7 +362,7 @@ struct LayerState {
     int64_t unit_begin = 0;
     K3Geom geo_s{};                   // steady units (param_subset: the subset slab instead of a p tile)
     int64_t unit_begin_s = 0;
-    cudaEvent_t d2h_ev[2] = {nullptr, nullptr};
+    cudaEvent_t d2h_ev[ZF_MAX_HSTAGE] = {};  // per host staging slot: this layer's D2H landed
     // f1: deferred CPU AdamW (reading R18)
     // dense over the current unselected columns (position u = column unsel_host[u]), remapped
     // at every refresh: the window update is then a contiguous, vectorised row loop
@@ -505,13 +506,21 @@ struct zf_ctx {
     int world = 1, rank = 0;
     ncclComm_t comm = nullptr;
     zf_host_allreduce_fn host_allreduce = nullptr;  // world > 1 without NCCL
+    // f4 (iii): norm exchange over peer memory (k_peer.cu; zf_peer_handle / zf_peer_open)
+    bool peer = false;
+    void* peer_region = nullptr;               // this rank's exchange region (cudaMalloc, IPC-exported)
+    void* peer_mapped[ZF_MAX_PEERS] = {};      // the peers' regions opened in this process
+    PeerArgs peer_args{};
+    unsigned long long peer_epoch = 0;
+    int32_t* peer_err_h = nullptr;             // mapped: a peer wait timed out
     void* host_allreduce_user = nullptr;
     float* norms_host = nullptr;
     int gdt = 0, pdt = 0, gsz = 2, psz = 2;
     std::vector<LayerState> L;
     int64_t total_m = 0, max_m = 0, k1_units = 0, k3_units = 0, k3_units_s = 0;
     bool has_empty = false;       // some layer has n = 0 rows on this rank
-    int n_stage = 1;
+    int n_stage = 1;              // device compact blocks (ring over steps)
+    int n_hstage = 2;             // pinned host staging slots (ring over steps; host_stages)
     float* norms = nullptr;
     std::vector<void*> dev_allocs, host_pinned;
     std::vector<float*> host_plain;
@@ -580,6 +589,9 @@ struct zf_ctx {
     std::deque<int64_t> jobs;
     int64_t h1_done = -1;
     bool stopping = false;
+    int h1_waiters = 0;           // threads blocked on H1 progress: H1 then processes what it has
+    int64_t h1_batches = 0, h1_batched_steps = 0;   // H1 passes and the steps they covered
+
     // accumulation windows as H1 sees them (fixed S, or Zen-auto decisions), and the log
     int64_t h1_win = 0;           // index of the window the next processed step belongs to
     bool h1_first = true;         // the next processed step starts a window
@@ -692,6 +704,8 @@ namespace zfh {
 // zf_host.cu
 void acc_row_bf16(float* acc, const uint16_t* src, int64_t n, bool first);
 void acc_row_f32(float* acc, const float* src, int64_t n, bool first);
+// b steps of one window in one pass: acc = (((first ? 0 : acc) + x_0) + x_1) ... + x_{b-1}
+void acc_row_multi(float* acc, const void* const* src, int b, int64_t n, bool first, bool bf16);
 zf_status f1_refresh(zf_ctx* c, void* const* params, cudaStream_t s);
 zf_status f1_window_end(zf_ctx* c, int64_t t, int buf, int64_t len, void* const* params, cudaStream_t s);
 zf_status f1_launch(zf_ctx* c, int64_t t, int buf, int64_t len, void* const* params);

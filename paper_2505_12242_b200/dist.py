@@ -98,3 +98,15 @@ def gloo_allreduce(group=None):
         t = torch.from_numpy(buf)          # shares memory with the library's pinned buffer
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     return fn
+
+
+def open_peer_exchange(ctx, group=None):
+    """Row a2 over peer memory (next row f4 (iii)): all-gather every rank's 64-byte
+    IPC handle of its norm-exchange region over `group` (rank order) and map the others
+    (``zf_peer_open``); the context's norm exchange then runs as kernels reading the peers'
+    device memory (NVLink / NVSwitch, or one shared GPU), with no NCCL launch."""
+    import torch.distributed as dist
+
+    handles = [None] * dist.get_world_size(group)
+    dist.all_gather_object(handles, ctx.peer_handle(), group=group)
+    ctx.peer_open(handles)

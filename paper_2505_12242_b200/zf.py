@@ -21,7 +21,7 @@ ZF_FP32, ZF_BF16 = 0, 1
 SYMBOLS = ["zf_status_string", "zf_last_error", "zf_version", "zf_k_for", "zf_column_norms", "zf_topk_columns",
            "zf_selective_adam", "zf_compact_unselected", "zf_nccl_unique_id", "zf_create", "zf_step", "zf_sync",
            "zf_selected", "zf_norms", "zf_optimizer_state", "zf_compact_buffer", "zf_host_accumulator", "zf_device_accumulator", "zf_window_log", "zf_set_host_allreduce", "zf_set_lr",
-           "zf_kernel_launches", "zf_profile", "zf_profile_read", "zf_params_changed", "zf_destroy"]
+           "zf_kernel_launches", "zf_profile", "zf_profile_read", "zf_params_changed", "zf_host_stats", "zf_peer_handle", "zf_peer_open", "zf_destroy"]
 
 
 class ZFError(RuntimeError):
@@ -47,7 +47,8 @@ class Config(ctypes.Structure):
                 ("cpu_update", ctypes.c_int32), ("warmup_steps", ctypes.c_int32),
                 ("auto_gamma", ctypes.c_float), ("state_offload", ctypes.c_int32),
                 ("device_accumulate", ctypes.c_int32), ("cpu_update_async", ctypes.c_int32),
-                ("param_subset", ctypes.c_int32), ("lagged_selection", ctypes.c_int32)]
+                ("param_subset", ctypes.c_int32), ("lagged_selection", ctypes.c_int32),
+                ("host_stages", ctypes.c_int32)]
 
 
 if not os.path.exists(_LIB_PATH):
@@ -95,6 +96,9 @@ lib.zf_set_host_allreduce.restype = _st
 lib.zf_set_lr.argtypes = [_vp, ctypes.c_double]; lib.zf_set_lr.restype = _st
 lib.zf_params_changed.argtypes = [_vp]; lib.zf_params_changed.restype = _st
 lib.zf_kernel_launches.argtypes = [_vp]; lib.zf_kernel_launches.restype = _i64
+lib.zf_peer_handle.argtypes = [_vp, _vp]; lib.zf_peer_handle.restype = _st
+lib.zf_peer_open.argtypes = [_vp, _vp]; lib.zf_peer_open.restype = _st
+lib.zf_host_stats.argtypes = [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]; lib.zf_host_stats.restype = _st
 lib.zf_destroy.argtypes = [_vp]; lib.zf_destroy.restype = _st
 lib.zf_profile.argtypes = [_vp, _i32]; lib.zf_profile.restype = _st
 lib.zf_profile_read.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64)]
@@ -211,7 +215,7 @@ class Context:
                  host_accumulate=False, host_threads=0, world=1, rank=0, nccl_id: bytes | None = None,
                  device: int | None = None, cpu_update=False, warmup_steps=0, auto_gamma=0.0,
                  state_offload=False, device_accumulate=False, host_allreduce=None, cpu_update_async=False,
-                 param_subset=True, lagged_selection=False):
+                 param_subset=True, lagged_selection=False, host_stages=0):
         self.layers = [l if isinstance(l, LayerShape) else LayerShape(*l) for l in layers]
         descs = (LayerDesc * len(self.layers))()
         for d, l in zip(descs, self.layers):
@@ -237,6 +241,7 @@ class Context:
         cfg.cpu_update_async = int(cpu_update_async)
         cfg.param_subset = int(param_subset)
         cfg.lagged_selection = int(lagged_selection)
+        cfg.host_stages = int(host_stages)
         self.cfg = cfg
         self.device = torch.cuda.current_device() if device is None else device
         h = ctypes.c_void_p()
@@ -297,6 +302,24 @@ class Context:
 
     def kernel_launches(self) -> int:
         return int(lib.zf_kernel_launches(self._h))
+
+    def peer_handle(self) -> bytes:
+        """This rank's 64-byte IPC handle of its norm-exchange region (f4 iii)."""
+        buf = ctypes.create_string_buffer(64)
+        _check(lib.zf_peer_handle(self._h, buf), "zf_peer_handle")
+        return buf.raw
+
+    def peer_open(self, handles) -> None:
+        """Map the other ranks' exchange regions (handles: one 64-byte handle per rank, rank
+        order); the norm exchange then runs over peer memory."""
+        raw = b"".join(bytes(h) for h in handles)
+        _check(lib.zf_peer_open(self._h, ctypes.create_string_buffer(raw, len(raw))), "zf_peer_open")
+
+    def host_stats(self):
+        """(H1 accumulation passes, steps they covered) so far."""
+        a, b = _i64(), _i64()
+        _check(lib.zf_host_stats(self._h, ctypes.byref(a), ctypes.byref(b)), "zf_host_stats")
+        return int(a.value), int(b.value)
 
     # views of library-owned state (device tensors share memory with the library)
     def selected(self, layer: int) -> torch.Tensor:

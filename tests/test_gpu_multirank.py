@@ -27,7 +27,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, steps, N, cpu_update, partition):
+def _worker(rank, world, port, steps, N, cpu_update, partition, exchange="host", lagged=False):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
@@ -39,7 +39,7 @@ def _worker(rank, world, port, steps, N, cpu_update, partition):
     from gpu_util import assert_bits_equal, assert_close_rel, selection_ok, to_np
     from oracle import oracle as orc
     from paper_2505_12242_b200 import zf
-    from paper_2505_12242_b200.dist import flat_partition, gloo_allreduce, shard_rows
+    from paper_2505_12242_b200.dist import flat_partition, gloo_allreduce, open_peer_exchange, shard_rows
     from synth import gpu
 
     torch.cuda.set_device(0)
@@ -48,14 +48,18 @@ def _worker(rank, world, port, steps, N, cpu_update, partition):
     local = [(b - a, m) for (a, b), (_, m) in zip(spans, SHAPES)]
     ctx = zf.Context([zf.LayerShape(n, m) for n, m in local], topk_ratio_ppm=100000, refresh_interval=N,
                      accum_interval=N, adam=zf.adam_params(lr=1e-3), offload=True, host_accumulate=True,
-                     cpu_update=cpu_update, world=world, rank=rank, host_allreduce=gloo_allreduce())
+                     cpu_update=cpu_update, world=world, rank=rank, lagged_selection=lagged,
+                     host_allreduce=gloo_allreduce() if exchange == "host" else None)
+    if exchange == "peer":
+        open_peer_exchange(ctx)   # f4 (iii): the partial norms summed over peer memory
+    prevG = None
     scales = [gpu.ColScale(m, li) for li, (_, m) in enumerate(SHAPES)]
     Gs = [torch.empty(n, m, dtype=torch.bfloat16, device="cuda") for n, m in local]
     Ps = [torch.empty(n, m, dtype=torch.bfloat16, device="cuda") for n, m in local]
     for li, P in enumerate(Ps):
         gpu.fill_param(P, li, row0=spans[li][0])
     oracle = [orc.OracleLayer(n=n, m=m, ratio_ppm=100000, refresh_interval=N, accum_interval=N,
-                              hp=orc.AdamHP(lr=1e-3), cpu_update=cpu_update) for n, m in SHAPES]
+                              hp=orc.AdamHP(lr=1e-3), cpu_update=cpu_update, lagged=lagged) for n, m in SHAPES]
     Po = [synth.param(n, m, li) for li, (n, m) in enumerate(SHAPES)]
     for t in range(steps):
         for li in range(len(SHAPES)):
@@ -64,12 +68,15 @@ def _worker(rank, world, port, steps, N, cpu_update, partition):
         ctx.step(t, Gs, Ps)
         ctx.sync()
         refresh = t % N == 0
+        Gfulls = [synth.grad(n, m, li, t, synth.col_scale_at(m, t, li)) for li, (n, m) in enumerate(SHAPES)]
         for li, ((n, m), (a, b)) in enumerate(zip(SHAPES, spans)):
             L = oracle[li]
-            Gfull = synth.grad(n, m, li, t, synth.col_scale_at(m, t, li))
+            Gfull = Gfulls[li]
             gidx = to_np(ctx.selected(li))
             if refresh:
-                onorms = orc.column_norms(Gfull)
+                # lagged selection (R24): a refresh after the first ranks by the previous step's norms
+                lag = lagged and t > 0
+                onorms = orc.column_norms(prevG[li] if lag else Gfull)
                 assert_close_rel(to_np(ctx.norms(li)), onorms, 1e-5, f"rank {rank} norms t={t} l={li}")
                 selection_ok(gidx, orc.topk(onorms, L.k), onorms)
             out = L.step(t, Gfull, Po[li], idx_override=gidx if refresh else None)
@@ -84,6 +91,7 @@ def _worker(rank, world, port, steps, N, cpu_update, partition):
             assert_bits_equal(ctx.compact_host(li).copy(), out[a:b], f"rank {rank} compact t={t} l={li}")
             assert_bits_equal(ctx.host_accumulator(li, 0).copy(), L.acc[(t // N) % 2][a:b],
                               f"rank {rank} acc t={t} l={li}")
+        prevG = Gfulls
     # every rank made the same selection
     sel = torch.from_numpy(np.concatenate([to_np(ctx.selected(li)) for li in range(len(SHAPES))]).astype(np.int64))
     gathered = [torch.empty_like(sel) for _ in range(world)]
@@ -98,6 +106,18 @@ def test_two_ranks_one_gpu_host_allreduce(cpu_update, partition):
     from paper_2505_12242_b200 import _build
     _build.build()
     mp.spawn(_worker, args=(2, _free_port(), 5, 2, cpu_update, partition), nprocs=2, join=True)
+
+
+@pytest.mark.parametrize("world,partition,lagged", [(2, "rows", False), (3, "rows", False), (2, "flat", False),
+                                                    (2, "rows", True)])
+def test_ranks_one_gpu_peer_exchange(world, partition, lagged):
+    """f4 (iii): the partial norms summed by k_peer's kernels reading the other ranks' device
+    memory through CUDA IPC mappings (the NVLink peer path; here the ranks share one GPU):
+    norms within rel 1e-5 of the oracle's, the same selection on every rank, each rank's
+    rows bit-exact -- also with the lagged selection (the exchange on the side stream)."""
+    from paper_2505_12242_b200 import _build
+    _build.build()
+    mp.spawn(_worker, args=(world, _free_port(), 7, 2, False, partition, "peer", lagged), nprocs=world, join=True)
 
 
 AUTO_SHAPES = [(64, 256), (96, 200), (128, 320)]
@@ -248,3 +268,22 @@ def test_llama2_7b_four_row_shards_one_gpu():
     from paper_2505_12242_b200 import _build
     _build.build()
     mp.spawn(_worker_fullsize, args=(4, _free_port(), 5, [0, 6, 224]), nprocs=4, join=True)
+
+
+def test_peer_exchange_state_errors():
+    """zf_peer_handle / zf_peer_open: ZF_ESTATE on a world-1 context and when opened before
+    the handle was made; world 2 with neither NCCL, peers nor a host callback cannot step."""
+    from paper_2505_12242_b200 import zf
+    one = zf.Context([zf.LayerShape(8, 64)], topk_ratio_ppm=100000, refresh_interval=2, accum_interval=2)
+    with pytest.raises(zf.ZFError, match="ESTATE|state"):
+        one.peer_handle()
+    one.close()
+    two = zf.Context([zf.LayerShape(8, 64)], topk_ratio_ppm=100000, refresh_interval=2, accum_interval=2,
+                     world=2, rank=0)
+    with pytest.raises(zf.ZFError):
+        two.peer_open([b"\0" * 64, b"\0" * 64])
+    G = torch.zeros(8, 64, dtype=torch.bfloat16, device="cuda")
+    P = torch.zeros(8, 64, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(zf.ZFError):
+        two.step(0, [G], [P])
+    two.close()

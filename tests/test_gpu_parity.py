@@ -730,3 +730,101 @@ def test_step_zen_auto_cap_refresh_and_warmup(zf, orc, gpu):
     tau warm-up steps."""
     iv = _run_auto(zf, orc, gpu, AUTO_SHAPES, "bf16", "bf16", 100000, 6, 3, 0.5, 14, cpu_update=True, warmup=2)
     assert max(iv) <= 3 and sum(iv) == 12, iv
+
+
+# ------------------------------------------------------------------ H1 in window batches (host_stages)
+@pytest.mark.parametrize("host_stages,S,N,gdt,cpu", [(8, 4, 8, "bf16", False), (3, 4, 8, "bf16", True),
+                                                     (2, 2, 4, "bf16", False), (6, 4, 8, "fp32", False),
+                                                     (16, 8, 8, "bf16", True)])
+def test_h1_window_batches(zf, orc, gpu, host_stages, S, N, gdt, cpu):
+    """H1 (row a8) accumulating several staged steps of a window in one pass: steps are issued
+    without a zf_sync inside a window, so H1 finds several staged steps (batches of up to
+    host_stages, never across a window end); the active and sealed accumulators, the f1
+    parameters and the window log equal the oracle's step-at-a-time sums bit for bit, and
+    H1 ran fewer passes than steps."""
+    shapes = [(96, 320), (64, 512), (128, 200)]
+    pdt = gdt
+    hp_o = orc.AdamHP(lr=1e-3)
+    ctx = zf.Context([zf.LayerShape(n, m) for n, m in shapes], grad_dtype=TDT[gdt], param_dtype=TDT[pdt],
+                     topk_ratio_ppm=100000, refresh_interval=N, accum_interval=S, adam=zf.adam_params(lr=1e-3),
+                     offload=True, host_accumulate=True, cpu_update=cpu, host_stages=host_stages)
+    scales = [gpu.ColScale(m, li) for li, (n, m) in enumerate(shapes)]
+    Gs = [torch.empty(n, m, dtype=TDT[gdt], device="cuda") for n, m in shapes]
+    Ps = [torch.empty(n, m, dtype=TDT[pdt], device="cuda") for n, m in shapes]
+    for li, P in enumerate(Ps):
+        gpu.fill_param(P, li)
+    layers = [orc.OracleLayer(n=n, m=m, ratio_ppm=100000, refresh_interval=N, accum_interval=S, hp=hp_o,
+                              cpu_update=cpu) for n, m in shapes]
+    Po = [np.ascontiguousarray(to_np(P)) for P in Ps]
+    steps = 3 * N
+    for t in range(steps):
+        for li, (G, sc) in enumerate(zip(Gs, scales)):
+            sc.advance_to(t)
+            gpu.fill_grad(G, li, t, sc)
+        Gn = [np.ascontiguousarray(to_np(G)) for G in Gs]
+        ctx.step(t, Gs, Ps)
+        refresh = t % N == 0
+        end = (t + 1) % S == 0
+        if refresh:
+            ctx.sync()  # the refresh's selection drives the oracle (O10)
+        for li, L in enumerate(layers):
+            L.step(t, Gn[li], Po[li], idx_override=to_np(ctx.selected(li)) if refresh else None)
+        if end:
+            ctx.sync()
+            for li, L in enumerate(layers):
+                assert_bits_equal(ctx.host_accumulator(li, 0).copy(), L.acc[(t // S) % 2], f"acc t={t} l={li}")
+                assert_bits_equal(ctx.host_accumulator(li, 1).copy(), L.sealed(t), f"sealed t={t} l={li}")
+                assert_bits_equal(np.ascontiguousarray(to_np(Ps[li])), Po[li], f"params t={t} l={li}")
+    log = ctx.window_log()
+    passes, covered = ctx.host_stats()
+    ctx.close()
+    assert [e for (e, end, *_r) in log if end] == [t for t in range(steps) if (t + 1) % S == 0]
+    assert covered == steps
+    if host_stages >= 3:
+        assert passes < steps, (passes, steps)
+
+
+@pytest.mark.parametrize("cpu", [False, True])
+def test_h1_window_batches_zen_auto(zf, orc, gpu, cpu):
+    """Zen-auto (R21) with H1 in window batches: H1 reads each staged step's K6 decision
+    before forming a batch, so batches never cross a variable-length window's end; no
+    zf_sync inside windows; final window log, both accumulators and the parameters equal
+    the oracle's."""
+    shapes, N, smax, gamma, steps = AUTO_SHAPES, 8, 8, 0.15, 24
+    hp_o = orc.AdamHP(lr=1e-3)
+    ctx = zf.Context([zf.LayerShape(n, m) for n, m in shapes], grad_dtype=torch.bfloat16,
+                     param_dtype=torch.bfloat16, topk_ratio_ppm=100000, refresh_interval=N, accum_interval=smax,
+                     adam=zf.adam_params(lr=1e-3), offload=True, host_accumulate=True, cpu_update=cpu,
+                     auto_gamma=gamma, host_stages=8)
+    scales = [gpu.ColScale(m, li) for li, (n, m) in enumerate(shapes)]
+    Gs = [torch.empty(n, m, dtype=torch.bfloat16, device="cuda") for n, m in shapes]
+    Ps = [torch.empty(n, m, dtype=torch.bfloat16, device="cuda") for n, m in shapes]
+    for li, P in enumerate(Ps):
+        gpu.fill_param(P, li)
+    model = orc.OracleModel([orc.OracleLayer(n=n, m=m, ratio_ppm=100000, refresh_interval=N, accum_interval=smax,
+                                             hp=hp_o, cpu_update=cpu) for n, m in shapes], auto_gamma=gamma)
+    Po = [np.ascontiguousarray(to_np(P)) for P in Ps]
+    for t in range(steps):
+        for li, (G, sc) in enumerate(zip(Gs, scales)):
+            sc.advance_to(t)
+            gpu.fill_grad(G, li, t, sc)
+        Gn = [np.ascontiguousarray(to_np(G)) for G in Gs]
+        ctx.step(t, Gs, Ps)
+        ov = None
+        if t % N == 0:
+            ctx.sync()
+            ov = [to_np(ctx.selected(li)) for li in range(len(shapes))]
+        w_before = model.w
+        model.step(t, Gn, Po, idx_overrides=ov)
+    ctx.sync()
+    ends = [e for (e, end, *_r) in ctx.window_log() if end]
+    assert ends == model.ends
+    for li, L in enumerate(model.layers):
+        assert_bits_equal(ctx.host_accumulator(li, 0).copy(), L.acc[w_before % 2], f"acc l={li}")
+        assert_bits_equal(ctx.host_accumulator(li, 1).copy(), L.acc[(model.w - 1) % 2], f"sealed l={li}")
+        assert_bits_equal(np.ascontiguousarray(to_np(Ps[li])), Po[li], f"params l={li}")
+    passes, covered = ctx.host_stats()
+    ctx.close()
+    assert covered == steps and passes < steps, (passes, covered)
+    iv = model.intervals()
+    assert min(iv) < smax, iv
