@@ -116,6 +116,26 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         : "memory");
 #endif
 }
+#ifdef ZF_MBAR_SLEEP_NS
+// consumer waits: back off with nanosleep between try_wait probes, so warps waiting for a
+// stage do not take issue slots from the working ones (experiment knob)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
+    uint32_t ok;
+    for (;;) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+        if (ok) return;
+        __nanosleep(ZF_MBAR_SLEEP_NS);
+    }
+}
+#else
+#define mbar_wait_sleep mbar_wait
+#endif
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
@@ -718,7 +738,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
     for (int it = grp;; it += K3_GROUPS) {
         const int st = it % K3_STAGES;
         if ((finished >> st) & 1u) continue;
-        mbar_wait(&full[st], (phase >> st) & 1u);
+        mbar_wait_sleep(&full[st], (phase >> st) & 1u);
         ZF_TICK(0);
         phase ^= 1u << st;
         const StageInfo& si = info[st];
