@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--refresh", type=int, default=4)
     ap.add_argument("--lr", type=float, default=1e-5)
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=12)
     ap.add_argument("--host-stages", type=int, default=0,
                     help="pinned host staging slots for the host-accumulation e2e line (0: 2*S, capped by "
                          "the host memory available)")
@@ -68,6 +68,9 @@ def parse():
     ap.add_argument("--no-lagged", action="store_true",
                     help="skip the f4 (ii) lagged-selection line (device time, and a training-loop proxy "
                          "with a synthetic compute-bound backward between steps)")
+    ap.add_argument("--exchange", choices=["auto", "nccl", "host", "peer"], default="auto",
+                    help="N>1 norm exchange (row a2): NCCL all-reduce, the host callback over gloo, or "
+                         "peer-memory kernels (f4 iii, k_peer.cu); auto = nccl, or host with --colocate")
     ap.add_argument("--colocate", action="store_true",
                     help="N > 1 ranks share the visible GPU(s) (rank r on cuda:r %% device_count): gloo process group "
                          "and the library's host all-reduce instead of NCCL -- runs the multi-rank path (launcher, "
@@ -341,18 +344,23 @@ def run_zenflow(args, rank, world):
         del sc
     torch.cuda.synchronize()
     nccl_id, host_ar = None, None
-    if world > 1 and not args.colocate:
+    exch = args.exchange if args.exchange != "auto" else ("host" if args.colocate else "nccl")
+    if world > 1 and exch == "nccl":
         from paper_2505_12242_b200.dist import broadcast_nccl_id
         nccl_id = broadcast_nccl_id()
-    elif world > 1:
+    elif world > 1 and exch == "host":
         from paper_2505_12242_b200.dist import gloo_allreduce
         host_ar = gloo_allreduce()
 
     def make_ctx(ratio_ppm, offload, **kw):
-        return zf.Context([zf.LayerShape(n, m) for n, m in shapes], topk_ratio_ppm=ratio_ppm,
-                          refresh_interval=args.refresh, accum_interval=args.refresh,
-                          adam=zf.adam_params(lr=args.lr), offload=offload, host_accumulate=offload,
-                          world=world, rank=rank, nccl_id=nccl_id, device=dev, host_allreduce=host_ar, **kw)
+        ctx = zf.Context([zf.LayerShape(n, m) for n, m in shapes], topk_ratio_ppm=ratio_ppm,
+                         refresh_interval=args.refresh, accum_interval=args.refresh,
+                         adam=zf.adam_params(lr=args.lr), offload=offload, host_accumulate=offload,
+                         world=world, rank=rank, nccl_id=nccl_id, device=dev, host_allreduce=host_ar, **kw)
+        if world > 1 and exch == "peer":
+            from paper_2505_12242_b200.dist import open_peer_exchange
+            open_peer_exchange(ctx)
+        return ctx
 
     import ctypes
     nl = len(shapes)
@@ -410,6 +418,14 @@ def run_zenflow(args, rank, world):
     alg = algorithmic_bytes(shapes, ks)
     sec = sector_bytes(shapes, idxs)
     g_bytes = sum(n * m * 2 for n, m in shapes)
+    if sim > 1:
+        par_desc = f"rank 0 of dp{sim} ({args.partition}) timed alone on 1 GPU, no all-reduce"
+    else:
+        par_desc = (f"dp{world} ({'flat ZeRO partition' if args.partition == 'flat' else 'row shards'}, "
+                    + {"host": "norm all-reduce over gloo via the host callback",
+                       "peer": "norm exchange over peer memory (k_peer)",
+                       "nccl": "NCCL norm all-reduce"}[exch]
+                    + (f", ranks co-located on {torch.cuda.device_count()} GPU(s))" if args.colocate else ")"))
     result = {
         "metric": METRIC, "value": ms_per_step, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False,
@@ -418,11 +434,7 @@ def run_zenflow(args, rank, world):
         "config": {"workload": f"{args.model}-all-linear-k{args.ratio_ppm // 10000}pct"
                                + (f"-rank0-of-dp{sim}" if sim > 1 else ""), "model": args.model,
                    "linears": nl, "elements": sum(n * m for n, m in full_shapes), "ratio_ppm": args.ratio_ppm,
-                   "refresh_interval": args.refresh, "parallelism": (f"dp{world} ({'flat ZeRO partition' if args.partition == 'flat' else 'row shards'}, "
-                                   + ("norm all-reduce over gloo via the host callback, ranks co-located on "
-                                      f"{torch.cuda.device_count()} GPU(s))" if args.colocate else "NCCL norm all-reduce)")
-                                   if sim == 1 else f"rank 0 of dp{sim} ({args.partition}) timed alone on 1 GPU, "
-                                   "no all-reduce"),
+                   "refresh_interval": args.refresh, "parallelism": par_desc,
                    "l2": "inputs larger than L2 (working set > 100 GB vs 126 MB L2); no flush needed",
                    "lr": args.lr},
         "phases_ms_per_launch": {"k3_update": k3_avg, "k1_norms": k1_ms / max(1, n_k1),

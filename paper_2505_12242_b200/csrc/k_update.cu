@@ -14,7 +14,7 @@
 // parameter-subset slab on steady steps, p's 32-byte sectors on refreshes) and
 // the fp32 moments.
 //  - persistent grid, one CTA per SM, warp-specialised: 4 producer warps (one
-//    thread each, one stage arena each) and 20 consumer warps in two groups of 10.
+//    thread each, one stage arena each) and 28 consumer warps in two groups of 14.
 //    Work units (R rows x c columns) are claimed dynamically, one atomic per unit;
 //    refresh and steady steps use their own unit shapes (a steady unit holds no p tile).
 //  - a producer prefetches the claimed unit's G rows / slabs into L2 while its arena is

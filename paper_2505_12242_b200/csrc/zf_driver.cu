@@ -94,7 +94,7 @@ zf_status build_tables(zf_ctx* c) {
             t.out = l.stage_dev[sb < c->n_stage ? sb : 0];
             t.out_ld = l.mk_pad;
             t.ucol = l.ucol[nw];
-            t.done = c->cfg.offload ? c->done + i : nullptr;
+            t.done = c->cfg.offload ? c->done + l.chunk : nullptr;
             const K3Geom& gg = refresh ? l.geo : l.geo_s;
             t.seg_cols = gg.seg_cols;
             t.nseg = gg.nseg;
@@ -362,7 +362,30 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
             ZF_CUDA(cudaMemcpy(l.mask_w, mw.data(), l.W * sizeof(uint32_t), cudaMemcpyHostToDevice));
             ZF_CUDA(cudaMemcpy(l.prefix_w, pw.data(), l.W * sizeof(int32_t), cudaMemcpyHostToDevice));
         }
-        for (int s = 0; s < c->n_stage; ++s) ZF_CTRY(c->dalloc(&l.stage_dev[s], (size_t)n * l.mk_pad * c->gsz, false));
+        l.stage_off = c->stage_bytes;
+        c->stage_bytes += ((int64_t)n * l.mk_pad * c->gsz + 255) / 256 * 256;
+    }
+    // the compact blocks of every layer back to back per staging slot; X1 copies chunks of
+    // consecutive layers (~512 MB) with one command each
+    for (int s = 0; s < c->n_stage; ++s) {
+        ZF_CTRY(c->dalloc(&c->stage_dev_blk[s], std::max<int64_t>(c->stage_bytes, 256), false));
+        for (auto& l : c->L) l.stage_dev[s] = static_cast<unsigned char*>(c->stage_dev_blk[s]) + l.stage_off;
+    }
+    {
+        static const int64_t chunk_target = getenv("ZF_X1_CHUNK_MB") ? atoll(getenv("ZF_X1_CHUNK_MB")) << 20 : 512ll << 20;
+        zf_ctx::Chunk ch;
+        for (int i = 0; i < (int)c->L.size(); ++i) {
+            LayerState& l = c->L[i];
+            if (ch.last == ch.first) ch.off = l.stage_off;
+            l.chunk = (int32_t)c->chunks.size();
+            ch.last = i + 1;
+            ch.bytes = l.stage_off + ((int64_t)l.d.n * l.mk_pad * c->gsz + 255) / 256 * 256 - ch.off;
+            if (ch.bytes >= chunk_target || i + 1 == (int)c->L.size()) {
+                c->chunks.push_back(ch);
+                ch = zf_ctx::Chunk{};
+                ch.first = ch.last = i + 1;
+            }
+        }
     }
     {
         int32_t* h = nullptr;
@@ -454,14 +477,14 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
     if (cfg->offload) {
         ZF_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
         for (int s = 0; s < 2; ++s) ZF_CUDA(cudaEventCreateWithFlags(&c->d2h_all[s], cudaEventDisableTiming));
-        for (auto& l : c->L) {
-            for (int s = 0; s < (c->devacc ? 0 : c->n_hstage); ++s) {  // per-step compact D2H (not with K7)
-                void* h = nullptr;
-                ZF_CUDA(cudaHostAlloc(&h, std::max<size_t>((size_t)l.d.n * l.mk_pad * c->gsz, 64), cudaHostAllocDefault));
-                c->host_pinned.push_back(h);
-                l.stage_host[s] = h;
-                ZF_CUDA(cudaEventCreateWithFlags(&l.d2h_ev[s], cudaEventDisableTiming | cudaEventBlockingSync));
-            }
+        for (int s = 0; s < (c->devacc ? 0 : c->n_hstage); ++s) {  // per-step compact D2H (not with K7)
+            void* h = nullptr;
+            ZF_CUDA(cudaHostAlloc(&h, std::max<size_t>((size_t)c->stage_bytes, 64), cudaHostAllocDefault));
+            c->host_pinned.push_back(h);
+            c->stage_host_blk[s] = h;
+            for (auto& l : c->L) l.stage_host[s] = static_cast<unsigned char*>(h) + l.stage_off;
+            for (auto& ch : c->chunks)
+                ZF_CUDA(cudaEventCreateWithFlags(&ch.ev[s], cudaEventDisableTiming | cudaEventBlockingSync));
         }
         void* fn = nullptr;
         cudaDriverEntryPointQueryResult q;
@@ -532,6 +555,10 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
             c->pool = new Pool(nt, c->numa_cpus);
             if (!c->devacc) c->h1 = std::thread([c] { pin_thread_to(c->numa_cpus); c->h1_loop(); });
         }
+        if (!c->devacc) {
+            for (auto& e : c->k3_step_ev) ZF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            c->x1 = std::thread([c] { pin_thread_to(c->numa_cpus); c->x1_loop(); });
+        }
     }
     // ---- NCCL (collective across ranks), or a pinned host buffer for the host all-reduce
     if (world > 1 && !nccl_id128) {
@@ -571,7 +598,7 @@ zf_status refresh_pointer_tables(zf_ctx* c, int variant, bool refresh, void* con
             t.vec_ok = aligned16(grads[i]) && ((c->L[i].d.ld_grad * c->gsz) % 16 == 0);
         }
         if (std::memcmp(c->h_norm_tab.data(), c->up_norm_tab.data(), nl * sizeof(NormLayer)) != 0) {
-            ZF_TRY(c->upload(c->d_norm_tab, c->h_norm_tab.data(), nl * sizeof(NormLayer), s));
+            ZF_TRY(c->upload_diff(c->d_norm_tab, c->h_norm_tab.data(), c->up_norm_tab.data(), nl * sizeof(NormLayer), s));
             c->up_norm_tab = c->h_norm_tab;
         }
     }
@@ -597,7 +624,7 @@ zf_status refresh_pointer_tables(zf_ctx* c, int variant, bool refresh, void* con
         }
     }
     if (std::memcmp(h.data(), up.data(), nl * sizeof(UpdLayer)) != 0) {
-        ZF_TRY(c->upload(d, h.data(), nl * sizeof(UpdLayer), s));
+        ZF_TRY(c->upload_diff(d, h.data(), up.data(), nl * sizeof(UpdLayer), s));
         up = h;
     }
     return ZF_OK;
@@ -665,10 +692,13 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
         return fail(ZF_ESTATE, "world > 1 needs an NCCL id at zf_create, zf_peer_open or zf_set_host_allreduce");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     c->last_stream = s;
+    c->tmark(-1);
+    c->trace_n++;
     ZF_CUDA(cudaSetDevice(c->device));
     // R23: the previous window's CPU update (computed while the caller ran its next forward /
     // backward) lands before this step touches any parameter
     ZF_TRY(f1_finish(c, s));
+    c->tmark(0);
     if (t0 < tau) return warmup_step(c, t0, grads, params, s);
     // the regular schedule (refreshes, windows, offload stages) counts from step tau (R20)
     const int64_t t = t0 - tau;
@@ -684,11 +714,15 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
     const bool lag_pre = c->lagged && (t + 1) % N == 0;
     const bool norms_now = (refresh && !lag_refresh) || c->autoz;  // Zen-auto reads every step's norms (R21)
     ZF_TRY(refresh_pointer_tables(c, variant, norms_now || lag_pre, grads, params, s));
+    c->tmark(1);
 
     if (c->cfg.offload) {
         // (K3 counts per-layer completions only when offloading; see build_tables)
         // the device staging buffer sb is free once the D2H copies issued two steps ago finished
-        if (c->d2h_issued[sb]) ZF_CUDA(cudaStreamWaitEvent(s, c->d2h_all[sb], 0));
+        if (c->d2h_issued[sb]) {
+            if (!c->devacc) ZF_TRY(c->x1_wait_issued(t - c->n_stage));   // d2h_all[sb] of step t - 2 recorded
+            ZF_CUDA(cudaStreamWaitEvent(s, c->d2h_all[sb], 0));
+        }
         if (c->cfg.host_accumulate && !c->devacc) {
             // host staging buffer sb is free once H1 consumed step t-2
             std::unique_lock<std::mutex> lk(c->mu);
@@ -701,6 +735,7 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
             }
         }
     }
+    c->tmark(2);
     if (norms_now) {
         zf_ctx::Pending pe;
         // layers with no rows on this rank (flat partitions, row f3) contribute zero norms
@@ -819,7 +854,9 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
     // prologue: the slots' {ss, bc2s} for this launch (after K2 wrote a refresh's step counts)
     ZF_CUDA(launch_slot_consts(prm.layers.dev, nl, c->max_m, prm.step_delta, c->adam, s));
     c->launches++;
+    c->tmark(3);
     ZF_CUDA(launch_update(prm, c->gdt, c->pdt, grid, s));
+    c->tmark(4);
     ZF_TRY(c->prof_end(&pe3, s));
     c->launches++;
     if (c->split) {
@@ -834,8 +871,8 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
     c->since += 1;
     c->psub_valid = c->cfg.param_subset != 0;  // this K3 (re)built or kept the subset block
     for (int i = 0; i < nl; ++i)
-        c->done_target[i] += (uint32_t)(steady_geo ? c->L[i].geo_s.units : c->L[i].geo.units) *
-                             (uint32_t)update_limits().consumer_warps;
+        c->done_target[c->L[i].chunk] += (uint32_t)(steady_geo ? c->L[i].geo_s.units : c->L[i].geo.units) *
+                                         (uint32_t)update_limits().consumer_warps;
     if (refresh) {
         c->cur ^= 1;
         c->have_sel = true;
@@ -867,46 +904,24 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
     ZF_CUDA(cudaEventRecord(c->step_done, s));
 
     if (c->cfg.offload && !c->devacc) {
-        // X1: per-layer D2H as soon as the layer's last unit finished (cyclic counter), into
-        // host staging slot hs
-        const int hs = (int)(t % c->n_hstage);
-        if (!c->wait_value) ZF_CUDA(cudaStreamWaitEvent(c->copy_stream, c->step_done, 0));
-        zf_ctx::Pending pe4;
-        bool pe4_open = false;
-        for (int i = 0; i < nl; ++i) {
-            LayerState& l = c->L[i];
-            if (c->wait_value) {
-                const uint32_t target = c->done_target[i];
-                CUresult r = c->wait_value(reinterpret_cast<CUstream>(c->copy_stream),
-                                           reinterpret_cast<CUdeviceptr>(c->done + i), target,
-                                           CU_STREAM_WAIT_VALUE_GEQ);
-                if (r != CUDA_SUCCESS) {  // stream memory ops unavailable: gate on the whole step
-                    c->wait_value = nullptr;
-                    ZF_CUDA(cudaStreamWaitEvent(c->copy_stream, c->step_done, 0));
-                }
-            }
-            // one flat copy of the pitched block (H1 reads the rows at the same pitch)
-            if (l.mk && l.d.n) {
-                if (!pe4_open) {  // phase 4: the step's D2H span, from the first copy's start
-                    ZF_TRY(c->prof_begin(4, c->copy_stream, &pe4));
-                    pe4_open = true;
-                }
-                ZF_CUDA(cudaMemcpyAsync(l.stage_host[hs], l.stage_dev[sb], (size_t)l.d.n * l.mk_pad * c->gsz,
-                                        cudaMemcpyDeviceToHost, c->copy_stream));
-            }
-            ZF_CUDA(cudaEventRecord(l.d2h_ev[hs], c->copy_stream));
+        // X1: this step's D2H commands (per chunk: wait for its layers' K3 units, copy, event)
+        // are issued by the X1 thread (x1_loop): submitting copies while the previous step's
+        // are still running can block the submitting thread for most of a step, which would
+        // hold the caller's next H2D back
+        ZF_CUDA(cudaEventRecord(c->k3_step_ev[sb], s));
+        zf_ctx::X1Job j;
+        j.t = t;
+        j.hs = (int)(t % c->n_hstage);
+        j.sb = sb;
+        j.targets = c->done_target;
+        {
+            std::lock_guard<std::mutex> lk(c->x1_mu);
+            c->x1_jobs.push_back(std::move(j));
         }
-        if (pe4_open) ZF_TRY(c->prof_end(&pe4, c->copy_stream));
-        ZF_CUDA(cudaEventRecord(c->d2h_all[sb], c->copy_stream));
+        c->x1_cv.notify_all();
         c->d2h_issued[sb] = true;
-        if (c->cfg.host_accumulate) {
-            {
-                std::lock_guard<std::mutex> lk(c->mu);
-                c->jobs.push_back(t);
-            }
-            c->cv.notify_all();
-        }
     }
+    c->tmark(5);
     if (c->cfg.cpu_update && refresh) ZF_TRY(f1_refresh(c, params, s));
     if (c->cfg.host_accumulate) {
         // the window decision of step t (fixed S, or Zen-auto's record) and, with f1, the
@@ -959,6 +974,7 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
             c->mw_len = 0;
         }
     }
+    c->tmark(6);
     return ZF_OK;
 }
 
@@ -972,6 +988,7 @@ extern "C" zf_status zf_sync(zf_ctx* c) {
         ZF_TRY(f1_finish(c, c->last_stream));
         ZF_CUDA(cudaStreamSynchronize(c->last_stream));
     }
+    if (c->cfg.offload && !c->devacc && c->last_t >= 0) ZF_TRY(c->x1_wait_issued(c->last_t));
     if (c->copy_stream) ZF_CUDA(cudaStreamSynchronize(c->copy_stream));
     if (c->lag_stream) ZF_CUDA(cudaStreamSynchronize(c->lag_stream));   // a lagged K1 (f4 ii)
     if (c->cfg.host_accumulate) {
@@ -993,6 +1010,14 @@ extern "C" zf_status zf_sync(zf_ctx* c) {
     if (c->peer_err_h && *(volatile int32_t*)c->peer_err_h) {
         *c->peer_err_h = 0;
         return fail(ZF_ENCCL, "peer-memory norm exchange: a peer did not arrive within the timeout");
+    }
+    if (c->trace && c->trace_n) {
+        fprintf(stderr, "[zf_step host ms/step over %lld] f1_finish %.2f tables %.2f waits %.2f norms+topk %.2f "
+                "k3_launch %.2f d2h_issue %.2f tail %.2f\n", (long long)c->trace_n, c->trace_ms[0] / c->trace_n,
+                c->trace_ms[1] / c->trace_n, c->trace_ms[2] / c->trace_n, c->trace_ms[3] / c->trace_n,
+                c->trace_ms[4] / c->trace_n, c->trace_ms[5] / c->trace_n, c->trace_ms[6] / c->trace_n);
+        std::fill(c->trace_ms, c->trace_ms + 10, 0.0);
+        c->trace_n = 0;
     }
     volatile int32_t* f = c->nonfinite_h;
     if (*f) {

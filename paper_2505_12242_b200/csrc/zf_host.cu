@@ -5,6 +5,14 @@
 
 zf_ctx::~zf_ctx() {
     if (f1_worker.joinable()) f1_worker.join();
+    if (x1.joinable()) {
+        {
+            std::lock_guard<std::mutex> lk(x1_mu);
+            x1_stop = true;
+        }
+        x1_cv.notify_all();
+        x1.join();
+    }
     if (h1.joinable()) {
         {
             std::lock_guard<std::mutex> lk(mu);
@@ -22,9 +30,11 @@ zf_ctx::~zf_ctx() {
     for (void* p : dev_allocs) cudaFree(p);
     for (void* p : host_pinned) cudaFreeHost(p);
     for (float* p : host_plain) std::free(p);
-    for (auto& l : L)
+    for (auto e : k3_step_ev)
+        if (e) cudaEventDestroy(e);
+    for (auto& ch : chunks)
         for (int i = 0; i < ZF_MAX_HSTAGE; ++i)
-            if (l.d2h_ev[i]) cudaEventDestroy(l.d2h_ev[i]);
+            if (ch.ev[i]) cudaEventDestroy(ch.ev[i]);
     for (auto e : ring_ev) cudaEventDestroy(e);
     for (auto e : d2h_all)
         if (e) cudaEventDestroy(e);
@@ -70,6 +80,71 @@ void zfh::acc_row_f32(float* __restrict__ acc, const float* __restrict__ src, in
         for (int64_t i = 0; i < n; ++i) acc[i] = 0.0f + src[i];
     } else {
         for (int64_t i = 0; i < n; ++i) acc[i] = acc[i] + src[i];
+    }
+}
+
+// X1: issue one step's D2H of the compact blocks -- per chunk of consecutive layers, wait on
+// the device until the chunk's K3 units are done (cuStreamWaitValue32 on its completion
+// counter; the whole step's K3 without stream memory ops), one copy into host slot hs, one
+// event -- then hand the step to H1.
+zf_status zf_ctx::x1_issue(const X1Job& j) {
+    if (!wait_value) ZF_CUDA(cudaStreamWaitEvent(copy_stream, k3_step_ev[j.sb], 0));
+    Pending pe4;
+    bool pe4_open = false;
+    for (size_t ci = 0; ci < chunks.size(); ++ci) {
+        Chunk& ch = chunks[ci];
+        if (wait_value) {
+            CUresult r = wait_value(reinterpret_cast<CUstream>(copy_stream), reinterpret_cast<CUdeviceptr>(done + ci),
+                                    j.targets[ci], CU_STREAM_WAIT_VALUE_GEQ);
+            if (r != CUDA_SUCCESS) {  // stream memory ops unavailable: gate on the whole step
+                wait_value = nullptr;
+                ZF_CUDA(cudaStreamWaitEvent(copy_stream, k3_step_ev[j.sb], 0));
+            }
+        }
+        if (ch.bytes > 0) {
+            if (!pe4_open) {  // phase 4: the step's D2H span, from the first copy's start
+                ZF_TRY(prof_begin(4, copy_stream, &pe4));
+                pe4_open = true;
+            }
+            ZF_CUDA(cudaMemcpyAsync(static_cast<unsigned char*>(stage_host_blk[j.hs]) + ch.off,
+                                    static_cast<unsigned char*>(stage_dev_blk[j.sb]) + ch.off, (size_t)ch.bytes,
+                                    cudaMemcpyDeviceToHost, copy_stream));
+        }
+        ZF_CUDA(cudaEventRecord(ch.ev[j.hs], copy_stream));
+    }
+    if (pe4_open) ZF_TRY(prof_end(&pe4, copy_stream));
+    ZF_CUDA(cudaEventRecord(d2h_all[j.sb], copy_stream));
+    if (cfg.host_accumulate) {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            jobs.push_back(j.t);
+        }
+        cv.notify_all();
+    }
+    return ZF_OK;
+}
+
+void zf_ctx::x1_loop() {
+    cudaSetDevice(device);
+    for (;;) {
+        X1Job j;
+        {
+            std::unique_lock<std::mutex> lk(x1_mu);
+            x1_cv.wait(lk, [&] { return x1_stop || !x1_jobs.empty(); });
+            if (x1_jobs.empty()) return;
+            j = std::move(x1_jobs.front());
+            x1_jobs.pop_front();
+        }
+        const zf_status st = x1_status == ZF_OK ? x1_issue(j) : x1_status;
+        {
+            std::lock_guard<std::mutex> lk(x1_mu);
+            if (st != ZF_OK && x1_status == ZF_OK) {
+                x1_status = st;
+                x1_error = zf_last_error();
+            }
+            x1_issued = j.t;
+        }
+        x1_cv.notify_all();
     }
 }
 
@@ -157,7 +232,7 @@ void zf_ctx::h1_loop() {
             const void* srcs[ZF_MAX_HSTAGE];
             for (int j = 0; j < b; ++j) {
                 const int hs = (int)(batch[j] % n_hstage);
-                cudaEventSynchronize(l.d2h_ev[hs]);
+                cudaEventSynchronize(chunks[l.chunk].ev[hs]);
                 srcs[j] = l.stage_host[hs];
             }
             const int64_t mk = l.mk, ld = l.mk_pad;

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <condition_variable>
 #include <cstdarg>
@@ -20,6 +21,7 @@
 #include <functional>
 #include <tuple>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -362,7 +364,8 @@ struct LayerState {
     int64_t unit_begin = 0;
     K3Geom geo_s{};                   // steady units (param_subset: the subset slab instead of a p tile)
     int64_t unit_begin_s = 0;
-    cudaEvent_t d2h_ev[ZF_MAX_HSTAGE] = {};  // per host staging slot: this layer's D2H landed
+    int32_t chunk = 0;                // X1 copy chunk (consecutive layers, one D2H per chunk)
+    int64_t stage_off = 0;            // byte offset of this layer's compact block in a staging slot
     // f1: deferred CPU AdamW (reading R18)
     // dense over the current unselected columns (position u = column unsel_host[u]), remapped
     // at every refresh: the window update is then a contiguous, vectorised row loop
@@ -521,6 +524,44 @@ struct zf_ctx {
     bool has_empty = false;       // some layer has n = 0 rows on this rank
     int n_stage = 1;              // device compact blocks (ring over steps)
     int n_hstage = 2;             // pinned host staging slots (ring over steps; host_stages)
+    // X1 in chunks: the layers' compact blocks sit back to back in one device / host block per
+    // staging slot, so a run of consecutive layers is ONE copy gated by ONE counter -- a few
+    // dozen copy-stream commands per step instead of three per layer (a deep queue of per-layer
+    // commands stalls the issuing thread once the previous step's copies still fill it)
+    struct Chunk {
+        int32_t first = 0, last = 0;      // layers [first, last)
+        int64_t off = 0, bytes = 0;       // byte range in a staging slot
+        cudaEvent_t ev[ZF_MAX_HSTAGE] = {};   // per host slot: this chunk's D2H landed
+    };
+    std::vector<Chunk> chunks;
+    // X1 issue thread (x1_loop): one job per offloaded step
+    struct X1Job {
+        int64_t t = 0;
+        int hs = 0, sb = 0;
+        std::vector<uint32_t> targets;   // per-chunk completion counts of this step's K3
+    };
+    std::thread x1;
+    std::mutex x1_mu;
+    std::condition_variable x1_cv;
+    std::deque<X1Job> x1_jobs;
+    int64_t x1_issued = -1;           // last step whose D2H commands are issued
+    bool x1_stop = false;
+    zf_status x1_status = ZF_OK;
+    std::string x1_error;
+    cudaEvent_t k3_step_ev[2] = {nullptr, nullptr};   // per device slot: the step's K3 done
+    std::mutex prof_mu;               // prof_begin / prof_end from the X1 thread
+    void x1_loop();
+    zf_status x1_issue(const X1Job& j);
+    // wait until step t's D2H commands are issued (and report an X1 thread error)
+    zf_status x1_wait_issued(int64_t t) {
+        std::unique_lock<std::mutex> lk(x1_mu);
+        x1_cv.wait(lk, [&] { return x1_issued >= t || x1_status != ZF_OK; });
+        if (x1_status != ZF_OK) return fail(x1_status, "X1 thread: %s", x1_error.c_str());
+        return ZF_OK;
+    }
+    int64_t stage_bytes = 0;      // one staging slot (every layer's compact block)
+    void* stage_dev_blk[2] = {nullptr, nullptr};
+    void* stage_host_blk[ZF_MAX_HSTAGE] = {};
     float* norms = nullptr;
     std::vector<void*> dev_allocs, host_pinned;
     std::vector<float*> host_plain;
@@ -575,6 +616,17 @@ struct zf_ctx {
     int64_t total_rows = 0;       // K3b chunks over all layers
     int64_t last_t = -1;          // regular-schedule index (t - tau) of the last regular step
     int64_t launches = 0;
+    // ZF_TRACE_STEP=1: host time spent in each part of zf_step, printed by zf_sync
+    bool trace = getenv("ZF_TRACE_STEP") != nullptr;
+    double trace_ms[10] = {};
+    int64_t trace_n = 0;
+    std::chrono::steady_clock::time_point trace_t;
+    void tmark(int i) {
+        if (!trace) return;
+        const auto now = std::chrono::steady_clock::now();
+        if (i >= 0) trace_ms[i] += std::chrono::duration<double, std::milli>(now - trace_t).count();
+        trace_t = now;
+    }
     cudaEvent_t step_done = nullptr, k3_done = nullptr;
     // offload
     cudaStream_t copy_stream = nullptr;
@@ -641,6 +693,7 @@ struct zf_ctx {
         p->phase = phase;
         p->a = p->b = nullptr;
         if (!profiling) return ZF_OK;
+        std::lock_guard<std::mutex> lk(prof_mu);
         if (ev_pool.empty()) {
             cudaEvent_t a, b;
             ZF_CUDA(cudaEventCreate(&a));
@@ -655,6 +708,7 @@ struct zf_ctx {
     }
     zf_status prof_end(Pending* p, cudaStream_t s) {
         if (!p->a) return ZF_OK;
+        std::lock_guard<std::mutex> lk(prof_mu);
         ZF_CUDA(cudaEventRecord(p->b, s));
         pending.push_back(*p);
         return ZF_OK;
@@ -672,6 +726,33 @@ struct zf_ctx {
         ZF_TRY(dev_alloc(&q, bytes));
         if (zero) ZF_CUDA(cudaMemset(q, 0, std::max<size_t>(bytes, 256)));
         *p = static_cast<T*>(q);
+        return ZF_OK;
+    }
+    // dst holds `old` (bytes, a multiple of 8): write the changed words of src by patch
+    // kernels (k_patch) in stream order -- no copy engine, no ring slot wait
+    std::unique_ptr<PatchArgs> patch;
+    zf_status upload_diff(void* dst, const void* src, const void* old, size_t bytes, cudaStream_t s) {
+        if (bytes % 8 != 0) return upload(dst, src, bytes, s);
+        if (!patch) patch.reset(new PatchArgs);
+        PatchArgs& a = *patch;
+        a.base = static_cast<unsigned long long*>(dst);
+        a.n = 0;
+        const unsigned long long* x = static_cast<const unsigned long long*>(src);
+        const unsigned long long* y = static_cast<const unsigned long long*>(old);
+        for (size_t w = 0; w < bytes / 8; ++w) {
+            if (x[w] == y[w]) continue;
+            a.off[a.n] = (uint32_t)w;
+            a.val[a.n] = x[w];
+            if (++a.n == ZF_PATCH_N) {
+                ZF_CUDA(launch_patch(a, s));
+                ++launches;
+                a.n = 0;
+            }
+        }
+        if (a.n) {
+            ZF_CUDA(launch_patch(a, s));
+            ++launches;
+        }
         return ZF_OK;
     }
     zf_status upload(void* dst, const void* src, size_t bytes, cudaStream_t s) {

@@ -154,3 +154,16 @@ extern "C" zf_status zf_compact_unselected(const void* G, zf_dtype gdt, int64_t 
     return ZF_OK;
 }
 
+namespace zf {
+namespace {
+__global__ void k_patch(const __grid_constant__ PatchArgs a) {
+    for (int i = threadIdx.x; i < a.n; i += blockDim.x) a.base[a.off[i]] = a.val[i];
+}
+}  // namespace
+
+cudaError_t launch_patch(const PatchArgs& a, cudaStream_t s) {
+    if (a.n <= 0) return cudaSuccess;
+    k_patch<<<1, 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
+}  // namespace zf

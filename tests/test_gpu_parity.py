@@ -278,7 +278,10 @@ def test_step_config1_fp32(zf, orc, gpu, NS):
     """BASELINE config 1: one 256x512 fp32 gradient, top-10%, selective AdamW +
     unselected accumulation; N = S in {1, 2, 4}, 8 steps (two windows at S=4)."""
     swaps, launches = _run_stateful(zf, orc, gpu, [(256, 512)], "fp32", "fp32", 100000, NS, NS, 8, offload=True)
-    assert launches == 2 * 8 + 2 * (8 // NS)   # per step: K3 prologue + K3; per refresh: K1 + K2
+    # per step: K3 prologue + K3; per refresh: K1 + K2; plus a table patch (k_patch) whenever
+    # a step's launch table differs from what the device holds (at most norm + update table)
+    base = 2 * 8 + 2 * (8 // NS)
+    assert base <= launches <= base + 2 * 8, launches
     assert swaps == 0
 
 
