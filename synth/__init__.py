@@ -110,7 +110,7 @@ def col_scale_init(m: int, layer: int, seed: int = SEED) -> np.ndarray:
 
 
 def col_scale_advance(e: np.ndarray, step: int, layer: int, seed: int = SEED) -> np.ndarray:
-    """Exponents at ``step`` (>0) from those at ``step-1``: each column is redrawn w.p. ~1%."""
+    """Exponents at ``step`` (>0) from those at ``step-1``: each column is redrawn w.p. ~0.03% (REDRAW_THRESHOLD / 2^32)."""
     m = e.shape[0]
     j = np.arange(m, dtype=np.uint64)
     hr = _hash(stream_key(seed, TAG_REDRAW, layer, step), j)

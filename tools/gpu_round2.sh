@@ -12,6 +12,8 @@ timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/${tag}_pytest_gpu.
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${tag}_smoke.log 2>&1
 timeout 900 python bench.py > gpurun_out/${tag}_bench_7b.jsonl 2> gpurun_out/${tag}_bench_7b.err
 timeout 600 python bench.py --gpus 2 --colocate --no-cpu-baseline --no-e2e > gpurun_out/${tag}_bench_7b_colocate2.jsonl 2> gpurun_out/${tag}_bench_7b_colocate2.err
+timeout 600 python bench.py --gpus 2 --colocate --exchange peer --no-cpu-baseline --no-e2e --no-k1pct --no-lr1e3 --no-lagged > gpurun_out/${tag}_bench_7b_colocate2_peer.jsonl 2> gpurun_out/${tag}_bench_7b_colocate2_peer.err
+timeout 300 python -c "import sys; sys.argv=['bench.py','--impl','reference','--steps','2','--warmup','0']; exec(open('bench.py').read())" > gpurun_out/${tag}_bench_reference.jsonl 2> gpurun_out/${tag}_bench_reference.err
 [ "$mode" = quick ] && exit 0
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv -k regex:"k_(update|column_norms|topk|scatter|accumulate|zen_auto|adam)" \
     --log-file gpurun_out/${tag}_launches_7b.csv python bench.py --steps 4 --warmup 3 --no-e2e --no-cpu-baseline --no-k1pct --no-lr1e3 --no-lagged \
