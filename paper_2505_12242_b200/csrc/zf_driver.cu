@@ -1239,6 +1239,7 @@ extern "C" zf_status zf_profile(zf_ctx* c, int32_t enable) {
 
 extern "C" zf_status zf_profile_read(zf_ctx* c, double* ms, int64_t* count) {
     if (!c) return fail(ZF_EINVAL, "ctx is NULL");
+    std::lock_guard<std::mutex> lk(c->prof_mu);   // the X1 thread records phase 4
     for (auto& p : c->pending) {
         ZF_CUDA(cudaEventSynchronize(p.b));
         float e = 0.0f;

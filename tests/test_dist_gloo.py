@@ -81,3 +81,36 @@ def test_shard_rows_product_helper():
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
     with pytest.raises(ValueError):
         shard_rows(10, 2, 2)
+
+
+def _peer_worker(rank, world, port):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2505_12242_b200.dist import open_peer_exchange
+
+    class FakeCtx:
+        """Stands in for zf.Context: a 64-byte handle per rank, and what peer_open receives."""
+        opened = None
+
+        def peer_handle(self):
+            return bytes([rank]) * 64
+
+        def peer_open(self, handles):
+            self.opened = handles
+
+    ctx = FakeCtx()
+    open_peer_exchange(ctx)
+    # every rank receives every rank's handle, in rank order (zf_peer_open maps handle q as rank q)
+    assert ctx.opened == [bytes([q]) * 64 for q in range(world)], ctx.opened
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_open_peer_exchange_gathers_handles_in_rank_order(world):
+    """f4 (iii) setup: dist.open_peer_exchange all-gathers the ranks' IPC handles over the
+    process group in rank order before zf_peer_open (the mapping itself needs a GPU:
+    tests/test_gpu_multirank.py)."""
+    mp.spawn(_peer_worker, args=(world, _free_port()), nprocs=world, join=True)
