@@ -13,7 +13,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${ta
 timeout 900 python bench.py > gpurun_out/${tag}_bench_7b.jsonl 2> gpurun_out/${tag}_bench_7b.err
 timeout 600 python bench.py --gpus 2 --colocate --no-cpu-baseline --no-e2e > gpurun_out/${tag}_bench_7b_colocate2.jsonl 2> gpurun_out/${tag}_bench_7b_colocate2.err
 timeout 600 python bench.py --gpus 2 --colocate --exchange peer --no-cpu-baseline --no-e2e --no-k1pct --no-lr1e3 --no-lagged > gpurun_out/${tag}_bench_7b_colocate2_peer.jsonl 2> gpurun_out/${tag}_bench_7b_colocate2_peer.err
-timeout 300 python -c "import sys; sys.argv=['bench.py','--impl','reference','--steps','2','--warmup','0']; exec(open('bench.py').read())" > gpurun_out/${tag}_bench_reference.jsonl 2> gpurun_out/${tag}_bench_reference.err
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${tag}_bench_reference.jsonl 2> gpurun_out/${tag}_bench_reference.err
 [ "$mode" = quick ] && exit 0
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv -k regex:"k_(update|column_norms|topk|scatter|accumulate|zen_auto|adam)" \
     --log-file gpurun_out/${tag}_launches_7b.csv python bench.py --steps 4 --warmup 3 --no-e2e --no-cpu-baseline --no-k1pct --no-lr1e3 --no-lagged \
@@ -26,9 +26,9 @@ for spec in "7b_k10:--ratio-ppm 100000" "7b_k1:--ratio-ppm 10000" "gpt2_k10:--mo
   ncu -i gpurun_out/${tag}_k3_${name}.ncu-rep --page details > gpurun_out/${tag}_k3_${name}.txt 2>&1
   ncu -i gpurun_out/${tag}_k3_${name}.ncu-rep --page raw --csv > gpurun_out/${tag}_k3_${name}_raw.csv 2>&1
 done
-timeout 300 python bench.py --model gpt2-small --no-e2e > gpurun_out/${tag}_bench_gpt2.jsonl 2> gpurun_out/${tag}_bench_gpt2.err
+timeout 300 python bench.py --model gpt2-small --no-e2e --no-lagged --steps 4000 > gpurun_out/${tag}_bench_gpt2.jsonl 2> gpurun_out/${tag}_bench_gpt2.err
 timeout 600 python bench.py --model llama2-13b --no-cpu-baseline > gpurun_out/${tag}_bench_13b.jsonl 2> gpurun_out/${tag}_bench_13b.err
-timeout 600 python bench.py --model llama2-13b --shard-of 8 --no-cpu-baseline > gpurun_out/${tag}_bench_13b_shard8.jsonl 2> gpurun_out/${tag}_bench_13b_shard8.err
-timeout 600 python bench.py --shard-of 8 --no-cpu-baseline > gpurun_out/${tag}_bench_7b_shard8.jsonl 2> gpurun_out/${tag}_bench_7b_shard8.err
+timeout 600 python bench.py --model llama2-13b --shard-of 8 --no-cpu-baseline --no-lagged --steps 300 > gpurun_out/${tag}_bench_13b_shard8.jsonl 2> gpurun_out/${tag}_bench_13b_shard8.err
+timeout 600 python bench.py --shard-of 8 --no-cpu-baseline --no-lagged --steps 600 > gpurun_out/${tag}_bench_7b_shard8.jsonl 2> gpurun_out/${tag}_bench_7b_shard8.err
 rm -f gpurun_out/*.ncu-rep.tmp
 du -sh gpurun_out
