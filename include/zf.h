@@ -264,8 +264,10 @@ zf_status zf_nccl_unique_id(void* out128 /* [host] 128 bytes */);
 /* Create a context on CUDA device `device`.  layers [host] [n_layers].
  * world/rank: data-parallel group; with world > 1, nccl_id128 [host] makes zf_create
  * a collective call that joins an NCCL communicator (every rank must call it); NULL
- * selects the host all-reduce callback (zf_set_host_allreduce).  Each rank passes the
- * row shard it owns (reading R13: rows [r*n/P, (r+1)*n/P) of every matrix). */
+ * selects the host all-reduce callback (zf_set_host_allreduce) or the peer-memory
+ * exchange (zf_peer_open).  With world == 1 an id is optional: it creates a one-rank
+ * communicator, so the NCCL exchange path runs (as a copy) on a single GPU.  Each rank
+ * passes the row shard it owns (reading R13: rows [r*n/P, (r+1)*n/P) of every matrix). */
 zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, const zf_config* cfg, int32_t world,
                     int32_t rank, const void* nccl_id128, int32_t device, zf_ctx** out);
 

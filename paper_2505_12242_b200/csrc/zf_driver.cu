@@ -372,7 +372,8 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
         for (auto& l : c->L) l.stage_dev[s] = static_cast<unsigned char*>(c->stage_dev_blk[s]) + l.stage_off;
     }
     {
-        static const int64_t chunk_target = getenv("ZF_X1_CHUNK_MB") ? atoll(getenv("ZF_X1_CHUNK_MB")) << 20 : 512ll << 20;
+        // ZF_X1_CHUNK_KB: chunk size override (tests use tiny chunks to exercise many counters)
+        const int64_t chunk_target = getenv("ZF_X1_CHUNK_KB") ? atoll(getenv("ZF_X1_CHUNK_KB")) << 10 : 512ll << 20;
         zf_ctx::Chunk ch;
         for (int i = 0; i < (int)c->L.size(); ++i) {
             LayerState& l = c->L[i];
@@ -565,7 +566,7 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
         ZF_CUDA(cudaHostAlloc(&c->norms_host, std::max<size_t>(c->total_m * sizeof(float), 64), cudaHostAllocDefault));
         c->host_pinned.push_back(c->norms_host);
     }
-    if (world > 1 && nccl_id128) {
+    if (nccl_id128) {   // (world 1 with an id: a one-rank communicator, the NCCL path on one GPU)
         ncclUniqueId id;
         std::memcpy(&id, nccl_id128, sizeof id);
         ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
@@ -747,7 +748,7 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
         ZF_CUDA(launch_norms(tn, c->k1_units, c->gdt, c->nonfinite_d, s));
         ZF_TRY(c->prof_end(&pe, s));
         c->launches++;
-        if (c->world > 1) {
+        if (c->world > 1 || c->comm) {
             ZF_TRY(c->prof_begin(1, s, &pe));
             if (c->comm) {
                 ZF_NCCL(ncclAllReduce(c->norms, c->norms, (size_t)c->total_m, ncclFloat32, ncclSum, c->comm, s));
@@ -838,7 +839,7 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
         ZF_CUDA(launch_norms(tn, c->k1_units, c->gdt, c->nonfinite_d, c->lag_stream));
         ZF_TRY(c->prof_end(&pe, c->lag_stream));
         c->launches++;
-        if (c->world > 1 && (c->comm || c->peer)) {
+        if (c->comm || (c->world > 1 && c->peer)) {
             ZF_TRY(c->prof_begin(1, c->lag_stream, &pe));
             if (c->comm)
                 ZF_NCCL(ncclAllReduce(c->norms, c->norms, (size_t)c->total_m, ncclFloat32, ncclSum, c->comm, c->lag_stream));

@@ -181,13 +181,14 @@ def test_compact_into_pinned_host(zf, orc, gpu, n, m, dt):
 # ------------------------------------------------------------------ zf_step vs oracle, multi-step
 def _run_stateful(zf, orc, gpu, shapes, gdt, pdt, ppm, N, S, steps, offload, lr=1e-3, wd=0.0, check_every=1,
                   tie=False, ld_pad=0, cpu_update=False, warmup=0, state_offload=False, devacc=False,
-                  cpu_async=False, side_stream=False, psub=True, poke=None, lagged=False):
+                  cpu_async=False, side_stream=False, psub=True, poke=None, lagged=False, host_stages=0):
     hp_o = orc.AdamHP(lr=lr, weight_decay=wd)
     ctx = zf.Context([zf.LayerShape(n, m, m + ld_pad, m + ld_pad) for n, m in shapes], grad_dtype=TDT[gdt],
                      param_dtype=TDT[pdt], topk_ratio_ppm=ppm, refresh_interval=N, accum_interval=S,
                      adam=zf.adam_params(lr=lr, weight_decay=wd), offload=offload, host_accumulate=offload, cpu_update=cpu_update,
                      warmup_steps=warmup, state_offload=state_offload, device_accumulate=devacc,
-                     cpu_update_async=cpu_async, param_subset=psub, lagged_selection=lagged)
+                     cpu_update_async=cpu_async, param_subset=psub, lagged_selection=lagged,
+                     host_stages=host_stages)
     scales = [gpu.ColScale(m, li) for li, (n, m) in enumerate(shapes)]
     Gs = [torch.empty(n, m + ld_pad, dtype=TDT[gdt], device="cuda")[:, :m] for n, m in shapes]
     Ps = [torch.empty(n, m + ld_pad, dtype=TDT[pdt], device="cuda")[:, :m] for n, m in shapes]
@@ -308,6 +309,32 @@ def test_step_warmup(zf, orc, gpu, tau, NS, pdt, cpu):
     gdt = "bf16" if pdt == "bf16" else "fp32"
     _run_stateful(zf, orc, gpu, shapes, gdt, pdt, 100000, NS, NS, tau + 6, offload=True, cpu_update=cpu,
                   warmup=tau)
+
+
+@pytest.mark.parametrize("lagged", [False, True])
+def test_step_nccl_one_rank(zf, orc, gpu, lagged):
+    """The NCCL exchange path on one GPU: world 1 with an NCCL id makes a one-rank
+    communicator, so every refresh runs ncclAllReduce on the flat norm vector (on the
+    caller's stream, or the side stream with the lagged selection) -- the multi-GPU code
+    path, exercised here; results bit-exact with the oracle, norms rel 1e-5."""
+    real = zf.Context
+    nid = zf.zf_nccl_unique_id()
+    try:
+        zf.Context = lambda *a, **kw: real(*a, nccl_id=nid, **kw)
+        _run_stateful(zf, orc, gpu, [(96, 320), (64, 512)], "bf16", "bf16", 100000, 2, 2, 6, offload=True,
+                      lagged=lagged)
+    finally:
+        zf.Context = real
+
+
+@pytest.mark.parametrize("host_stages", [2, 4])
+def test_step_x1_many_chunks(zf, orc, gpu, monkeypatch, host_stages):
+    """X1 with 16-KB chunks (ZF_X1_CHUNK_KB): many chunks, each gated by its own K3
+    completion counter and copied by the X1 thread, layers without rows among them; the host
+    compact blocks, both accumulators and everything else bit-exact."""
+    monkeypatch.setenv("ZF_X1_CHUNK_KB", "16")
+    shapes = [(0, 512), (37, 1001), (96, 300), (0, 4096), (64, 512), (130, 257), (0, 77), (20, 2000)]
+    _run_stateful(zf, orc, gpu, shapes, "bf16", "bf16", 100000, 2, 2, 6, offload=True, host_stages=host_stages)
 
 
 @pytest.mark.parametrize("shapes,gdt,NS,tau,cpu", [([(256, 512)], "fp32", 2, 0, False),
