@@ -747,8 +747,10 @@ def run_zenflow(args, rank, world):
             avail = int([l.split()[1] for l in open("/proc/meminfo") if l.startswith("MemAvailable")][0]) * 1024
         except Exception:  # noqa: BLE001
             avail = 0
+        # every rank of this node allocates at once: each takes its share of what is available
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
         hstages = args.host_stages or 2 * S_
-        while hstages > 2 and hstages * d2h_host + acc_bytes + h2d > 0.85 * avail:
+        while hstages > 2 and hstages * d2h_host + acc_bytes + h2d > 0.85 * avail / max(1, local_world):
             hstages -= 1
         link["host_stages"] = hstages
         ms_host = e2e_run(False, host_stages=hstages)
