@@ -672,7 +672,7 @@ struct zf_ctx {
     AutoRecord* auto_rec_h = nullptr;   // mapped pinned ring [AUTO_RING]
     AutoRecord* auto_rec_d = nullptr;
     cudaEvent_t auto_ev[8] = {};
-    static constexpr int AUTO_RING = 8;
+    static constexpr int AUTO_RING = 2 * ZF_MAX_HSTAGE;   // > the steps H1 may lag behind zf_step (host_stages)
     // device-side window accumulation (K7; device_accumulate)
     bool devacc = false;
     AccLayer* d_acc_tab = nullptr;

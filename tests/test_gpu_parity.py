@@ -814,8 +814,8 @@ def test_h1_window_batches(zf, orc, gpu, host_stages, S, N, gdt, cpu):
         assert passes < steps, (passes, steps)
 
 
-@pytest.mark.parametrize("cpu", [False, True])
-def test_h1_window_batches_zen_auto(zf, orc, gpu, cpu):
+@pytest.mark.parametrize("cpu,host_stages", [(False, 8), (True, 8), (False, 16)])
+def test_h1_window_batches_zen_auto(zf, orc, gpu, cpu, host_stages):
     """Zen-auto (R21) with H1 in window batches: H1 reads each staged step's K6 decision
     before forming a batch, so batches never cross a variable-length window's end; no
     zf_sync inside windows; final window log, both accumulators and the parameters equal
@@ -825,7 +825,7 @@ def test_h1_window_batches_zen_auto(zf, orc, gpu, cpu):
     ctx = zf.Context([zf.LayerShape(n, m) for n, m in shapes], grad_dtype=torch.bfloat16,
                      param_dtype=torch.bfloat16, topk_ratio_ppm=100000, refresh_interval=N, accum_interval=smax,
                      adam=zf.adam_params(lr=1e-3), offload=True, host_accumulate=True, cpu_update=cpu,
-                     auto_gamma=gamma, host_stages=8)
+                     auto_gamma=gamma, host_stages=host_stages)
     scales = [gpu.ColScale(m, li) for li, (n, m) in enumerate(shapes)]
     Gs = [torch.empty(n, m, dtype=torch.bfloat16, device="cuda") for n, m in shapes]
     Ps = [torch.empty(n, m, dtype=torch.bfloat16, device="cuda") for n, m in shapes]
