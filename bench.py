@@ -68,6 +68,9 @@ def parse():
     ap.add_argument("--no-lagged", action="store_true",
                     help="skip the f4 (ii) lagged-selection line (device time, and a training-loop proxy "
                          "with a synthetic compute-bound backward between steps)")
+    ap.add_argument("--refresh-group-mb", type=int, default=64,
+                    help="the f4 (i) line: refresh steps run K1 -> K2 -> K3 per group of layers of at most "
+                         "this many MB of gradients (G re-read from L2); 0 skips the line")
     ap.add_argument("--exchange", choices=["auto", "nccl", "host", "peer"], default="auto",
                     help="N>1 norm exchange (row a2): NCCL all-reduce, the host callback over gloo, or "
                          "peer-memory kernels (f4 iii, k_peer.cu); auto = nccl, or host with --colocate")
@@ -474,8 +477,8 @@ def run_zenflow(args, rank, world):
         result["k1_roofline"] = {"bound": "hbm", "achieved": g_bytes / (k1_avg * 1e-3) / 1e9, "peak": hbm_peak,
                                  "unit": "GB/s", "frac": g_bytes / (k1_avg * 1e-3) / 1e9 / hbm_peak}
 
-    def k3_line(ctx_ppm, lr=None, tag=""):
-        ctx = make_ctx(ctx_ppm, False) if lr is None else zf.Context(
+    def k3_line(ctx_ppm, lr=None, tag="", **kw):
+        ctx = make_ctx(ctx_ppm, False, **kw) if lr is None else zf.Context(
             [zf.LayerShape(n, m) for n, m in shapes], topk_ratio_ppm=ctx_ppm, refresh_interval=args.refresh,
             accum_interval=args.refresh, adam=zf.adam_params(lr=lr), world=world, rank=rank, nccl_id=nccl_id,
             device=dev, host_allreduce=host_ar)
@@ -502,6 +505,14 @@ def run_zenflow(args, rank, world):
     #      (and read-modify-writes) the p sectors the lr 1e-5 headline mostly skips
     if not args.no_lr1e3 and args.lr != 1e-3:
         result["lr_1e-3"] = k3_line(args.ratio_ppm, lr=1e-3, tag="lr1e3")
+
+    # ---- f4 (i): refresh steps in groups of layers (K1 -> K2 -> K3 per group, G re-read from L2)
+    if args.refresh_group_mb > 0 and world == 1:
+        rg = k3_line(args.ratio_ppm, tag="rgroup", refresh_group_mb=args.refresh_group_mb)
+        result["refresh_in_groups"] = {"group_mb": args.refresh_group_mb, "ms_per_step": rg["ms_per_step"],
+                                       "k1_ms": rg["k1_ms"], "k3_ms": rg["k3_ms"],
+                                       "note": "K1/K3 ms are per group launch here; compare ms_per_step with "
+                                               "the whole-model passes of the main line"}
 
     # ---- f4 (ii) lagged selection: device time of the same loop, and a training-loop proxy in
     #      which each step is preceded by a compute-bound "backward" (bf16 GEMMs on the caller's

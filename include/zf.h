@@ -254,6 +254,15 @@ typedef struct {
                                          element and step towards 3 (2·accum_interval slots:
                                          whole windows, overlapped with the next window's
                                          copies).  Range [0, 16]; ZF_EINVAL otherwise.   */
+    int32_t refresh_group_mb;         /* > 0: next row f4 (i) -- a refresh step runs K1 ->
+                                         K2 -> K3 per group of consecutive layers whose
+                                         gradients total <= this many MB, so K3 re-reads a
+                                         group's G while it is still in the 126 MB L2 from
+                                         K1, instead of K1 over the whole model and then K3
+                                         over it.  Results are identical.  world 1 only,
+                                         not with auto_gamma / lagged_selection / the
+                                         split update; 0 (default) = whole-model passes
+                                         (measured faster on Llama-2-7B).  */
 } zf_config;
 
 typedef struct zf_ctx zf_ctx;

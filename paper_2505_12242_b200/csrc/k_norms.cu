@@ -46,14 +46,14 @@ __device__ __forceinline__ int find_layer(const Table<NormLayer>& t, int64_t u) 
 
 template <int DT>
 __global__ void __launch_bounds__(K1_THREADS)
-k_column_norms(const __grid_constant__ Table<NormLayer> table, int32_t* nonfinite) {
+k_column_norms(const __grid_constant__ Table<NormLayer> table, int32_t* nonfinite, int64_t unit_off) {
     using E = Elt<DT>;
     constexpr int VEC = E::VEC;
     constexpr int CB = 32 * VEC;
     __shared__ float red[K1_WARPS][CB];
     __shared__ int s_last;
 
-    const int64_t u = blockIdx.x;
+    const int64_t u = blockIdx.x + unit_off;   // (unit_off: a launch over a subset of the layers)
     const int li = find_layer(table, u);
     const NormLayer& L = table[li];
     const int64_t lu = u - L.unit_begin;
@@ -150,13 +150,14 @@ k_column_norms(const __grid_constant__ Table<NormLayer> table, int32_t* nonfinit
 int norms_rows_per_block() { return K1_RB; }
 int norms_cols_per_block(int gdt) { return 32 * (gdt == DT_BF16 ? 8 : 4); }
 
-cudaError_t launch_norms(const Table<NormLayer>& t, int64_t total_units, int gdt, int32_t* nonfinite, cudaStream_t s) {
+cudaError_t launch_norms(const Table<NormLayer>& t, int64_t total_units, int gdt, int32_t* nonfinite, cudaStream_t s,
+                         int64_t unit_off) {
     if (total_units <= 0) return cudaSuccess;
     if (total_units > 0x7fffffff) return cudaErrorInvalidValue;
     if (gdt == DT_BF16)
-        k_column_norms<DT_BF16><<<(unsigned)total_units, K1_THREADS, 0, s>>>(t, nonfinite);
+        k_column_norms<DT_BF16><<<(unsigned)total_units, K1_THREADS, 0, s>>>(t, nonfinite, unit_off);
     else
-        k_column_norms<DT_F32><<<(unsigned)total_units, K1_THREADS, 0, s>>>(t, nonfinite);
+        k_column_norms<DT_F32><<<(unsigned)total_units, K1_THREADS, 0, s>>>(t, nonfinite, unit_off);
     return cudaGetLastError();
 }
 

@@ -512,7 +512,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
             // claim and look up the next unit before waiting for its arena
             const uint32_t cl = atomicAdd(prm.claim, 1u) - prm.claim_base;
             StageInfo si{};
-            si.u = (int64_t)cl < prm.total_units ? (int64_t)cl : -1;
+            si.u = (int64_t)cl < prm.total_units ? (int64_t)cl + prm.unit_offset : -1;
             const UpdLayer* Lp = nullptr;
             UnitGeom g{};
             if (si.u >= 0) {

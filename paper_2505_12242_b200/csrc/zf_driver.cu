@@ -232,6 +232,9 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
     if (cfg->device_accumulate && !cfg->host_accumulate)
         return fail(ZF_EINVAL, "device_accumulate requires host_accumulate (it moves that accumulation onto the GPU)");
     ZF_TRY(check_hp(&cfg->adam));
+    if (cfg->refresh_group_mb < 0) return fail(ZF_EINVAL, "refresh_group_mb must be >= 0");
+    if (cfg->refresh_group_mb > 0 && (world > 1 || cfg->auto_gamma > 0.0f || cfg->lagged_selection))
+        return fail(ZF_EINVAL, "refresh_group_mb: world 1 only, not with auto_gamma or lagged_selection");
     if (cfg->host_stages < 0 || cfg->host_stages > ZF_MAX_HSTAGE)
         return fail(ZF_EINVAL, "host_stages must be in [0, %d]", ZF_MAX_HSTAGE);
     if (world < 1 || rank < 0 || rank >= world) return fail(ZF_EINVAL, "bad world/rank");
@@ -364,6 +367,33 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
         }
         l.stage_off = c->stage_bytes;
         c->stage_bytes += ((int64_t)n * l.mk_pad * c->gsz + 255) / 256 * 256;
+    }
+    if (cfg->refresh_group_mb > 0) {
+        // f4 (i): consecutive layers whose gradients fit the budget refresh together
+        const int64_t budget = (int64_t)cfg->refresh_group_mb << 20;
+        zf_ctx::RGroup g;
+        int64_t bytes = 0;
+        const int nl_ = (int)c->L.size();
+        for (int i = 0; i < nl_; ++i) {
+            const LayerState& l = c->L[i];
+            const int64_t lb = l.d.n * l.d.m * c->gsz;
+            if (i > g.a && bytes + lb > budget) {
+                g.b = i;
+                c->rgroups.push_back(g);
+                g = zf_ctx::RGroup{};
+                g.a = i;
+                bytes = 0;
+            }
+            bytes += lb;
+        }
+        g.b = nl_;
+        c->rgroups.push_back(g);
+        for (auto& gg : c->rgroups) {
+            gg.k1_off = c->L[gg.a].norm_unit_begin;
+            gg.k1_units = (gg.b < nl_ ? c->L[gg.b].norm_unit_begin : c->k1_units) - gg.k1_off;
+            gg.k3_off = c->L[gg.a].unit_begin;
+            gg.k3_units = (gg.b < nl_ ? c->L[gg.b].unit_begin : c->k3_units) - gg.k3_off;
+        }
     }
     // the compact blocks of every layer back to back per staging slot; X1 copies chunks of
     // consecutive layers (~512 MB) with one command each
@@ -714,6 +744,8 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
     const bool lag_refresh = c->lagged && refresh && c->have_sel;
     const bool lag_pre = c->lagged && (t + 1) % N == 0;
     const bool norms_now = (refresh && !lag_refresh) || c->autoz;  // Zen-auto reads every step's norms (R21)
+    // f4 (i): this refresh runs K1 -> K2 -> K3 per group of layers (G re-read from L2)
+    const bool grouped = refresh && !c->rgroups.empty() && c->have_sel && !c->split;
     ZF_TRY(refresh_pointer_tables(c, variant, norms_now || lag_pre, grads, params, s));
     c->tmark(1);
 
@@ -737,7 +769,7 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
         }
     }
     c->tmark(2);
-    if (norms_now) {
+    if (norms_now && !grouped) {
         zf_ctx::Pending pe;
         // layers with no rows on this rank (flat partitions, row f3) contribute zero norms
         if (c->has_empty) ZF_CUDA(cudaMemsetAsync(c->norms, 0, c->total_m * sizeof(float), s));
@@ -780,17 +812,18 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
             ZF_TRY(c->prof_end(&pe, s));
         }
     }
-    if (refresh) {
+    const int32_t old_delta = c->since;   // K2's remap: launches since the old selection was made
+    if (refresh && !grouped) {
         zf_ctx::Pending pe;
         Table<TopkLayer> tk{};
         tk.dev = c->have_sel ? c->d_topk_tab[c->cur ^ 1] : (from_warmup ? c->d_topk_w : c->d_topk_tab[2]);
         tk.n = nl;
         ZF_TRY(c->prof_begin(2, s, &pe));
-        ZF_CUDA(launch_topk(tk, c->max_m, c->since, c->nonfinite_d, s));
-        c->since = 0;
+        ZF_CUDA(launch_topk(tk, c->max_m, old_delta, c->nonfinite_d, s));
         ZF_TRY(c->prof_end(&pe, s));
         c->launches++;
     }
+    if (refresh) c->since = 0;
     // first refresh writes set 1 (variant built with cur=0, refresh=1 -> new set 1)
     UpdParams prm{};
     prm.layers.dev = from_warmup ? c->d_upd_x[sb & 1] : c->d_upd_tab[variant];
@@ -850,16 +883,52 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
         ZF_CUDA(cudaEventRecord(c->norm_ready, c->lag_stream));
         c->lag_pending = true;
     }
-    zf_ctx::Pending pe3;
-    ZF_TRY(c->prof_begin(3, s, &pe3));
-    // prologue: the slots' {ss, bc2s} for this launch (after K2 wrote a refresh's step counts)
-    ZF_CUDA(launch_slot_consts(prm.layers.dev, nl, c->max_m, prm.step_delta, c->adam, s));
-    c->launches++;
-    c->tmark(3);
-    ZF_CUDA(launch_update(prm, c->gdt, c->pdt, grid, s));
-    c->tmark(4);
-    ZF_TRY(c->prof_end(&pe3, s));
-    c->launches++;
+    if (grouped) {
+        // f4 (i): per group of layers K1 -> K2 -> K3 prologue -> K3, so K3 finds the group's G
+        // in L2 where K1 just read it (same tables, unit ranges offset to the group)
+        if (c->has_empty) ZF_CUDA(cudaMemsetAsync(c->norms, 0, c->total_m * sizeof(float), s));
+        const TopkLayer* tkd = c->d_topk_tab[c->cur ^ 1];
+        for (const auto& g : c->rgroups) {
+            const int gn = g.b - g.a;
+            zf_ctx::Pending pa, pb, pc;
+            Table<NormLayer> tn{};
+            tn.dev = c->d_norm_tab + g.a;
+            tn.n = gn;
+            ZF_TRY(c->prof_begin(0, s, &pa));
+            ZF_CUDA(launch_norms(tn, g.k1_units, c->gdt, c->nonfinite_d, s, g.k1_off));
+            ZF_TRY(c->prof_end(&pa, s));
+            Table<TopkLayer> tk{};
+            tk.dev = tkd + g.a;
+            tk.n = gn;
+            ZF_TRY(c->prof_begin(2, s, &pb));
+            ZF_CUDA(launch_topk(tk, c->max_m, old_delta, c->nonfinite_d, s));
+            ZF_TRY(c->prof_end(&pb, s));
+            UpdParams pg = prm;
+            pg.layers.dev = prm.layers.dev + g.a;
+            pg.layers.n = gn;
+            pg.total_units = g.k3_units;
+            pg.unit_offset = g.k3_off;
+            pg.claim_base = c->claim_base;
+            const int gg = (int)std::min<int64_t>(c->grid, std::max<int64_t>(g.k3_units, 1));
+            ZF_TRY(c->prof_begin(3, s, &pc));
+            ZF_CUDA(launch_slot_consts(pg.layers.dev, gn, c->max_m, pg.step_delta, c->adam, s));
+            ZF_CUDA(launch_update(pg, c->gdt, c->pdt, gg, s));
+            ZF_TRY(c->prof_end(&pc, s));
+            c->launches += g.k3_units > 0 ? 4 : 3;
+            if (g.k3_units > 0) c->claim_base += (uint32_t)(g.k3_units + (int64_t)gg * update_limits().producers);
+        }
+    } else {
+        zf_ctx::Pending pe3;
+        ZF_TRY(c->prof_begin(3, s, &pe3));
+        // prologue: the slots' {ss, bc2s} for this launch (after K2 wrote a refresh's step counts)
+        ZF_CUDA(launch_slot_consts(prm.layers.dev, nl, c->max_m, prm.step_delta, c->adam, s));
+        c->launches++;
+        c->tmark(3);
+        ZF_CUDA(launch_update(prm, c->gdt, c->pdt, grid, s));
+        c->tmark(4);
+        ZF_TRY(c->prof_end(&pe3, s));
+        c->launches++;
+    }
     if (c->split) {
         // K3b: AdamW over the dense [n, k] blocks K3a filled (phase 7)
         zf_ctx::Pending pe7;
@@ -868,7 +937,7 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
         ZF_TRY(c->prof_end(&pe7, s));
         c->launches++;
     }
-    c->claim_base += (uint32_t)(units + (int64_t)grid * update_limits().producers);
+    if (!grouped) c->claim_base += (uint32_t)(units + (int64_t)grid * update_limits().producers);
     c->since += 1;
     c->psub_valid = c->cfg.param_subset != 0;  // this K3 (re)built or kept the subset block
     for (int i = 0; i < nl; ++i)

@@ -534,6 +534,12 @@ struct zf_ctx {
         cudaEvent_t ev[ZF_MAX_HSTAGE] = {};   // per host slot: this chunk's D2H landed
     };
     std::vector<Chunk> chunks;
+    // f4 (i): refresh in groups of layers (refresh_group_mb): layers [a, b), their K1 / K3 units
+    struct RGroup {
+        int32_t a = 0, b = 0;
+        int64_t k1_off = 0, k1_units = 0, k3_off = 0, k3_units = 0;
+    };
+    std::vector<RGroup> rgroups;
     // X1 issue thread (x1_loop): one job per offloaded step
     struct X1Job {
         int64_t t = 0;
@@ -671,8 +677,8 @@ struct zf_ctx {
     AutoState* auto_state = nullptr;
     AutoRecord* auto_rec_h = nullptr;   // mapped pinned ring [AUTO_RING]
     AutoRecord* auto_rec_d = nullptr;
-    cudaEvent_t auto_ev[8] = {};
     static constexpr int AUTO_RING = 2 * ZF_MAX_HSTAGE;   // > the steps H1 may lag behind zf_step (host_stages)
+    cudaEvent_t auto_ev[AUTO_RING] = {};
     // device-side window accumulation (K7; device_accumulate)
     bool devacc = false;
     AccLayer* d_acc_tab = nullptr;

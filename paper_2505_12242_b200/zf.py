@@ -48,7 +48,7 @@ class Config(ctypes.Structure):
                 ("auto_gamma", ctypes.c_float), ("state_offload", ctypes.c_int32),
                 ("device_accumulate", ctypes.c_int32), ("cpu_update_async", ctypes.c_int32),
                 ("param_subset", ctypes.c_int32), ("lagged_selection", ctypes.c_int32),
-                ("host_stages", ctypes.c_int32)]
+                ("host_stages", ctypes.c_int32), ("refresh_group_mb", ctypes.c_int32)]
 
 
 if not os.path.exists(_LIB_PATH):
@@ -215,7 +215,7 @@ class Context:
                  host_accumulate=False, host_threads=0, world=1, rank=0, nccl_id: bytes | None = None,
                  device: int | None = None, cpu_update=False, warmup_steps=0, auto_gamma=0.0,
                  state_offload=False, device_accumulate=False, host_allreduce=None, cpu_update_async=False,
-                 param_subset=True, lagged_selection=False, host_stages=0):
+                 param_subset=True, lagged_selection=False, host_stages=0, refresh_group_mb=0):
         self.layers = [l if isinstance(l, LayerShape) else LayerShape(*l) for l in layers]
         descs = (LayerDesc * len(self.layers))()
         for d, l in zip(descs, self.layers):
@@ -242,6 +242,7 @@ class Context:
         cfg.param_subset = int(param_subset)
         cfg.lagged_selection = int(lagged_selection)
         cfg.host_stages = int(host_stages)
+        cfg.refresh_group_mb = int(refresh_group_mb)
         self.cfg = cfg
         self.device = torch.cuda.current_device() if device is None else device
         h = ctypes.c_void_p()

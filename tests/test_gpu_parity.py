@@ -181,14 +181,15 @@ def test_compact_into_pinned_host(zf, orc, gpu, n, m, dt):
 # ------------------------------------------------------------------ zf_step vs oracle, multi-step
 def _run_stateful(zf, orc, gpu, shapes, gdt, pdt, ppm, N, S, steps, offload, lr=1e-3, wd=0.0, check_every=1,
                   tie=False, ld_pad=0, cpu_update=False, warmup=0, state_offload=False, devacc=False,
-                  cpu_async=False, side_stream=False, psub=True, poke=None, lagged=False, host_stages=0):
+                  cpu_async=False, side_stream=False, psub=True, poke=None, lagged=False, host_stages=0,
+                  refresh_group_mb=0):
     hp_o = orc.AdamHP(lr=lr, weight_decay=wd)
     ctx = zf.Context([zf.LayerShape(n, m, m + ld_pad, m + ld_pad) for n, m in shapes], grad_dtype=TDT[gdt],
                      param_dtype=TDT[pdt], topk_ratio_ppm=ppm, refresh_interval=N, accum_interval=S,
                      adam=zf.adam_params(lr=lr, weight_decay=wd), offload=offload, host_accumulate=offload, cpu_update=cpu_update,
                      warmup_steps=warmup, state_offload=state_offload, device_accumulate=devacc,
                      cpu_update_async=cpu_async, param_subset=psub, lagged_selection=lagged,
-                     host_stages=host_stages)
+                     host_stages=host_stages, refresh_group_mb=refresh_group_mb)
     scales = [gpu.ColScale(m, li) for li, (n, m) in enumerate(shapes)]
     Gs = [torch.empty(n, m + ld_pad, dtype=TDT[gdt], device="cuda")[:, :m] for n, m in shapes]
     Ps = [torch.empty(n, m + ld_pad, dtype=TDT[pdt], device="cuda")[:, :m] for n, m in shapes]
@@ -325,6 +326,26 @@ def test_step_nccl_one_rank(zf, orc, gpu, lagged):
                       lagged=lagged)
     finally:
         zf.Context = real
+
+
+@pytest.mark.parametrize("shapes,gdt,NS,cpu", [([(512, 1024), (96, 320), (0, 512), (37, 1001), (640, 1024), (64, 512)],
+                                                "bf16", 2, False),
+                                               ([(512, 1024), (130, 257), (700, 900)], "fp32", 4, True)])
+def test_step_refresh_in_groups(zf, orc, gpu, shapes, gdt, NS, cpu):
+    """f4 (i): refresh steps run K1 -> K2 -> K3 per group of layers (1-MB groups: single
+    layers and runs of small ones, a layer without rows among them) -- the unit ranges of
+    each launch offset to its group; everything bit-exact with the oracle."""
+    _run_stateful(zf, orc, gpu, shapes, gdt, gdt, 100000, NS, NS, 3 * NS + 1, offload=True, cpu_update=cpu,
+                  refresh_group_mb=1)
+
+
+def test_refresh_groups_argument_errors(zf):
+    with pytest.raises(zf.ZFError):
+        zf.Context([zf.LayerShape(8, 64)], topk_ratio_ppm=100000, refresh_interval=2, accum_interval=2,
+                   refresh_group_mb=-1)
+    with pytest.raises(zf.ZFError):
+        zf.Context([zf.LayerShape(8, 64)], topk_ratio_ppm=100000, refresh_interval=2, accum_interval=2,
+                   refresh_group_mb=8, lagged_selection=True)
 
 
 @pytest.mark.parametrize("host_stages", [2, 4])
