@@ -462,16 +462,29 @@ def run_zenflow(args, rank, world):
                           "sector_compulsory_bytes_per_launch": sec,
                           "achieved_sector_GBs": sec / (k3_avg * 1e-3) / 1e9,
                           "frac_sector": sec / (k3_avg * 1e-3) / 1e9 / hbm_peak, "traffic": None}
-    prof_path = os.path.join(ROOT, "profiles", "k3_dram_traffic.json")
-    if os.path.exists(prof_path):
-        d = json.load(open(prof_path))
-        if d.get("workload") == result["config"]["workload"] and world == 1:
-            tr = d.get("traffic_bytes_per_launch")
-            result["roofline"]["traffic"] = tr
-            result["roofline"]["traffic_source"] = d.get("source")
-            # DRAM bytes the kernel actually moves (ncu) over its live average duration
-            result["roofline"]["achieved_dram_GBs"] = tr / (k3_avg * 1e-3) / 1e9
-            result["roofline"]["frac_dram"] = tr / (k3_avg * 1e-3) / 1e9 / hbm_peak
+    def add_traffic(roof, workload, k3_ms):
+        # DRAM bytes the kernel actually moves per launch (committed ncu captures) over its
+        # live average duration: the launch-list average of the default command, else the
+        # one-launch full capture of the workload
+        tr, src = None, None
+        p1 = os.path.join(ROOT, "profiles", "k3_dram_traffic.json")
+        p2 = os.path.join(ROOT, "profiles", "k3_dram_traffic_ncu_full.json")
+        if os.path.exists(p1):
+            d = json.load(open(p1))
+            if d.get("workload") == workload:
+                tr, src = d.get("traffic_bytes_per_launch"), d.get("source")
+        if tr is None and os.path.exists(p2):
+            d = json.load(open(p2))
+            e = d.get("by_workload", {}).get(workload)
+            if e:
+                tr, src = e["traffic_bytes_per_launch"], d.get("source")
+        if tr is not None and world == 1:
+            roof["traffic"] = tr
+            roof["traffic_source"] = src
+            roof["achieved_dram_GBs"] = tr / (k3_ms * 1e-3) / 1e9
+            roof["frac_dram"] = tr / (k3_ms * 1e-3) / 1e9 / hbm_peak
+
+    add_traffic(result["roofline"], result["config"]["workload"], k3_avg)
     if n_k1:
         k1_avg = k1_ms / n_k1
         result["k1_roofline"] = {"bound": "hbm", "achieved": g_bytes / (k1_avg * 1e-3) / 1e9, "peak": hbm_peak,
@@ -501,6 +514,7 @@ def run_zenflow(args, rank, world):
     if not args.no_k1pct and args.ratio_ppm != 10000:
         result["k1pct"] = k3_line(10000, tag="k1pct")
         result["k1pct"]["workload"] = f"{args.model}-all-linear-k1pct"
+        add_traffic(result["k1pct"]["roofline"], result["k1pct"]["workload"], result["k1pct"]["k3_ms"])
     # ---- the main config at lr 1e-3: nearly every selected bf16 value changes, so K3 stores
     #      (and read-modify-writes) the p sectors the lr 1e-5 headline mostly skips
     if not args.no_lr1e3 and args.lr != 1e-3:
