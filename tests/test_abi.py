@@ -101,9 +101,34 @@ def test_create_validation(zf):
     assert L.zf_create(descs, 1, ctypes.byref(cfg), 1, 0, None, 0, ctypes.byref(h)) == zf.ZF_EINVAL
     assert b"auto_gamma" in L.zf_last_error()
     cfg.auto_gamma = 0.0
+    cfg.host_accumulate = 1
+    cfg.host_stages = 17                                                               # > 16 staging slots
+    assert L.zf_create(descs, 1, ctypes.byref(cfg), 1, 0, None, 0, ctypes.byref(h)) == zf.ZF_EINVAL
+    assert b"host_stages" in L.zf_last_error()
+    cfg.host_stages = 0
+    cfg.refresh_group_mb = -1
+    assert L.zf_create(descs, 1, ctypes.byref(cfg), 1, 0, None, 0, ctypes.byref(h)) == zf.ZF_EINVAL
+    cfg.refresh_group_mb = 64                                                          # grouped refresh: world 1 only
+    assert L.zf_create(descs, 1, ctypes.byref(cfg), 2, 0, None, 0, ctypes.byref(h)) == zf.ZF_EINVAL
+    assert b"refresh_group_mb" in L.zf_last_error()
+    cfg.refresh_group_mb = 0
+    cfg.lagged_selection, cfg.auto_gamma = 1, 1.0                                      # lag + Zen-auto exclusive
+    assert L.zf_create(descs, 1, ctypes.byref(cfg), 1, 0, None, 0, ctypes.byref(h)) == zf.ZF_EINVAL
+    cfg.lagged_selection, cfg.auto_gamma = 0, 0.0
     descs[0].ld_grad = 7
     assert L.zf_create(descs, 1, ctypes.byref(cfg), 1, 0, None, 0, ctypes.byref(h)) == zf.ZF_EINVAL
     assert not h.value
+
+
+def test_null_context_calls(zf):
+    """Context calls reject a NULL context with ZF_EINVAL (no GPU needed)."""
+    L = zf.lib
+    a, b = ctypes.c_int64(), ctypes.c_int64()
+    assert L.zf_host_stats(None, ctypes.byref(a), ctypes.byref(b)) == zf.ZF_EINVAL
+    buf = ctypes.create_string_buffer(64 * 2)
+    assert L.zf_peer_handle(None, buf) == zf.ZF_EINVAL
+    assert L.zf_peer_open(None, buf) == zf.ZF_EINVAL
+    assert L.zf_sync(None) == zf.ZF_EINVAL
 
 
 def test_product_does_not_import_oracle():
