@@ -30,9 +30,10 @@
 //    its rows; explicit round-to-nearest intrinsics in the oracle's op order), each
 //    changed p value stored straight to HBM; then compaction by gather (8 bf16 outputs per
 //    thread per vector store, coalesced across the warp).
-//  - with offload, each consumer warp bumps a per-layer counter after its share of
-//    a unit (red.release); the copy stream waits on it (cuStreamWaitValue32) to
-//    start the layer's device->host copy.
+//  - with offload, a unit's producer bumps its layer chunk's completion counter once the
+//    stage's consumer warps all released the unit (one red.release per unit, cumulative
+//    over their stores); the copy stream waits on it (cuStreamWaitValue32) to start the
+//    chunk's device->host copy.
 #include <cstdlib>
 
 #include "zf_internal.cuh"
@@ -508,6 +509,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
         const uint64_t pol_first = evict_first_policy();
         const uint64_t pol_last = evict_last_policy();
         int hint = 0;
+        uint32_t* prev_done = nullptr;   // completion counter of the unit last staged in this arena
         for (int it = 0;; ++it) {
             // claim and look up the next unit before waiting for its arena
             const uint32_t cl = atomicAdd(prm.claim, 1u) - prm.claim_base;
@@ -577,7 +579,13 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
                 }
             }
 #endif
-            if (it > 0) mbar_wait(&empty[st], (it - 1) & 1);
+            if (it > 0) {
+                mbar_wait(&empty[st], (it - 1) & 1);
+                // every consumer warp of the stage's previous unit arrived (release, CTA scope;
+                // this wait acquires): one GPU-scope release publishes all their compact-block
+                // stores to the layer chunk's completion counter (X1's copy engine waits on it)
+                if (prev_done) red_release_add(prev_done, 1u);
+            }
             unsigned char* A = smem + st * K3_ARENA;
             if (si.u < 0) {
                 info[st] = si;
@@ -691,6 +699,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
             si.ucol = L.ucol;
             si.done = L.done;
             info[st] = si;
+            prev_done = si.done;
             mbar_expect_tx(&full[st], tx);  // the single arrival of this phase
         }
         return;
@@ -930,11 +939,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
         ZF_TICK(2);
         // stage fully consumed by this warp
         __syncwarp();
-        if (lane == 0) {
-            uint32_t* done = si.done;
-            mbar_arrive(&empty[st]);
-            if (done) red_release_add(done, 1u);  // per-warp completion count (offload only)
-        }
+        if (lane == 0) mbar_arrive(&empty[st]);   // (the producer then counts the unit for X1)
         ZF_TICK(4);
 #ifdef ZF_K3_PROF
         pc[5] += 1;  // units
@@ -1013,7 +1018,7 @@ void set_attr() {
 UpdLimits update_limits() {
     UpdLimits l;
     l.arena_bytes = K3_ARENA;
-    l.consumer_warps = K3_GW;  // warps that process (and count) each unit
+    l.consumer_warps = 1;      // completion-counter increments per unit (one, by the stage's producer)
     l.producers = K3_STAGES;
     return l;
 }
