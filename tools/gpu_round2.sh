@@ -16,12 +16,12 @@ timeout 600 python bench.py --gpus 2 --colocate --exchange peer --no-cpu-baselin
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${tag}_bench_reference.jsonl 2> gpurun_out/${tag}_bench_reference.err
 [ "$mode" = quick ] && exit 0
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv -k regex:"k_(update|column_norms|topk|scatter|accumulate|zen_auto|adam)" \
-    --log-file gpurun_out/${tag}_launches_7b.csv python bench.py --steps 4 --warmup 3 --no-e2e --no-cpu-baseline --no-k1pct --no-lr1e3 --no-lagged \
+    --log-file gpurun_out/${tag}_launches_7b.csv python bench.py --steps 4 --warmup 3 --no-e2e --no-cpu-baseline --no-k1pct --no-lr1e3 --no-lagged --refresh-group-mb 0 \
     > gpurun_out/${tag}_ncu_bench.log 2>&1
 for spec in "7b_k10:--ratio-ppm 100000" "7b_k1:--ratio-ppm 10000" "gpt2_k10:--model gpt2-small"; do
   name=${spec%%:*}; args=${spec#*:}
   timeout 1300 ncu --set full --clock-control none --import-source on -k regex:k_update -s 3 -c 1 \
-      -o gpurun_out/${tag}_k3_${name} python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-k1pct --no-lr1e3 --no-lagged $args \
+      -o gpurun_out/${tag}_k3_${name} python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-k1pct --no-lr1e3 --no-lagged --refresh-group-mb 0 $args \
       > gpurun_out/${tag}_k3_${name}.log 2>&1
   ncu -i gpurun_out/${tag}_k3_${name}.ncu-rep --page details > gpurun_out/${tag}_k3_${name}.txt 2>&1
   ncu -i gpurun_out/${tag}_k3_${name}.ncu-rep --page raw --csv > gpurun_out/${tag}_k3_${name}_raw.csv 2>&1
