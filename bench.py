@@ -270,7 +270,7 @@ def host_dram_probe():
     """Host DRAM bandwidth of this box's cores on H1's access patterns (tools/host_membw.c,
     built here with the host compiler, all cores, 2 GiB fp32 arrays); {} if unavailable."""
     import subprocess as _sp
-    exe = "/tmp/zf_host_membw"
+    exe = f"/tmp/zf_host_membw_{os.getpid()}"
     src = os.path.join(ROOT, "tools", "host_membw.c")
     try:
         if not os.path.exists(exe) or os.path.getmtime(exe) < os.path.getmtime(src):
@@ -807,7 +807,7 @@ def run_zenflow(args, rank, world):
                                                (h2d + d2h_host) / link["bidir_peak_GBs"]) / 1e9 * 1e3
         link["host_link_floor_k7_ms"] = max(h2d / link["h2d_peak_GBs"], d2h_dev / link["d2h_peak_GBs"],
                                             (h2d + d2h_dev) / link["bidir_peak_GBs"]) / 1e9 * 1e3
-        link["host_dram"] = host_dram_probe()
+        link["host_dram"] = host_dram_probe() if rank == 0 else {"skipped": "rank 0 probes the host"}
         if link["host_dram"].get("accB1_GBs"):
             # H1's floor on this host: its bytes per step at the probe's one-step-pass rate
             link["h1_floor_ms"] = h1_bytes / (link["host_dram"]["accB1_GBs"] * 1e9) * 1e3
