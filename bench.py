@@ -273,10 +273,10 @@ def host_dram_probe():
     exe = f"/tmp/zf_host_membw_{os.getpid()}"
     src = os.path.join(ROOT, "tools", "host_membw.c")
     try:
-        if not os.path.exists(exe) or os.path.getmtime(exe) < os.path.getmtime(src):
-            _sp.run(["gcc", "-O3", "-march=native", "-fopenmp", src, "-o", exe], check=True, capture_output=True,
-                    timeout=120)
+        _sp.run(["gcc", "-O3", "-march=native", "-fopenmp", src, "-o", exe], check=True, capture_output=True,
+                timeout=120)
         out = _sp.run([exe, "2", str(os.cpu_count())], capture_output=True, text=True, timeout=300).stdout
+        os.remove(exe)
         return json.loads(out.strip().splitlines()[-1])
     except Exception as ex:  # noqa: BLE001
         return {"error": str(ex)[-120:]}
