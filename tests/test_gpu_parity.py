@@ -879,3 +879,41 @@ def test_h1_window_batches_zen_auto(zf, orc, gpu, cpu, host_stages):
     assert covered == steps and passes < steps, (passes, covered)
     iv = model.intervals()
     assert min(iv) < smax, iv
+
+
+# ------------------------------------------------------------------ randomized configurations
+def _random_config(seed):
+    rng = np.random.default_rng(0x5EED + seed)
+    nl = int(rng.integers(1, 4))
+    shapes = []
+    for _ in range(nl):
+        n = int(rng.choice([0, 1, 7, 33, 64, 130, 257])) if nl > 1 else int(rng.choice([1, 33, 130, 257]))
+        m = int(rng.choice([33, 96, 300, 512, 777, 1025, 2048]))
+        shapes.append((n, m))
+    if all(n == 0 for n, _ in shapes):
+        shapes[0] = (17, shapes[0][1])
+    gdt = str(rng.choice(["bf16", "fp32"]))
+    pdt = gdt if rng.random() < 0.7 else ("fp32" if gdt == "bf16" else "bf16")
+    S = int(rng.choice([1, 2, 4]))
+    N = S * int(rng.choice([1, 2]))
+    ppm = int(rng.choice([2000, 10000, 100000, 250000, 1000000]))
+    kw = dict(offload=bool(rng.random() < 0.8), psub=bool(rng.random() < 0.7), lr=float(rng.choice([1e-3, 1e-4])))
+    if kw["offload"]:
+        kw["cpu_update"] = bool(rng.random() < 0.4)
+        kw["host_stages"] = int(rng.choice([0, 3, 8]))
+    if rng.random() < 0.3:
+        kw["lagged"] = True
+    if rng.random() < 0.3:
+        kw["warmup"] = int(rng.integers(1, 3))
+    return shapes, gdt, pdt, ppm, N, S, kw
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_step_random_configurations(zf, orc, gpu, seed):
+    """Seeded random mixes of the context's options (shapes incl. rows-less and ragged layers,
+    fp32 / bf16 / mixed dtypes, ratios 0.2%..100%, N and S, offload, f1, host staging slots,
+    param_subset, lagged selection, warm-up), each run for three refresh periods: selection,
+    moments, step counts, parameters, compact blocks and accumulators bit-exact."""
+    shapes, gdt, pdt, ppm, N, S, kw = _random_config(seed)
+    steps = kw.get("warmup", 0) + 3 * N + 1
+    _run_stateful(zf, orc, gpu, shapes, gdt, pdt, ppm, N, S, steps, **kw)
