@@ -901,6 +901,8 @@ def _random_config(seed):
     if kw["offload"]:
         kw["cpu_update"] = bool(rng.random() < 0.4)
         kw["host_stages"] = int(rng.choice([0, 3, 8]))
+        kw["devacc"] = bool(rng.random() < 0.25)
+    kw["state_offload"] = bool(rng.random() < 0.15)
     if rng.random() < 0.3:
         kw["lagged"] = True
     if rng.random() < 0.3:
@@ -912,7 +914,8 @@ def _random_config(seed):
 def test_step_random_configurations(zf, orc, gpu, seed):
     """Seeded random mixes of the context's options (shapes incl. rows-less and ragged layers,
     fp32 / bf16 / mixed dtypes, ratios 0.2%..100%, N and S, offload, f1, host staging slots,
-    param_subset, lagged selection, warm-up), each run for three refresh periods: selection,
+    K7 device accumulation, state swap-out, param_subset, lagged selection, warm-up), each
+    run for three refresh periods: selection,
     moments, step counts, parameters, compact blocks and accumulators bit-exact."""
     shapes, gdt, pdt, ppm, N, S, kw = _random_config(seed)
     steps = kw.get("warmup", 0) + 3 * N + 1
