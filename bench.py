@@ -346,12 +346,18 @@ def run_zenflow(args, rank, world):
         sgpu.fill_param(Ps[li], li, row0=row0s[li])
         del sc
     torch.cuda.synchronize()
-    nccl_id, host_ar = None, None
+    host_ar = None
     exch = args.exchange if args.exchange != "auto" else ("host" if args.colocate else "nccl")
-    if world > 1 and exch == "nccl":
-        from paper_2505_12242_b200.dist import broadcast_nccl_id
-        nccl_id = broadcast_nccl_id()
-    elif world > 1 and exch == "host":
+
+    def nccl_id():
+        # a NCCL unique id serves ONE communicator: every context gets a fresh one (rank 0
+        # makes it, torch.distributed broadcasts it; all ranks create contexts in the same order)
+        if world > 1 and exch == "nccl":
+            from paper_2505_12242_b200.dist import broadcast_nccl_id
+            return broadcast_nccl_id()
+        return None
+
+    if world > 1 and exch == "host":
         from paper_2505_12242_b200.dist import gloo_allreduce
         host_ar = gloo_allreduce()
 
@@ -359,7 +365,7 @@ def run_zenflow(args, rank, world):
         ctx = zf.Context([zf.LayerShape(n, m) for n, m in shapes], topk_ratio_ppm=ratio_ppm,
                          refresh_interval=args.refresh, accum_interval=args.refresh,
                          adam=zf.adam_params(lr=args.lr), offload=offload, host_accumulate=offload,
-                         world=world, rank=rank, nccl_id=nccl_id, device=dev, host_allreduce=host_ar, **kw)
+                         world=world, rank=rank, nccl_id=nccl_id(), device=dev, host_allreduce=host_ar, **kw)
         if world > 1 and exch == "peer":
             from paper_2505_12242_b200.dist import open_peer_exchange
             open_peer_exchange(ctx)
@@ -493,7 +499,7 @@ def run_zenflow(args, rank, world):
     def k3_line(ctx_ppm, lr=None, tag="", **kw):
         ctx = make_ctx(ctx_ppm, False, **kw) if lr is None else zf.Context(
             [zf.LayerShape(n, m) for n, m in shapes], topk_ratio_ppm=ctx_ppm, refresh_interval=args.refresh,
-            accum_interval=args.refresh, adam=zf.adam_params(lr=lr), world=world, rank=rank, nccl_id=nccl_id,
+            accum_interval=args.refresh, adam=zf.adam_params(lr=lr), world=world, rank=rank, nccl_id=nccl_id(),
             device=dev, host_allreduce=host_ar)
         msx, profx, _ = timed_run(ctx, args.steps, args.warmup, tag)
         idxx = [ctx.selected(li).cpu().numpy() for li in range(nl)]

@@ -267,7 +267,8 @@ typedef struct {
 
 typedef struct zf_ctx zf_ctx;
 
-/* Rank 0 creates the NCCL unique id; the caller broadcasts its 128 bytes. */
+/* Rank 0 creates the NCCL unique id; the caller broadcasts its 128 bytes.  One id per
+ * zf_create: a NCCL unique id bootstraps exactly one communicator. */
 zf_status zf_nccl_unique_id(void* out128 /* [host] 128 bytes */);
 
 /* Create a context on CUDA device `device`.  layers [host] [n_layers].

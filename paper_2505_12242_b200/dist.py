@@ -30,6 +30,9 @@ def shard_rows(n: int, world: int, rank: int) -> tuple[int, int]:
 
 
 def broadcast_nccl_id(group=None) -> bytes:
+    """A fresh NCCL unique id from rank 0, broadcast to the group.  Call it once per
+    ``zf.Context`` (an id bootstraps exactly one communicator), on every rank in the same
+    order."""
     import torch.distributed as dist
     from . import zf
     obj = [zf.zf_nccl_unique_id() if dist.get_rank(group) == 0 else None]

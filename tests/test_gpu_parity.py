@@ -348,6 +348,18 @@ def test_refresh_groups_argument_errors(zf):
                    refresh_group_mb=8, lagged_selection=True)
 
 
+def test_nccl_one_rank_contexts_in_sequence(zf, orc, gpu):
+    """Several contexts one after another, each with its own NCCL id (an id bootstraps one
+    communicator; bench.py makes a fresh one per context), each bit-exact."""
+    real = zf.Context
+    try:
+        zf.Context = lambda *a, **kw: real(*a, nccl_id=zf.zf_nccl_unique_id(), **kw)
+        for _ in range(3):
+            _run_stateful(zf, orc, gpu, [(64, 512)], "bf16", "bf16", 100000, 2, 2, 3, offload=False)
+    finally:
+        zf.Context = real
+
+
 @pytest.mark.parametrize("host_stages", [2, 4])
 def test_step_x1_many_chunks(zf, orc, gpu, monkeypatch, host_stages):
     """X1 with 16-KB chunks (ZF_X1_CHUNK_KB): many chunks, each gated by its own K3
