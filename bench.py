@@ -413,7 +413,9 @@ def run_zenflow(args, rank, world):
     mine = {"rank": rank, "device": dev, "k3_ms": prof["k3_update"][0] / max(1, prof["k3_update"][1]),
             "k3_alg_GBs": algorithmic_bytes(shapes, ks) / (prof["k3_update"][0] / max(1, prof["k3_update"][1]) * 1e-3)
             / 1e9 if prof["k3_update"][1] else None, "ms_per_step": ms_total / args.steps,
-            "elements": sum(n * m for n, m in shapes)}
+            "elements": sum(n * m for n, m in shapes),
+            # the last selection of every layer, hashed: identical on every rank
+            "selection_sha1": __import__("hashlib").sha1(b"".join(i.tobytes() for i in idxs)).hexdigest()[:16]}
     per_rank = [mine]
     if world > 1:
         per_rank = [None] * world
@@ -451,6 +453,7 @@ def run_zenflow(args, rank, world):
                                  "allreduce": (ar_ms / max(1, prof["allreduce"][1])) if world > 1 else None},
         "gpu_launches": launches,
         "per_rank": per_rank if world > 1 else None,
+        "selection_identical_across_ranks": (len({r["selection_sha1"] for r in per_rank}) == 1) if world > 1 else None,
         "clocks": clk,
     }
     if world > 1 and prof["allreduce"][1]:
