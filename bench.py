@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--refresh", type=int, default=4)
     ap.add_argument("--lr", type=float, default=1e-5)
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=24)
+    ap.add_argument("--e2e-steps", type=int, default=48)
     ap.add_argument("--host-stages", type=int, default=0,
                     help="pinned host staging slots for the host-accumulation e2e line (0: 2*S, capped by "
                          "the host memory available)")
