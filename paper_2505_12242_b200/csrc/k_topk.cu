@@ -212,7 +212,10 @@ __global__ void k_build_mask(const int32_t* __restrict__ idx, int64_t k, int64_t
     __syncthreads();
     for (int64_t s = tid; s < k; s += K2_THREADS) {
         const int32_t c = idx[s];
-        if (c < 0 || c >= m || (s > 0 && idx[s - 1] >= c)) { *bad = 1; continue; }
+        if (c < 0 || c >= m || (s > 0 && idx[s - 1] >= c)) {   // skipped, so never out of bounds
+            if (bad) *bad = 1;
+            continue;
+        }
         atomicOr(&mask[c >> 5], 1u << (c & 31));
     }
     __syncthreads();

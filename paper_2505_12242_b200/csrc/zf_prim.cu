@@ -118,17 +118,15 @@ extern "C" zf_status zf_compact_unselected(const void* G, zf_dtype gdt, int64_t 
     const int64_t W = (m + 31) / 32;
     uint32_t* mask = nullptr;
     int32_t* prefix = nullptr;
-    int32_t* bad = nullptr;
     uint16_t* ucol = nullptr;
     ZF_TRY(sc.get(&mask, (W + 8) * sizeof(uint32_t), true));    // padded: K3 stages words in 16-byte groups
     ZF_TRY(sc.get(&prefix, (W + 8) * sizeof(int32_t), true));
     ZF_TRY(sc.get(&ucol, (m - k + 16) * sizeof(uint16_t), true));
-    // k_build_mask skips (and flags here) entries that are out of range or not ascending, so a bad
-    // idx cannot make it write out of bounds; the flag is not read back (zf.h: idx is unchecked)
-    ZF_TRY(sc.get(&bad, sizeof(int32_t), true));
+    // k_build_mask skips entries that are out of range or not ascending, so a bad idx cannot make
+    // it write out of bounds (zf.h: idx is not validated -- that would need a host round trip)
     ZF_TRY(sc.get(&prm.claim, sizeof(uint32_t), true));
     const K3Geom geo = k3_geom(n, m, k, gsz, gsz, false, false);
-    ZF_CUDA(launch_build_mask(idx, k, m, mask, prefix, ucol, geo.seg_cols, gsz, bad, s));
+    ZF_CUDA(launch_build_mask(idx, k, m, mask, prefix, ucol, geo.seg_cols, gsz, nullptr, s));
     L.G = G;
     L.n = n;
     L.m = m;
