@@ -234,12 +234,12 @@ typedef struct {
                                          P:505-508 "cache and reuse selected channel
                                          indices", reading R24): a refresh at regular step
                                          t > 0 selects by the column norms of step t-1's
-                                         gradient, which K1 (and the norm all-reduce when
+                                         gradient, which K1 (and the norm exchange when
                                          world > 1) computes on the library's side stream
-                                         at the end of step t-1 -- the refresh step makes a
-                                         single pass over G, and the norm pass overlaps
-                                         whatever the caller runs next (its forward /
-                                         backward).  The first refresh uses its own step's
+                                         during step t-1 (enqueued with that step's K3, it
+                                         overlaps K3's tail and whatever the caller runs
+                                         next) -- the refresh step makes a single pass
+                                         over G.  The first refresh uses its own step's
                                          gradient.  Contract: the gradient buffers of a
                                          step t with (t+1) % N == 0 must stay valid until
                                          the next zf_step or zf_sync (e.g. double-buffered
