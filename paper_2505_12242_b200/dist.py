@@ -15,7 +15,11 @@
   n_local elements).
 * ``broadcast_nccl_id`` -- rank 0 creates the 128-byte NCCL unique id through the
   C-ABI (``zf_nccl_unique_id``) and ``torch.distributed`` broadcasts it; every rank
-  then passes it to ``zf_create`` (the norm all-reduce runs inside ``zf_step``).
+  then passes it to ``zf_create`` (the norm all-reduce runs inside ``zf_step``).  One id
+  per context.
+* ``gloo_allreduce`` -- the host all-reduce callback (ranks without NCCL, e.g. sharing a GPU).
+* ``open_peer_exchange`` -- the peer-memory exchange (f4 iii): all-gather the ranks' IPC
+  handles, map them (``zf_peer_open``).
 """
 from __future__ import annotations
 
