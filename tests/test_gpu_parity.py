@@ -914,6 +914,10 @@ def _random_config(seed):
         kw["cpu_update"] = bool(rng.random() < 0.4)
         kw["host_stages"] = int(rng.choice([0, 3, 8]))
         kw["devacc"] = bool(rng.random() < 0.25)
+        if kw["cpu_update"] and rng.random() < 0.5:
+            kw["cpu_async"] = True
+        if rng.random() < 0.2:
+            kw["side_stream"] = True
     kw["state_offload"] = bool(rng.random() < 0.15)
     if rng.random() < 0.3:
         kw["lagged"] = True
@@ -922,11 +926,12 @@ def _random_config(seed):
     return shapes, gdt, pdt, ppm, N, S, kw
 
 
-@pytest.mark.parametrize("seed", range(40))
+@pytest.mark.parametrize("seed", range(60))
 def test_step_random_configurations(zf, orc, gpu, seed):
     """Seeded random mixes of the context's options (shapes incl. rows-less and ragged layers,
     fp32 / bf16 / mixed dtypes, ratios 0.2%..100%, N and S, offload, f1, host staging slots,
-    K7 device accumulation, state swap-out, param_subset, lagged selection, warm-up), each
+    K7 device accumulation, state swap-out, overlapped f1, a caller side stream, param_subset,
+    lagged selection, warm-up), each
     run for three refresh periods: selection,
     moments, step counts, parameters, compact blocks and accumulators bit-exact."""
     shapes, gdt, pdt, ppm, N, S, kw = _random_config(seed)
