@@ -143,3 +143,31 @@ def test_product_does_not_import_oracle():
         if f.endswith((".py", ".cpp")):
             txt = open(os.path.join(ROOT, "oracle", f)).read()
             assert "import paper_2505_12242_b200" not in txt and "zf_internal" not in txt and "zf.h" not in txt
+
+
+def test_struct_layouts_match_the_header(zf, tmp_path):
+    """The ctypes mirrors of zf_config / zf_adam_params / zf_layer_desc have the header's field
+    order, offsets and sizes (a silent mismatch would misconfigure every context): a small C
+    program including include/zf.h prints offsetof / sizeof for each field."""
+    import shutil
+    import subprocess
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    structs = {"zf_config": zf.Config, "zf_adam_params": zf.AdamParams, "zf_layer_desc": zf.LayerDesc}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "zf.h"', "int main(void) {"]
+    for cname, cls in structs.items():
+        lines.append(f'  printf("{cname} size %zu\\n", sizeof({cname}));')
+        for fname, _t in cls._fields_:
+            lines.append(f'  printf("{cname}.{fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines.append("  return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run([cc, "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = dict(l.rsplit(" ", 1) for l in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                          check=True).stdout.splitlines())
+    for cname, cls in structs.items():
+        assert int(got[f"{cname} size"]) == ctypes.sizeof(cls), cname
+        for fname, _t in cls._fields_:
+            assert int(got[f"{cname}.{fname}"]) == getattr(cls, fname).offset, (cname, fname)
