@@ -26,8 +26,9 @@
 //    sources, the unselected-column list) is not staged: every unit of a layer reads the
 //    same arrays, so the consumers read them through L1 and the arenas carry only data
 //    (more bytes in flight per SM).  Waits are hardware-suspended (mbarrier.try_wait).
-//  - consumers: slot-major AdamW (a slot's column and bias corrections read once for all
-//    its rows; explicit round-to-nearest intrinsics in the oracle's op order), each
+//  - consumers: AdamW over the unit's (row, slot) pairs taken row-major (a warp's lanes hold
+//    consecutive slots of one row: conflict-free slab reads, coalesced moment stores;
+//    explicit round-to-nearest intrinsics in the oracle's op order; adam_unit_b), each
 //    changed p value stored straight to HBM; then compaction by gather (8 bf16 outputs per
 //    thread per vector store, coalesced across the warp).
 //  - with offload, a unit's producer bumps its layer chunk's completion counter once the
@@ -707,9 +708,9 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
 
     // ===================== consumer warps =====================
     // Two groups of K3_GW warps; group g consumes stages g, g+2, ...  Per unit:
-    //  (1) AdamW on the unit's (row, slot) pairs by all threads of the group, slot-major
-    //      (a slot's column and bias corrections read once for all its rows); each changed p
-    //      value is stored straight to HBM;
+    //  (1) AdamW on the unit's (row, slot) pairs by all threads of the group, row-major
+    //      (adam_unit_b; the slot-major adam_unit serves the unstaged-moment paths and the
+    //      ZF_K3_SLOTMAJOR build); each changed p value is stored straight to HBM;
     //  (2) compaction by gather, warp-wide windows of one row: lane l writes outputs
     //      8l..8l+7 (bf16; 4 for fp32) of the window with one 16-byte store, reading the
     //      staged tile at the unselected-column offsets (the layer's list, through L1);
