@@ -40,6 +40,18 @@ def test_bf16_round_matches_torch(orc):
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
 
 
+def test_bf16_nan_with_low_payload_stays_nan(orc):
+    """A NaN whose payload sits only in the 16 dropped bits must stay a NaN in bf16 (torch's
+    cast gives a NaN too), not collapse to the infinity that plain truncation of 0x7f800001
+    gives -- the non-finite check (R15) relies on it.  Sign and payload are not compared:
+    torch returns one canonical NaN."""
+    for bits in (0x7F800001, 0xFF800001, 0x7F80FFFF, 0x7FC00000):
+        x = np.array([bits], np.uint32).view(np.float32)
+        want = orc.bf16_bits_to_f32(_bf16(x))
+        got = orc.to_bf16(x)
+        assert np.isnan(orc.bf16_bits_to_f32(got)).all() and np.isnan(want).all(), hex(bits)
+
+
 # ------------------------------------------------------------------ O2  k
 def test_k_closed_form_table(orc):
     for m, k10, k1 in _golden("k_table.json")["rows"]:
@@ -109,11 +121,52 @@ def test_norms_shard_sum(orc):
         assert np.allclose(sum(parts), whole, rtol=1e-12, atol=0)
 
 
+def test_strided_rows_read_only_the_first_m_columns(orc):
+    """Row i of G / p starts at i*ld (SURVEY §8(b) layout, ld >= m): the C oracle called on a
+    padded buffer gives the norms (against numpy's float64 sum of squares), the compaction
+    and the AdamW results of the dense [n, m] matrix, and never touches the padding."""
+    import ctypes
+    rng = np.random.default_rng(7)
+    n, m, ld = 9, 13, 21
+    Gp = np.full((n, ld), 1.0e3, np.float32)
+    Gp[:, :m] = rng.standard_normal((n, m)).astype(np.float32)
+    G = np.ascontiguousarray(Gp[:, :m])
+    L = orc.lib()
+    vp = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    norms = np.empty(m, np.float32)
+    assert L.oracle_column_norms(vp(Gp), orc.F32, n, m, ld, vp(norms)) == 0
+    want = (G.astype(np.float64) ** 2).sum(axis=0).astype(np.float32)
+    assert np.array_equal(norms, want)
+    idx = np.array([1, 4, 12], np.int32)
+    out = np.empty((n, m - 3), np.float32)
+    L.oracle_compact(vp(Gp), orc.F32, n, m, ld, vp(idx), 3, vp(out))
+    assert np.array_equal(out, np.delete(G, idx, axis=1))
+    Pp = np.full((n, ld), -7.0, np.float32)
+    Pp[:, :m] = rng.standard_normal((n, m)).astype(np.float32)
+    P = np.ascontiguousarray(Pp[:, :m])
+    M1, V1, s1 = np.zeros((n, 3), np.float32), np.zeros((n, 3), np.float32), np.zeros(3, np.int32)
+    M2, V2, s2 = M1.copy(), V1.copy(), s1.copy()
+    L.oracle_selective_adamw(vp(Pp), orc.F32, ld, vp(Gp), orc.F32, ld, n, vp(idx), 3, vp(M1), vp(V1), vp(s1),
+                             1e-3, 0.9, 0.999, 1e-8, 0.0, 1)
+    orc.selective_adamw(P, G, idx, M2, V2, s2, orc.AdamHP())
+    assert np.array_equal(Pp[:, :m], P) and np.array_equal(M1, M2) and np.array_equal(V1, V2)
+    assert np.all(Pp[:, m:] == -7.0)
+
+
 def test_norms_reject_nonfinite(orc):
     G = np.ones((4, 4), np.float32)
     G[2, 1] = np.nan
     with pytest.raises(FloatingPointError):
         orc.column_norms(G)
+
+
+def test_topk_rejects_nonfinite_norms(orc):
+    """SPEC S:44 / S:108 reject non-finite input (reading R15): a NaN or infinite norm is an
+    error, not a column that wins (inf) or loses (NaN) the ranking."""
+    for bad in (np.nan, np.inf):
+        norms = np.array([1.0, bad, 0.5, 2.0], np.float32)
+        with pytest.raises(FloatingPointError):
+            orc.topk(norms, 2)
 
 
 # ------------------------------------------------------------------ O3  top-k
@@ -434,6 +487,8 @@ def test_window_double_buffer(orc):
     assert np.array_equal(layer.acc[0], outs[0] + outs[1])
     assert np.array_equal(layer.acc[1], outs[2] + outs[3])
     assert layer.sealed(3) is layer.acc[1] and layer.sealed(1) is layer.acc[0]
+    assert layer.sealed(2) is layer.acc[0]      # mid-window: the last SEALED window, not the active one
+    assert layer.sealed(0) is None              # nothing sealed before the first window ends
 
 
 def test_accumulate_S1_is_the_compact_gradient(orc):
@@ -521,6 +576,55 @@ def test_f1_migration_takes_current_value(orc):
     G2[:, 5] = 7.0                                     # window 1: column 5 on the GPU, 2 back on the CPU
     L.step(2, G2, P)
     assert np.array_equal(L.master[:, 2], p2) and L.th[2] == 0 and np.all(L.Mh[:, 2] == 0)
+
+
+def test_f1_reentering_column_restarts_from_the_step1_closed_form(orc):
+    """Reading R18 on whole windows: column 5 is CPU-updated in window 0 (g = +0.25), moves to
+    the GPU in window 1, and re-enters the CPU set in window 2 with g = -0.25.  It re-enters
+    with zero host moments and step count, so its window-2 flush is the bias-corrected step-1
+    move -lr*g/(|g|+eps) = +lr (to 4e-8), and its host step count is 1.  Keeping window 0's
+    moments or count would give a different move (+0.05 lr, +0.07 lr or +0.74 lr)."""
+    n, m, lr = 3, 8, 1e-3
+    L = orc.OracleLayer(n=n, m=m, ratio_ppm=125000, refresh_interval=2, accum_interval=2, cpu_update=True,
+                        hp=orc.AdamHP(lr=lr))
+    P = np.zeros((n, m), np.float32)
+
+    def G(spike, g5):
+        x = np.full((n, m), 0.25, np.float32)
+        x[:, 5] = g5
+        x[:, spike] = 7.0
+        return x
+
+    for t, (spike, g5) in enumerate([(2, 0.25), (2, 0.25), (5, 0.0), (5, 0.0)]):
+        L.step(t, G(spike, g5), P)
+    assert L.idx.tolist() == [5]
+    before = P[:, 5].copy()
+    L.step(4, G(2, -0.25), P)
+    assert np.array_equal(P[:, 5], before)              # mid-window: unchanged
+    L.step(5, G(2, -0.25), P)
+    assert L.idx.tolist() == [2] and L.th[5] == 1
+    assert np.allclose(P[:, 5] - before, _step1_move(-0.25, lr=lr), rtol=1e-5, atol=0)
+    assert np.array_equal(L.Mh[:, 5], np.full(n, np.float32(0.1) * np.float32(-0.25), np.float32))
+
+
+def test_f1_flush_leaves_the_selected_columns_alone_bf16(orc):
+    """bf16 parameters: a window flush writes only theta^(c) (the unselected columns); the
+    selected column keeps the GPU-side AdamW result (two step-1-shaped moves of -lr*g/(|g|+eps)
+    on a constant g, each rounded to bf16), not a value from the host master."""
+    n, m, lr = 3, 8, 2.0 ** -7
+    L = orc.OracleLayer(n=n, m=m, ratio_ppm=125000, refresh_interval=2, accum_interval=2, cpu_update=True,
+                        hp=orc.AdamHP(lr=lr))
+    P = _bf16(np.full((n, m), 0.5, np.float32))
+    G = np.full((n, m), 0.25, np.float32)
+    G[:, 3] = 4.0
+    L.step(0, G, P)
+    L.step(1, G, P)
+    assert L.idx.tolist() == [3]
+    sel = orc.bf16_bits_to_f32(P[:, 3])
+    want = orc.bf16_round(orc.bf16_round(0.5 + _step1_move(4.0, lr=lr)) + _step1_move(4.0, lr=lr))
+    assert np.all(sel == np.float32(want)) and want < 0.5
+    cpu = orc.bf16_bits_to_f32(P[:, [0, 1, 2, 4, 5, 6, 7]])
+    assert np.all(cpu == np.float32(orc.bf16_round(0.5 + _step1_move(0.25, lr=lr))))
 
 
 # ------------------------------------------------------------------ f2: warm-up (reading R20)
