@@ -45,7 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                      "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nccl, "include")]
     # a change of compile flags (e.g. ZF_NVCC_EXTRA experiments) forces a rebuild
     stamp = os.path.join(BUILD, "flags.txt")
-    flags = " ".join(common)
+    flags = " ".join(common).replace(ROOT, "<root>")   # a copy of the tree reuses its objects
     if not os.path.exists(stamp) or open(stamp).read() != flags:
         force = True
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
