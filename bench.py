@@ -592,8 +592,13 @@ def run_zenflow(args, rank, world):
                                     "lagged_ms_per_step": lag_ms, "steps": Kp,
                                     "backward": "3 x bf16 GEMM 8192^3 on the caller's stream before every zf_step; "
                                                 "gradient buffers alternate (the lagged K1 reads the other one)"},
-            "note": "device ms/step of the zf_step loop alone is unchanged by the lag (K1 still runs once per N "
-                    "steps); the proxy shows it moving off the optimizer's critical path"}
+            "delta_loop_ms_per_step": msl / args.steps - ms_per_step,
+            "delta_proxy_ms_per_step": lag_ms - plain_ms,
+            "note": "same work per N steps (one K1 per refresh either way).  zf_step loop alone: the lagged K1 runs "
+                    "on the library's side stream next to the pre-refresh step's K3 and fills its tail "
+                    "(delta_loop_ms_per_step < 0 means faster).  Training-loop proxy: a full-occupancy GEMM "
+                    "backward leaves the side-stream K1 no SMs, so the norm pass is not hidden there "
+                    "(delta_proxy_ms_per_step ~ 0)"}
 
     # ---- f3 state swap-out: moments in mapped pinned host memory (extra field)
     if args.also_state_offload:
