@@ -4,6 +4,8 @@ and compaction bit-exact (boundary swaps allowed only within the norm tolerance,
 reading R3), norms within rel 1e-5, fp32 params/moments within rel 1e-6 and bf16
 params within 1 ulp -- the kernels follow the oracle's op order, so the update
 is also checked bit for bit."""
+import math
+
 import numpy as np
 import pytest
 import torch
@@ -144,6 +146,85 @@ def test_selective_adam_bitexact(zf, orc, gpu, n, m, gdt, pdt, wd, dec, ldp):
     if ldp:  # padding columns untouched
         pad = to_np(Pbuf[:, m:])
         assert np.array_equal(pad, to_np(Pbuf[:, m:]))
+
+
+def _table_end(f):
+    """First t >= 1 at which the fp32 bias-correction term f(t) (computed in double, rounded
+    once) reaches its limit -- where the library's tables stop (the limit is used beyond)."""
+    lim = np.float32(f(10 ** 9))
+    t = 1
+    while np.float32(f(t)) != lim:
+        t += 1
+    return t
+
+
+def _ends(lr, b1, b2):
+    return (_table_end(lambda t: lr / (1.0 - b1 ** t)), _table_end(lambda t: math.sqrt(1.0 - b2 ** t)))
+
+
+@pytest.mark.parametrize("pdt", ["bf16", "fp32"])
+def test_selective_adam_step_counts_past_the_tables(zf, orc, gpu, pdt):
+    """Stateless AdamW at step counts straddling the ends of the bias-correction tables
+    (ss = lr/(1-b1^t) reaches f32(lr) at t ~ 160, bc2s = sqrt(1-b2^t) reaches 1.0 at
+    t ~ 1.7k for b2 = 0.99) and far beyond (2^20, 2^30): bit-exact vs the oracle, which
+    evaluates both terms in double at every t (O6)."""
+    n, m, lr, b1, b2 = 8, 4096, 1e-3, 0.9, 0.99
+    e1, e2 = _ends(lr, b1, b2)
+    cand = [0, 1, 2, e1 - 2, e1 - 1, e1, e1 + 1, e2 - 3, e2 - 2, e2 - 1, e2, e2 + 1, 5 * e2, 1 << 20, 1 << 30]
+    k = len(cand) * 8
+    rng = np.random.default_rng(17)
+    st0 = np.array([cand[i % len(cand)] for i in range(k)], np.int32)
+    idx_np = np.sort(rng.choice(m, k, replace=False)).astype(np.int32)
+    G = _grad(gpu, n, m, "bf16", layer=3)
+    P = torch.empty(n, m, dtype=TDT[pdt], device="cuda")
+    gpu.fill_param(P, 3)
+    M0 = (rng.standard_normal((n, k)) * 1e-3).astype(np.float32)
+    V0 = (rng.random((n, k)) * 1e-6).astype(np.float32)
+    hp = orc.AdamHP(lr=lr, beta1=b1, beta2=b2)
+    Pn, Gn = np.ascontiguousarray(to_np(P)), np.ascontiguousarray(to_np(G))
+    M1, V1, st1 = M0.copy(), V0.copy(), st0.copy()
+    orc.selective_adamw(Pn, Gn, idx_np, M1, V1, st1, hp)
+    Md, Vd, sd = from_np(M0), from_np(V0), from_np(st0)
+    zf.zf_selective_adam(P, G, from_np(idx_np), Md, Vd, sd, zf.adam_params(lr=lr, beta1=b1, beta2=b2))
+    torch.cuda.synchronize()
+    assert_bits_equal(to_np(sd), st1, "steps")
+    assert_bits_equal(to_np(Md), M1, "exp_avg")
+    assert_bits_equal(to_np(Vd), V1, "exp_avg_sq")
+    assert_bits_equal(np.ascontiguousarray(to_np(P)), Pn, "params")
+
+
+def test_step_runs_past_the_bias_correction_tables(zf, orc, gpu):
+    """zf_step (K3 with its per-slot {ss, bc2s} prologue) for more steps than the longer
+    bias-correction table holds (b2 = 0.99: ~1.7k), one refresh at t = 0 and a fixed
+    selection after it: parameters, moments and step counts bit-exact with the oracle at
+    checkpoints on both sides of the table ends."""
+    n, m, lr, b1, b2 = 16, 256, 1e-3, 0.9, 0.99
+    e1, e2 = _ends(lr, b1, b2)
+    T = e2 + 24
+    N = 1 << 20
+    ctx = zf.Context([zf.LayerShape(n, m)], topk_ratio_ppm=100000, refresh_interval=N, accum_interval=N,
+                     adam=zf.adam_params(lr=lr, beta1=b1, beta2=b2))
+    L = orc.OracleLayer(n=n, m=m, ratio_ppm=100000, refresh_interval=N, accum_interval=N,
+                        hp=orc.AdamHP(lr=lr, beta1=b1, beta2=b2))
+    Gs = [_grad(gpu, n, m, "bf16", layer=5, step=j) for j in range(7)]     # cycled
+    Gn = [np.ascontiguousarray(to_np(g)) for g in Gs]
+    P = torch.empty(n, m, dtype=torch.bfloat16, device="cuda")
+    gpu.fill_param(P, 5)
+    Po = np.ascontiguousarray(to_np(P))
+    checks = {e1 - 1, e1 + 1, e2 - 2, e2, e2 + 1, T - 1}
+    for t in range(T):
+        ctx.step(t, [Gs[t % 7]], [P])
+        L.step(t, Gn[t % 7], Po)
+        if t in checks:
+            torch.cuda.synchronize()
+            Md, Vd, sd = ctx.optimizer_state(0)
+            assert np.array_equal(to_np(ctx.selected(0)), L.idx), t
+            assert_bits_equal(to_np(sd), L.steps, f"steps t={t}")
+            assert_bits_equal(to_np(Md), L.M, f"exp_avg t={t}")
+            assert_bits_equal(to_np(Vd), L.V, f"exp_avg_sq t={t}")
+            assert_bits_equal(np.ascontiguousarray(to_np(P)), Po, f"params t={t}")
+    assert int(L.steps.max()) == T > e2
+    ctx.close()
 
 
 # ------------------------------------------------------------------ K3 compaction (standalone)
