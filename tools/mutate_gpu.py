@@ -15,9 +15,9 @@ import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CS = "paper_2505_12242_b200/csrc/"
-NORMS, TOPK, UPD, INT, ACC, HOST, SCAT, DRV, AUTO = (CS + f for f in (
+NORMS, TOPK, UPD, INT, ACC, HOST, SCAT, DRV, AUTO, PEER, ADAM = (CS + f for f in (
     "k_norms.cu", "k_topk.cu", "k_update.cu", "zf_internal.cuh", "k_accum.cu", "zf_host.cu", "k_scatter.cu",
-    "zf_driver.cu", "k_auto.cu"))
+    "zf_driver.cu", "k_auto.cu", "k_peer.cu", "k_adam.cu"))
 
 # (name, file, [(old, new, occurrence)])  occurrence: 0-based index of `old` to replace
 MUTANTS = [
@@ -56,6 +56,21 @@ MUTANTS = [
     ("driver refresh every step", DRV, [("const bool refresh = (t % N) == 0;", "const bool refresh = true;", 0)]),
     ("driver window end off by one", DRV, [("bool end = (t + 1) % c->cfg.accum_interval == 0;", "bool end = t % c->cfg.accum_interval == 0;", 0)]),
     ("K6 gamma ignored", AUTO, [("(st.A > 0.0 && st.A >= gamma * i)", "(st.A > 0.0 && st.A >= i)", 0)]),
+    # batch 2: exchange, non-finite detection, dense AdamW, Zen-auto / K7 state, f1 gather, lag ordering
+    ("peer reduce drops the last rank", PEER, [("for (int q = 1; q < a.world; ++q) s = __fadd_rn", "for (int q = 1; q + 1 < a.world; ++q) s = __fadd_rn", 0)]),
+    ("peer gather skips rank 0's slice", PEER, [("for (int q = 0; q < a.world; ++q) {\n        const int64_t j0 = a.M * q / a.world", "for (int q = 1; q < a.world; ++q) {\n        const int64_t j0 = a.M * q / a.world", 0)]),
+    ("lagged refresh does not wait for the side-stream norms", DRV, [("if (c->lag_pending) ZF_CUDA(cudaStreamWaitEvent(s, c->norm_ready, 0));", "(void)0;", 0)]),
+    ("K1 non-finite flag dropped", NORMS, [("if (!isfinite(s) && nonfinite) *nonfinite = 1;", "(void)s;", 0), ("if (!isfinite(s) && nonfinite) *nonfinite = 1;", "(void)s;", 0)]),
+    ("K3 AdamW non-finite check dropped", UPD, [("if constexpr (GE::SIZE == 2) nfacc |= ((uint32_t)gb[j] & 0x7f80u) + 0x0080u;", "if constexpr (GE::SIZE == 2) (void)0;", 0)]),
+    ("K3 compaction non-finite check dropped", UPD, [("nf2 = __hmax2_nan(nf2, __hmax2_nan(__habs2(*reinterpret_cast<const __nv_bfloat162*>(&o.x)),", "(void)__hmax2_nan(nf2, __hmax2_nan(__habs2(*reinterpret_cast<const __nv_bfloat162*>(&o.x)),", 0),
+                                                    ("nf2 = __hmax2_nan(nf2, __hmax2_nan(__habs2(*reinterpret_cast<const __nv_bfloat162*>(&o.z)),", "(void)__hmax2_nan(nf2, __hmax2_nan(__habs2(*reinterpret_cast<const __nv_bfloat162*>(&o.z)),", 0)]),
+    ("dense AdamW remap entering moment 1e-3", ADAM, [("m = src >= 0 ? L.m_in[row * L.k_in + src] : 0.0f;", "m = src >= 0 ? L.m_in[row * L.k_in + src] : 1.0e-3f;", 0),
+                                                      ("m[j] = src >= 0 ? __ldcs(L.m_in + (int64_t)row * L.k_in + src) : 0.0f;", "m[j] = src >= 0 ? __ldcs(L.m_in + (int64_t)row * L.k_in + src) : 1.0e-3f;", 0)]),
+    ("dense AdamW range-miss fallback skipped", ADAM, [("    if (!ok) {\n#pragma unroll\n        for (int j = 0; j < V; ++j) {", "    if (false) {\n#pragma unroll\n        for (int j = 0; j < V; ++j) {", 0)]),
+    ("K6 smax off by one", AUTO, [("st.len >= smax", "st.len > smax", 0)]),
+    ("K7 Zen-auto buffer parity", ACC, [("buf = (int)(st->win & 1);", "buf = (int)((st->win + 1) & 1);", 0)]),
+    ("f1 refresh gather column shifted", SCAT, [("buf[q] = P[i * ldp + __ldg(cols + e)];", "buf[q] = P[i * ldp + __ldg(cols + (e > 0 ? e - 1 : e))];", 0)]),
+
 ]
 
 
