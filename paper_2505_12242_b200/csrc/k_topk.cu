@@ -238,7 +238,24 @@ __global__ void k_add_const(const int32_t* __restrict__ src, int32_t* dst, int64
         dst[s] = src[s] + delta;
 }
 
+// Test knob (ZF_TEST_LAG_DELAY_US): holds its stream for `us` microseconds of global time, so
+// a parity test can make the lagged side-stream K1 finish late and check the refresh waits.
+__global__ void k_spin(uint64_t ns) {
+    uint64_t t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+        __nanosleep(1000);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (t - t0 < ns);
+}
+
 }  // namespace
+
+cudaError_t launch_spin(int32_t us, cudaStream_t s) {
+    if (us <= 0) return cudaSuccess;
+    k_spin<<<1, 1, 0, s>>>((uint64_t)us * 1000ull);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_add_const(const int32_t* src, int32_t* dst, int64_t k, int32_t delta, cudaStream_t s) {
     if (k <= 0) return cudaSuccess;

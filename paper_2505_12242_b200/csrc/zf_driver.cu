@@ -479,6 +479,7 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
     ZF_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
     c->lagged = cfg->lagged_selection != 0;
     if (c->lagged) {
+        c->lag_delay_us = getenv("ZF_TEST_LAG_DELAY_US") ? atoi(getenv("ZF_TEST_LAG_DELAY_US")) : 0;
         ZF_CUDA(cudaStreamCreateWithFlags(&c->lag_stream, cudaStreamNonBlocking));
         ZF_CUDA(cudaEventCreateWithFlags(&c->lag_in, cudaEventDisableTiming));
         ZF_CUDA(cudaEventCreateWithFlags(&c->norm_ready, cudaEventDisableTiming));
@@ -868,6 +869,7 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
         Table<NormLayer> tn{};
         tn.dev = c->d_norm_tab;
         tn.n = nl;
+        if (c->lag_delay_us > 0) ZF_CUDA(launch_spin(c->lag_delay_us, c->lag_stream));   // test knob
         ZF_TRY(c->prof_begin(0, c->lag_stream, &pe));
         ZF_CUDA(launch_norms(tn, c->k1_units, c->gdt, c->nonfinite_d, c->lag_stream));
         ZF_TRY(c->prof_end(&pe, c->lag_stream));

@@ -617,6 +617,7 @@ struct zf_ctx {
     cudaStream_t lag_stream = nullptr;
     cudaEvent_t lag_in = nullptr, norm_ready = nullptr;
     bool lag_pending = false;     // a lagged K1 was enqueued and not yet waited for
+    int32_t lag_delay_us = 0;     // test knob ZF_TEST_LAG_DELAY_US: delay before the lagged K1
     int numa_node = -1;           // NUMA node of the GPU (-1: not reported)
     std::vector<int> numa_cpus;   // its CPUs: host threads and first-touch allocations run there
     int64_t total_rows = 0;       // K3b chunks over all layers

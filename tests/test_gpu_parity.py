@@ -699,6 +699,63 @@ def test_step_nonfinite_reported(zf, gpu):
     ctx.close()
 
 
+@pytest.mark.parametrize("dt", ["bf16", "fp32"])
+@pytest.mark.parametrize("where", ["selected", "unselected"])
+@pytest.mark.parametrize("bad", [float("inf"), float("nan")])
+def test_step_nonfinite_on_a_steady_step(zf, gpu, dt, where, bad):
+    """Steady steps run no K1: a non-finite gradient must be caught by K3 itself -- by its
+    AdamW (a selected column) or by its compaction (an unselected one) -- and reported by
+    zf_sync as ZF_ENONFINITE (SPEC S:44 / S:266, reading R15)."""
+    n, m = 64, 512
+    ctx = zf.Context([zf.LayerShape(n, m)], grad_dtype=TDT[dt], param_dtype=TDT[dt], topk_ratio_ppm=100000,
+                     refresh_interval=4, accum_interval=4)
+    G = _grad(gpu, n, m, dt)
+    P = torch.zeros(n, m, dtype=TDT[dt], device="cuda")
+    ctx.step(0, [G], [P])
+    ctx.sync()
+    sel = set(to_np(ctx.selected(0)).tolist())
+    col = sorted(sel)[3] if where == "selected" else next(j for j in range(m) if j not in sel)
+    G2 = G.clone()
+    G2[7, col] = bad
+    ctx.step(1, [G2], [P])
+    with pytest.raises(zf.ZFError) as e:
+        ctx.sync()
+    assert e.value.status == zf.ZF_ENONFINITE
+    ctx.close()
+
+
+def test_lagged_refresh_waits_for_the_side_stream_norms(zf, orc, monkeypatch):
+    """f4 (ii): the refresh step must wait for the previous step's side-stream K1.  The test
+    knob ZF_TEST_LAG_DELAY_US holds the side stream 50 ms before every lagged K1, the steps
+    are enqueued back to back without zf_sync (gradients resident, as the contract asks), and
+    every step's gradient ranks different columns first; selection, parameters and moments
+    after six steps (refreshes at 0, 2, 4) must equal the oracle's."""
+    monkeypatch.setenv("ZF_TEST_LAG_DELAY_US", "50000")
+    n, m, N, T = 64, 512, 2, 6
+    rng = np.random.default_rng(11)
+    Gh = [(rng.standard_normal((n, m)) * rng.permutation(np.geomspace(1e-3, 1.0, m))[None, :]).astype(np.float32)
+          for _ in range(T)]
+    Gd = [torch.from_numpy(g).cuda() for g in Gh]
+    P = torch.zeros(n, m, device="cuda")
+    Po = np.zeros((n, m), np.float32)
+    ctx = zf.Context([zf.LayerShape(n, m)], grad_dtype=torch.float32, param_dtype=torch.float32,
+                     topk_ratio_ppm=100000, refresh_interval=N, accum_interval=N, lagged_selection=True)
+    L = orc.OracleLayer(n=n, m=m, ratio_ppm=100000, refresh_interval=N, accum_interval=N, lagged=True)
+    torch.cuda.synchronize()
+    for t in range(T):
+        ctx.step(t, [Gd[t]], [P])
+    ctx.sync()
+    for t in range(T):
+        L.step(t, Gh[t], Po)
+    Md, Vd, sd = ctx.optimizer_state(0)
+    assert_bits_equal(to_np(ctx.selected(0)), L.idx, "idx")
+    assert_bits_equal(to_np(sd), L.steps, "steps")
+    assert_bits_equal(to_np(Md), L.M, "exp_avg")
+    assert_bits_equal(to_np(Vd), L.V, "exp_avg_sq")
+    assert_bits_equal(np.ascontiguousarray(to_np(P)), Po, "params")
+    ctx.close()
+
+
 def test_step_state_errors(zf, gpu):
     ctx = zf.Context([zf.LayerShape(8, 64)], refresh_interval=4, accum_interval=4)
     G = _grad(gpu, 8, 64, "bf16")
