@@ -109,3 +109,13 @@ def test_flat_partition_norm_exchange_gloo(tmp_path):
             got = np.load(tmp_path / f"norms_{r}_{li}.npy").astype(np.float64)
             assert np.all(np.abs(got - want) <= 1e-6 * np.abs(want) + 1e-30), li
     assert np.array_equal(np.load(tmp_path / "sel_0.npy"), np.load(tmp_path / "sel_1.npy"))
+
+
+def test_flat_partition_snaps_to_the_nearest_row():
+    """Worked example of the row snapping (module doc of dist.flat_partition): one 10x100
+    matrix over 3 ranks has element boundaries 333 and 666, which snap to the nearest row
+    starts 300 (33 past a row start) and 700 (34 before one): rows [0,3), [3,7), [7,10).
+    Two matrices [(4, 10), (6, 10)] over 2 ranks: boundary 50 = row 1 of the second matrix."""
+    from paper_2505_12242_b200.dist import flat_partition
+    assert [flat_partition([(10, 100)], 3, r) for r in range(3)] == [[(0, 3)], [(3, 7)], [(7, 10)]]
+    assert [flat_partition([(4, 10), (6, 10)], 2, r) for r in range(2)] == [[(0, 4), (0, 1)], [(4, 4), (1, 6)]]

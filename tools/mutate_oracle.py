@@ -120,33 +120,63 @@ MUTANTS = [
 ]
 
 
+# host-side product logic (data-parallel plumbing, byte accounting), run against the whole CPU
+# suite (`-m "not gpu"`): (name, file, old, new)
+DIST, BENCH = "paper_2505_12242_b200/dist.py", "bench.py"
+HOST_MUTANTS = [
+    ("shard_rows remainder to the last ranks", DIST, "return start, start + base + (1 if rank < rem else 0)", "start = rank * base + max(0, rank - (world - rem)); return start, start + base + (1 if rank >= world - rem else 0)"),
+    ("flat_partition snaps every boundary up", DIST, "return offs[lo] + (i + (1 if 2 * o >= m else 0)) * m", "return offs[lo] + (i + (1 if o > 0 else 0)) * m"),
+    ("flat_partition first row floored", DIST, "r0 = min(n, max(0, -(-(a - o) // m)))", "r0 = min(n, max(0, (a - o) // m))"),
+    ("flat_partition last row floored", DIST, "r1 = min(n, max(0, -(-(b - o) // m)))", "r1 = min(n, max(0, (b - o) // m))"),
+    ("segment_map stride = rows", DIST, "out.append((li, sid, base + int(c), m, rows))", "out.append((li, sid, base + int(c), rows, rows))"),
+    ("segment_map base advances by n*m", DIST, "base += rows * m", "base += n * m"),
+    ("gloo all-reduce MAX", DIST, "dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)", "dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)"),
+    ("peer handles in reverse rank order", DIST, "ctx.peer_open(handles)", "ctx.peer_open(handles[::-1])"),
+    ("algorithmic bytes: compact block m wide", BENCH, "tot += n * m * gsz + n * (m - k) * gsz + n * k * (2 * psz + 16)", "tot += n * m * gsz + n * m * gsz + n * k * (2 * psz + 16)"),
+    ("algorithmic bytes: moments read only", BENCH, "tot += n * m * gsz + n * (m - k) * gsz + n * k * (2 * psz + 16)", "tot += n * m * gsz + n * (m - k) * gsz + n * k * (2 * psz + 8)"),
+    ("sector bytes: 64-byte sectors", BENCH, "sectors = len(np.unique((np.asarray(idx, np.int64) * psz) // 32))", "sectors = len(np.unique((np.asarray(idx, np.int64) * psz) // 64))"),
+]
+
 # mutants that cannot change any result on the oracle's valid domain (reported, not counted)
 EQUIVALENT = {
     "O2 no k >= 1 clamp": "for m >= 1 and ppm in [1, 1e6] (the validated domain), ceil(m*ppm/1e6) >= 1 already",
+    "flat_partition first row floored": "the boundaries are snapped to row starts, so (a - o) is a multiple of m "
+                                        "inside the matrix and clamped outside it: floor = ceil",
+    "flat_partition last row floored": "as above for b",
 }
+
+
+def _copy(d, full):
+    """Scratch copy: the whole tree for host mutants (the whole CPU suite runs), else only
+    what the pin suite needs (the oracle rebuilds from source)."""
+    if full:
+        shutil.copytree(ROOT, d, dirs_exist_ok=True,
+                        ignore=shutil.ignore_patterns(".git", "gpurun_out", "__pycache__", "build", "baseline"))
+        return
+    for sub in ("oracle", "tests", "synth"):
+        shutil.copytree(os.path.join(ROOT, sub), os.path.join(d, sub), ignore=shutil.ignore_patterns("*.so", "__pycache__"))
+    shutil.copy(os.path.join(ROOT, "__graft_entry__.py"), d)
+    shutil.copytree(os.path.join(ROOT, "paper_2505_12242_b200"), os.path.join(d, "paper_2505_12242_b200"),
+                    ignore=shutil.ignore_patterns("__pycache__", "build"))
+    so = "synth/libzfsynth_host.so"
+    if os.path.exists(os.path.join(ROOT, so)):
+        shutil.copy(os.path.join(ROOT, so), os.path.join(d, so))
 
 
 def run_one(mut, keep=False):
     name, f, old, new = mut
     d = tempfile.mkdtemp(prefix="zfmut_")
+    host = not f.startswith("oracle/")
     try:
-        for sub in ("oracle", "tests", "synth"):
-            shutil.copytree(os.path.join(ROOT, sub), os.path.join(d, sub),
-                            ignore=shutil.ignore_patterns("*.so", "__pycache__"))
-        for fn in ("__graft_entry__.py",):
-            shutil.copy(os.path.join(ROOT, fn), d)
-        shutil.copytree(os.path.join(ROOT, "paper_2505_12242_b200"), os.path.join(d, "paper_2505_12242_b200"),
-                        ignore=shutil.ignore_patterns("__pycache__", "build"))
-        for so in ("synth/libzfsynth_host.so",):
-            if os.path.exists(os.path.join(ROOT, so)):
-                shutil.copy(os.path.join(ROOT, so), os.path.join(d, so))
+        _copy(d, host)
         p = os.path.join(d, f)
         src = open(p).read()
         if src.count(old) != 1:
             return name, "BAD-PATTERN", src.count(old)
         open(p, "w").write(src.replace(old, new))
-        r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_oracle_pins.py", "-x", "-q",
-                            "-p", "no:cacheprovider"], cwd=d, capture_output=True, text=True, timeout=900)
+        suite = ["tests", "-m", "not gpu"] if host else ["tests/test_oracle_pins.py"]
+        r = subprocess.run([sys.executable, "-m", "pytest", *suite, "-x", "-q", "-p", "no:cacheprovider"],
+                           cwd=d, capture_output=True, text=True, timeout=900)
         tail = (r.stdout.strip().splitlines() or [""])[-1]
         if r.returncode == 0:
             return name, "SURVIVED", tail
@@ -161,8 +191,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("-j", type=int, default=8)
     ap.add_argument("-k", default="")
+    ap.add_argument("--host", action="store_true", help="the host-side product mutants (CPU suite) instead")
     a = ap.parse_args()
-    muts = [m for m in MUTANTS if a.k in m[0]]
+    muts = [m for m in (HOST_MUTANTS if a.host else MUTANTS) if a.k in m[0]]
     with ThreadPoolExecutor(a.j) as ex:
         res = list(ex.map(run_one, muts))
     res = [(n, "EQUIVALENT" if (s == "SURVIVED" and n in EQUIVALENT) else s, EQUIVALENT.get(n, i)) for n, s, i in res]
@@ -172,8 +203,9 @@ def main():
     killed = sum(1 for r in res if r[1] == "KILLED")
     print(f"{killed}/{len(res) - eq} killed ({eq} equivalent)")
     if not a.k:
-        with open(os.path.join(ROOT, "profiles", "oracle_mutation.json"), "w") as fh:
-            json.dump({"suite": "tests/test_oracle_pins.py", "killed": killed, "non_equivalent": len(res) - eq,
+        name = "host_mutation.json" if a.host else "oracle_mutation.json"
+        with open(os.path.join(ROOT, "profiles", name), "w") as fh:
+            json.dump({"suite": 'tests -m "not gpu"' if a.host else "tests/test_oracle_pins.py", "killed": killed, "non_equivalent": len(res) - eq,
                        "mutants": [{"mutant": n, "result": s, "detail": str(i)} for n, s, i in res]}, fh, indent=1)
 
 
