@@ -71,6 +71,13 @@ MUTANTS = [
     ("K7 Zen-auto buffer parity", ACC, [("buf = (int)(st->win & 1);", "buf = (int)((st->win + 1) & 1);", 0)]),
     ("f1 refresh gather column shifted", SCAT, [("buf[q] = P[i * ldp + __ldg(cols + e)];", "buf[q] = P[i * ldp + __ldg(cols + (e > 0 ? e - 1 : e))];", 0)]),
 
+    # batch 3: launch-table patches, remap step delta, H1 one-step adds, warm-up length, K6 statistic, X1 gate
+    ("k_patch skips the last word", CS + "zf_prim.cu", [("for (int i = threadIdx.x; i < a.n; i += blockDim.x) a.base[a.off[i]] = a.val[i];", "for (int i = threadIdx.x; i + 1 < a.n; i += blockDim.x) a.base[a.off[i]] = a.val[i];", 0)]),
+    ("K2 remap step delta dropped", TOPK, [("L.new_steps[s] = src >= 0 ? __ldg(L.old_steps + src) + old_delta : 0;", "L.new_steps[s] = src >= 0 ? __ldg(L.old_steps + src) : 0;", 0)]),
+    ("H1 one-step add dropped", HOST, [("            acc[i] = acc[i] + x;", "            acc[i] = x;", 0)]),
+    ("warm-up one step longer", DRV, [("if (t0 < tau) return warmup_step(c, t0, grads, params, s);", "if (t0 <= tau) return warmup_step(c, t0, grads, params, s);", 0)]),
+    ("K6 sums squared norms", AUTO, [("const double x = sqrt((double)__ldg(L.norms + j));", "const double x = (double)__ldg(L.norms + j);", 0)]),
+    ("X1 copy gated one unit early", DRV, [("c->done_target[c->L[i].chunk] += (uint32_t)(steady_geo ? c->L[i].geo_s.units : c->L[i].geo.units) *", "c->done_target[c->L[i].chunk] += (uint32_t)((steady_geo ? c->L[i].geo_s.units : c->L[i].geo.units) - 1) *", 0)]),
 ]
 
 
