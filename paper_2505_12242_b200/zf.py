@@ -195,6 +195,10 @@ class _DevView:
 
 def _view(ptr: int, shape, torch_dtype) -> torch.Tensor:
     typestr = {torch.float32: "<f4", torch.int32: "<i4", torch.bfloat16: "<u2"}[torch_dtype]
+    if any(int(d) == 0 for d in shape):
+        # an empty view (a layer with no rows on this rank): its pointer may sit one past the
+        # end of the library's block, which torch refuses to wrap; nothing to alias anyway
+        return torch.empty(tuple(int(d) for d in shape), dtype=torch_dtype, device="cuda")
     t = torch.as_tensor(_DevView(ptr, shape, typestr), device="cuda")
     return t.view(torch.bfloat16) if torch_dtype == torch.bfloat16 else t
 

@@ -462,12 +462,16 @@ def test_step_state_offload(zf, orc, gpu, shapes, gdt, NS, tau, cpu):
                   warmup=tau, state_offload=True)
 
 
+@pytest.mark.parametrize("shapes,offload", [([(0, 512), (37, 1001), (0, 4096), (64, 512), (0, 77)], True),
+                                            ([(33, 300), (0, 777)], True), ([(33, 33), (0, 1025)], False)])
 @pytest.mark.parametrize("cpu", [False, True])
-def test_step_layers_without_rows(zf, orc, gpu, cpu):
+def test_step_layers_without_rows(zf, orc, gpu, shapes, offload, cpu):
     """Flat partitions (row f3): matrices with no rows on this rank (n = 0) ride along --
-    zero norms, the same selection rule, nothing else -- while the others stay bit-exact."""
-    shapes = [(0, 512), (37, 1001), (0, 4096), (64, 512), (0, 77)]
-    _run_stateful(zf, orc, gpu, shapes, "bf16", "bf16", 100000, 2, 2, 5, offload=True, cpu_update=cpu)
+    zero norms, the same selection rule, nothing else -- while the others stay bit-exact.
+    A rows-less LAST layer's empty views sit at the end of the library's blocks (found by the
+    600-seed random soak, `profiles/r02ao_pytest_random600.log`)."""
+    _run_stateful(zf, orc, gpu, shapes, "bf16", "bf16", 100000, 2, 2, 5, offload=offload,
+                  cpu_update=cpu and offload)
 
 
 @pytest.mark.parametrize("shapes,gdt,NS,tau,cpu", [([(256, 512)], "fp32", 2, 0, False),
