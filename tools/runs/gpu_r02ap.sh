@@ -1,0 +1,6 @@
+tag=r02ap
+mkdir -p gpurun_out
+python -m paper_2505_12242_b200._build > gpurun_out/${tag}_build.log 2>&1
+ZF_RANDOM_SEEDS=1000 timeout 3000 python -m pytest tests/test_gpu_parity.py -m gpu -q -k random_configurations > gpurun_out/${tag}_pytest_random1000.log 2>&1; echo "rc=$?" >> gpurun_out/${tag}_pytest_random1000.log
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/${tag}_pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/${tag}_pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${tag}_smoke.log 2>&1
