@@ -1066,8 +1066,13 @@ def _random_config(seed):
         kw["lagged"] = True
     if rng.random() < 0.3:
         kw["warmup"] = int(rng.integers(1, 3))
-    if seed >= 60 and not kw.get("lagged") and rng.random() < 0.15:
-        kw["refresh_group_mb"] = 1     # f4 (i) grouped refresh (seeds past the default 60 only)
+    if seed >= 60:   # soak-only draws (the default 60 seeds keep their configurations)
+        if not kw.get("lagged") and rng.random() < 0.15:
+            kw["refresh_group_mb"] = 1     # f4 (i) grouped refresh
+        if rng.random() < 0.2:
+            kw["poke"] = {int(rng.integers(1, 3 * N))}   # the caller rewrites p (zf_params_changed)
+        if rng.random() < 0.15:            # one larger, ragged layer
+            shapes.append((int(rng.integers(200, 520)), int(rng.integers(2000, 4100))))
     return shapes, gdt, pdt, ppm, N, S, kw
 
 
