@@ -27,7 +27,8 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, steps, N, cpu_update, partition, exchange="host", lagged=False):
+def _worker(rank, world, port, steps, N, cpu_update, partition, exchange="host", lagged=False, shapes=None,
+            ppm=100000, dt="bf16"):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
@@ -43,10 +44,13 @@ def _worker(rank, world, port, steps, N, cpu_update, partition, exchange="host",
     from synth import gpu
 
     torch.cuda.set_device(0)
+    SHAPES = shapes or globals()["SHAPES"]
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float32
     spans = (flat_partition(SHAPES, world, rank) if partition == "flat"
              else [shard_rows(n, world, rank) for n, _ in SHAPES])
     local = [(b - a, m) for (a, b), (_, m) in zip(spans, SHAPES)]
-    ctx = zf.Context([zf.LayerShape(n, m) for n, m in local], topk_ratio_ppm=100000, refresh_interval=N,
+    ctx = zf.Context([zf.LayerShape(n, m) for n, m in local], grad_dtype=tdt, param_dtype=tdt,
+                     topk_ratio_ppm=ppm, refresh_interval=N,
                      accum_interval=N, adam=zf.adam_params(lr=1e-3), offload=True, host_accumulate=True,
                      cpu_update=cpu_update, world=world, rank=rank, lagged_selection=lagged,
                      host_allreduce=gloo_allreduce() if exchange == "host" else None)
@@ -54,13 +58,13 @@ def _worker(rank, world, port, steps, N, cpu_update, partition, exchange="host",
         open_peer_exchange(ctx)   # f4 (iii): the partial norms summed over peer memory
     prevG = None
     scales = [gpu.ColScale(m, li) for li, (_, m) in enumerate(SHAPES)]
-    Gs = [torch.empty(n, m, dtype=torch.bfloat16, device="cuda") for n, m in local]
-    Ps = [torch.empty(n, m, dtype=torch.bfloat16, device="cuda") for n, m in local]
+    Gs = [torch.empty(n, m, dtype=tdt, device="cuda") for n, m in local]
+    Ps = [torch.empty(n, m, dtype=tdt, device="cuda") for n, m in local]
     for li, P in enumerate(Ps):
         gpu.fill_param(P, li, row0=spans[li][0])
-    oracle = [orc.OracleLayer(n=n, m=m, ratio_ppm=100000, refresh_interval=N, accum_interval=N,
+    oracle = [orc.OracleLayer(n=n, m=m, ratio_ppm=ppm, refresh_interval=N, accum_interval=N,
                               hp=orc.AdamHP(lr=1e-3), cpu_update=cpu_update, lagged=lagged) for n, m in SHAPES]
-    Po = [synth.param(n, m, li) for li, (n, m) in enumerate(SHAPES)]
+    Po = [synth.param(n, m, li, dtype=dt) for li, (n, m) in enumerate(SHAPES)]
     for t in range(steps):
         for li in range(len(SHAPES)):
             scales[li].advance_to(t)
@@ -68,7 +72,7 @@ def _worker(rank, world, port, steps, N, cpu_update, partition, exchange="host",
         ctx.step(t, Gs, Ps)
         ctx.sync()
         refresh = t % N == 0
-        Gfulls = [synth.grad(n, m, li, t, synth.col_scale_at(m, t, li)) for li, (n, m) in enumerate(SHAPES)]
+        Gfulls = [synth.grad(n, m, li, t, synth.col_scale_at(m, t, li), dtype=dt) for li, (n, m) in enumerate(SHAPES)]
         for li, ((n, m), (a, b)) in enumerate(zip(SHAPES, spans)):
             L = oracle[li]
             Gfull = Gfulls[li]
@@ -120,6 +124,35 @@ def test_ranks_one_gpu_peer_exchange(world, partition, lagged):
     mp.spawn(_worker, args=(world, _free_port(), 7, 2, False, partition, "peer", lagged), nprocs=world, join=True)
 
 
+def _random_ranks_config(seed):
+    rng = np.random.default_rng(0xD15 + seed)
+    world = int(rng.choice([2, 2, 3, 4]))
+    shapes = [(int(rng.choice([1, 5, 33, 130, 256])), int(rng.choice([33, 257, 512, 1001, 2048])))
+              for _ in range(int(rng.integers(1, 4)))]
+    partition = str(rng.choice(["rows", "flat"]))
+    exchange = str(rng.choice(["host", "peer"]))
+    N = int(rng.choice([1, 2, 4]))
+    ppm = int(rng.choice([10000, 100000, 250000]))
+    dt = str(rng.choice(["bf16", "fp32"]))
+    lagged = bool(rng.random() < 0.3)
+    cpu_update = bool(rng.random() < 0.3)
+    return world, shapes, partition, exchange, N, ppm, dt, lagged, cpu_update
+
+
+# ZF_RANDOM_MR_SEEDS widens the sweep (a soak run; the default suite runs the first 4)
+@pytest.mark.parametrize("seed", range(int(os.environ.get("ZF_RANDOM_MR_SEEDS", "4"))))
+def test_ranks_random_configurations(seed):
+    """Seeded random multi-rank mixes on one GPU: 2-4 ranks, row or flat partitions (incl.
+    ranks with no rows of a matrix), the gloo host exchange or the peer-memory kernels, N,
+    ratio, bf16 / fp32, lagged selection, f1 -- every rank's rows bit-exact vs the oracle on
+    the full matrices and identical selections on all ranks."""
+    world, shapes, partition, exchange, N, ppm, dt, lagged, cpu_update = _random_ranks_config(seed)
+    from paper_2505_12242_b200 import _build
+    _build.build()
+    mp.spawn(_worker, args=(world, _free_port(), 2 * N + 2, N, cpu_update, partition, exchange, lagged, shapes, ppm,
+                            dt), nprocs=world, join=True)
+
+
 AUTO_SHAPES = [(64, 256), (96, 200), (128, 320)]
 
 
@@ -145,7 +178,8 @@ def _worker_auto(rank, world, port, steps, gamma):
     spans = [shard_rows(n, world, rank) for n, _ in AUTO_SHAPES]
     local = [(b - a, m) for (a, b), (_, m) in zip(spans, AUTO_SHAPES)]
     N = 8
-    ctx = zf.Context([zf.LayerShape(n, m) for n, m in local], topk_ratio_ppm=100000, refresh_interval=N,
+    ctx = zf.Context([zf.LayerShape(n, m) for n, m in local], grad_dtype=tdt, param_dtype=tdt,
+                     topk_ratio_ppm=ppm, refresh_interval=N,
                      accum_interval=N, adam=zf.adam_params(lr=1e-3), offload=True, host_accumulate=True,
                      world=world, rank=rank, host_allreduce=gloo_allreduce(), auto_gamma=gamma)
     scales = [gpu.ColScale(m, li) for li, (_, m) in enumerate(AUTO_SHAPES)]
