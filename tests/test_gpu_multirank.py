@@ -181,8 +181,7 @@ def _worker_auto(rank, world, port, steps, gamma):
     spans = [shard_rows(n, world, rank) for n, _ in AUTO_SHAPES]
     local = [(b - a, m) for (a, b), (_, m) in zip(spans, AUTO_SHAPES)]
     N = 8
-    ctx = zf.Context([zf.LayerShape(n, m) for n, m in local], grad_dtype=tdt, param_dtype=tdt,
-                     topk_ratio_ppm=ppm, refresh_interval=N,
+    ctx = zf.Context([zf.LayerShape(n, m) for n, m in local], topk_ratio_ppm=100000, refresh_interval=N,
                      accum_interval=N, adam=zf.adam_params(lr=1e-3), offload=True, host_accumulate=True,
                      world=world, rank=rank, host_allreduce=gloo_allreduce(), auto_gamma=gamma)
     scales = [gpu.ColScale(m, li) for li, (_, m) in enumerate(AUTO_SHAPES)]
