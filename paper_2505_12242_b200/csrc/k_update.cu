@@ -369,7 +369,7 @@ __device__ __forceinline__ void adam_unit(const StageInfo& si, unsigned char* A,
 template <int GDT, int PDT, bool PST, bool REMAP, bool PSUB, int NCT = K3_AWARPS * 32, int NB = ZF_K3_NB>
 __device__ __forceinline__ void adam_unit_b(const StageInfo& si, unsigned char* A, const UpdParams& prm, int ctid,
                                             uint32_t& nfacc) {
-    static_assert(!PSUB || (!REMAP && !PST), "the subset slab is staged on steady steps only");
+    static_assert(!PSUB || !PST, "a unit stages the p tile or a subset slab, not both");
     using GE = Elt<GDT>;
     using PE = Elt<PDT>;
     using GB = typename GE::bits;
@@ -420,7 +420,11 @@ __device__ __forceinline__ void adam_unit_b(const StageInfo& si, unsigned char* 
                 const int row = rr[j];
                 const int cl = cc[j] - c0;
                 gb[j] = sG[row * sw + cl];
-                if constexpr (PSUB) po[j] = sPs[so[j] - s0];
+                if constexpr (PSUB && REMAP) {
+                    // refresh from the previous subset block (mode 3): a retained slot's value from
+                    // its old row (staged like the old moments), an entering slot's from p
+                    po[j] = src[j] >= row * kin ? sPs[src[j]] : gP[pa[j] + c0 + cc[j]];
+                } else if constexpr (PSUB) po[j] = sPs[so[j] - s0];
                 else if constexpr (PST) po[j] = sP[row * sw + cl];
                 else po[j] = pmode == 2 ? gS[so[j]] : gP[pa[j] + c0 + cc[j]];
                 if constexpr (REMAP) {
@@ -445,7 +449,7 @@ __device__ __forceinline__ void adam_unit_b(const StageInfo& si, unsigned char* 
                 const PB pnew = PE::from_f(p);
                 if (prm.debug_mode < 9 || prm.debug_mode > 14) {
                     if (pnew != po[j]) gP[pa[j]] = pnew;
-                    if (pmode == 1 || (pmode == 2 && pnew != po[j])) gS[so[j]] = pnew;
+                    if (pmode == 1 || pmode == 3 || (pmode == 2 && pnew != po[j])) gS[so[j]] = pnew;  // 1, 3: rebuild
                 } else if (prm.debug_mode == 12) {   // experiments: 9 no p / subset stores; 12 no subset stores
                     if (pnew != po[j]) gP[pa[j]] = pnew;
                 } else if (prm.debug_mode == 13) {   // 13 no p stores
@@ -548,12 +552,15 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
                 if (prm.do_adam && si.s1 > si.s0 && L.psub_mode == 2 && L.mv_tma)
                     bulk_prefetch_l2(static_cast<const unsigned char*>(L.psub) + (g.r0 * L.k + si.s0) * PSZ,
                                      ((g.Rr - 1) * L.k + si.s1 - si.s0) * PSZ);
+                if (prm.do_adam && si.s1 > si.s0 && L.psub_mode == 3 && L.mv_tma)
+                    bulk_prefetch_l2(static_cast<const unsigned char*>(L.psub_in) + g.r0 * L.k_in * PSZ,
+                                     (int64_t)g.Rr * L.k_in * PSZ);
 #ifndef ZF_K3_NO_PSUB_PPF
                 // with the subset slab, still pull the unit's p rows into L2 when the selection
                 // touches most of p's sectors: the changed values' stores then hit cached sectors
                 // instead of each waiting on a partial-sector fill (measured: steady K3 9.48 ->
                 // 9.36 ms at lr 1e-5, 10.33 -> 9.83 ms at lr 1e-3, Llama-2-7B k = 10%)
-                if (prm.do_adam && si.s1 > si.s0 && L.psub_mode == 2 && L.p_dense) {
+                if (prm.do_adam && si.s1 > si.s0 && (L.psub_mode == 2 || L.psub_mode == 3) && L.p_dense) {
                     const unsigned char* P = static_cast<const unsigned char*>(L.P);
                     for (int r = 0; r < g.Rr; ++r)
                         bulk_prefetch_l2(P + ((g.r0 + r) * L.ldp + g.c0) * PSZ, (int64_t)sw * PSZ);
@@ -649,6 +656,10 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
                     // the [R, s0:s1) slab (same layout as the moment slab)
                     const int64_t e0 = g.r0 * L.k + si.s0, e1 = (g.r0 + g.Rr - 1) * L.k + si.s1;
                     si.ePs = stage_elems<PSZ>(A, &off, L.psub, e0, e1, &full[st], &tx, &si.oPs);
+                } else if (si.psub_mode == 3 && si.mstaged) {
+                    // refresh from the previous block: the unit's full old rows, like the old moments
+                    si.ePs = stage_elems<PSZ>(A, &off, L.psub_in, g.r0 * L.k_in, (g.r0 + g.Rr) * L.k_in, &full[st],
+                                              &tx, &si.oPs);
                 }
                 if (si.pstaged) {
                     const unsigned char* P = static_cast<const unsigned char*>(L.P);
@@ -773,6 +784,8 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k_update(const __grid_constant_
 #ifndef ZF_K3_SLOTMAJOR
             if (si.psub_mode == 2 && si.mstaged) {
                 adam_unit_b<GDT, PDT, false, false, true>(si, A, prm, ctid, nfacc);
+            } else if (si.psub_mode == 3 && si.mstaged) {
+                adam_unit_b<GDT, PDT, false, true, true>(si, A, prm, ctid, nfacc);
             } else if (si.pstaged && si.mstaged) {
                 if (si.remap) adam_unit_b<GDT, PDT, true, true, false>(si, A, prm, ctid, nfacc);
                 else adam_unit_b<GDT, PDT, true, false, false>(si, A, prm, ctid, nfacc);

@@ -102,7 +102,11 @@ zf_status build_tables(zf_ctx* c) {
             t.units = gg.units;
             t.unit_begin = refresh ? l.unit_begin : l.unit_begin_s;
             t.mv_tma = gg.mv_ok ? 1 : 0;
-            t.psub = l.psub;
+            {   // subset blocks ping-pong with the moment sets (a refresh writes the other one)
+                void* blk[2] = {l.psub, l.psub2 ? l.psub2 : l.psub};
+                t.psub = blk[nw];
+                t.psub_in = blk[cur];
+            }
             t.psub_mode = l.psub ? 1 : 0;   // set per step (refresh_pointer_tables)
             t.sbv = l.sbv;
             t.gsel = l.gsel;
@@ -346,6 +350,10 @@ extern "C" zf_status zf_create(const zf_layer_desc* layers, int32_t n_layers, co
         // padded: K3 stages the subset with 16-byte-granular bulk copies.  The split update keeps
         // p's selected values in this dense block even without param_subset (rebuilt every step)
         if ((cfg->param_subset || c->split) && n > 0) ZF_CTRY(c->dalloc(&l.psub, ((size_t)n * k + 16) * c->psz, false));
+#if ZF_REFRESH_SUBSET
+        // refresh steps read the retained columns' p values from the previous block (mode 3)
+        if (cfg->param_subset && !c->split && n > 0) ZF_CTRY(c->dalloc(&l.psub2, ((size_t)n * k + 16) * c->psz, false));
+#endif
         if (c->split && n > 0) ZF_CTRY(c->dalloc(&l.gsel, ((size_t)n * k + 16) * c->gsz, false));
         if (c->tau > 0) {
             // the warm-up set: all m columns selected (slot = column), zero moments and counts
@@ -653,6 +661,23 @@ zf_status refresh_pointer_tables(zf_ctx* c, int variant, bool refresh, void* con
             const bool steady = variant >= 0 && ((variant >> 1) & 1) == 0;
             h[i].psub_mode = steady && c->psub_valid && c->cfg.param_subset ? 2 : 1;
             if (steady && c->cfg.param_subset) h[i].p_tma = 0;
+            if (variant >= 0 && !steady && c->subset_refresh) {
+                h[i].psub_mode = 3;
+                h[i].p_tma = 0;
+            }
+        }
+        if (variant >= 0 && ((variant >> 1) & 1) == 1 && !c->split) {
+            // a refresh: the steady unit shapes (no p tile) when it reads the retained columns'
+            // values from the previous subset block (mode 3), else its own (p tile) -- for every
+            // layer, rows-less ones included, so the unit ranges stay one consistent sequence
+            const LayerState& l = c->L[i];
+            const K3Geom& gg = c->subset_refresh ? l.geo_s : l.geo;
+            h[i].seg_cols = gg.seg_cols;
+            h[i].nseg = gg.nseg;
+            h[i].R = gg.R;
+            h[i].units = gg.units;
+            h[i].unit_begin = c->subset_refresh ? l.unit_begin_s : l.unit_begin;
+            h[i].mv_tma = gg.mv_ok ? 1 : 0;
         }
     }
     if (std::memcmp(h.data(), up.data(), nl * sizeof(UpdLayer)) != 0) {
@@ -747,6 +772,9 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
     const bool norms_now = (refresh && !lag_refresh) || c->autoz;  // Zen-auto reads every step's norms (R21)
     // f4 (i): this refresh runs K1 -> K2 -> K3 per group of layers (G re-read from L2)
     const bool grouped = refresh && !c->rgroups.empty() && c->have_sel && !c->split;
+    // a refresh with a valid subset block builds the new one from it (mode 3, steady unit shapes)
+    c->subset_refresh = ZF_REFRESH_SUBSET && refresh && !from_warmup && !grouped && c->have_sel && c->psub_valid &&
+                        c->cfg.param_subset && !c->split;
     ZF_TRY(refresh_pointer_tables(c, variant, norms_now || lag_pre, grads, params, s));
     c->tmark(1);
 
@@ -829,7 +857,8 @@ extern "C" zf_status zf_step(zf_ctx* c, int64_t t0, void* const* grads, void* co
     UpdParams prm{};
     prm.layers.dev = from_warmup ? c->d_upd_x[sb & 1] : c->d_upd_tab[variant];
     prm.layers.n = nl;
-    const bool steady_geo = !refresh && !from_warmup;  // (a first refresh after warm-up is a refresh)
+    // (a first refresh after warm-up is a refresh; a mode-3 refresh runs the steady unit shapes)
+    const bool steady_geo = (!refresh || c->subset_refresh) && !from_warmup;
     const int64_t units = steady_geo ? c->k3_units_s : c->k3_units;
     prm.total_units = units;
     prm.claim = c->claim;

@@ -351,6 +351,7 @@ struct LayerState {
     float* mom[2] = {nullptr, nullptr};
     float* vel[2] = {nullptr, nullptr};
     void* psub = nullptr;             // param_subset: [n, k] dense copy of p[:, idx] (HBM)
+    void* psub2 = nullptr;            // its ping-pong partner (blocks follow the moment sets' cur)
     float2* sbv = nullptr;            // [max(k, m during warm-up)] per-slot {ss, bc2s} of the next K3
     void* gsel = nullptr;             // split update: [n, k] selected gradients (K3a -> K3b)
     int64_t row_begin = 0;            // K3b: prefix of ceil(n*k / 8) over layers (its chunks)
@@ -612,6 +613,7 @@ struct zf_ctx {
     int cur = 0;
     bool have_sel = false;
     bool psub_valid = false;      // param_subset: the block holds p[:, idx] (set by a K3 in mode 1)
+    bool subset_refresh = false;  // this step's refresh reads retained p values from the old block (mode 3)
     bool split = false;           // regular steps run K3a (compaction + extraction) then K3b (dense AdamW)
     bool lagged = false;          // f4 (ii): refresh norms from the previous step (K1 on lag_stream)
     cudaStream_t lag_stream = nullptr;
