@@ -19,9 +19,11 @@
 //    refresh and steady steps use their own unit shapes (a steady unit holds no p tile).
 //  - a producer prefetches the claimed unit's G rows / slabs into L2 while its arena is
 //    still being consumed, then stages the unit's DATA into its arena with bulk copies
-//    (cp.async.bulk, the TMA engine) completing on one mbarrier: the G tile, the p tile
-//    (refresh, when the selection touches most of p's 32-byte sectors) or the dense
-//    parameter-subset slab (steady), and the moment slabs (or the old rows on a refresh).
+//    (cp.async.bulk, the TMA engine) completing on one mbarrier: the G tile, the dense
+//    parameter-subset slab (steady) or the previous subset block's old rows (a refresh:
+//    retained columns' p values; entering ones are loaded from p), or the p tile (a refresh
+//    without a valid block, when the selection touches most of p's 32-byte sectors), and the
+//    moment slabs (or the old rows on a refresh).
 //    The layer's selection METADATA (selected columns, per-slot bias corrections, remap
 //    sources, the unselected-column list) is not staged: every unit of a layer reads the
 //    same arrays, so the consumers read them through L1 and the arenas carry only data
