@@ -40,7 +40,7 @@ MUTANTS = [
     ("K3 bias correction past the table", INT, [("return t < h.sb_len ? __ldg(h.sb_tab + t) : make_float2(h.ss_inf, 1.0f);", "return t < h.sb_len ? __ldg(h.sb_tab + t) : make_float2(h.ss_inf, 0.5f);", 0)]),
     ("K3 v stores m", UPD, [("__stcs(si.v_out + so[j], vv[j]);", "__stcs(si.v_out + so[j], mm[j]);", 0)]),
     ("K3 changed p not stored", UPD, [("if (pnew != po[j]) gP[pa[j]] = pnew;\n                    if (pmode == 1", "if (false) gP[pa[j]] = pnew;\n                    if (pmode == 1", 0)]),
-    ("K3 subset block not updated", UPD, [("if (pmode == 1 || (pmode == 2 && pnew != po[j])) gS[so[j]] = pnew;\n                } else if (prm.debug_mode == 12)", "if (pmode == 1) gS[so[j]] = pnew;\n                } else if (prm.debug_mode == 12)", 0)]),
+    ("K3 subset block not updated", UPD, [("if (pmode == 1 || pmode == 3 || (pmode == 2 && pnew != po[j])) gS[so[j]] = pnew;", "if (pmode == 1 || pmode == 3) gS[so[j]] = pnew;", 0)]),
     ("K3 remap entering moments stale", UPD, [("mm[j] = ok ? sM[src[j]] : 0.0f;", "mm[j] = ok ? sM[src[j]] : sM[so[j] - s0];", 0)]),
     ("K3 compaction halves swapped", UPD, [("o.w = lds_u16(rowa + (u.w & 0xffffu)) | (lds_u16(rowa + (u.w >> 16)) << 16);", "o.w = lds_u16(rowa + (u.w >> 16)) | (lds_u16(rowa + (u.w & 0xffffu)) << 16);", 0)]),
     ("K3 compaction head/tail offset +1", UPD, [("const uint32_t bo = ((uint32_t)__ldg(gU + q) - base) & 0xffffu;", "const uint32_t bo = ((uint32_t)__ldg(gU + q) - base + GSZ) & 0xffffu;", 0)]),
@@ -78,6 +78,12 @@ MUTANTS = [
     ("warm-up one step longer", DRV, [("if (t0 < tau) return warmup_step(c, t0, grads, params, s);", "if (t0 <= tau) return warmup_step(c, t0, grads, params, s);", 0)]),
     ("K6 sums squared norms", AUTO, [("const double x = sqrt((double)__ldg(L.norms + j));", "const double x = (double)__ldg(L.norms + j);", 0)]),
     ("X1 copy gated one unit early", DRV, [("c->done_target[c->L[i].chunk] += (uint32_t)(steady_geo ? c->L[i].geo_s.units : c->L[i].geo.units) *", "c->done_target[c->L[i].chunk] += (uint32_t)((steady_geo ? c->L[i].geo_s.units : c->L[i].geo.units) - 1) *", 0)]),
+    # batch 4: the refresh from the previous parameter-subset block (psub_mode 3)
+    ("K3 subset refresh: retained value from the new slot", UPD, [("po[j] = src[j] >= row * kin ? sPs[src[j]] : gP[pa[j] + c0 + cc[j]];", "po[j] = src[j] >= row * kin ? sPs[so[j] - s0] : gP[pa[j] + c0 + cc[j]];", 0)]),
+    ("K3 subset refresh: entering value zero", UPD, [("po[j] = src[j] >= row * kin ? sPs[src[j]] : gP[pa[j] + c0 + cc[j]];", "po[j] = src[j] >= row * kin ? sPs[src[j]] : (PB)0;", 0)]),
+    ("subset blocks not ping-ponged", DRV, [("t.psub_in = blk[cur];", "t.psub_in = blk[nw];", 0)]),
+    ("subset refresh ignores psub_valid", DRV, [("c->have_sel && c->psub_valid &&", "c->have_sel &&", 0)]),
+    ("subset refresh block not rebuilt", UPD, [("if (pmode == 1 || pmode == 3 || (pmode == 2 && pnew != po[j])) gS[so[j]] = pnew;", "if (pmode == 1 || (pmode >= 2 && pnew != po[j])) gS[so[j]] = pnew;", 0)]),
 ]
 
 
