@@ -567,13 +567,15 @@ def test_lagged_selection_needs_fixed_windows(zf):
                    lagged_selection=True)
 
 
+@pytest.mark.parametrize("poke", [{2, 5, 6}, {4, 8}])
 @pytest.mark.parametrize("ppm", [100000, 10000])
-def test_params_changed_rereads_the_selected_columns(zf, orc, gpu, ppm):
-    """param_subset: the caller rewrites p between refreshes (t = 2, 5, 6) and calls
-    zf_params_changed; the next steady steps use the new values (bit-exact vs the oracle,
-    which sees the same writes)."""
+def test_params_changed_rereads_the_selected_columns(zf, orc, gpu, ppm, poke):
+    """param_subset: the caller rewrites p between refreshes (t = 2, 5, 6) or right before a
+    refresh (t = 4, 8: that refresh must read p, not the previous subset block) and calls
+    zf_params_changed; the next steps use the new values (bit-exact vs the oracle, which sees
+    the same writes)."""
     _run_stateful(zf, orc, gpu, [(128, 4096), (96, 700)], "bf16", "bf16", ppm, 4, 4, 9, offload=False,
-                  poke={2, 5, 6})
+                  poke=poke)
 
 
 def test_cpu_update_async_is_stale_until_the_next_call(zf, gpu):
